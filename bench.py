@@ -1,0 +1,304 @@
+#!/usr/bin/env python
+"""Benchmark: committed spin-flip events/s of the synchronous-relaxation
+n-fold way (arXiv cs/0405053) on BASELINE config 4 (16384^2, 4x4 regions,
+T=2, H=0, iid spins, W=0.5, t=50), strips over N GPUs.
+
+A "step" is one window of committed time (one full relaxation to the fixed
+point + commit = every §8(a) row).  W warm-up windows, then K timed windows,
+continuing the same trajectory (t_end is extended past 50 only if W+K > 100).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ising|reference]
+
+Prints one JSON line (rank 0).  --impl reference times the CPU oracle (the
+reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads  # noqa: E402
+
+METRIC = "committed spin-flip events/s"
+UNIT = "events/s"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------------
+# clocks sampled during the timed region (B200_PROFILING.md recipe)
+# --------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------
+# reference arm / cpu baseline: the oracle as it stands, on a bounded sample
+# --------------------------------------------------------------------------
+def oracle_sample(seconds_hint: float = 15.0):
+    """c4's dynamics (T=2, H=0, 4x4 regions, iid start, same seed) on a
+    2048^2 sub-lattice for t in [0, t_s); returns (events, wall s, sample)."""
+    import oracle
+    w = workloads.get("c4")
+    L = 2048
+    t_s = 1.0
+    spins = workloads.initial_spins(L, L, "random", seed=w.seed)
+    t0 = time.perf_counter()
+    r = oracle.des_run(L, L, 4, 4, w.rates(), w.seed, spins, t_s)
+    dt = time.perf_counter() - t0
+    return r["n_events"], dt, f"oracle O1 on a {L}x{L} lattice (c4 dynamics: 4x4 regions, T=2, H=0), t in [0,{t_s})"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+    except Exception:
+        pass
+    w = workloads.get("c4")
+    L, t_win = 1024, w.W
+    spins = workloads.initial_spins(L, L, "random", seed=w.seed)
+    evs, secs = [], []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        r = oracle.des_run(L, L, 4, 4, w.rates(), w.seed, spins, t_win)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            evs.append(r["n_events"])
+            secs.append(dt)
+    val = sum(evs) / sum(secs)
+    sample = f"oracle O1, one window [0,{t_win}) of c4 dynamics on a {L}x{L} sub-lattice per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / len(secs),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "c4 sample: 1024^2 sub-lattice, 4x4 regions, T=2, H=0, iid +-1 seed 1, one window W=0.5"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------
+# the B200 arm
+# --------------------------------------------------------------------------
+def run_ising(args):
+    import torch
+    from paper_cs_0405053_b200 import FLAG_DIGEST, IsingSR
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    exchange = None
+    if world > 1:
+        import torch.distributed as dist
+        from paper_cs_0405053_b200.dist import make_exchange
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        exchange = make_exchange(rank, world, local)
+
+    w = workloads.get(args.config)
+    nwin = args.warmup + args.steps
+    t_end = max(w.t_end, nwin * w.W)
+    spins = w.spins()
+    flags = FLAG_DIGEST
+    stream = torch.cuda.current_stream(local)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), spins, w.W, t_end, w.seed, J=w.J, H=w.H, T=w.T,
+                  flags=flags, rank=rank, world=world, device=local, stream=stream.cuda_stream,
+                  exchange=exchange)
+    for _ in range(args.warmup):
+        sim.run_window()
+        sim.commit()
+    st0 = sim.stats()
+    launches0 = sim.launch_count()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    gs = []
+    ev = 0
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            gs.append(sim.run_window())
+            ev += sim.commit()
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    st1 = sim.stats()
+    launches = sim.launch_count() - launches0
+    # whole-job numbers: events summed, time max over ranks
+    tot_ev, max_ms = ev, ms
+    region_ms = st1["region_ms"] - st0["region_ms"]
+    region_bytes = st1["region_bytes"] - st0["region_bytes"]
+    nlaunch = st1["region_launches"] - st0["region_launches"]
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([float(ev), region_bytes], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t)
+        m = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        tot_ev, max_ms = int(t[0].item()), float(m[0].item())
+    digest, count = sim.digests()
+    sim.close()
+
+    # e2e: the public API from host buffers -- init (H2D of the lattice from
+    # pinned memory + device packing) + K windows + D2H of the final spins
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.from_numpy(spins).pin_memory()
+        barrier()
+        t0 = time.perf_counter()
+        sim2 = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), pinned.numpy(), w.W, t_end, w.seed, flags=flags,
+                       rank=rank, world=world, device=local, stream=stream.cuda_stream, exchange=exchange)
+        ev2 = 0
+        for _ in range(args.steps):
+            sim2.run_window()
+            ev2 += sim2.commit()
+        out = sim2.spins()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        sim2.close()
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([float(ev2), dt], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t[:1])
+            dist.all_reduce(t[1:], op=dist.ReduceOp.MAX)
+            ev2, dt = t[0].item(), t[1].item()
+        e2e = {"value": ev2 / dt, "unit": UNIT,
+               "h2d_bytes_per_step": spins.nbytes / args.steps,
+               "d2h_bytes_per_step": (out.nbytes * world + 8 * args.steps) / args.steps,
+               "includes": "ising_sr_init from pinned host spins (H2D + pack) + K windows + D2H of final spins"}
+
+    if rank != 0:
+        return 0
+    peak, peak_kind = _peaks()
+    achieved = (region_bytes / (region_ms * 1e-3)) / 1e9 if region_ms > 0 else 0.0
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+            "kernel": "region_kernel<4,4> (K1 trajectory + fused diff)",
+            "bytes_per_launch": region_bytes / max(nlaunch, 1),
+            "ms_per_launch": region_ms / max(nlaunch, 1),
+            "share_of_step": region_ms / ms if ms > 0 else None}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        n_ev, secs, sample = oracle_sample()
+        cpu = {"value": n_ev / secs, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
+    line = {
+        "metric": METRIC, "value": tot_ev / (max_ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {w.Lx}x{w.Ly} periodic, {w.bx}x{w.by} regions, T={w.T}, H={w.H}, "
+                               f"iid +-1 seed {w.seed}, W={w.W}, windows {args.warmup}..{nwin - 1} "
+                               f"(t {args.warmup * w.W}..{nwin * w.W})",
+                   "regions": w.n_regions, "l2": "inputs larger than L2 (state+histories >> 126 MB)",
+                   "parallelism": f"strips{world}"},
+        "events": tot_ev,
+        "iterations_per_window": {"mean": float(np.mean(gs)), "max": int(max(gs)), "min": int(min(gs)),
+                                  "ln_N": math.log(w.n_regions)},
+        "bytes_alg_per_event": region_bytes / max(ev, 1),
+        "gpu_launches": launches,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=97)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ising", choices=["ising", "reference"])
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ising(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

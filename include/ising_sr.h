@@ -1,0 +1,191 @@
+/*
+ * include/ising_sr.h -- C ABI of libising_sr.so, the B200 (sm_100a) engine for
+ * the synchronous-relaxation parallel n-fold way Ising simulation of
+ * Lubachevsky & Weiss, arXiv cs/0405053 ("the paper"; P:n = line n of its
+ * text).
+ *
+ * What the library computes.  The periodic Lx x Ly lattice G is
+ * cut into bx x by regions G_i, one per virtual processing element
+ * (P:494-500); region id = region_row * (Lx/bx) + region_col.  Simulated time
+ * advances in windows [t_c, t_c + W) (committed time and step size T_max,
+ * P:320-335, 400-402).  Within a window every region repeatedly regenerates its
+ * continuous-time n-fold-way history from its own
+ * counter-based random list, integrating its total rate
+ * over break points caused by the neighbours' boundary flips of the previous
+ * iteration (eqs. lambdataua..newtau); the boundary histories are
+ * compared with the previous iteration's and the iteration repeats until no
+ * history changes.  The fixed point is the unique
+ * trajectory of the per-region-stream dynamics; it is
+ * independent of W and of the number of shards.
+ *
+ * Bit-level semantics (Philox layout, E(U), Lambda fold order, selection,
+ * candidate bump, tie order) are frozen in DESIGN.md §3; results are
+ * bit-reproducible across runs, W and shard counts.
+ *
+ * Conventions (all entry points):
+ *  - every call returns ising_sr_status (0 = OK, < 0 = error) unless noted;
+ *  - host buffers are owned by the caller; `init` copies `spins`;
+ *  - device state is owned by the library (cudaMalloc on cfg.device);
+ *  - one ctx per rank / shard; a ctx is not thread-safe;
+ *  - all device work is issued on cfg.stream (a cudaStream_t; NULL = the
+ *    library creates its own stream); calls that return host data
+ *    synchronize that stream;
+ *  - after a CUDA error every later call returns ISING_SR_E_CUDA (sticky).
+ */
+#ifndef ISING_SR_H
+#define ISING_SR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ising_sr_ctx ising_sr_ctx; /* opaque; owned by the library */
+
+typedef enum {
+  ISING_SR_OK = 0,
+  ISING_SR_E_INVALID_ARG = -1, /* NULL pointer, bad rate/W/t_end, unsupported region shape */
+  ISING_SR_E_DIMENSION = -2,   /* Lx or Ly < 3 (neighbours must be distinct) */
+  ISING_SR_E_PARTITION = -3,   /* bx, by do not divide Lx, Ly; strips do not divide region rows */
+  ISING_SR_E_DIVERGED = -4,    /* max_iterations reached without a fixed point */
+  ISING_SR_E_CAPACITY = -5,    /* boundary-history capacity cannot be grown further */
+  ISING_SR_E_CUDA = -6,        /* CUDA runtime error (sticky) */
+  ISING_SR_E_NCCL = -7,        /* exchange callback reported failure */
+  ISING_SR_E_OOM = -8,         /* device allocation failed */
+  ISING_SR_E_STATE = -9        /* call out of order (commit without a converged window, run past t_end) */
+} ising_sr_status;
+
+/* cfg.flags */
+#define ISING_SR_FLAG_LOG_EVENTS 0x1u /* commit writes the window's compact event log (get_events) */
+#define ISING_SR_FLAG_DIGEST 0x2u     /* maintain per-region event digests (get_digests) */
+
+/* Halo exchange between strips (world > 1).  Rank q owns a band of region
+ * rows; "up" is toward region row 0 (rank q-1, periodic), "down" toward rank
+ * q+1.  After each relaxation iteration the library calls the exchange
+ * callback with device pointers into the current iteration's boundary-history
+ * buffers; the callee must
+ *   (a) copy my send_up chunks into rank (q-1)'s recv_from_down chunks and my
+ *       send_down chunks into rank (q+1)'s recv_from_up chunks (periodic in
+ *       q; with world == 2 both go to the other rank), chunk k being
+ *       chunk_bytes[k] long, and
+ *   (b) replace flags[0..1] (device int32 {changed, overflow}) by their
+ *       maximum over all ranks (the "UNTIL all PEs detect no difference" of
+ *       P:427-429).
+ * send_up = my first region row's north-edge histories (count row, time
+ * block, position block); send_down = my last row's south-edge histories.
+ * Work may be enqueued on `stream` (the ctx stream) and must be ordered on it
+ * on return.  Return 0 on success (anything else -> ISING_SR_E_NCCL). */
+typedef struct {
+  int32_t nchunks;          /* 3: counts (u8), times (f64), positions (u8) */
+  void* send_up[4];
+  void* send_down[4];
+  void* recv_from_up[4];    /* ghost row above my strip: up neighbour's south edges */
+  void* recv_from_down[4];  /* ghost row below my strip: down neighbour's north edges */
+  size_t chunk_bytes[4];
+  int32_t* flags;           /* device int32[2]: {changed, overflow}; all-reduce(max) */
+  void* stream;             /* cudaStream_t of the ctx */
+} ising_sr_halo;
+
+typedef int (*ising_sr_exchange_fn)(void* user, const ising_sr_halo* halo);
+
+typedef struct {
+  int32_t Lx, Ly;           /* lattice, periodic both ways; >= 3                 */
+  int32_t bx, by;           /* region size; divides Lx, Ly; supported: 1,2,4,8 (square)      */
+  double J, H, T;           /* recorded for observables; the dynamics use `rate` only        */
+  double rate[10];          /* r_k = lambda p_k, class k = 5(s+1)/2 + u          */
+  double W;                 /* window length = the paper's T_max, > 0            */
+  double t_end;             /* simulate events with tau < t_end                              */
+  uint64_t seed;            /* Philox key/counter seed                         */
+  int32_t max_iterations;   /* relaxation iterations per window before E_DIVERGED; 0 = 1000  */
+  int32_t hist_capacity;    /* initial boundary-history slots per region edge; 0 = auto      */
+  uint32_t flags;           /* ISING_SR_FLAG_*                                               */
+  int32_t rank, world;      /* this ctx owns region rows [rank*RY/world, (rank+1)*RY/world)  */
+  int32_t device;           /* CUDA ordinal                                                  */
+  void* stream;             /* cudaStream_t; NULL = library-owned stream                     */
+  ising_sr_exchange_fn exchange; /* required iff world > 1                                  */
+  void* exchange_user;
+} ising_sr_config;
+
+typedef struct {
+  double t_c;               /* committed time                                                */
+  int64_t windows;          /* committed windows                                             */
+  int64_t events_total;     /* committed events (this rank)                                  */
+  int64_t events_last_window;
+  int32_t g_last, g_max;    /* relaxation iterations of the last window / max    */
+  int64_t g_hist[64];       /* histogram of g over committed windows (g >= 63 -> bin 63)     */
+  int32_t f_last, f_max;    /* max own-boundary events of a region in an iteration */
+  int64_t iterations_total; /* relaxation iterations run (all windows, incl. retries)        */
+  int32_t overflow_retries; /* windows restarted after history-capacity overflow             */
+  int32_t hist_capacity;    /* current slots per region edge                                 */
+  int64_t recomputations_total; /* region trajectories computed (sum over iterations)        */
+  double bytes_alg_last_window; /* algorithmic HBM bytes of the last window   */
+  double ms_last_window;    /* device time of run_window + commit of the last window          */
+  /* cumulative instrumentation of the region-trajectory kernel (all windows):
+   * launches, device time (CUDA events on the ctx stream around each launch)
+   * and algorithmic bytes */
+  int64_t region_launches;
+  double region_ms;
+  double region_bytes;
+} ising_sr_stats;
+
+/* Validate cfg, allocate device state, copy the full Ly*Lx row-major spin
+ * configuration (1 = up, 0 = down; caller-owned, copied) and set committed
+ * time 0.  Each rank passes the whole lattice and keeps its strip. */
+ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, ising_sr_ctx** out);
+
+/* Relax the window [t_c, min(t_c + W, t_end)) to the fixed point.
+ * Deterministic and idempotent until commit.  *g_out = iterations run,
+ * including the final no-change iteration.  E_DIVERGED leaves the committed
+ * state untouched.  E_STATE if t_c >= t_end. */
+ising_sr_status ising_sr_run_window(ising_sr_ctx* ctx, int32_t* g_out);
+
+/* Commit the converged window: committed state <- fixed point, t_c += W
+ * (P:430).  *events_out = events committed in the window on this rank.
+ * E_STATE without a converged run_window. */
+ising_sr_status ising_sr_commit(ising_sr_ctx* ctx, int64_t* events_out);
+
+/* Convenience: run_window + commit until t_c >= t_end. */
+ising_sr_status ising_sr_run(ising_sr_ctx* ctx, int64_t* events_out);
+
+ising_sr_status ising_sr_stats_get(const ising_sr_ctx* ctx, ising_sr_stats* out);
+
+/* Own strip's committed spins, (Ly/world) x Lx row-major, 1 = up. */
+ising_sr_status ising_sr_get_spins(ising_sr_ctx* ctx, uint8_t* out);
+
+/* Last committed window's event log (requires FLAG_LOG_EVENTS), ordered by
+ * region id then time: time, global region id, local site (row*bx + col).
+ * Copies min(cap, n) entries; *n = number of events in the window. */
+ising_sr_status ising_sr_get_events(ising_sr_ctx* ctx, double* t, uint32_t* region, uint16_t* site,
+                                    int64_t cap, int64_t* n);
+
+/* Per own region (region-id order): digest chain over all committed events,
+ * h <- mix64(mix64(h ^ tau_bits) ^ site) (requires FLAG_DIGEST), and the
+ * committed event count n.  Either pointer may be NULL. */
+ising_sr_status ising_sr_get_digests(ising_sr_ctx* ctx, uint64_t* digest, uint64_t* count);
+
+/* Step-level API used by multi-rank drivers (the loop of run_window, one
+ * iteration at a time).  begin_window starts a window; iterate runs one
+ * relaxation iteration (all own regions) and returns this rank's local
+ * {changed, overflow} in flags_out (no exchange); halo fills the exchange
+ * descriptor of the iteration just run; end_iterations declares the window
+ * converged after `g` iterations (global decision of the caller). */
+ising_sr_status ising_sr_begin_window(ising_sr_ctx* ctx);
+ising_sr_status ising_sr_iterate(ising_sr_ctx* ctx, int32_t flags_out[2]);
+ising_sr_status ising_sr_halo_get(ising_sr_ctx* ctx, ising_sr_halo* out);
+ising_sr_status ising_sr_end_iterations(ising_sr_ctx* ctx, int32_t g);
+/* g == -1 in end_iterations: some rank overflowed its history capacity; the
+ * library doubles the capacity (the same on every rank) and the caller
+ * restarts the window with begin_window. */
+
+/* Number of kernel launches issued by this ctx so far (instrumentation). */
+int64_t ising_sr_launch_count(const ising_sr_ctx* ctx);
+
+void ising_sr_destroy(ising_sr_ctx* ctx); /* NULL-safe */
+const char* ising_sr_strerror(ising_sr_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISING_SR_H */

@@ -1,0 +1,11 @@
+"""B200-native synchronous-relaxation parallel n-fold way (arXiv cs/0405053).
+
+The product is ``libising_sr.so`` (C ABI in ``include/ising_sr.h``): sm_100a
+CUDA kernels for the region trajectories, the fused history diff, commit and
+log replay, plus the host relaxation loop.  This package is its thin Python
+binding (``binding.IsingSR``) and the multi-rank driver (``dist``).
+"""
+from .binding import (FLAG_DIGEST, FLAG_LOG_EVENTS, IsingSR, IsingSRError, from_workload,  # noqa: F401
+                      load_library)
+
+__all__ = ["IsingSR", "IsingSRError", "from_workload", "load_library", "FLAG_DIGEST", "FLAG_LOG_EVENTS"]

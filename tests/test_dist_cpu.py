@@ -1,0 +1,75 @@
+"""World-size-2 (and 3) gloo tests of the strip-halo exchange protocol on CPU.
+
+Checks that rank q's send_up lands in rank q-1's recv_from_down, its
+send_down in rank q+1's recv_from_up (periodic), and that the flag
+all-reduce is a MAX -- the host-side logic of the N>1 path."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_cs_0405053_b200.dist import halo_exchange, neighbours
+        sizes = [5, 3 * 8, 3]
+        su = [torch.full((n,), 10 * rank + 1, dtype=torch.uint8) for n in sizes]
+        sd = [torch.full((n,), 10 * rank + 2, dtype=torch.uint8) for n in sizes]
+        ru = [torch.zeros(n, dtype=torch.uint8) for n in sizes]
+        rd = [torch.zeros(n, dtype=torch.uint8) for n in sizes]
+        flags = torch.tensor([1 if rank == world - 1 else 0, 1 if rank == 0 else 0], dtype=torch.int32)
+        halo_exchange(su, sd, ru, rd, flags, rank, world)
+        up, down = neighbours(rank, world)
+        ok = all(int(t[0]) == 10 * up + 2 and bool((t == t[0]).all()) for t in ru)
+        ok &= all(int(t[0]) == 10 * down + 1 and bool((t == t[0]).all()) for t in rd)
+        ok &= flags.tolist() == [1, 1]
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_exchange_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res[r] for r in range(world)), res
+
+
+def test_strip_partition_rule():
+    """Region rows split into equal contiguous strips; the C ABI rejects
+    strips that do not divide (E_PARTITION)."""
+    import ctypes
+    import numpy as np
+    from paper_cs_0405053_b200 import _build, binding
+    _build.build()
+    L = binding.load_library()
+    c = binding.Config()
+    c.Lx, c.Ly, c.bx, c.by = 16, 12, 4, 4   # 3 region rows
+    for k in range(10):
+        c.rate[k] = 1.0
+    c.W, c.t_end, c.world, c.rank = 1.0, 1.0, 2, 0
+    c.exchange = binding.EXCHANGE_FN(lambda u, h: 0)
+    h = ctypes.c_void_p()
+    s = np.zeros(16 * 12, dtype=np.uint8)
+    assert L.ising_sr_init(ctypes.byref(c), s.ctypes.data, ctypes.byref(h)) == -3

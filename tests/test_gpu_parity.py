@@ -1,0 +1,175 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle,
+bit-exact -- final spins, per-region event counts, per-region digests of the
+full (fp64 time bits, site) sequences, and the per-window event logs.
+
+Tolerance: none.  Both sides implement the same IEEE operation sequence
+(DESIGN.md §3), so every fp64 event time must agree to the bit.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_cs_0405053_b200 import FLAG_DIGEST, FLAG_LOG_EVENTS, IsingSR, IsingSRError  # noqa: E402
+
+
+def run_gpu(w, flags=FLAG_DIGEST | FLAG_LOG_EVENTS, per_window_logs=False, **kw):
+    sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed, flags=flags, **kw)
+    logs, gs = [], []
+    total = 0
+    while True:
+        try:
+            g = sim.run_window()
+        except IsingSRError as e:
+            if e.status == -9:  # past t_end
+                break
+            raise
+        gs.append(g)
+        total += sim.commit()
+        if per_window_logs:
+            logs.append(sim.events())
+    dig, cnt = sim.digests()
+    out = {"spins": sim.spins(), "digest": dig, "count": cnt, "events": total, "g": gs,
+           "logs": logs, "stats": sim.stats()}
+    sim.close()
+    return out
+
+
+def check_against_oracle(w, gpu=None, logs=True):
+    ref = oracle.des_workload(w, log_cap=10**7 if logs else 0)
+    gpu = gpu or run_gpu(w, per_window_logs=logs)
+    assert gpu["events"] == ref["n_events"]
+    assert np.array_equal(gpu["count"], ref["count"])
+    assert np.array_equal(gpu["spins"], ref["spins"])
+    if gpu["digest"] is not None:
+        assert np.array_equal(gpu["digest"], ref["digest"])
+    if logs and gpu["logs"]:
+        # window w holds the oracle events with t in [fl(w W), fl((w+1) W))
+        t_all, r_all, s_all = ref["log_t"], ref["log_region"], ref["log_site"]
+        for k, (t, r, s) in enumerate(gpu["logs"]):
+            lo = k * w.W
+            hi = min((k + 1) * w.W, w.t_end)
+            sel = (t_all >= lo) & (t_all < hi)
+            order = np.lexsort((t_all[sel], r_all[sel]))  # region, then time
+            assert np.array_equal(t, t_all[sel][order]), f"window {k} times"
+            assert np.array_equal(r, r_all[sel][order]), f"window {k} regions"
+            assert np.array_equal(s, s_all[sel][order]), f"window {k} sites"
+    return ref, gpu
+
+
+def test_c1_bit_exact_full():
+    """BASELINE config 1 in full: 16x16, 4x4 regions, T=1.5, W=1, t=10."""
+    w = workloads.get("c1")
+    ref, gpu = check_against_oracle(w)
+    assert ref["n_events"] > 300
+    assert max(gpu["g"]) >= 2  # real relaxation happened
+
+
+@pytest.mark.parametrize("geom", [
+    # Lx, Ly, bx, by, T, H, W, t_end, init
+    (16, 16, 1, 1, 2.269, 0.0, 0.5, 4.0, "random"),
+    (16, 16, 2, 2, 1.5, 0.0, 1.0, 6.0, "random"),
+    (24, 16, 4, 4, 4.0, 0.3, 0.25, 3.0, "random"),
+    (32, 32, 8, 8, 2.269, 0.0, 0.375, 8.0, "up"),
+    (16, 24, 4, 8, 2.0, -0.2, 0.7, 5.0, "random"),
+    (24, 16, 8, 4, 3.0, 0.0, 1.3, 5.0, "random"),
+    (12, 20, 4, 2, 1.8, 0.1, 0.5, 6.0, "random"),
+    (20, 12, 2, 4, 2.5, 0.0, 0.9, 6.0, "random"),
+    (9, 9, 1, 1, 1.2, 0.0, 2.0, 10.0, "random"),
+    (3, 3, 1, 1, 2.0, 0.0, 1.0, 30.0, "random"),
+])
+def test_geometries_bit_exact(geom):
+    Lx, Ly, bx, by, T, H, W, t_end, init = geom
+    w = workloads.Workload("g", Lx, Ly, bx, by, T=T, H=H, W=W, t_end=t_end, init=init, seed=7)
+    check_against_oracle(w)
+
+
+@pytest.mark.parametrize("geom", [(8, 8, 8, 8), (4, 4, 4, 4), (16, 8, 4, 8), (8, 16, 8, 4), (8, 4, 8, 4)])
+def test_regions_spanning_a_dimension(geom):
+    """Regions covering the lattice height and/or width wrap inside the region
+    (no ghost on that axis); one region covering the lattice has g == 1."""
+    Lx, Ly, bx, by = geom
+    w = workloads.Workload("span", Lx, Ly, bx, by, T=2.0, W=0.8, t_end=6.0, seed=3)
+    ref, gpu = check_against_oracle(w)
+    if Lx == bx and Ly == by:
+        assert set(gpu["g"]) == {1}
+
+
+def test_single_region_equals_single_stream_bkl():
+    w = workloads.Workload("one", 8, 8, 8, 8, T=2.269, W=1.0, t_end=10.0, seed=5)
+    gpu = run_gpu(w, per_window_logs=True)
+    b = oracle.bkl_run(8, 8, w.rates(), 5, w.spins(), 10.0, log_cap=10**6)
+    t = np.concatenate([l[0] for l in gpu["logs"]])
+    s = np.concatenate([l[2] for l in gpu["logs"]])
+    assert np.array_equal(t, b["log_t"]) and np.array_equal(s, b["log_site"])
+
+
+def test_c2_full_bit_exact():
+    """BASELINE config 2 in full: 256^2, 8x8 regions, T=2.269, all up, W=0.375, t=100."""
+    w = workloads.get("c2")
+    check_against_oracle(w, logs=False)
+
+
+@pytest.mark.parametrize("W", [0.25, 1.0, 4.0, 2.125, 0.1])
+def test_window_invariance(W):
+    """The fixed point does not depend on W (windows only schedule work)."""
+    w = workloads.Workload("wi", 32, 32, 4, 4, T=2.0, W=W, t_end=8.0, seed=11)
+    check_against_oracle(w, logs=False)
+
+
+def test_capacity_overflow_retry_is_exact():
+    w = workloads.Workload("cap", 32, 32, 4, 4, T=4.0, W=2.0, t_end=6.0, seed=2)
+    gpu = run_gpu(w, per_window_logs=False, hist_capacity=1)
+    assert gpu["stats"]["overflow_retries"] >= 1
+    check_against_oracle(w, gpu=gpu, logs=False)
+
+
+def test_diverged_window_is_not_committed():
+    w = workloads.Workload("div", 32, 32, 2, 2, T=2.0, W=4.0, t_end=8.0, seed=4)
+    sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed, max_iterations=2)
+    with pytest.raises(IsingSRError) as e:
+        sim.run_window()
+    assert e.value.status == -4
+    with pytest.raises(IsingSRError) as e:
+        sim.commit()
+    assert e.value.status == -9
+    assert np.array_equal(sim.spins(), w.spins())  # committed state untouched
+    st = sim.stats()
+    assert st["windows"] == 0 and st["events_total"] == 0
+    sim.close()
+
+
+def test_determinism_and_idempotence():
+    w = workloads.Workload("det", 64, 64, 4, 4, T=2.269, W=0.6, t_end=3.0, seed=8)
+    a = run_gpu(w)
+    b = run_gpu(w)
+    assert a["g"] == b["g"]
+    assert np.array_equal(a["digest"], b["digest"])
+    # re-running an uncommitted window gives the same fixed point and g
+    sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed)
+    g1 = sim.run_window()
+    g2 = sim.run_window()
+    assert g1 == g2 == a["g"][0]
+    sim.commit()
+    sim.close()
+
+
+def test_c4_full_lattice_prefix():
+    """BASELINE config 4 at its full size (16384^2, 4x4 regions, T=2, W=0.5) on
+    the prefix t < 0.02: every region's digest and count, and all spins."""
+    w = workloads.get("c4", t_end=0.02)
+    ref = oracle.des_workload(w)
+    gpu = run_gpu(w, flags=FLAG_DIGEST)
+    assert gpu["events"] == ref["n_events"] > 10**6
+    assert np.array_equal(gpu["count"], ref["count"])
+    assert np.array_equal(gpu["digest"], ref["digest"])
+    assert np.array_equal(gpu["spins"], ref["spins"])
