@@ -104,7 +104,7 @@ typedef struct {
   int32_t rank, world;      /* this ctx owns region rows [rank*RY/world, (rank+1)*RY/world)  */
   int32_t device;           /* CUDA ordinal                                                  */
   void* stream;             /* cudaStream_t; NULL = library-owned stream                     */
-  ising_sr_exchange_fn exchange; /* required iff world > 1                                  */
+  ising_sr_exchange_fn exchange; /* world > 1: used by run_window (step API: unused)       */
   void* exchange_user;
 } ising_sr_config;
 
@@ -167,17 +167,22 @@ ising_sr_status ising_sr_get_digests(ising_sr_ctx* ctx, uint64_t* digest, uint64
 
 /* Step-level API used by multi-rank drivers (the loop of run_window, one
  * iteration at a time).  begin_window starts a window; iterate runs one
- * relaxation iteration (all own regions) and returns this rank's local
- * {changed, overflow} in flags_out (no exchange); halo fills the exchange
- * descriptor of the iteration just run; end_iterations declares the window
- * converged after `g` iterations (global decision of the caller). */
+ * relaxation iteration (the regions whose incoming histories changed; all
+ * regions in the window's first iteration) and returns this rank's local
+ * {changed, overflow} in flags_out; for world > 1, halo_get then describes
+ * the send/receive ghost rows of that iteration (same contract as the
+ * exchange callback, flags excluded), and after the caller has moved them
+ * exchange_done marks the regions next to changed ghosts for the next
+ * iteration.  end_iterations declares the window converged after `g`
+ * iterations (the caller's global decision: no rank changed).
+ * g == -1 in end_iterations: some rank overflowed its history capacity; the
+ * library doubles the capacity (the same on every rank) and the caller
+ * restarts the window with begin_window. */
 ising_sr_status ising_sr_begin_window(ising_sr_ctx* ctx);
 ising_sr_status ising_sr_iterate(ising_sr_ctx* ctx, int32_t flags_out[2]);
 ising_sr_status ising_sr_halo_get(ising_sr_ctx* ctx, ising_sr_halo* out);
+ising_sr_status ising_sr_exchange_done(ising_sr_ctx* ctx);
 ising_sr_status ising_sr_end_iterations(ising_sr_ctx* ctx, int32_t g);
-/* g == -1 in end_iterations: some rank overflowed its history capacity; the
- * library doubles the capacity (the same on every rank) and the caller
- * restarts the window with begin_window. */
 
 /* Number of kernel launches issued by this ctx so far (instrumentation). */
 int64_t ising_sr_launch_count(const ising_sr_ctx* ctx);

@@ -70,7 +70,8 @@ _lib = None
 
 EXPORTS = ["ising_sr_init", "ising_sr_run_window", "ising_sr_commit", "ising_sr_run",
            "ising_sr_stats_get", "ising_sr_get_spins", "ising_sr_get_events", "ising_sr_get_digests",
-           "ising_sr_begin_window", "ising_sr_iterate", "ising_sr_halo_get", "ising_sr_end_iterations",
+           "ising_sr_begin_window", "ising_sr_iterate", "ising_sr_halo_get", "ising_sr_exchange_done",
+           "ising_sr_end_iterations",
            "ising_sr_launch_count", "ising_sr_destroy", "ising_sr_strerror"]
 
 
@@ -95,6 +96,7 @@ def load_library(path: str = LIB_PATH):
     L.ising_sr_begin_window.argtypes = [vp]
     L.ising_sr_iterate.argtypes = [vp, vp]
     L.ising_sr_halo_get.argtypes = [vp, ctypes.POINTER(Halo)]
+    L.ising_sr_exchange_done.argtypes = [vp]
     L.ising_sr_end_iterations.argtypes = [vp, i32]
     L.ising_sr_launch_count.argtypes = [vp]
     L.ising_sr_launch_count.restype = i64
@@ -197,6 +199,9 @@ class IsingSR:
         h = Halo()
         _check(self._L.ising_sr_halo_get(self._h, ctypes.byref(h)), "ising_sr_halo_get")
         return h
+
+    def exchange_done(self):
+        _check(self._L.ising_sr_exchange_done(self._h), "ising_sr_exchange_done")
 
     def end_iterations(self, g: int):
         _check(self._L.ising_sr_end_iterations(self._h, g), "ising_sr_end_iterations")

@@ -59,24 +59,45 @@ struct StateView {
   unsigned long long* dig;
 };
 
+// Boundary histories of one slot: cnt[4][RYl][RX], t/pos[4][RYl][K][RX].
+// Every region edge has two slots; which one holds its latest history is
+// recorded in the region's selector word (see latest_of).
 struct EdgeView {
-  uint8_t* cnt;  // [4][rows_s][RX]
-  double* t;     // [4][rows_s][K][RX]
-  uint8_t* pos;  // [4][rows_s][K][RX]
+  uint8_t* cnt;
+  double* t;
+  uint8_t* pos;
+};
+
+// A ghost row received from a neighbouring strip (world > 1):
+// cnt[RX], stamp[RX] (global iteration of the last change), t/pos[K][RX].
+struct GhostView {
+  uint8_t* cnt;
+  uint32_t* stamp;
+  double* t;
+  uint8_t* pos;
 };
 
 struct KArgs {
   StateView in, out;
-  EdgeView prev, cur;
+  EdgeView ed[2];
+  unsigned long long* sel;      // per region selector word
+  GhostView gh_up, gh_down;     // world > 1: rows above / below the strip
   int RX, RYl, RYg, row0, world;
   int K;
-  long long cstride;  // elements per edge in cnt  (rows_s * RX)
-  long long tstride;  // elements per edge in t/pos (rows_s * K * RX)
-  int first;          // iteration 1: canonical assumption
+  long long cstride;  // elements per edge in cnt  (RYl * RX)
+  long long tstride;  // elements per edge in t/pos (RYl * K * RX)
+  unsigned it_K;      // global iteration stamp of this launch (>= 1)
+  unsigned it_K0;     // stamp of the window's first iteration
+  int first;          // window's first iteration: canonical assumption
   int digest;
   double t_w;         // window end
   unsigned long long seed;
   double rate[10];
+  const uint32_t* wl_in;   // regions to recompute (nullptr: all regions)
+  int n_work;              // number of regions to recompute
+  uint32_t* wl_out;        // worklist of the next iteration
+  unsigned* wl_out_count;
+  uint32_t* dirty;         // per region: last stamp it was queued for
   int* flags;                   // [0] changed, [1] overflow
   unsigned long long* stats;    // [0] events [1] entries out [2] entries in [3] entries cmp [4] f max [5] regions
   // log replay
@@ -85,6 +106,38 @@ struct KArgs {
   uint16_t* log_site;
   const unsigned long long* log_off;
 };
+
+// Selector word of a region (64 bits, written only by its own thread, read
+// racily by neighbours -- a 64-bit aligned store/load is single-copy atomic
+// and both the old and the new value decode to the same answer):
+//   bits 0-3  slot of the latest history of edge e
+//   bits 4-7  edges changed at K_last
+//   bits 8-11 edges holding a history written in this window (as of K_last)
+//   bits 12-15 the same before the K_last change
+//   bits 32-63 K_last, global iteration of the last change
+// latest_of(): the edge's latest history as of the end of iteration K-1.
+struct Latest {
+  int slot;
+  bool valid;  // false: canonical empty history
+};
+
+__device__ __forceinline__ Latest latest_of(unsigned long long v, int e, unsigned K, unsigned K0) {
+  const unsigned Kl = (unsigned)(v >> 32);
+  const unsigned slots = (unsigned)v & 0xF, ch = ((unsigned)v >> 4) & 0xF;
+  const unsigned ne = ((unsigned)v >> 8) & 0xF, nep = ((unsigned)v >> 12) & 0xF;
+  if (Kl < K0) return {0, false};
+  if (Kl < K) return {(int)((slots >> e) & 1u), ((ne >> e) & 1u) != 0};
+  return {(int)(((slots ^ ch) >> e) & 1u), ((nep >> e) & 1u) != 0};  // changed concurrently in K
+}
+
+__device__ __forceinline__ unsigned long long sel_after_change(unsigned long long v, unsigned chmask, unsigned K,
+                                                               unsigned K0) {
+  const unsigned Kl = (unsigned)(v >> 32);
+  const unsigned slots = (unsigned)v & 0xF;
+  const unsigned ne_old = Kl >= K0 ? (((unsigned)v >> 8) & 0xF) : 0u;
+  const unsigned lo = (slots ^ chmask) | (chmask << 4) | ((ne_old | chmask) << 8) | (ne_old << 12);
+  return ((unsigned long long)K << 32) | lo;
+}
 
 // bit-sliced per-site count of up neighbours: m[u] = sites with exactly u.
 template <class G>
@@ -230,8 +283,14 @@ __device__ __forceinline__ unsigned long long compress_halo(typename G::M gN, ty
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
 // ---------------------------------------------------------------------------
-// K1: one relaxation iteration for every region of the shard (LOG = false),
-// or the commit-time replay that writes the compact event log (LOG = true).
+// K1: one relaxation iteration for the regions of the worklist (all regions
+// in the window's first iteration), or the commit-time replay that writes
+// the compact event log (LOG = true; all regions, latest histories).
+//
+// Only regions with a changed incoming history are recomputed: a region
+// whose inputs did not change would regenerate exactly its previous history
+// (the same presimulated random list), so skipping it does not
+// change the iteration count g or any result.
 // ---------------------------------------------------------------------------
 template <int BX, int BY, bool LOG>
 __global__ void __launch_bounds__(128) region_kernel(const KArgs a) {
@@ -240,13 +299,14 @@ __global__ void __launch_bounds__(128) region_kernel(const KArgs a) {
   using ST = typename G::ST;
   using HT = typename G::HT;
 
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  const int nreg = a.RX * a.RYl;
-  const bool live = idx < nreg;
-  const int r = live ? idx / a.RX : 0;
-  const int c = live ? idx - r * a.RX : 0;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = tid < a.n_work;
+  const int idx = live ? (a.wl_in ? (int)a.wl_in[tid] : tid) : 0;
+  const int r = idx / a.RX;
+  const int c = idx - r * a.RX;
   const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
   const uint32_t gid = (uint32_t)((a.row0 + r) * a.RX + c);
+  const unsigned K = a.it_K, K0 = a.it_K0;
 
   unsigned long long n_ev = 0, n_out = 0, n_in = 0, n_cmp = 0, n_bev = 0;
   bool changed = false, overflow = false;
@@ -261,44 +321,67 @@ __global__ void __launch_bounds__(128) region_kernel(const KArgs a) {
     uint32_t n = a.in.n[idx];
     unsigned long long dig = a.digest ? a.in.dig[idx] : 0ull;
 
-    // ---- incoming boundary histories of the previous iteration ----
+    // ---- incoming boundary histories (latest as of the previous iteration) ----
     // direction d's neighbour wrote them as its opposite edge (d ^ 1).
-    const int srow = r + 1;  // storage row of my region row
-    int nrow[4], ncol[4];
+    const int gr = a.row0 + r;
     uint32_t nid[4];
-    {
-      const int rn = a.world == 1 ? ((r - 1 + a.RYl) % a.RYl) + 1 : r;      // north neighbour row
-      const int rs = a.world == 1 ? ((r + 1) % a.RYl) + 1 : r + 2;          // south neighbour row
-      const int gr = a.row0 + r;
-      nrow[EDGE_N] = rn; ncol[EDGE_N] = c; nid[EDGE_N] = (uint32_t)(((gr - 1 + a.RYg) % a.RYg) * a.RX + c);
-      nrow[EDGE_S] = rs; ncol[EDGE_S] = c; nid[EDGE_S] = (uint32_t)(((gr + 1) % a.RYg) * a.RX + c);
-      const int cw = (c - 1 + a.RX) % a.RX, ce = (c + 1) % a.RX;
-      nrow[EDGE_W] = srow; ncol[EDGE_W] = cw; nid[EDGE_W] = (uint32_t)(gr * a.RX + cw);
-      nrow[EDGE_E] = srow; ncol[EDGE_E] = ce; nid[EDGE_E] = (uint32_t)(gr * a.RX + ce);
-    }
-    int hcnt[4], hidx[4], hpos[4];
+    nid[EDGE_N] = (uint32_t)(((gr - 1 + a.RYg) % a.RYg) * a.RX + c);
+    nid[EDGE_S] = (uint32_t)(((gr + 1) % a.RYg) * a.RX + c);
+    nid[EDGE_W] = (uint32_t)(gr * a.RX + (c - 1 + a.RX) % a.RX);
+    nid[EDGE_E] = (uint32_t)(gr * a.RX + (c + 1) % a.RX);
+    // cursor of each incoming history, packed: cnt | idx << 8 | pos << 16 |
+    // source << 24 (source 0/1 = slot, 2 = ghost row above, 3 = below);
+    // hoff = element offset of entry 0, entry q at hoff + q * RX
+    unsigned hm[4], hoff[4];
     double ht[4];
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
+      hm[d] = 0; hoff[d] = 0; ht[d] = dinf();
       const bool axis_off = (d < 2) ? wrapY : wrapX;
-      hcnt[d] = (a.first || axis_off) ? 0
-                : (int)a.prev.cnt[(long long)(d ^ 1) * a.cstride + (long long)nrow[d] * a.RX + ncol[d]];
-      hidx[d] = 0;
-      ht[d] = dinf();
-      hpos[d] = 0;
-      if (hcnt[d] > 0) {
-        const long long off = (long long)(d ^ 1) * a.tstride + ((long long)nrow[d] * a.K) * a.RX + ncol[d];
-        ht[d] = a.prev.t[off];
-        hpos[d] = a.prev.pos[off];
+      if (a.first || axis_off) continue;
+      const bool ghost = a.world > 1 && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
+      unsigned cnt = 0, src = 0;
+      if (ghost) {
+        const GhostView& g = d == EDGE_N ? a.gh_up : a.gh_down;
+        cnt = g.cnt[c];
+        src = d == EDGE_N ? 2u : 3u;
+        hoff[d] = (unsigned)c;
+      } else {
+        const int nr = d == EDGE_N ? (r - 1 + a.RYl) % a.RYl : d == EDGE_S ? (r + 1) % a.RYl : r;
+        const int nc = d == EDGE_W ? (c - 1 + a.RX) % a.RX : d == EDGE_E ? (c + 1) % a.RX : c;
+        const unsigned long long v = __ldcg(&a.sel[(long long)nr * a.RX + nc]);
+        const Latest L = latest_of(v, d ^ 1, K, K0);
+        if (L.valid) {
+          const EdgeView& E = L.slot ? a.ed[1] : a.ed[0];
+          cnt = E.cnt[(long long)(d ^ 1) * a.cstride + (long long)nr * a.RX + nc];
+          src = (unsigned)L.slot;
+          hoff[d] = (unsigned)((long long)(d ^ 1) * a.tstride + ((long long)nr * a.K) * a.RX + nc);
+        }
       }
-      n_in += hcnt[d];
+      unsigned pos = 0;
+      if (cnt > 0) {
+        const double* T = src == 0 ? a.ed[0].t : src == 1 ? a.ed[1].t : src == 2 ? a.gh_up.t : a.gh_down.t;
+        const uint8_t* P = src == 0 ? a.ed[0].pos : src == 1 ? a.ed[1].pos : src == 2 ? a.gh_up.pos : a.gh_down.pos;
+        ht[d] = T[hoff[d]];
+        pos = P[hoff[d]];
+      }
+      hm[d] = cnt | (pos << 16) | (src << 24);
+      n_in += cnt;
     }
-    // own previous histories (for the fused diff)
-    int oc[4], pc[4];
+
+    // ---- own latest histories (fused diff, statement (c)) ----
+    // packed per edge: new count | latest count << 8 | latest slot << 16 | diverged << 17
+    const unsigned long long vown = LOG ? 0ull : a.sel[idx];
+    unsigned om[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      oc[e] = 0;
-      pc[e] = (LOG || a.first) ? 0 : (int)a.prev.cnt[(long long)e * a.cstride + (long long)srow * a.RX + c];
+      const unsigned ps = (unsigned)((vown >> e) & 1ull);
+      unsigned pc = 0;
+      if (!LOG) {
+        const Latest L = latest_of(vown, e, K, K0);
+        if (L.valid) pc = (ps ? a.ed[1] : a.ed[0]).cnt[(long long)e * a.cstride + (long long)r * a.RX + c];
+      }
+      om[e] = (pc << 8) | (ps << 16);
     }
     const unsigned long long log_base = LOG ? a.log_off[idx] : 0ull;
 
@@ -317,7 +400,8 @@ __global__ void __launch_bounds__(128) region_kernel(const KArgs a) {
       uint32_t nb = 0xffffffffu;
 #pragma unroll
       for (int d = 0; d < 4; ++d) {
-        if (hidx[d] < hcnt[d] && (ht[d] < tb || (ht[d] == tb && nid[d] < nb))) {
+        const bool pend = ((hm[d] >> 8) & 0xFFu) < (hm[d] & 0xFFu);
+        if (pend && (ht[d] < tb || (ht[d] == tb && nid[d] < nb))) {
           dstar = d;
           tb = ht[d];
           nb = nid[d];
@@ -342,7 +426,8 @@ __global__ void __launch_bounds__(128) region_kernel(const KArgs a) {
           a.log_region[o] = gid;
           a.log_site[o] = (uint16_t)site;
         } else {
-          // own boundary history
+          // own boundary history; an edge history is
+          // written only once it diverges from its latest version
           bool bev = false;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -352,24 +437,38 @@ __global__ void __launch_bounds__(128) region_kernel(const KArgs a) {
                                         : (!wrapX && sc == BX - 1);
             if (on) {
               bev = true;
-              const int k = oc[e];
+              const unsigned k = om[e] & 0xFFu;
+              const unsigned pc = (om[e] >> 8) & 0xFFu;
+              const unsigned ps = (om[e] >> 16) & 1u;
+              bool dve = (om[e] >> 17) & 1u;
               const uint8_t p = (uint8_t)(e < 2 ? sc : sr);
-              if (k < a.K) {
-                const long long off = (long long)e * a.tstride + ((long long)srow * a.K + k) * a.RX + c;
-                a.cur.t[off] = tc;
-                a.cur.pos[off] = p;
-                if (k >= pc[e]) {
-                  changed = true;
-                } else {
+              if ((int)k < a.K) {
+                const long long base = (long long)e * a.tstride + ((long long)r * a.K) * a.RX + c;
+                const EdgeView& Pold = ps ? a.ed[1] : a.ed[0];
+                const EdgeView& Pnew = ps ? a.ed[0] : a.ed[1];
+                bool same = false;
+                if (!dve && k < pc) {
                   ++n_cmp;
-                  const double pt = a.prev.t[off];
-                  const uint8_t pp = a.prev.pos[off];
-                  if (__double_as_longlong(pt) != __double_as_longlong(tc) || pp != p) changed = true;
+                  same = __double_as_longlong(Pold.t[base + (long long)k * a.RX]) == __double_as_longlong(tc) &&
+                         Pold.pos[base + (long long)k * a.RX] == p;
+                }
+                if (!same) {
+                  if (!dve) {  // copy the agreeing prefix into the new slot
+                    for (unsigned q = 0; q < k; ++q) {
+                      Pnew.t[base + (long long)q * a.RX] = Pold.t[base + (long long)q * a.RX];
+                      Pnew.pos[base + (long long)q * a.RX] = Pold.pos[base + (long long)q * a.RX];
+                    }
+                    dve = true;
+                  }
+                  Pnew.t[base + (long long)k * a.RX] = tc;
+                  Pnew.pos[base + (long long)k * a.RX] = p;
+                  ++n_out;
                 }
               } else {
                 overflow = true;
               }
-              oc[e] = k + 1;
+              const unsigned kk = k < 255u ? k + 1 : 255u;
+              om[e] = kk | (pc << 8) | (ps << 16) | ((unsigned)dve << 17);
             }
           }
           n_bev += bev ? 1 : 0;
@@ -385,18 +484,23 @@ __global__ void __launch_bounds__(128) region_kernel(const KArgs a) {
 #pragma unroll
         for (int d = 0; d < 4; ++d) {
           if (d == dstar) {
-            const int p = hpos[d];
+            const int p = (int)((hm[d] >> 16) & 0xFFu);
             if (d == EDGE_N) gN ^= G::ONE << p;
             else if (d == EDGE_S) gS ^= G::ONE << ((BY - 1) * BX + p);
             else if (d == EDGE_W) gW ^= G::ONE << (p * BX);
             else gE ^= G::ONE << (p * BX + BX - 1);
-            const int nx = ++hidx[d];
-            if (nx < hcnt[d]) {
-              const long long off =
-                  (long long)(d ^ 1) * a.tstride + ((long long)nrow[d] * a.K + nx) * a.RX + ncol[d];
-              ht[d] = a.prev.t[off];
-              hpos[d] = a.prev.pos[off];
+            const unsigned nx = ((hm[d] >> 8) & 0xFFu) + 1;
+            const unsigned src = hm[d] >> 24;
+            unsigned pos = 0;
+            if (nx < (hm[d] & 0xFFu)) {
+              const double* T = src == 0 ? a.ed[0].t : src == 1 ? a.ed[1].t : src == 2 ? a.gh_up.t : a.gh_down.t;
+              const uint8_t* P =
+                  src == 0 ? a.ed[0].pos : src == 1 ? a.ed[1].pos : src == 2 ? a.gh_up.pos : a.gh_down.pos;
+              const unsigned long long off = (unsigned long long)hoff[d] + (unsigned long long)nx * a.RX;
+              ht[d] = T[off];
+              pos = P[off];
             }
+            hm[d] = (hm[d] & 0xFF0000FFu) | (nx << 8) | (pos << 16);
           }
         }
       }
@@ -413,11 +517,41 @@ __global__ void __launch_bounds__(128) region_kernel(const KArgs a) {
     }
 
     if (!LOG) {
+      unsigned chmask = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        if (oc[e] != pc[e]) changed = true;
-        a.cur.cnt[(long long)e * a.cstride + (long long)srow * a.RX + c] = (uint8_t)(oc[e] < a.K ? oc[e] : a.K);
-        n_out += oc[e];
+        const unsigned oc = om[e] & 0xFFu, pc = (om[e] >> 8) & 0xFFu, ps = (om[e] >> 16) & 1u;
+        bool dve = (om[e] >> 17) & 1u;
+        if ((int)oc > a.K) overflow = true;
+        const EdgeView& Pold = ps ? a.ed[1] : a.ed[0];
+        const EdgeView& Pnew = ps ? a.ed[0] : a.ed[1];
+        if (!dve && oc != pc) {
+          // new history is a strict prefix of the latest one: copy it over
+          const long long base = (long long)e * a.tstride + ((long long)r * a.K) * a.RX + c;
+          for (unsigned q = 0; q < oc && (int)q < a.K; ++q) {
+            Pnew.t[base + (long long)q * a.RX] = Pold.t[base + (long long)q * a.RX];
+            Pnew.pos[base + (long long)q * a.RX] = Pold.pos[base + (long long)q * a.RX];
+          }
+          dve = true;
+        }
+        if (dve) {
+          chmask |= 1u << e;
+          Pnew.cnt[(long long)e * a.cstride + (long long)r * a.RX + c] = (uint8_t)((int)oc < a.K ? oc : a.K);
+        }
+      }
+      if (chmask) {
+        changed = true;
+        a.sel[idx] = sel_after_change(vown, chmask, K, K0);
+        // neighbours across changed edges must be recomputed next iteration
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (!((chmask >> e) & 1u)) continue;
+          if (a.world > 1 && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
+          const int nr = e == EDGE_N ? (r - 1 + a.RYl) % a.RYl : e == EDGE_S ? (r + 1) % a.RYl : r;
+          const int nc = e == EDGE_W ? (c - 1 + a.RX) % a.RX : e == EDGE_E ? (c + 1) % a.RX : c;
+          const int nidx = nr * a.RX + nc;
+          if (atomicMax(&a.dirty[nidx], K + 1) < K + 1) a.wl_out[atomicAdd(a.wl_out_count, 1u)] = (uint32_t)nidx;
+        }
       }
       // tentative end-of-window state (committed by pointer swap at commit)
       ((ST*)a.out.spins)[idx] = (ST)spins;
@@ -458,6 +592,53 @@ __global__ void __launch_bounds__(128) region_kernel(const KArgs a) {
       }
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// K4 (world > 1): pack the latest north-edge histories of the strip's first
+// region row and south-edge histories of its last row into the send rows,
+// with the stamp of their last change (the neighbour marks its adjacent
+// regions dirty when the stamp equals the current iteration).
+// ---------------------------------------------------------------------------
+__global__ void pack_kernel(const KArgs a, GhostView send_up, GhostView send_down) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 2 * a.RX) return;
+  const bool up = i < a.RX;
+  const int c = up ? i : i - a.RX;
+  const int r = up ? 0 : a.RYl - 1;
+  const int e = up ? EDGE_N : EDGE_S;
+  const GhostView& g = up ? send_up : send_down;
+  const unsigned long long v = a.sel[(long long)r * a.RX + c];
+  // latest as of the end of this iteration
+  const Latest L = latest_of(v, e, a.it_K + 1, a.it_K0);
+  int cnt = 0;
+  if (L.valid) {
+    const EdgeView& E = a.ed[L.slot];
+    cnt = E.cnt[(long long)e * a.cstride + (long long)r * a.RX + c];
+    const long long base = (long long)e * a.tstride + ((long long)r * a.K) * a.RX + c;
+    for (int q = 0; q < cnt; ++q) {
+      g.t[(long long)q * a.RX + c] = E.t[base + (long long)q * a.RX];
+      g.pos[(long long)q * a.RX + c] = E.pos[base + (long long)q * a.RX];
+    }
+  }
+  g.cnt[c] = (uint8_t)cnt;
+  const unsigned Kl = (unsigned)(v >> 32);
+  const bool ch_now = Kl == a.it_K && ((v >> (4 + e)) & 1ull);
+  g.stamp[c] = ch_now ? a.it_K : 0u;
+}
+
+// after the exchange: regions next to a ghost row that changed in this
+// iteration are recomputed in the next one
+__global__ void mark_kernel(const KArgs a, GhostView up, GhostView down) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 2 * a.RX) return;
+  const bool isup = i < a.RX;
+  const int c = isup ? i : i - a.RX;
+  const GhostView& g = isup ? up : down;
+  if (g.stamp[c] != a.it_K) return;
+  const int r = isup ? 0 : a.RYl - 1;
+  const int nidx = r * a.RX + c;
+  if (atomicMax(&a.dirty[nidx], a.it_K + 1) < a.it_K + 1) a.wl_out[atomicAdd(a.wl_out_count, 1u)] = (uint32_t)nidx;
 }
 
 // ---------------------------------------------------------------------------

@@ -21,6 +21,7 @@
 namespace {
 
 using isr::EdgeView;
+using isr::GhostView;
 using isr::KArgs;
 using isr::StateView;
 
@@ -147,7 +148,7 @@ __global__ void scan_apply(const uint32_t* n1, const uint32_t* n0, int N, const 
 struct ising_sr_ctx {
   ising_sr_config cfg;
   const ShapeOps* ops = nullptr;
-  int RX = 0, RYg = 0, RYl = 0, row0 = 0, nreg = 0, rows_s = 0;
+  int RX = 0, RYg = 0, RYl = 0, row0 = 0, nreg = 0;
   int K = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -157,10 +158,18 @@ struct ising_sr_ctx {
   StateView st[2] = {};
   int comm = 0;  // index of the committed state
   EdgeView ed[2] = {};
-  int* d_flags = nullptr;               // [4]
+  unsigned long long* sel = nullptr;  // per region selector word
+  uint32_t* dirty = nullptr;          // per region: last stamp queued for
+  uint32_t* wl[2] = {nullptr, nullptr};
+  unsigned* d_wlc = nullptr;          // [2] worklist counts
+  GhostView gsend[2] = {}, grecv[2] = {};  // [0] = up, [1] = down  (world > 1)
+  void* gbuf = nullptr;
+  size_t gchunk[4] = {0, 0, 0, 0};
+  int* d_flags = nullptr;                 // [4]
   unsigned long long* d_stats = nullptr;  // [8]
-  int* h_flags = nullptr;               // pinned mirror [4]
+  int* h_flags = nullptr;                 // pinned mirror [4]
   unsigned long long* h_stats = nullptr;  // pinned mirror [8]
+  unsigned* h_wlc = nullptr;              // pinned mirror [2]
   // log
   double* log_t = nullptr;
   uint32_t* log_region = nullptr;
@@ -175,7 +184,10 @@ struct ising_sr_ctx {
   // window state
   long long w = 0;
   double t_c = 0.0, t_w = 0.0;
+  unsigned Kglob = 0;  // global iteration stamp (monotone across windows)
+  unsigned K0 = 1;     // stamp of the current window's first iteration
   int it = 0;
+  int n_work = 0;      // regions to recompute in the next iteration
   bool in_window = false, converged = false;
   int g = 0;
   // per-window accumulators
@@ -195,10 +207,10 @@ ising_sr_status fail_cuda(ising_sr_ctx* c, cudaError_t e, const char* where) {
   return ISING_SR_E_CUDA;
 }
 
-#define CK(ctx, expr)                                                     \
-  do {                                                                    \
-    cudaError_t _e = (expr);                                              \
-    if (_e != cudaSuccess) return fail_cuda((ctx), _e, #expr);            \
+#define CK(ctx, expr)                                          \
+  do {                                                         \
+    cudaError_t _e = (expr);                                   \
+    if (_e != cudaSuccess) return fail_cuda((ctx), _e, #expr); \
   } while (0)
 
 template <class T>
@@ -213,13 +225,23 @@ void free_edges(ising_sr_ctx* c) {
     cudaFree(e.pos);
     e = EdgeView{};
   }
+  cudaFree(c->gbuf);
+  c->gbuf = nullptr;
+  for (int i = 0; i < 2; ++i) {
+    c->gsend[i] = GhostView{};
+    c->grecv[i] = GhostView{};
+  }
 }
 
+// Boundary-history slots sized for K entries per region edge, plus (world > 1)
+// four ghost rows: send up/down and receive from up/down, each laid out as
+// cnt[RX] | stamp[RX] | t[K][RX] | pos[K][RX] (the exchange chunks).
 ising_sr_status alloc_edges(ising_sr_ctx* c, int K) {
   free_edges(c);
   c->K = K;
-  const size_t cn = (size_t)4 * c->rows_s * c->RX;
+  const size_t cn = (size_t)4 * c->RYl * c->RX;
   const size_t tn = cn * (size_t)K;
+  if (tn >= (1ull << 32)) return ISING_SR_E_CAPACITY;  // kernel offsets are 32-bit
   for (auto& e : c->ed) {
     if (dmalloc(&e.cnt, cn) != cudaSuccess || dmalloc(&e.t, tn) != cudaSuccess ||
         dmalloc(&e.pos, tn) != cudaSuccess) {
@@ -227,8 +249,32 @@ ising_sr_status alloc_edges(ising_sr_ctx* c, int K) {
       free_edges(c);
       return ISING_SR_E_OOM;
     }
-    // ghost rows must read as "no events" before the first exchange
-    CK(c, cudaMemsetAsync(e.cnt, 0, cn, c->stream));
+  }
+  if (c->cfg.world > 1) {
+    const size_t RX = (size_t)c->RX;
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    c->gchunk[0] = RX;
+    c->gchunk[1] = RX * 4;
+    c->gchunk[2] = RX * (size_t)K * 8;
+    c->gchunk[3] = RX * (size_t)K;
+    const size_t one = al(c->gchunk[0]) + al(c->gchunk[1]) + al(c->gchunk[2]) + al(c->gchunk[3]);
+    if (cudaMalloc(&c->gbuf, 4 * one) != cudaSuccess) {
+      cudaGetLastError();
+      free_edges(c);
+      return ISING_SR_E_OOM;
+    }
+    CK(c, cudaMemsetAsync(c->gbuf, 0, 4 * one, c->stream));
+    GhostView* views[4] = {&c->gsend[0], &c->gsend[1], &c->grecv[0], &c->grecv[1]};
+    for (int i = 0; i < 4; ++i) {
+      char* b = (char*)c->gbuf + i * one;
+      views[i]->cnt = (uint8_t*)b;
+      b += al(c->gchunk[0]);
+      views[i]->stamp = (uint32_t*)b;
+      b += al(c->gchunk[1]);
+      views[i]->t = (double*)b;
+      b += al(c->gchunk[2]);
+      views[i]->pos = (uint8_t*)b;
+    }
   }
   return ISING_SR_OK;
 }
@@ -248,59 +294,94 @@ ising_sr_status check(const ising_sr_ctx* c) {
   return c->sticky;
 }
 
-KArgs base_args(ising_sr_ctx* c, int it_parity_prev, int it_parity_cur, bool first) {
+KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   KArgs a;
   std::memset(&a, 0, sizeof a);
   a.in = c->st[c->comm];
   a.out = c->st[c->comm ^ 1];
-  a.prev = c->ed[it_parity_prev];
-  a.cur = c->ed[it_parity_cur];
+  a.ed[0] = c->ed[0];
+  a.ed[1] = c->ed[1];
+  a.sel = c->sel;
+  a.gh_up = c->grecv[0];
+  a.gh_down = c->grecv[1];
   a.RX = c->RX;
   a.RYl = c->RYl;
   a.RYg = c->RYg;
   a.row0 = c->row0;
   a.world = c->cfg.world;
   a.K = c->K;
-  a.cstride = (long long)c->rows_s * c->RX;
-  a.tstride = (long long)c->rows_s * c->K * c->RX;
+  a.cstride = (long long)c->RYl * c->RX;
+  a.tstride = (long long)c->RYl * c->K * c->RX;
+  a.it_K = K;
+  a.it_K0 = c->K0;
   a.first = first ? 1 : 0;
   a.digest = (c->cfg.flags & ISING_SR_FLAG_DIGEST) ? 1 : 0;
   a.t_w = c->t_w;
   a.seed = c->cfg.seed;
   for (int k = 0; k < 10; ++k) a.rate[k] = c->cfg.rate[k];
+  a.dirty = c->dirty;
   a.flags = c->d_flags;
   a.stats = c->d_stats;
   return a;
 }
 
-// algorithmic bytes of one iteration: state in + out per
-// recomputed region, 3 count bytes x 4 edges, 9 bytes per history entry
-// written, read by the neighbour, and compared.
+// algorithmic bytes of one iteration: per recomputed region
+// the committed state read + tentative state written, the selector words
+// (own + 4 neighbours) and 8 count bytes; 9 bytes per history entry written,
+// read as a break point, and compared.
 double iteration_bytes(const ising_sr_ctx* c, const unsigned long long* s) {
   const double S = (double)c->ops->spin_bytes + (double)c->ops->halo_bytes + 8 + 8 + 4 +
                    ((c->cfg.flags & ISING_SR_FLAG_DIGEST) ? 8 : 0);
   const double regions = (double)s[5];
-  return regions * (2.0 * S + 12.0) + 9.0 * ((double)s[1] + (double)s[2] + (double)s[3]);
+  return regions * (2.0 * S + 5 * 8.0 + 8.0) + 9.0 * ((double)s[1] + (double)s[2] + (double)s[3]);
 }
 
 ising_sr_status launch_iteration(ising_sr_ctx* c) {
   ++c->it;
-  const int cur = c->it & 1, prev = cur ^ 1;
+  const unsigned K = ++c->Kglob;
+  const bool first = c->it == 1;
+  const int nw = first ? c->nreg : c->n_work;
   CK(c, cudaMemsetAsync(c->d_flags, 0, 4 * sizeof(int), c->stream));
   CK(c, cudaMemsetAsync(c->d_stats, 0, 8 * sizeof(unsigned long long), c->stream));
-  KArgs a = base_args(c, prev, cur, c->it == 1);
+  CK(c, cudaMemsetAsync(c->d_wlc + ((K + 1) & 1), 0, sizeof(unsigned), c->stream));
+  KArgs a = base_args(c, K, first);
+  a.wl_in = first ? nullptr : c->wl[K & 1];
+  a.n_work = nw;
+  a.wl_out = c->wl[(K + 1) & 1];
+  a.wl_out_count = c->d_wlc + ((K + 1) & 1);
   CK(c, cudaEventRecord(c->kev0, c->stream));
-  c->ops->region(a, c->nreg, c->stream);
+  if (nw > 0) {
+    c->ops->region(a, nw, c->stream);
+    ++c->launches;
+    CK(c, cudaGetLastError());
+  }
+  CK(c, cudaEventRecord(c->kev1, c->stream));
+  if (c->cfg.world > 1) {
+    isr::pack_kernel<<<(2 * c->RX + 127) / 128, 128, 0, c->stream>>>(a, c->gsend[0], c->gsend[1]);
+    ++c->launches;
+    CK(c, cudaGetLastError());
+  }
+  return ISING_SR_OK;
+}
+
+ising_sr_status mark_ghosts(ising_sr_ctx* c) {
+  if (c->cfg.world <= 1) return ISING_SR_OK;
+  const unsigned K = c->Kglob;
+  KArgs a = base_args(c, K, c->it == 1);
+  a.wl_out = c->wl[(K + 1) & 1];
+  a.wl_out_count = c->d_wlc + ((K + 1) & 1);
+  isr::mark_kernel<<<(2 * c->RX + 127) / 128, 128, 0, c->stream>>>(a, c->grecv[0], c->grecv[1]);
   ++c->launches;
   CK(c, cudaGetLastError());
-  CK(c, cudaEventRecord(c->kev1, c->stream));
   return ISING_SR_OK;
 }
 
 ising_sr_status read_flags(ising_sr_ctx* c) {
+  const unsigned K = c->Kglob;
   CK(c, cudaMemcpyAsync(c->h_flags, c->d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaMemcpyAsync(c->h_stats, c->d_stats, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                         c->stream));
+  CK(c, cudaMemcpyAsync(c->h_wlc, c->d_wlc + ((K + 1) & 1), sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   float kms = 0.f;
   CK(c, cudaEventElapsedTime(&kms, c->kev0, c->kev1));
@@ -311,35 +392,24 @@ ising_sr_status read_flags(ising_sr_ctx* c) {
   c->stats.iterations_total++;
   c->stats.recomputations_total += (long long)c->h_stats[5];
   c->win_bytes += ib;
-  c->win_events = c->h_stats[0];
+  c->win_events += c->h_stats[0];  // events of the recomputed regions (see commit)
   c->win_f = std::max(c->win_f, (int)c->h_stats[4]);
+  c->n_work = (int)c->h_wlc[0];
   return ISING_SR_OK;
 }
 
 void fill_halo(ising_sr_ctx* c, ising_sr_halo* h) {
   std::memset(h, 0, sizeof *h);
-  const EdgeView& e = c->ed[c->it & 1];
-  const size_t RX = (size_t)c->RX, K = (size_t)c->K;
-  const size_t cst = (size_t)c->rows_s * RX, tst = cst * K;
-  const size_t rowN = 1, rowS = (size_t)c->RYl;  // storage rows of my first / last region row
-  const size_t gUp = 0, gDown = (size_t)c->RYl + 1;
-  h->nchunks = 3;
-  h->chunk_bytes[0] = RX;
-  h->chunk_bytes[1] = K * RX * sizeof(double);
-  h->chunk_bytes[2] = K * RX;
-  const size_t N = isr::EDGE_N, S = isr::EDGE_S;
-  h->send_up[0] = e.cnt + N * cst + rowN * RX;
-  h->send_up[1] = e.t + N * tst + rowN * K * RX;
-  h->send_up[2] = e.pos + N * tst + rowN * K * RX;
-  h->send_down[0] = e.cnt + S * cst + rowS * RX;
-  h->send_down[1] = e.t + S * tst + rowS * K * RX;
-  h->send_down[2] = e.pos + S * tst + rowS * K * RX;
-  h->recv_from_up[0] = e.cnt + S * cst + gUp * RX;
-  h->recv_from_up[1] = e.t + S * tst + gUp * K * RX;
-  h->recv_from_up[2] = e.pos + S * tst + gUp * K * RX;
-  h->recv_from_down[0] = e.cnt + N * cst + gDown * RX;
-  h->recv_from_down[1] = e.t + N * tst + gDown * K * RX;
-  h->recv_from_down[2] = e.pos + N * tst + gDown * K * RX;
+  h->nchunks = 4;
+  for (int k = 0; k < 4; ++k) h->chunk_bytes[k] = c->gchunk[k];
+  const GhostView* v[4] = {&c->gsend[0], &c->gsend[1], &c->grecv[0], &c->grecv[1]};
+  void** dst[4] = {h->send_up, h->send_down, h->recv_from_up, h->recv_from_down};
+  for (int i = 0; i < 4; ++i) {
+    dst[i][0] = v[i]->cnt;
+    dst[i][1] = v[i]->stamp;
+    dst[i][2] = v[i]->t;
+    dst[i][3] = v[i]->pos;
+  }
   h->flags = c->d_flags;
   h->stream = (void*)c->stream;
 }
@@ -359,6 +429,8 @@ void start_window(ising_sr_ctx* c) {
   const double next = (double)(c->w + 1) * c->cfg.W;
   c->t_w = next < c->cfg.t_end ? next : c->cfg.t_end;
   c->it = 0;
+  c->K0 = c->Kglob + 1;  // every selector stamp < K0 now reads as "empty"
+  c->n_work = c->nreg;
   c->in_window = true;
   c->converged = false;
   c->g = 0;
@@ -402,10 +474,16 @@ void ising_sr_destroy(ising_sr_ctx* c) {
     cudaFree(s.dig);
   }
   free_edges(c);
+  cudaFree(c->sel);
+  cudaFree(c->dirty);
+  cudaFree(c->wl[0]);
+  cudaFree(c->wl[1]);
+  cudaFree(c->d_wlc);
   cudaFree(c->d_flags);
   cudaFree(c->d_stats);
   cudaFreeHost(c->h_flags);
   cudaFreeHost(c->h_stats);
+  cudaFreeHost(c->h_wlc);
   cudaFree(c->log_t);
   cudaFree(c->log_region);
   cudaFree(c->log_site);
@@ -430,13 +508,11 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
     if (!(r >= 0.0) || std::isinf(r)) return ISING_SR_E_INVALID_ARG;
   const int world = cfg->world < 1 ? 1 : cfg->world;
   if (cfg->rank < 0 || cfg->rank >= world) return ISING_SR_E_INVALID_ARG;
-  if (world > 1 && !cfg->exchange) return ISING_SR_E_INVALID_ARG;
   const ShapeOps* ops = find_ops(cfg->bx, cfg->by);
   if (!ops) return ISING_SR_E_INVALID_ARG;
   const int RX = cfg->Lx / cfg->bx, RY = cfg->Ly / cfg->by;
   if (RY % world) return ISING_SR_E_PARTITION;
-  if ((long long)RX * RY > 0xffffffffLL) return ISING_SR_E_INVALID_ARG;
-  if (world > 1 && RY / world < 1) return ISING_SR_E_PARTITION;
+  if ((long long)RX * RY > 0x7fffffffLL) return ISING_SR_E_INVALID_ARG;
 
   ising_sr_ctx* c = new (std::nothrow) ising_sr_ctx();
   if (!c) return ISING_SR_E_OOM;
@@ -449,7 +525,6 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   c->RYl = RY / world;
   c->row0 = cfg->rank * c->RYl;
   c->nreg = c->RX * c->RYl;
-  c->rows_s = c->RYl + 2;
   std::memset(&c->stats, 0, sizeof c->stats);
 
   auto bail = [&](ising_sr_status s) {
@@ -465,17 +540,24 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   }
   const size_t n = (size_t)c->nreg;
   for (auto& s : c->st) {
-    if (cudaMalloc(&s.spins, n * ops->spin_bytes) != cudaSuccess || cudaMalloc(&s.halo, n * ops->halo_bytes) != cudaSuccess ||
-        dmalloc(&s.ts, n) != cudaSuccess || dmalloc(&s.R, n) != cudaSuccess || dmalloc(&s.n, n) != cudaSuccess ||
-        dmalloc(&s.dig, n) != cudaSuccess)
+    if (cudaMalloc(&s.spins, n * ops->spin_bytes) != cudaSuccess ||
+        cudaMalloc(&s.halo, n * ops->halo_bytes) != cudaSuccess || dmalloc(&s.ts, n) != cudaSuccess ||
+        dmalloc(&s.R, n) != cudaSuccess || dmalloc(&s.n, n) != cudaSuccess || dmalloc(&s.dig, n) != cudaSuccess)
       return bail(ISING_SR_E_OOM);
   }
-  if (dmalloc(&c->d_flags, 4) != cudaSuccess || dmalloc(&c->d_stats, 8) != cudaSuccess ||
+  if (dmalloc(&c->sel, n) != cudaSuccess || dmalloc(&c->dirty, n) != cudaSuccess ||
+      dmalloc(&c->wl[0], n) != cudaSuccess || dmalloc(&c->wl[1], n) != cudaSuccess ||
+      dmalloc(&c->d_wlc, 2) != cudaSuccess || dmalloc(&c->d_flags, 4) != cudaSuccess ||
+      dmalloc(&c->d_stats, 8) != cudaSuccess ||
       cudaMallocHost((void**)&c->h_flags, 4 * sizeof(int)) != cudaSuccess ||
       cudaMallocHost((void**)&c->h_stats, 8 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMallocHost((void**)&c->h_wlc, 2 * sizeof(unsigned)) != cudaSuccess ||
       dmalloc(&c->d_off, n) != cudaSuccess || dmalloc(&c->d_bsum, (n + kThreads - 1) / kThreads) != cudaSuccess ||
       dmalloc(&c->d_total, 1) != cudaSuccess)
     return bail(ISING_SR_E_OOM);
+  if (cudaMemsetAsync(c->sel, 0, n * 8, c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->dirty, 0, n * 4, c->stream) != cudaSuccess)
+    return bail(ISING_SR_E_CUDA);
   if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
       cudaEventCreate(&c->kev0) != cudaSuccess || cudaEventCreate(&c->kev1) != cudaSuccess)
     return bail(ISING_SR_E_CUDA);
@@ -491,7 +573,9 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   const int y_first = c->row0 * by - 1;
   for (int q = 0; q < rows; ++q) {
     const int y = ((y_first + q) % Ly + Ly) % Ly;
-    for (int x = 0; x < Lx; ++x) buf[(size_t)q * Lx + x] = spins[(size_t)y * Lx + x] ? 1 : 0;
+    const uint8_t* src = spins + (size_t)y * Lx;
+    uint8_t* dst = buf.data() + (size_t)q * Lx;
+    for (int x = 0; x < Lx; ++x) dst[x] = src[x] ? 1 : 0;
   }
   uint8_t* dbuf = nullptr;
   if (cudaMalloc(&dbuf, buf.size()) != cudaSuccess) return bail(ISING_SR_E_OOM);
@@ -534,8 +618,20 @@ ising_sr_status ising_sr_iterate(ising_sr_ctx* c, int32_t flags_out[2]) {
 ising_sr_status ising_sr_halo_get(ising_sr_ctx* c, ising_sr_halo* out) {
   ising_sr_status s = check(c);
   if (s) return s;
-  if (!out || !c->in_window || c->it < 1) return ISING_SR_E_STATE;
+  if (!out || !c->in_window || c->it < 1 || c->cfg.world < 2) return ISING_SR_E_STATE;
   fill_halo(c, out);
+  return ISING_SR_OK;
+}
+
+ising_sr_status ising_sr_exchange_done(ising_sr_ctx* c) {
+  ising_sr_status s = check(c);
+  if (s) return s;
+  if (!c->in_window || c->it < 1) return ISING_SR_E_STATE;
+  if ((s = mark_ghosts(c))) return s;
+  const unsigned K = c->Kglob;
+  CK(c, cudaMemcpyAsync(c->h_wlc, c->d_wlc + ((K + 1) & 1), sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  c->n_work = (int)c->h_wlc[0];
   return ISING_SR_OK;
 }
 
@@ -561,9 +657,11 @@ ising_sr_status ising_sr_run_window(ising_sr_ctx* c, int32_t* g_out) {
   for (;;) {
     if ((s = launch_iteration(c))) return s;
     if (c->cfg.world > 1) {
+      if (!c->cfg.exchange) return ISING_SR_E_INVALID_ARG;
       ising_sr_halo h;
       fill_halo(c, &h);
       if (c->cfg.exchange(c->cfg.exchange_user, &h) != 0) return ISING_SR_E_NCCL;
+      if ((s = mark_ghosts(c))) return s;
     }
     if ((s = read_flags(c))) return s;
     if (c->h_flags[1]) {  // history capacity overflow: grow and restart the window
@@ -589,19 +687,24 @@ ising_sr_status ising_sr_commit(ising_sr_ctx* c, int64_t* events_out) {
   ising_sr_status s = check(c);
   if (s) return s;
   if (!c->in_window || !c->converged) return ISING_SR_E_STATE;
-  const int fin = c->g & 1;
-  if (c->cfg.flags & ISING_SR_FLAG_LOG_EVENTS) {
-    const StateView& s0 = c->st[c->comm];
-    const StateView& s1 = c->st[c->comm ^ 1];
-    const int nb = (c->nreg + kThreads - 1) / kThreads;
-    scan_block_sums<<<nb, kThreads, 0, c->stream>>>(s1.n, s0.n, c->nreg, c->d_bsum);
-    scan_top<<<1, 1024, 0, c->stream>>>(c->d_bsum, nb, c->d_total);
+  const StateView& s0 = c->st[c->comm];
+  const StateView& s1 = c->st[c->comm ^ 1];
+  const int nb = (c->nreg + kThreads - 1) / kThreads;
+  // e_i = n_next - n_comm: scan for the log offsets and the window's total
+  scan_block_sums<<<nb, kThreads, 0, c->stream>>>(s1.n, s0.n, c->nreg, c->d_bsum);
+  scan_top<<<1, 1024, 0, c->stream>>>(c->d_bsum, nb, c->d_total);
+  c->launches += 2;
+  const bool log = (c->cfg.flags & ISING_SR_FLAG_LOG_EVENTS) != 0;
+  if (log) {
     scan_apply<<<nb, kThreads, 0, c->stream>>>(s1.n, s0.n, c->nreg, c->d_bsum, c->d_off);
-    c->launches += 3;
-    CK(c, cudaGetLastError());
-    unsigned long long total = 0;
-    CK(c, cudaMemcpyAsync(&total, c->d_total, sizeof total, cudaMemcpyDeviceToHost, c->stream));
-    CK(c, cudaStreamSynchronize(c->stream));
+    c->launches++;
+  }
+  CK(c, cudaGetLastError());
+  unsigned long long total = 0;
+  CK(c, cudaMemcpyAsync(&total, c->d_total, sizeof total, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  c->win_events = total;
+  if (log) {
     if ((long long)total > c->log_cap) {
       cudaFree(c->log_t);
       cudaFree(c->log_region);
@@ -618,7 +721,9 @@ ising_sr_status ising_sr_commit(ising_sr_ctx* c, int64_t* events_out) {
       }
       c->log_cap = cap;
     }
-    KArgs a = base_args(c, fin, fin, false);
+    // replay every region against the final (latest) histories
+    KArgs a = base_args(c, c->Kglob + 1, false);
+    a.n_work = c->nreg;
     a.log_t = c->log_t;
     a.log_region = c->log_region;
     a.log_site = c->log_site;
@@ -698,7 +803,8 @@ ising_sr_status ising_sr_get_events(ising_sr_ctx* c, double* t, uint32_t* region
   const long long m = std::min<long long>(cap, c->log_n);
   if (m > 0) {
     if (t) CK(c, cudaMemcpyAsync(t, c->log_t, m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    if (region) CK(c, cudaMemcpyAsync(region, c->log_region, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    if (region)
+      CK(c, cudaMemcpyAsync(region, c->log_region, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
     if (site) CK(c, cudaMemcpyAsync(site, c->log_site, m * sizeof(uint16_t), cudaMemcpyDeviceToHost, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
   }

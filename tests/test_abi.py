@@ -63,7 +63,6 @@ def _cfg(**kw):
     (dict(W=0.0), -1), (dict(W=-1.0), -1),
     (dict(rates=[-1.0] + [1.0] * 9), -1),
     (dict(bx=3, by=5, Lx=15, Ly=15), -1),        # unsupported region shape
-    (dict(world=2, rank=0), -1),                  # world > 1 needs an exchange callback
     (dict(rank=3, world=2), -1),
 ])
 def test_init_validation_errors(lib, kw, status):
