@@ -59,11 +59,11 @@ struct StateView {
   unsigned long long* dig;
 };
 
-// Boundary histories of one slot: cnt[4][RYl][RX], t/pos[4][RYl][K][RX].
-// Every region edge has two slots; which one holds its latest history is
-// recorded in the region's selector word (see latest_of).
+// Boundary histories of one slot: t/pos[4][RYl][K][RX] (entry q of edge e of
+// region (r, c) at ((e * RYl + r) * K + q) * RX + c).  Every region edge has
+// two slots; which one holds its latest history, and how many entries it
+// has, is recorded in the region's selector words (see latest_word).
 struct EdgeView {
-  uint8_t* cnt;
   double* t;
   uint8_t* pos;
 };
@@ -80,11 +80,10 @@ struct GhostView {
 struct KArgs {
   StateView in, out;
   EdgeView ed[2];
-  unsigned long long* sel;      // per region selector word
+  unsigned long long* sel;      // per region: 2 selector words (parity K & 1)
   GhostView gh_up, gh_down;     // world > 1: rows above / below the strip
   int RX, RYl, RYg, row0, world;
   int K;
-  long long cstride;  // elements per edge in cnt  (RYl * RX)
   long long tstride;  // elements per edge in t/pos (RYl * K * RX)
   unsigned it_K;      // global iteration stamp of this launch (>= 1)
   unsigned it_K0;     // stamp of the window's first iteration
@@ -95,6 +94,7 @@ struct KArgs {
   double rate[10];
   const uint32_t* wl_in;   // regions to recompute (nullptr: all regions)
   int n_work;              // number of regions to recompute
+  int tile;                // work items per block (lane-persistent scheduling)
   uint32_t* wl_out;        // worklist of the next iteration
   unsigned* wl_out_count;
   uint32_t* dirty;         // per region: last stamp it was queued for
@@ -107,36 +107,36 @@ struct KArgs {
   const unsigned long long* log_off;
 };
 
-// Selector word of a region (64 bits, written only by its own thread, read
-// racily by neighbours -- a 64-bit aligned store/load is single-copy atomic
-// and both the old and the new value decode to the same answer):
-//   bits 0-3  slot of the latest history of edge e
-//   bits 4-7  edges changed at K_last
-//   bits 8-11 edges holding a history written in this window (as of K_last)
-//   bits 12-15 the same before the K_last change
-//   bits 32-63 K_last, global iteration of the last change
-// latest_of(): the edge's latest history as of the end of iteration K-1.
-struct Latest {
-  int slot;
-  bool valid;  // false: canonical empty history
-};
+// Selector words of a region: two 64-bit words.  When its histories change
+// in iteration K the region's thread overwrites the OLDER of its two words
+// with stamp K; readers take the word with the largest stamp below K, which
+// therefore is never the one being written (a 64-bit aligned store is
+// single-copy atomic, so the word being written reads either as its old,
+// older-stamped value or with stamp K, and is ignored either way).  Layout:
+//   bits 0-3   slot holding the history of edge e
+//   bits 4-31  4 x 7-bit entry counts (edge e at bit 4 + 7e)
+//   bits 32-63 stamp: global iteration of the change
+// A stamp below K0 (before this window) means "canonical empty history".
+constexpr int CNT_BITS = 7;
+constexpr int CNT_MAX = (1 << CNT_BITS) - 1;
 
-__device__ __forceinline__ Latest latest_of(unsigned long long v, int e, unsigned K, unsigned K0) {
-  const unsigned Kl = (unsigned)(v >> 32);
-  const unsigned slots = (unsigned)v & 0xF, ch = ((unsigned)v >> 4) & 0xF;
-  const unsigned ne = ((unsigned)v >> 8) & 0xF, nep = ((unsigned)v >> 12) & 0xF;
-  if (Kl < K0) return {0, false};
-  if (Kl < K) return {(int)((slots >> e) & 1u), ((ne >> e) & 1u) != 0};
-  return {(int)(((slots ^ ch) >> e) & 1u), ((nep >> e) & 1u) != 0};  // changed concurrently in K
+// index (0/1) of the word with the largest stamp below K
+__device__ __forceinline__ int latest_index(ulonglong2 w, unsigned K) {
+  const unsigned s0 = (unsigned)(w.x >> 32), s1 = (unsigned)(w.y >> 32);
+  const bool v0 = s0 < K, v1 = s1 < K;
+  return (v0 && (!v1 || s0 >= s1)) ? 0 : 1;
 }
 
-__device__ __forceinline__ unsigned long long sel_after_change(unsigned long long v, unsigned chmask, unsigned K,
-                                                               unsigned K0) {
-  const unsigned Kl = (unsigned)(v >> 32);
-  const unsigned slots = (unsigned)v & 0xF;
-  const unsigned ne_old = Kl >= K0 ? (((unsigned)v >> 8) & 0xF) : 0u;
-  const unsigned lo = (slots ^ chmask) | (chmask << 4) | ((ne_old | chmask) << 8) | (ne_old << 12);
-  return ((unsigned long long)K << 32) | lo;
+__device__ __forceinline__ unsigned long long latest_word(ulonglong2 w, unsigned K) {
+  const int i = latest_index(w, K);
+  const unsigned long long v = i ? w.y : w.x;
+  return (unsigned)(v >> 32) < K ? v : 0ull;
+}
+
+__device__ __forceinline__ bool word_valid(unsigned long long v, unsigned K0) { return (unsigned)(v >> 32) >= K0; }
+__device__ __forceinline__ int word_slot(unsigned long long v, int e) { return (int)((v >> e) & 1ull); }
+__device__ __forceinline__ unsigned word_count(unsigned long long v, int e) {
+  return (unsigned)((v >> (4 + CNT_BITS * e)) & CNT_MAX);
 }
 
 // bit-sliced per-site count of up neighbours: m[u] = sites with exactly u.
@@ -291,276 +291,351 @@ __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000
 // whose inputs did not change would regenerate exactly its previous history
 // (the same presimulated random list), so skipping it does not
 // change the iteration count g or any result.
+//
+// Lane-persistent scheduling: each block owns a tile of `tile` consecutive
+// work items; every lane pulls its next region from the block's shared
+// queue the moment its current region reaches the window end, so a warp no
+// longer idles while its slowest region finishes (region histories have
+// Poisson-distributed lengths).
 // ---------------------------------------------------------------------------
+template <class G>
+struct Lane {
+  using M = typename G::M;
+  // region
+  int idx;
+  uint32_t gid;
+  M spins, gN, gS, gW, gE;
+  double ts, R, V, lam, tc;
+  uint32_t n;
+  unsigned long long dig;
+  // incoming history cursors: cnt | idx << 8 | pos << 16 | source << 24
+  unsigned hm[4], hoff[4];
+  double ht[4];
+  // own edges: new count | latest count << 8 | latest slot << 16 | diverged << 17
+  unsigned om[4];
+  unsigned long long vown;
+  int whalf;      // selector word to overwrite on change
+  unsigned n_ev;  // events of this region (log offset)
+  unsigned bev;   // own boundary events of this region
+};
+
+template <class G, bool LOG>
+__device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx) {
+  using M = typename G::M;
+  const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
+  const unsigned K = a.it_K, K0 = a.it_K0;
+  const int r = idx / a.RX, c = idx - r * a.RX;
+  L.idx = idx;
+  L.gid = (uint32_t)((a.row0 + r) * a.RX + c);
+  L.spins = (M)((const typename G::ST*)a.in.spins)[idx];
+  expand_halo<G>((unsigned long long)((const typename G::HT*)a.in.halo)[idx], L.gN, L.gS, L.gW, L.gE);
+  L.ts = a.in.ts[idx];
+  L.R = a.in.R[idx];
+  L.n = a.in.n[idx];
+  L.dig = a.digest ? a.in.dig[idx] : 0ull;
+  L.n_ev = 0;
+  L.bev = 0;
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    L.hm[d] = 0;
+    L.hoff[d] = 0;
+    L.ht[d] = dinf();
+    const bool axis_off = (d < 2) ? wrapY : wrapX;
+    if (a.first || axis_off) continue;
+    const bool ghost = a.world > 1 && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
+    unsigned cnt = 0, src = 0;
+    if (ghost) {
+      const GhostView& g = d == EDGE_N ? a.gh_up : a.gh_down;
+      cnt = g.cnt[c];
+      src = d == EDGE_N ? 2u : 3u;
+      L.hoff[d] = (unsigned)c;
+    } else {
+      const int nr = d == EDGE_N ? (r - 1 + a.RYl) % a.RYl : d == EDGE_S ? (r + 1) % a.RYl : r;
+      const int nc = d == EDGE_W ? (c - 1 + a.RX) % a.RX : d == EDGE_E ? (c + 1) % a.RX : c;
+      const ulonglong2 wp = __ldcg(reinterpret_cast<const ulonglong2*>(a.sel) + ((long long)nr * a.RX + nc));
+      const unsigned long long v = latest_word(wp, K);
+      if (word_valid(v, K0)) {
+        cnt = word_count(v, d ^ 1);
+        src = (unsigned)word_slot(v, d ^ 1);
+        L.hoff[d] = (unsigned)((long long)(d ^ 1) * a.tstride + ((long long)nr * a.K) * a.RX + nc);
+      }
+    }
+    unsigned pos = 0;
+    if (cnt > 0) {
+      const double* T = src == 0 ? a.ed[0].t : src == 1 ? a.ed[1].t : src == 2 ? a.gh_up.t : a.gh_down.t;
+      const uint8_t* P = src == 0 ? a.ed[0].pos : src == 1 ? a.ed[1].pos : src == 2 ? a.gh_up.pos : a.gh_down.pos;
+      L.ht[d] = T[L.hoff[d]];
+      pos = P[L.hoff[d]];
+    }
+    L.hm[d] = cnt | (pos << 16) | (src << 24);
+  }
+  L.vown = 0ull;
+  L.whalf = 0;
+  if (!LOG) {
+    const ulonglong2 wp = reinterpret_cast<const ulonglong2*>(a.sel)[idx];
+    const int li = latest_index(wp, K);
+    const unsigned long long v = li ? wp.y : wp.x;
+    L.vown = word_valid(v, K0) ? v : (v & 0xFull);  // outside the window: slots only, counts 0
+    L.whalf = li ^ 1;  // overwrite the older word
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const unsigned ps = (unsigned)word_slot(L.vown, e);
+    const unsigned pc = word_count(L.vown, e);
+    L.om[e] = (pc << 8) | (ps << 16);
+  }
+  // pair n: U already spent into R (carried), V selects the next atom
+  double U;
+  draw_pair(a.seed, L.gid, L.n, U, L.V);
+  Classes<G> C;
+  C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
+  L.lam = fold_lambda<G>(C, a.rate);
+  L.tc = cand_time(L.ts, L.R, L.lam);
+}
+
+// One step of the region's history: the earliest of its own candidate event
+// and the pending break points.  Returns false when the region has reached
+// the window end.
+template <class G, bool LOG>
+__device__ __forceinline__ bool lane_step(const KArgs& a, Lane<G>& L, unsigned& n_out, unsigned& n_cmp,
+                                          bool& overflow) {
+  constexpr int BX = G::BX, BY = G::BY;
+  const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
+  // neighbour ids in (time, id) order (R10)
+  const int c = (int)(L.gid % (uint32_t)a.RX);
+  const int gr = (int)(L.gid / (uint32_t)a.RX);
+  int dstar = -1;
+  double tb = dinf();
+  uint32_t nb = 0xffffffffu;
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    const bool pend = ((L.hm[d] >> 8) & 0xFFu) < (L.hm[d] & 0xFFu);
+    if (pend) {
+      const uint32_t nid = d == EDGE_N ? (uint32_t)(((gr - 1 + a.RYg) % a.RYg) * a.RX + c)
+                         : d == EDGE_S ? (uint32_t)(((gr + 1) % a.RYg) * a.RX + c)
+                         : d == EDGE_W ? (uint32_t)(gr * a.RX + (c - 1 + a.RX) % a.RX)
+                                       : (uint32_t)(gr * a.RX + (c + 1) % a.RX);
+      if (L.ht[d] < tb || (L.ht[d] == tb && nid < nb)) {
+        dstar = d;
+        tb = L.ht[d];
+        nb = nid;
+      }
+    }
+  }
+  const bool bp = dstar >= 0 && (tb < L.tc || (tb == L.tc && nb < L.gid));
+  const bool ev = !bp && L.tc < a.t_w;
+  if (!bp && !ev) return false;
+  if (ev) {
+    // ---- own event at tc ----
+    int site;
+    {
+      Classes<G> C;
+      C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
+      site = select_site<G>(C, a.rate, L.V, L.lam);
+    }
+    L.spins ^= G::ONE << site;
+    const int sr = site / BX, sc = site - sr * BX;
+    if (a.digest)
+      L.dig = mix64(mix64(L.dig ^ (unsigned long long)__double_as_longlong(L.tc)) ^ (unsigned long long)site);
+    if (LOG) {
+      const unsigned long long o = a.log_off[L.idx] + L.n_ev;
+      a.log_t[o] = L.tc;
+      a.log_region[o] = L.gid;
+      a.log_site[o] = (uint16_t)site;
+    } else {
+      // own boundary history; an edge history is
+      // written only once it diverges from its latest version
+      const int r = L.idx / a.RX;
+      bool on_edge = false;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool on = e == EDGE_N ? (!wrapY && sr == 0)
+                      : e == EDGE_S ? (!wrapY && sr == BY - 1)
+                      : e == EDGE_W ? (!wrapX && sc == 0)
+                                    : (!wrapX && sc == BX - 1);
+        if (!on) continue;
+        on_edge = true;
+        const unsigned k = L.om[e] & 0xFFu;
+        const unsigned pc = (L.om[e] >> 8) & 0xFFu;
+        const unsigned ps = (L.om[e] >> 16) & 1u;
+        bool dve = (L.om[e] >> 17) & 1u;
+        const uint8_t p = (uint8_t)(e < 2 ? sc : sr);
+        if ((int)k < a.K) {
+          const unsigned base = (unsigned)((long long)e * a.tstride + ((long long)r * a.K) * a.RX + c);
+          const EdgeView& Pold = ps ? a.ed[1] : a.ed[0];
+          const EdgeView& Pnew = ps ? a.ed[0] : a.ed[1];
+          bool same = false;
+          if (!dve && k < pc) {
+            ++n_cmp;
+            const unsigned o = base + k * (unsigned)a.RX;
+            same = __double_as_longlong(Pold.t[o]) == __double_as_longlong(L.tc) && Pold.pos[o] == p;
+          }
+          if (!same) {
+            if (!dve) {  // copy the agreeing prefix into the new slot
+              for (unsigned q = 0; q < k; ++q) {
+                const unsigned o = base + q * (unsigned)a.RX;
+                Pnew.t[o] = Pold.t[o];
+                Pnew.pos[o] = Pold.pos[o];
+              }
+              dve = true;
+            }
+            const unsigned o = base + k * (unsigned)a.RX;
+            Pnew.t[o] = L.tc;
+            Pnew.pos[o] = p;
+            ++n_out;
+          }
+        } else {
+          overflow = true;
+        }
+        const unsigned kk = k < 255u ? k + 1 : 255u;
+        L.om[e] = kk | (pc << 8) | (ps << 16) | ((unsigned)dve << 17);
+      }
+      L.bev += on_edge ? 1u : 0u;
+    }
+    ++L.n_ev;
+    L.ts = L.tc;
+  } else {
+    // ---- break point at tb (eqs. lambdataua..newtau) ----
+    const double Rn = __dsub_rn(L.R, __dmul_rn(L.lam, __dsub_rn(tb, L.ts)));
+    L.R = Rn < 0.0 ? 0.0 : Rn;
+    L.ts = tb;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      if (d != dstar) continue;
+      const int p = (int)((L.hm[d] >> 16) & 0xFFu);
+      if (d == EDGE_N) L.gN ^= G::ONE << p;
+      else if (d == EDGE_S) L.gS ^= G::ONE << ((BY - 1) * BX + p);
+      else if (d == EDGE_W) L.gW ^= G::ONE << (p * BX);
+      else L.gE ^= G::ONE << (p * BX + BX - 1);
+      const unsigned nx = ((L.hm[d] >> 8) & 0xFFu) + 1;
+      const unsigned src = L.hm[d] >> 24;
+      unsigned pos = 0;
+      if (nx < (L.hm[d] & 0xFFu)) {
+        const double* T = src == 0 ? a.ed[0].t : src == 1 ? a.ed[1].t : src == 2 ? a.gh_up.t : a.gh_down.t;
+        const uint8_t* P = src == 0 ? a.ed[0].pos : src == 1 ? a.ed[1].pos : src == 2 ? a.gh_up.pos : a.gh_down.pos;
+        const unsigned off = L.hoff[d] + nx * (unsigned)a.RX;
+        L.ht[d] = T[off];
+        pos = P[off];
+      }
+      L.hm[d] = (L.hm[d] & 0xFF0000FFu) | (nx << 8) | (pos << 16);
+    }
+  }
+  {
+    Classes<G> C;
+    C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
+    L.lam = fold_lambda<G>(C, a.rate);
+  }
+  if (ev) {
+    // next pair of the list; the unused remainder carries over
+    ++L.n;
+    double U;
+    draw_pair(a.seed, L.gid, L.n, U, L.V);
+    L.R = expvar(U);
+  }
+  L.tc = cand_time(L.ts, L.R, L.lam);
+  return true;
+}
+
+template <class G>
+__device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& changed, bool& overflow) {
+  const int idx = L.idx;
+  const int r = idx / a.RX, c = idx - r * a.RX;
+  const unsigned K = a.it_K;
+  unsigned chmask = 0;
+  unsigned long long word = L.vown & 0xFFFFFFFFull;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const unsigned oc = L.om[e] & 0xFFu, pc = (L.om[e] >> 8) & 0xFFu, ps = (L.om[e] >> 16) & 1u;
+    bool dve = (L.om[e] >> 17) & 1u;
+    if ((int)oc > a.K) overflow = true;
+    const EdgeView& Pold = ps ? a.ed[1] : a.ed[0];
+    const EdgeView& Pnew = ps ? a.ed[0] : a.ed[1];
+    if (!dve && oc != pc) {
+      // new history is a strict prefix of the latest one: copy it over
+      const unsigned base = (unsigned)((long long)e * a.tstride + ((long long)r * a.K) * a.RX + c);
+      for (unsigned q = 0; q < oc && (int)q < a.K; ++q) {
+        const unsigned o = base + q * (unsigned)a.RX;
+        Pnew.t[o] = Pold.t[o];
+        Pnew.pos[o] = Pold.pos[o];
+      }
+      dve = true;
+    }
+    if (dve) {
+      chmask |= 1u << e;
+      const unsigned nc = (int)oc < a.K ? oc : (unsigned)a.K;
+      word = (word & ~((unsigned long long)CNT_MAX << (4 + CNT_BITS * e))) |
+             ((unsigned long long)nc << (4 + CNT_BITS * e));
+    }
+  }
+  if (chmask) {
+    changed = true;
+    // new word: changed edges move to the other slot with their new counts
+    word = ((unsigned long long)K << 32) | ((word & 0xFFFFFFF0ull) | ((word ^ chmask) & 0xFull));
+    a.sel[2 * (long long)idx + L.whalf] = word;
+    // neighbours across changed edges must be recomputed next iteration
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (!((chmask >> e) & 1u)) continue;
+      if (a.world > 1 && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
+      const int nr = e == EDGE_N ? (r - 1 + a.RYl) % a.RYl : e == EDGE_S ? (r + 1) % a.RYl : r;
+      const int nc = e == EDGE_W ? (c - 1 + a.RX) % a.RX : e == EDGE_E ? (c + 1) % a.RX : c;
+      a.dirty[nr * a.RX + nc] = K + 1;  // same value from every writer: a plain store suffices
+    }
+  }
+  // tentative end-of-window state (committed by pointer swap at commit)
+  ((typename G::ST*)a.out.spins)[idx] = (typename G::ST)L.spins;
+  ((typename G::HT*)a.out.halo)[idx] = (typename G::HT)compress_halo<G>(L.gN, L.gS, L.gW, L.gE);
+  a.out.ts[idx] = L.ts;
+  a.out.R[idx] = L.R;
+  a.out.n[idx] = L.n;
+  if (a.digest) a.out.dig[idx] = L.dig;
+}
+
 template <int BX, int BY, bool LOG>
 __global__ void __launch_bounds__(128) region_kernel(const KArgs a) {
   using G = Geo<BX, BY>;
-  using M = typename G::M;
-  using ST = typename G::ST;
-  using HT = typename G::HT;
+  __shared__ unsigned q_next;
+  const int tile_begin = blockIdx.x * a.tile;
+  const int tile_n = min(a.tile, a.n_work - tile_begin);
+  if (threadIdx.x == 0) q_next = blockDim.x;  // the first blockDim items are taken statically
+  __syncthreads();
 
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = tid < a.n_work;
-  const int idx = live ? (a.wl_in ? (int)a.wl_in[tid] : tid) : 0;
-  const int r = idx / a.RX;
-  const int c = idx - r * a.RX;
-  const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
-  const uint32_t gid = (uint32_t)((a.row0 + r) * a.RX + c);
-  const unsigned K = a.it_K, K0 = a.it_K0;
-
-  unsigned long long n_ev = 0, n_out = 0, n_in = 0, n_cmp = 0, n_bev = 0;
+  unsigned n_ev = 0, n_out = 0, n_in = 0, n_cmp = 0, n_bev = 0, n_reg = 0;
   bool changed = false, overflow = false;
-
-  if (live) {
-    // ---- committed state (the old tau_m becomes tau_0) ----
-    M spins = (M)((const ST*)a.in.spins)[idx];
-    M gN, gS, gW, gE;
-    expand_halo<G>((unsigned long long)((const HT*)a.in.halo)[idx], gN, gS, gW, gE);
-    double ts = a.in.ts[idx];
-    double R = a.in.R[idx];
-    uint32_t n = a.in.n[idx];
-    unsigned long long dig = a.digest ? a.in.dig[idx] : 0ull;
-
-    // ---- incoming boundary histories (latest as of the previous iteration) ----
-    // direction d's neighbour wrote them as its opposite edge (d ^ 1).
-    const int gr = a.row0 + r;
-    uint32_t nid[4];
-    nid[EDGE_N] = (uint32_t)(((gr - 1 + a.RYg) % a.RYg) * a.RX + c);
-    nid[EDGE_S] = (uint32_t)(((gr + 1) % a.RYg) * a.RX + c);
-    nid[EDGE_W] = (uint32_t)(gr * a.RX + (c - 1 + a.RX) % a.RX);
-    nid[EDGE_E] = (uint32_t)(gr * a.RX + (c + 1) % a.RX);
-    // cursor of each incoming history, packed: cnt | idx << 8 | pos << 16 |
-    // source << 24 (source 0/1 = slot, 2 = ghost row above, 3 = below);
-    // hoff = element offset of entry 0, entry q at hoff + q * RX
-    unsigned hm[4], hoff[4];
-    double ht[4];
-#pragma unroll
-    for (int d = 0; d < 4; ++d) {
-      hm[d] = 0; hoff[d] = 0; ht[d] = dinf();
-      const bool axis_off = (d < 2) ? wrapY : wrapX;
-      if (a.first || axis_off) continue;
-      const bool ghost = a.world > 1 && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
-      unsigned cnt = 0, src = 0;
-      if (ghost) {
-        const GhostView& g = d == EDGE_N ? a.gh_up : a.gh_down;
-        cnt = g.cnt[c];
-        src = d == EDGE_N ? 2u : 3u;
-        hoff[d] = (unsigned)c;
-      } else {
-        const int nr = d == EDGE_N ? (r - 1 + a.RYl) % a.RYl : d == EDGE_S ? (r + 1) % a.RYl : r;
-        const int nc = d == EDGE_W ? (c - 1 + a.RX) % a.RX : d == EDGE_E ? (c + 1) % a.RX : c;
-        const unsigned long long v = __ldcg(&a.sel[(long long)nr * a.RX + nc]);
-        const Latest L = latest_of(v, d ^ 1, K, K0);
-        if (L.valid) {
-          const EdgeView& E = L.slot ? a.ed[1] : a.ed[0];
-          cnt = E.cnt[(long long)(d ^ 1) * a.cstride + (long long)nr * a.RX + nc];
-          src = (unsigned)L.slot;
-          hoff[d] = (unsigned)((long long)(d ^ 1) * a.tstride + ((long long)nr * a.K) * a.RX + nc);
+  Lane<G> L;
+  // Refill in batches: lanes whose region reached the window end wait until
+  // at least REFILL lanes of the warp are idle, then publish and reload
+  // together, so the (memory-heavy) load/publish path runs converged.
+  constexpr int REFILL = 12;
+  bool active = false, pending = false, exhausted = false;
+  int item = threadIdx.x;  // the first blockDim items are taken statically
+  for (;;) {
+    const unsigned idle = __ballot_sync(0xffffffffu, !active);
+    if (__popc(idle) >= REFILL || idle == 0xffffffffu) {
+      if (!active) {
+        if (pending) {
+          if (!LOG) lane_finish<G>(a, L, changed, overflow);
+          n_ev += L.n_ev;
+          n_bev = max(n_bev, L.bev);
+          pending = false;
         }
-      }
-      unsigned pos = 0;
-      if (cnt > 0) {
-        const double* T = src == 0 ? a.ed[0].t : src == 1 ? a.ed[1].t : src == 2 ? a.gh_up.t : a.gh_down.t;
-        const uint8_t* P = src == 0 ? a.ed[0].pos : src == 1 ? a.ed[1].pos : src == 2 ? a.gh_up.pos : a.gh_down.pos;
-        ht[d] = T[hoff[d]];
-        pos = P[hoff[d]];
-      }
-      hm[d] = cnt | (pos << 16) | (src << 24);
-      n_in += cnt;
-    }
-
-    // ---- own latest histories (fused diff, statement (c)) ----
-    // packed per edge: new count | latest count << 8 | latest slot << 16 | diverged << 17
-    const unsigned long long vown = LOG ? 0ull : a.sel[idx];
-    unsigned om[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const unsigned ps = (unsigned)((vown >> e) & 1ull);
-      unsigned pc = 0;
-      if (!LOG) {
-        const Latest L = latest_of(vown, e, K, K0);
-        if (L.valid) pc = (ps ? a.ed[1] : a.ed[0]).cnt[(long long)e * a.cstride + (long long)r * a.RX + c];
-      }
-      om[e] = (pc << 8) | (ps << 16);
-    }
-    const unsigned long long log_base = LOG ? a.log_off[idx] : 0ull;
-
-    // pair n: U already spent into R (carried), V selects the next atom
-    double U, V;
-    draw_pair(a.seed, gid, n, U, V);
-    Classes<G> C;
-    C.build(spins, gN, gS, gW, gE, wrapX, wrapY);
-    double lam = fold_lambda<G>(C, a.rate);
-    double tc = cand_time(ts, R, lam);
-
-    for (;;) {
-      // earliest pending break point, (time, neighbour id) order (R10)
-      int dstar = -1;
-      double tb = dinf();
-      uint32_t nb = 0xffffffffu;
-#pragma unroll
-      for (int d = 0; d < 4; ++d) {
-        const bool pend = ((hm[d] >> 8) & 0xFFu) < (hm[d] & 0xFFu);
-        if (pend && (ht[d] < tb || (ht[d] == tb && nid[d] < nb))) {
-          dstar = d;
-          tb = ht[d];
-          nb = nid[d];
-        }
-      }
-      const bool bp = dstar >= 0 && (tb < tc || (tb == tc && nb < gid));
-      const bool ev = !bp && tc < a.t_w;
-      if (!bp && !ev) break;
-      double tnew;
-      if (ev) {
-        // ---- own event at tc ----
-        const int site = select_site<G>(C, a.rate, V, lam);
-        spins ^= G::ONE << site;
-        tnew = tc;
-        const int sr = site / BX, sc = site - sr * BX;
-        if (a.digest) {
-          dig = mix64(mix64(dig ^ (unsigned long long)__double_as_longlong(tc)) ^ (unsigned long long)site);
-        }
-        if (LOG) {
-          const unsigned long long o = log_base + n_ev;
-          a.log_t[o] = tc;
-          a.log_region[o] = gid;
-          a.log_site[o] = (uint16_t)site;
-        } else {
-          // own boundary history; an edge history is
-          // written only once it diverges from its latest version
-          bool bev = false;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const bool on = e == EDGE_N ? (!wrapY && sr == 0)
-                          : e == EDGE_S ? (!wrapY && sr == BY - 1)
-                          : e == EDGE_W ? (!wrapX && sc == 0)
-                                        : (!wrapX && sc == BX - 1);
-            if (on) {
-              bev = true;
-              const unsigned k = om[e] & 0xFFu;
-              const unsigned pc = (om[e] >> 8) & 0xFFu;
-              const unsigned ps = (om[e] >> 16) & 1u;
-              bool dve = (om[e] >> 17) & 1u;
-              const uint8_t p = (uint8_t)(e < 2 ? sc : sr);
-              if ((int)k < a.K) {
-                const long long base = (long long)e * a.tstride + ((long long)r * a.K) * a.RX + c;
-                const EdgeView& Pold = ps ? a.ed[1] : a.ed[0];
-                const EdgeView& Pnew = ps ? a.ed[0] : a.ed[1];
-                bool same = false;
-                if (!dve && k < pc) {
-                  ++n_cmp;
-                  same = __double_as_longlong(Pold.t[base + (long long)k * a.RX]) == __double_as_longlong(tc) &&
-                         Pold.pos[base + (long long)k * a.RX] == p;
-                }
-                if (!same) {
-                  if (!dve) {  // copy the agreeing prefix into the new slot
-                    for (unsigned q = 0; q < k; ++q) {
-                      Pnew.t[base + (long long)q * a.RX] = Pold.t[base + (long long)q * a.RX];
-                      Pnew.pos[base + (long long)q * a.RX] = Pold.pos[base + (long long)q * a.RX];
-                    }
-                    dve = true;
-                  }
-                  Pnew.t[base + (long long)k * a.RX] = tc;
-                  Pnew.pos[base + (long long)k * a.RX] = p;
-                  ++n_out;
-                }
-              } else {
-                overflow = true;
-              }
-              const unsigned kk = k < 255u ? k + 1 : 255u;
-              om[e] = kk | (pc << 8) | (ps << 16) | ((unsigned)dve << 17);
-            }
+        if (!exhausted) {
+          if (item < 0) item = (int)atomicAdd(&q_next, 1u);
+          if (item < tile_n) {
+            const int idx = a.wl_in ? (int)a.wl_in[tile_begin + item] : tile_begin + item;
+            lane_load<G, LOG>(a, L, idx);
+            n_in += (L.hm[0] & 0xFFu) + (L.hm[1] & 0xFFu) + (L.hm[2] & 0xFFu) + (L.hm[3] & 0xFFu);
+            ++n_reg;
+            active = pending = true;
+          } else {
+            exhausted = true;
           }
-          n_bev += bev ? 1 : 0;
-        }
-        ++n_ev;
-      } else {
-        // ---- break point at tb (eqs. lambdataua..newtau) ----
-        double Rn = __dsub_rn(R, __dmul_rn(lam, __dsub_rn(tb, ts)));
-        R = Rn < 0.0 ? 0.0 : Rn;
-        tnew = tb;
-        // toggle the ghost spin and advance that history's cursor; unrolled
-        // over the four directions so the cursor state stays in registers
-#pragma unroll
-        for (int d = 0; d < 4; ++d) {
-          if (d == dstar) {
-            const int p = (int)((hm[d] >> 16) & 0xFFu);
-            if (d == EDGE_N) gN ^= G::ONE << p;
-            else if (d == EDGE_S) gS ^= G::ONE << ((BY - 1) * BX + p);
-            else if (d == EDGE_W) gW ^= G::ONE << (p * BX);
-            else gE ^= G::ONE << (p * BX + BX - 1);
-            const unsigned nx = ((hm[d] >> 8) & 0xFFu) + 1;
-            const unsigned src = hm[d] >> 24;
-            unsigned pos = 0;
-            if (nx < (hm[d] & 0xFFu)) {
-              const double* T = src == 0 ? a.ed[0].t : src == 1 ? a.ed[1].t : src == 2 ? a.gh_up.t : a.gh_down.t;
-              const uint8_t* P =
-                  src == 0 ? a.ed[0].pos : src == 1 ? a.ed[1].pos : src == 2 ? a.gh_up.pos : a.gh_down.pos;
-              const unsigned long long off = (unsigned long long)hoff[d] + (unsigned long long)nx * a.RX;
-              ht[d] = T[off];
-              pos = P[off];
-            }
-            hm[d] = (hm[d] & 0xFF0000FFu) | (nx << 8) | (pos << 16);
-          }
+          item = -1;
         }
       }
-      ts = tnew;
-      C.build(spins, gN, gS, gW, gE, wrapX, wrapY);
-      lam = fold_lambda<G>(C, a.rate);
-      if (ev) {
-        // next pair of the list; the unused remainder carries over
-        ++n;
-        draw_pair(a.seed, gid, n, U, V);
-        R = expvar(U);
-      }
-      tc = cand_time(ts, R, lam);
+      if (__all_sync(0xffffffffu, exhausted && !active)) break;
     }
-
-    if (!LOG) {
-      unsigned chmask = 0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const unsigned oc = om[e] & 0xFFu, pc = (om[e] >> 8) & 0xFFu, ps = (om[e] >> 16) & 1u;
-        bool dve = (om[e] >> 17) & 1u;
-        if ((int)oc > a.K) overflow = true;
-        const EdgeView& Pold = ps ? a.ed[1] : a.ed[0];
-        const EdgeView& Pnew = ps ? a.ed[0] : a.ed[1];
-        if (!dve && oc != pc) {
-          // new history is a strict prefix of the latest one: copy it over
-          const long long base = (long long)e * a.tstride + ((long long)r * a.K) * a.RX + c;
-          for (unsigned q = 0; q < oc && (int)q < a.K; ++q) {
-            Pnew.t[base + (long long)q * a.RX] = Pold.t[base + (long long)q * a.RX];
-            Pnew.pos[base + (long long)q * a.RX] = Pold.pos[base + (long long)q * a.RX];
-          }
-          dve = true;
-        }
-        if (dve) {
-          chmask |= 1u << e;
-          Pnew.cnt[(long long)e * a.cstride + (long long)r * a.RX + c] = (uint8_t)((int)oc < a.K ? oc : a.K);
-        }
-      }
-      if (chmask) {
-        changed = true;
-        a.sel[idx] = sel_after_change(vown, chmask, K, K0);
-        // neighbours across changed edges must be recomputed next iteration
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if (!((chmask >> e) & 1u)) continue;
-          if (a.world > 1 && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
-          const int nr = e == EDGE_N ? (r - 1 + a.RYl) % a.RYl : e == EDGE_S ? (r + 1) % a.RYl : r;
-          const int nc = e == EDGE_W ? (c - 1 + a.RX) % a.RX : e == EDGE_E ? (c + 1) % a.RX : c;
-          const int nidx = nr * a.RX + nc;
-          if (atomicMax(&a.dirty[nidx], K + 1) < K + 1) a.wl_out[atomicAdd(a.wl_out_count, 1u)] = (uint32_t)nidx;
-        }
-      }
-      // tentative end-of-window state (committed by pointer swap at commit)
-      ((ST*)a.out.spins)[idx] = (ST)spins;
-      ((HT*)a.out.halo)[idx] = (HT)compress_halo<G>(gN, gS, gW, gE);
-      a.out.ts[idx] = ts;
-      a.out.R[idx] = R;
-      a.out.n[idx] = n;
-      if (a.digest) a.out.dig[idx] = dig;
-    }
+    if (active && !lane_step<G, LOG>(a, L, n_out, n_cmp, overflow)) active = false;
   }
 
   if (!LOG) {
@@ -568,27 +643,27 @@ __global__ void __launch_bounds__(128) region_kernel(const KArgs a) {
     const unsigned full = 0xffffffffu;
     const unsigned anych = __ballot_sync(full, changed);
     const unsigned anyov = __ballot_sync(full, overflow);
-    unsigned long long v0 = n_ev, v1 = n_out, v2 = n_in, v3 = n_cmp;
-    unsigned fmax = (unsigned)n_bev;
+    unsigned long long v0 = n_ev, v1 = n_out, v2 = n_in, v3 = n_cmp, v5 = n_reg;
+    unsigned fmax = n_bev;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       v0 += __shfl_xor_sync(full, v0, o);
       v1 += __shfl_xor_sync(full, v1, o);
       v2 += __shfl_xor_sync(full, v2, o);
       v3 += __shfl_xor_sync(full, v3, o);
+      v5 += __shfl_xor_sync(full, v5, o);
       fmax = max(fmax, __shfl_xor_sync(full, fmax, o));
     }
-    const unsigned nlive = __popc(__ballot_sync(full, live));
     if ((threadIdx.x & 31) == 0) {
       if (anych) atomicOr(&a.flags[0], 1);
       if (anyov) atomicOr(&a.flags[1], 1);
-      if (nlive) {
+      if (v5) {
         atomicAdd(&a.stats[0], v0);
         atomicAdd(&a.stats[1], v1);
         atomicAdd(&a.stats[2], v2);
         atomicAdd(&a.stats[3], v3);
         atomicMax(&a.stats[4], (unsigned long long)fmax);
-        atomicAdd(&a.stats[5], (unsigned long long)nlive);
+        atomicAdd(&a.stats[5], v5);
       }
     }
   }
@@ -608,13 +683,13 @@ __global__ void pack_kernel(const KArgs a, GhostView send_up, GhostView send_dow
   const int r = up ? 0 : a.RYl - 1;
   const int e = up ? EDGE_N : EDGE_S;
   const GhostView& g = up ? send_up : send_down;
-  const unsigned long long v = a.sel[(long long)r * a.RX + c];
+  const ulonglong2 wp = reinterpret_cast<const ulonglong2*>(a.sel)[(long long)r * a.RX + c];
   // latest as of the end of this iteration
-  const Latest L = latest_of(v, e, a.it_K + 1, a.it_K0);
+  const unsigned long long v = latest_word(wp, a.it_K + 1);
   int cnt = 0;
-  if (L.valid) {
-    const EdgeView& E = a.ed[L.slot];
-    cnt = E.cnt[(long long)e * a.cstride + (long long)r * a.RX + c];
+  if (word_valid(v, a.it_K0)) {
+    const EdgeView& E = word_slot(v, e) ? a.ed[1] : a.ed[0];
+    cnt = (int)word_count(v, e);
     const long long base = (long long)e * a.tstride + ((long long)r * a.K) * a.RX + c;
     for (int q = 0; q < cnt; ++q) {
       g.t[(long long)q * a.RX + c] = E.t[base + (long long)q * a.RX];
@@ -622,8 +697,10 @@ __global__ void pack_kernel(const KArgs a, GhostView send_up, GhostView send_dow
     }
   }
   g.cnt[c] = (uint8_t)cnt;
-  const unsigned Kl = (unsigned)(v >> 32);
-  const bool ch_now = Kl == a.it_K && ((v >> (4 + e)) & 1ull);
+  // changed in this iteration: the word was rewritten now and edge e moved
+  // slot relative to the previous latest word (the other one)
+  const unsigned long long other = latest_index(wp, a.it_K + 1) ? wp.x : wp.y;
+  const bool ch_now = (unsigned)(v >> 32) == a.it_K && (((v ^ other) >> e) & 1ull);
   g.stamp[c] = ch_now ? a.it_K : 0u;
 }
 
@@ -638,7 +715,33 @@ __global__ void mark_kernel(const KArgs a, GhostView up, GhostView down) {
   if (g.stamp[c] != a.it_K) return;
   const int r = isup ? 0 : a.RYl - 1;
   const int nidx = r * a.RX + c;
-  if (atomicMax(&a.dirty[nidx], a.it_K + 1) < a.it_K + 1) a.wl_out[atomicAdd(a.wl_out_count, 1u)] = (uint32_t)nidx;
+  a.dirty[nidx] = a.it_K + 1;
+}
+
+// Ordered worklist of the next iteration: regions whose dirty stamp equals
+// `stamp`, compacted in region order within each 256-region block (one
+// atomic per block), so the next iteration's loads stay coalesced.
+__global__ void __launch_bounds__(256) compact_kernel(const uint32_t* dirty, int n, uint32_t stamp, uint32_t* wl,
+                                                      unsigned* count) {
+  __shared__ unsigned wsum[8];
+  __shared__ unsigned base;
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  const bool take = i < n && dirty[i] == stamp;
+  const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned m = __ballot_sync(0xffffffffu, take);
+  if (lane == 0) wsum[wid] = __popc(m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned s = 0;
+    for (int w = 0; w < 8; ++w) {
+      const unsigned t = wsum[w];
+      wsum[w] = s;
+      s += t;
+    }
+    base = s ? atomicAdd(count, s) : 0u;
+  }
+  __syncthreads();
+  if (take) wl[base + wsum[wid] + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
 }
 
 // ---------------------------------------------------------------------------

@@ -47,12 +47,12 @@ ShapeOps make_ops() {
   o.by = BY;
   o.spin_bytes = sizeof(typename G::ST);
   o.halo_bytes = sizeof(typename G::HT);
-  o.region = [](const KArgs& a, int nreg, cudaStream_t s) {
-    const int grid = (nreg + kThreads - 1) / kThreads;
+  o.region = [](const KArgs& a, int n, cudaStream_t s) {
+    const int grid = (n + a.tile - 1) / a.tile;
     isr::region_kernel<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
   };
-  o.replay = [](const KArgs& a, int nreg, cudaStream_t s) {
-    const int grid = (nreg + kThreads - 1) / kThreads;
+  o.replay = [](const KArgs& a, int n, cudaStream_t s) {
+    const int grid = (n + a.tile - 1) / a.tile;
     isr::region_kernel<BX, BY, true><<<grid, kThreads, 0, s>>>(a);
   };
   o.init = [](const uint8_t* buf, int Lx, int RX, int RYl, int row0, unsigned long long seed, StateView st,
@@ -220,7 +220,6 @@ cudaError_t dmalloc(T** p, size_t count) {
 
 void free_edges(ising_sr_ctx* c) {
   for (auto& e : c->ed) {
-    cudaFree(e.cnt);
     cudaFree(e.t);
     cudaFree(e.pos);
     e = EdgeView{};
@@ -243,8 +242,7 @@ ising_sr_status alloc_edges(ising_sr_ctx* c, int K) {
   const size_t tn = cn * (size_t)K;
   if (tn >= (1ull << 32)) return ISING_SR_E_CAPACITY;  // kernel offsets are 32-bit
   for (auto& e : c->ed) {
-    if (dmalloc(&e.cnt, cn) != cudaSuccess || dmalloc(&e.t, tn) != cudaSuccess ||
-        dmalloc(&e.pos, tn) != cudaSuccess) {
+    if (dmalloc(&e.t, tn) != cudaSuccess || dmalloc(&e.pos, tn) != cudaSuccess) {
       cudaGetLastError();
       free_edges(c);
       return ISING_SR_E_OOM;
@@ -286,12 +284,18 @@ int auto_capacity(const ising_sr_config& cfg) {
   for (double r : cfg.rate) rmax = std::max(rmax, r);
   const double mu = std::max(cfg.bx, cfg.by) * rmax * cfg.W;
   const int K = (int)std::ceil(mu + 6.0 * std::sqrt(mu) + 8.0);
-  return std::min(std::max(K, 8), 255);
+  return std::min(std::max(K, 8), isr::CNT_MAX);
 }
 
 ising_sr_status check(const ising_sr_ctx* c) {
   if (!c) return ISING_SR_E_INVALID_ARG;
   return c->sticky;
+}
+
+// work items per block: enough blocks for >= 4 per SM, at most 16 items per lane
+int tile_for(int n) {
+  const int per = std::max(1, std::min(16, n / (kThreads * 148 * 4)));
+  return kThreads * per;
 }
 
 KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
@@ -310,7 +314,6 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   a.row0 = c->row0;
   a.world = c->cfg.world;
   a.K = c->K;
-  a.cstride = (long long)c->RYl * c->RX;
   a.tstride = (long long)c->RYl * c->K * c->RX;
   a.it_K = K;
   a.it_K0 = c->K0;
@@ -326,14 +329,23 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
 }
 
 // algorithmic bytes of one iteration: per recomputed region
-// the committed state read + tentative state written, the selector words
-// (own + 4 neighbours) and 8 count bytes; 9 bytes per history entry written,
-// read as a break point, and compared.
+// the committed state read + tentative state written, the selector word
+// pairs read (own + 4 neighbours, 16 B each) and one selector word written;
+// 9 bytes per history entry written, read as a break point, and compared.
 double iteration_bytes(const ising_sr_ctx* c, const unsigned long long* s) {
   const double S = (double)c->ops->spin_bytes + (double)c->ops->halo_bytes + 8 + 8 + 4 +
                    ((c->cfg.flags & ISING_SR_FLAG_DIGEST) ? 8 : 0);
   const double regions = (double)s[5];
-  return regions * (2.0 * S + 5 * 8.0 + 8.0) + 9.0 * ((double)s[1] + (double)s[2] + (double)s[3]);
+  return regions * (2.0 * S + 5 * 16.0 + 8.0) + 9.0 * ((double)s[1] + (double)s[2] + (double)s[3]);
+}
+
+ising_sr_status compact_worklist(ising_sr_ctx* c) {
+  const unsigned K = c->Kglob;
+  isr::compact_kernel<<<(c->nreg + 255) / 256, 256, 0, c->stream>>>(c->dirty, c->nreg, K + 1, c->wl[(K + 1) & 1],
+                                                                     c->d_wlc + ((K + 1) & 1));
+  ++c->launches;
+  CK(c, cudaGetLastError());
+  return ISING_SR_OK;
 }
 
 ising_sr_status launch_iteration(ising_sr_ctx* c) {
@@ -347,6 +359,7 @@ ising_sr_status launch_iteration(ising_sr_ctx* c) {
   KArgs a = base_args(c, K, first);
   a.wl_in = first ? nullptr : c->wl[K & 1];
   a.n_work = nw;
+  a.tile = tile_for(nw);
   a.wl_out = c->wl[(K + 1) & 1];
   a.wl_out_count = c->d_wlc + ((K + 1) & 1);
   CK(c, cudaEventRecord(c->kev0, c->stream));
@@ -360,6 +373,8 @@ ising_sr_status launch_iteration(ising_sr_ctx* c) {
     isr::pack_kernel<<<(2 * c->RX + 127) / 128, 128, 0, c->stream>>>(a, c->gsend[0], c->gsend[1]);
     ++c->launches;
     CK(c, cudaGetLastError());
+  } else {
+    return compact_worklist(c);
   }
   return ISING_SR_OK;
 }
@@ -373,7 +388,7 @@ ising_sr_status mark_ghosts(ising_sr_ctx* c) {
   isr::mark_kernel<<<(2 * c->RX + 127) / 128, 128, 0, c->stream>>>(a, c->grecv[0], c->grecv[1]);
   ++c->launches;
   CK(c, cudaGetLastError());
-  return ISING_SR_OK;
+  return compact_worklist(c);
 }
 
 ising_sr_status read_flags(ising_sr_ctx* c) {
@@ -415,8 +430,8 @@ void fill_halo(ising_sr_ctx* c, ising_sr_halo* h) {
 }
 
 ising_sr_status grow_capacity(ising_sr_ctx* c) {
-  if (c->K >= 255) return ISING_SR_E_CAPACITY;
-  const int K = std::min(255, c->K * 2);
+  if (c->K >= isr::CNT_MAX) return ISING_SR_E_CAPACITY;
+  const int K = std::min(isr::CNT_MAX, c->K * 2);
   ising_sr_status s = alloc_edges(c, K);
   if (s != ISING_SR_OK) return s;
   c->stats.overflow_retries++;
@@ -545,7 +560,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
         dmalloc(&s.R, n) != cudaSuccess || dmalloc(&s.n, n) != cudaSuccess || dmalloc(&s.dig, n) != cudaSuccess)
       return bail(ISING_SR_E_OOM);
   }
-  if (dmalloc(&c->sel, n) != cudaSuccess || dmalloc(&c->dirty, n) != cudaSuccess ||
+  if (dmalloc(&c->sel, 2 * n) != cudaSuccess || dmalloc(&c->dirty, n) != cudaSuccess ||
       dmalloc(&c->wl[0], n) != cudaSuccess || dmalloc(&c->wl[1], n) != cudaSuccess ||
       dmalloc(&c->d_wlc, 2) != cudaSuccess || dmalloc(&c->d_flags, 4) != cudaSuccess ||
       dmalloc(&c->d_stats, 8) != cudaSuccess ||
@@ -555,13 +570,13 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
       dmalloc(&c->d_off, n) != cudaSuccess || dmalloc(&c->d_bsum, (n + kThreads - 1) / kThreads) != cudaSuccess ||
       dmalloc(&c->d_total, 1) != cudaSuccess)
     return bail(ISING_SR_E_OOM);
-  if (cudaMemsetAsync(c->sel, 0, n * 8, c->stream) != cudaSuccess ||
+  if (cudaMemsetAsync(c->sel, 0, n * 16, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->dirty, 0, n * 4, c->stream) != cudaSuccess)
     return bail(ISING_SR_E_CUDA);
   if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
       cudaEventCreate(&c->kev0) != cudaSuccess || cudaEventCreate(&c->kev1) != cudaSuccess)
     return bail(ISING_SR_E_CUDA);
-  const int K0 = cfg->hist_capacity > 0 ? std::min(cfg->hist_capacity, 255) : auto_capacity(*cfg);
+  const int K0 = cfg->hist_capacity > 0 ? std::min(cfg->hist_capacity, isr::CNT_MAX) : auto_capacity(*cfg);
   ising_sr_status s = alloc_edges(c, K0);
   if (s != ISING_SR_OK) return bail(s);
   c->stats.hist_capacity = c->K;
@@ -724,6 +739,7 @@ ising_sr_status ising_sr_commit(ising_sr_ctx* c, int64_t* events_out) {
     // replay every region against the final (latest) histories
     KArgs a = base_args(c, c->Kglob + 1, false);
     a.n_work = c->nreg;
+    a.tile = tile_for(c->nreg);
     a.log_t = c->log_t;
     a.log_region = c->log_region;
     a.log_site = c->log_site;
