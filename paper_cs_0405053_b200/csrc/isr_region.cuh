@@ -194,25 +194,62 @@ __device__ __forceinline__ int popc_m(M x) {
   else return __popc(x);
 }
 
-// j-th (0-based) set bit of x, LSB first (local row-major order)
-template <class M>
+// j-th (0-based) set bit of x, LSB first (local row-major order): binary
+// search on popcounts of halves
+template <class M, int NBITS>
 __device__ __forceinline__ int nth_bit(M x, int j) {
-  if constexpr (sizeof(M) == 8) {
-    const uint32_t lo = (uint32_t)x;
-    const int pl = __popc(lo);
-    if (j < pl) return (int)__fns(lo, 0, j + 1);
-    return 32 + (int)__fns((uint32_t)(x >> 32), 0, j - pl + 1);
-  } else {
-    return (int)__fns((uint32_t)x, 0, j + 1);
+  int pos = 0;
+  if constexpr (NBITS > 32) {
+    const int c = __popc((uint32_t)x);
+    if (j >= c) { j -= c; x >>= 32; pos += 32; }
+  }
+  uint32_t y = (uint32_t)x;
+  if constexpr (NBITS > 16) {
+    const int c = __popc(y & 0xFFFFu);
+    if (j >= c) { j -= c; y >>= 16; pos += 16; }
+  }
+  if constexpr (NBITS > 8) {
+    const int c = __popc(y & 0xFFu);
+    if (j >= c) { j -= c; y >>= 8; pos += 8; }
+  }
+  if constexpr (NBITS > 4) {
+    const int c = __popc(y & 0xFu);
+    if (j >= c) { j -= c; y >>= 4; pos += 4; }
+  }
+  if constexpr (NBITS > 2) {
+    const int c = __popc(y & 0x3u);
+    if (j >= c) { j -= c; y >>= 2; pos += 2; }
+  }
+  if constexpr (NBITS > 1) {
+    const int c = (int)(y & 1u);
+    if (j >= c) pos += 1;
+  }
+  return pos;
+}
+
+// Products fl(N * r_k) for N = 0..NS, one table per block in shared memory:
+// the fold below adds exactly the values __dmul_rn((double)N_k, r_k) would
+// give, so the result is bit-identical to multiplying in place.
+template <class G>
+struct ProdTable {
+  double v[10][G::NS + 1];
+  __device__ __forceinline__ double at(int k, int n) const { return v[k][n]; }
+};
+
+template <class G>
+__device__ __forceinline__ void fill_prod(ProdTable<G>& T, const double* rate) {
+  for (int i = threadIdx.x; i < 10 * (G::NS + 1); i += blockDim.x) {
+    const int k = i / (G::NS + 1), n = i - k * (G::NS + 1);
+    T.v[k][n] = __dmul_rn((double)n, rate[k]);
   }
 }
 
 // eq. biglambda, fixed fold order (R3): c_k = c_{k-1} + N_k r_k
 template <class G>
-__device__ __forceinline__ double fold_lambda(const Classes<G>& C, const double* rate) {
+__device__ __forceinline__ double fold_lambda(const Classes<G>& C, const ProdTable<G>& T) {
   double c = 0.0;
 #pragma unroll
-  for (int k = 0; k < 10; ++k) c = __dadd_rn(c, __dmul_rn((double)popc_m(C.mask(k)), rate[k]));
+  for (int k = 0; k < 10; ++k) c = __dadd_rn(c, T.at(k, popc_m(C.mask(k))));
   return c;
 }
 
@@ -220,13 +257,14 @@ __device__ __forceinline__ double fold_lambda(const Classes<G>& C, const double*
 // in x = V*Lambda space: k* = first k with x <= c_k,
 // j = min(floor((x - c_{k*-1}) / r_k*), N_k* - 1); returns the local site.
 template <class G>
-__device__ __forceinline__ int select_site(const Classes<G>& C, const double* rate, double V, double lam) {
+__device__ __forceinline__ int select_site(const Classes<G>& C, const ProdTable<G>& T, const double* rate,
+                                           double V, double lam) {
   const double x = __dmul_rn(V, lam);
   double c = 0.0, cprev = 0.0;
   int ks = -1;
 #pragma unroll
   for (int k = 0; k < 10; ++k) {
-    const double cn = __dadd_rn(c, __dmul_rn((double)popc_m(C.mask(k)), rate[k]));
+    const double cn = __dadd_rn(c, T.at(k, popc_m(C.mask(k))));
     if (ks < 0 && x <= cn) {
       ks = k;
       cprev = c;
@@ -240,10 +278,13 @@ __device__ __forceinline__ int select_site(const Classes<G>& C, const double* ra
   }
   const typename G::M mk = C.mask(ks);
   const int nk = popc_m(mk);
-  long long j = (long long)floor(__ddiv_rn(__dsub_rn(x, cprev), rate[ks]));
+  const double a = __dsub_rn(x, cprev);
+  const double rk = rate[ks];
+  const double q = rk == 1.0 ? a : __ddiv_rn(a, rk);  // a / 1.0 == a exactly
+  long long j = (long long)floor(q);
   if (j > nk - 1) j = nk - 1;
   if (j < 0) j = 0;
-  return nth_bit(mk, (int)j);
+  return nth_bit<typename G::M, G::NS>(mk, (int)j);
 }
 
 // Expand/compress the stored ghost bits (N[BX] S[BX] W[BY] E[BY]) to/from
@@ -298,131 +339,236 @@ __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000
 // longer idles while its slowest region finishes (region histories have
 // Poisson-distributed lengths).
 // ---------------------------------------------------------------------------
+// Per-lane shared-memory stage of the incoming histories: up to CI entries
+// per direction are copied global -> shared with cp.async when a region is
+// loaded (one memory latency per refill batch, many loads in flight), so
+// the break-point merge inside the step loop reads shared memory only.
+constexpr int NT = 128;  // threads per block of K1
+constexpr int CI = 4;    // staged entries per incoming direction
+
+struct Stage {
+  double t[4][CI][NT];
+  uint32_t p[4][CI][NT];  // 4-byte word holding the position byte, then the byte itself
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
+}
+
 template <class G>
 struct Lane {
   using M = typename G::M;
-  // region
   int idx;
-  uint32_t gid;
+  uint32_t gid;    // global region id (Philox key, tie order)
+  unsigned obase;  // (r * K) * RX + c: own-edge history offset without the edge term
   M spins, gN, gS, gW, gE;
   double ts, R, V, lam, tc;
   uint32_t n;
   unsigned long long dig;
   // incoming history cursors: cnt | idx << 8 | pos << 16 | source << 24
-  unsigned hm[4], hoff[4];
+  // (source 0/1 = slot, 2/3 = ghost row above/below; bit 28 = staged in smem)
+  unsigned hm[4];
   double ht[4];
-  // own edges: new count | latest count << 8 | latest slot << 16 | diverged << 17
+  // own edges: new count | latest count << 8 | latest slot << 16
   unsigned om[4];
-  unsigned long long vown;
   int whalf;      // selector word to overwrite on change
   unsigned n_ev;  // events of this region (log offset)
   unsigned bev;   // own boundary events of this region
 };
 
+__device__ __forceinline__ uint32_t region_gid(const KArgs& a, int idx) {
+  const int r = idx / a.RX, c = idx - r * a.RX;
+  return (uint32_t)((a.row0 + r) * a.RX + c);
+}
+
+// element offset of entry 0 of the history that direction d reads
+__device__ __forceinline__ unsigned in_off(const KArgs& a, int idx, int d, unsigned src) {
+  const int r = idx / a.RX, c = idx - r * a.RX;
+  if (src >= 2) return (unsigned)c;
+  const int nr = d == EDGE_N ? (r - 1 + a.RYl) % a.RYl : d == EDGE_S ? (r + 1) % a.RYl : r;
+  const int nc = d == EDGE_W ? (c - 1 + a.RX) % a.RX : d == EDGE_E ? (c + 1) % a.RX : c;
+  return (unsigned)((long long)(d ^ 1) * a.tstride + ((long long)nr * a.K) * a.RX + nc);
+}
+
+__device__ __forceinline__ const double* src_t(const KArgs& a, unsigned src) {
+  return src == 0 ? a.ed[0].t : src == 1 ? a.ed[1].t : src == 2 ? a.gh_up.t : a.gh_down.t;
+}
+__device__ __forceinline__ const uint8_t* src_p(const KArgs& a, unsigned src) {
+  return src == 0 ? a.ed[0].pos : src == 1 ? a.ed[1].pos : src == 2 ? a.gh_up.pos : a.gh_down.pos;
+}
+
 template <class G, bool LOG>
-__device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx) {
+__device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, Stage& S, const ProdTable<G>& PT) {
   using M = typename G::M;
   const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
   const unsigned K = a.it_K, K0 = a.it_K0;
+  const int lane = threadIdx.x;
   const int r = idx / a.RX, c = idx - r * a.RX;
   L.idx = idx;
   L.gid = (uint32_t)((a.row0 + r) * a.RX + c);
-  L.spins = (M)((const typename G::ST*)a.in.spins)[idx];
-  expand_halo<G>((unsigned long long)((const typename G::HT*)a.in.halo)[idx], L.gN, L.gS, L.gW, L.gE);
-  L.ts = a.in.ts[idx];
-  L.R = a.in.R[idx];
-  L.n = a.in.n[idx];
-  L.dig = a.digest ? a.in.dig[idx] : 0ull;
+  L.obase = (unsigned)(((long long)r * a.K) * a.RX + c);
   L.n_ev = 0;
   L.bev = 0;
+  // selector words first: they gate the history loads
+  ulonglong2 wp_own = make_ulonglong2(0ull, 0ull);
+  if (!LOG) wp_own = reinterpret_cast<const ulonglong2*>(a.sel)[idx];
+  unsigned cnt[4], src[4];
 #pragma unroll
   for (int d = 0; d < 4; ++d) {
-    L.hm[d] = 0;
-    L.hoff[d] = 0;
-    L.ht[d] = dinf();
+    cnt[d] = 0;
+    src[d] = 0;
     const bool axis_off = (d < 2) ? wrapY : wrapX;
     if (a.first || axis_off) continue;
     const bool ghost = a.world > 1 && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
-    unsigned cnt = 0, src = 0;
     if (ghost) {
-      const GhostView& g = d == EDGE_N ? a.gh_up : a.gh_down;
-      cnt = g.cnt[c];
-      src = d == EDGE_N ? 2u : 3u;
-      L.hoff[d] = (unsigned)c;
+      cnt[d] = (d == EDGE_N ? a.gh_up : a.gh_down).cnt[c];
+      src[d] = d == EDGE_N ? 2u : 3u;
     } else {
       const int nr = d == EDGE_N ? (r - 1 + a.RYl) % a.RYl : d == EDGE_S ? (r + 1) % a.RYl : r;
       const int nc = d == EDGE_W ? (c - 1 + a.RX) % a.RX : d == EDGE_E ? (c + 1) % a.RX : c;
       const ulonglong2 wp = __ldcg(reinterpret_cast<const ulonglong2*>(a.sel) + ((long long)nr * a.RX + nc));
       const unsigned long long v = latest_word(wp, K);
       if (word_valid(v, K0)) {
-        cnt = word_count(v, d ^ 1);
-        src = (unsigned)word_slot(v, d ^ 1);
-        L.hoff[d] = (unsigned)((long long)(d ^ 1) * a.tstride + ((long long)nr * a.K) * a.RX + nc);
+        cnt[d] = word_count(v, d ^ 1);
+        src[d] = (unsigned)word_slot(v, d ^ 1);
       }
     }
-    unsigned pos = 0;
-    if (cnt > 0) {
-      const double* T = src == 0 ? a.ed[0].t : src == 1 ? a.ed[1].t : src == 2 ? a.gh_up.t : a.gh_down.t;
-      const uint8_t* P = src == 0 ? a.ed[0].pos : src == 1 ? a.ed[1].pos : src == 2 ? a.gh_up.pos : a.gh_down.pos;
-      L.ht[d] = T[L.hoff[d]];
-      pos = P[L.hoff[d]];
-    }
-    L.hm[d] = cnt | (pos << 16) | (src << 24);
   }
-  L.vown = 0ull;
+  // committed state (the old tau_m becomes tau_0)
+  L.spins = (M)((const typename G::ST*)a.in.spins)[idx];
+  expand_halo<G>((unsigned long long)((const typename G::HT*)a.in.halo)[idx], L.gN, L.gS, L.gW, L.gE);
+  L.ts = a.in.ts[idx];
+  L.R = a.in.R[idx];
+  L.n = a.in.n[idx];
+  L.dig = a.digest ? a.in.dig[idx] : 0ull;
+  // stage the incoming histories (or, above CI entries, read them lazily)
+  bool staged_any = false;
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    L.ht[d] = dinf();
+    unsigned flags = 0;
+    if (cnt[d] > 0) {
+      const unsigned off = in_off(a, idx, d, src[d]);
+      const double* T = src_t(a, src[d]);
+      const uint8_t* P = src_p(a, src[d]);
+      if (cnt[d] <= (unsigned)CI) {
+        flags = 1u << 28;
+        staged_any = true;
+#pragma unroll
+        for (int q = 0; q < CI; ++q) {
+          if (q < (int)cnt[d]) {
+            const unsigned o = off + (unsigned)q * (unsigned)a.RX;
+            cp_async8(&S.t[d][q][lane], T + o);
+            cp_async4(&S.p[d][q][lane], P + (o & ~3u));
+          }
+        }
+      } else {
+        L.ht[d] = T[off];
+        flags |= (unsigned)P[off] << 16;
+      }
+    }
+    L.hm[d] = cnt[d] | (src[d] << 24) | flags;
+  }
+  if (staged_any) {
+    cp_async_wait_all();
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      if (!(L.hm[d] & (1u << 28))) continue;
+      const unsigned off = in_off(a, idx, d, src[d]);
+#pragma unroll
+      for (int q = 0; q < CI; ++q)
+        if (q < (int)cnt[d]) {
+          const unsigned o = off + (unsigned)q * (unsigned)a.RX;
+          S.p[d][q][lane] = (S.p[d][q][lane] >> (8u * (o & 3u))) & 0xFFu;
+        }
+      L.ht[d] = S.t[d][0][lane];
+      L.hm[d] |= S.p[d][0][lane] << 16;
+    }
+  }
+  // own latest histories: slot and count per edge (fused diff at finish)
+  unsigned long long vown = 0ull;
   L.whalf = 0;
   if (!LOG) {
-    const ulonglong2 wp = reinterpret_cast<const ulonglong2*>(a.sel)[idx];
-    const int li = latest_index(wp, K);
-    const unsigned long long v = li ? wp.y : wp.x;
-    L.vown = word_valid(v, K0) ? v : (v & 0xFull);  // outside the window: slots only, counts 0
-    L.whalf = li ^ 1;  // overwrite the older word
+    const int li = latest_index(wp_own, K);
+    const unsigned long long v = li ? wp_own.y : wp_own.x;
+    vown = word_valid(v, K0) ? v : (v & 0xFull);  // outside the window: slots only, counts 0
+    L.whalf = li ^ 1;                             // overwrite the older word
   }
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const unsigned ps = (unsigned)word_slot(L.vown, e);
-    const unsigned pc = word_count(L.vown, e);
-    L.om[e] = (pc << 8) | (ps << 16);
-  }
+  for (int e = 0; e < 4; ++e)
+    L.om[e] = (word_count(vown, e) << 8) | ((unsigned)word_slot(vown, e) << 16);
   // pair n: U already spent into R (carried), V selects the next atom
   double U;
   draw_pair(a.seed, L.gid, L.n, U, L.V);
   Classes<G> C;
   C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
-  L.lam = fold_lambda<G>(C, a.rate);
+  L.lam = fold_lambda<G>(C, PT);
   L.tc = cand_time(L.ts, L.R, L.lam);
 }
 
 // One step of the region's history: the earliest of its own candidate event
 // and the pending break points.  Returns false when the region has reached
 // the window end.
+// neighbour id in direction d (only needed to order exactly equal times)
+__device__ __forceinline__ uint32_t neighbour_id(const KArgs& a, uint32_t gid, int d) {
+  const int c = (int)(gid % (uint32_t)a.RX);
+  const int gr = (int)(gid / (uint32_t)a.RX);
+  return d == EDGE_N ? (uint32_t)(((gr - 1 + a.RYg) % a.RYg) * a.RX + c)
+       : d == EDGE_S ? (uint32_t)(((gr + 1) % a.RYg) * a.RX + c)
+       : d == EDGE_W ? (uint32_t)(gr * a.RX + (c - 1 + a.RX) % a.RX)
+                     : (uint32_t)(gr * a.RX + (c + 1) % a.RX);
+}
+
 template <class G, bool LOG>
-__device__ __forceinline__ bool lane_step(const KArgs& a, Lane<G>& L, unsigned& n_out, unsigned& n_cmp,
-                                          bool& overflow) {
+__device__ __forceinline__ bool lane_step(const KArgs& a, Lane<G>& L, const Stage& S, const ProdTable<G>& PT,
+                                          unsigned& n_out, bool& overflow) {
   constexpr int BX = G::BX, BY = G::BY;
   const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
-  // neighbour ids in (time, id) order (R10)
-  const int c = (int)(L.gid % (uint32_t)a.RX);
-  const int gr = (int)(L.gid / (uint32_t)a.RX);
+  const int lane = threadIdx.x;
+  const uint32_t gid = L.gid;
+  // earliest pending break point, (time, neighbour id) order (R10);
+  // ids are computed only for exactly equal times
   int dstar = -1;
   double tb = dinf();
-  uint32_t nb = 0xffffffffu;
+  bool tie = false;
 #pragma unroll
   for (int d = 0; d < 4; ++d) {
     const bool pend = ((L.hm[d] >> 8) & 0xFFu) < (L.hm[d] & 0xFFu);
     if (pend) {
-      const uint32_t nid = d == EDGE_N ? (uint32_t)(((gr - 1 + a.RYg) % a.RYg) * a.RX + c)
-                         : d == EDGE_S ? (uint32_t)(((gr + 1) % a.RYg) * a.RX + c)
-                         : d == EDGE_W ? (uint32_t)(gr * a.RX + (c - 1 + a.RX) % a.RX)
-                                       : (uint32_t)(gr * a.RX + (c + 1) % a.RX);
-      if (L.ht[d] < tb || (L.ht[d] == tb && nid < nb)) {
+      if (L.ht[d] < tb) {
         dstar = d;
         tb = L.ht[d];
-        nb = nid;
+      } else if (L.ht[d] == tb) {
+        tie = true;
       }
     }
   }
-  const bool bp = dstar >= 0 && (tb < L.tc || (tb == L.tc && nb < L.gid));
+  uint32_t nb = dstar >= 0 ? 0u : 0xffffffffu;
+  if (tie || (dstar >= 0 && tb == L.tc)) {
+    // rare: resolve exact ties by region id
+    nb = 0xffffffffu;
+    dstar = -1;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const bool pend = ((L.hm[d] >> 8) & 0xFFu) < (L.hm[d] & 0xFFu);
+      if (pend && L.ht[d] == tb) {
+        const uint32_t nid = neighbour_id(a, gid, d);
+        if (nid < nb) {
+          dstar = d;
+          nb = nid;
+        }
+      }
+    }
+  }
+  const bool bp = dstar >= 0 && (tb < L.tc || (tb == L.tc && nb < gid));
   const bool ev = !bp && L.tc < a.t_w;
   if (!bp && !ev) return false;
   if (ev) {
@@ -431,7 +577,7 @@ __device__ __forceinline__ bool lane_step(const KArgs& a, Lane<G>& L, unsigned& 
     {
       Classes<G> C;
       C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
-      site = select_site<G>(C, a.rate, L.V, L.lam);
+      site = select_site<G>(C, PT, a.rate, L.V, L.lam);
     }
     L.spins ^= G::ONE << site;
     const int sr = site / BX, sc = site - sr * BX;
@@ -440,12 +586,11 @@ __device__ __forceinline__ bool lane_step(const KArgs& a, Lane<G>& L, unsigned& 
     if (LOG) {
       const unsigned long long o = a.log_off[L.idx] + L.n_ev;
       a.log_t[o] = L.tc;
-      a.log_region[o] = L.gid;
+      a.log_region[o] = gid;
       a.log_site[o] = (uint16_t)site;
     } else {
-      // own boundary history; an edge history is
-      // written only once it diverges from its latest version
-      const int r = L.idx / a.RX;
+      // own boundary history, written to the free slot;
+      // compared with the latest one when the region finishes
       bool on_edge = false;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -456,39 +601,16 @@ __device__ __forceinline__ bool lane_step(const KArgs& a, Lane<G>& L, unsigned& 
         if (!on) continue;
         on_edge = true;
         const unsigned k = L.om[e] & 0xFFu;
-        const unsigned pc = (L.om[e] >> 8) & 0xFFu;
-        const unsigned ps = (L.om[e] >> 16) & 1u;
-        bool dve = (L.om[e] >> 17) & 1u;
-        const uint8_t p = (uint8_t)(e < 2 ? sc : sr);
         if ((int)k < a.K) {
-          const unsigned base = (unsigned)((long long)e * a.tstride + ((long long)r * a.K) * a.RX + c);
-          const EdgeView& Pold = ps ? a.ed[1] : a.ed[0];
-          const EdgeView& Pnew = ps ? a.ed[0] : a.ed[1];
-          bool same = false;
-          if (!dve && k < pc) {
-            ++n_cmp;
-            const unsigned o = base + k * (unsigned)a.RX;
-            same = __double_as_longlong(Pold.t[o]) == __double_as_longlong(L.tc) && Pold.pos[o] == p;
-          }
-          if (!same) {
-            if (!dve) {  // copy the agreeing prefix into the new slot
-              for (unsigned q = 0; q < k; ++q) {
-                const unsigned o = base + q * (unsigned)a.RX;
-                Pnew.t[o] = Pold.t[o];
-                Pnew.pos[o] = Pold.pos[o];
-              }
-              dve = true;
-            }
-            const unsigned o = base + k * (unsigned)a.RX;
-            Pnew.t[o] = L.tc;
-            Pnew.pos[o] = p;
-            ++n_out;
-          }
+          const unsigned o = (unsigned)(e * a.tstride) + L.obase + k * (unsigned)a.RX;
+          const EdgeView& Pnew = ((L.om[e] >> 16) & 1u) ? a.ed[0] : a.ed[1];
+          Pnew.t[o] = L.tc;
+          Pnew.pos[o] = (uint8_t)(e < 2 ? sc : sr);
+          ++n_out;
         } else {
           overflow = true;
         }
-        const unsigned kk = k < 255u ? k + 1 : 255u;
-        L.om[e] = kk | (pc << 8) | (ps << 16) | ((unsigned)dve << 17);
+        if (k < 255u) L.om[e] += 1u;
       }
       L.bev += on_edge ? 1u : 0u;
     }
@@ -508,14 +630,17 @@ __device__ __forceinline__ bool lane_step(const KArgs& a, Lane<G>& L, unsigned& 
       else if (d == EDGE_W) L.gW ^= G::ONE << (p * BX);
       else L.gE ^= G::ONE << (p * BX + BX - 1);
       const unsigned nx = ((L.hm[d] >> 8) & 0xFFu) + 1;
-      const unsigned src = L.hm[d] >> 24;
       unsigned pos = 0;
       if (nx < (L.hm[d] & 0xFFu)) {
-        const double* T = src == 0 ? a.ed[0].t : src == 1 ? a.ed[1].t : src == 2 ? a.gh_up.t : a.gh_down.t;
-        const uint8_t* P = src == 0 ? a.ed[0].pos : src == 1 ? a.ed[1].pos : src == 2 ? a.gh_up.pos : a.gh_down.pos;
-        const unsigned off = L.hoff[d] + nx * (unsigned)a.RX;
-        L.ht[d] = T[off];
-        pos = P[off];
+        if (L.hm[d] & (1u << 28)) {
+          L.ht[d] = S.t[d][nx][lane];
+          pos = S.p[d][nx][lane];
+        } else {
+          const unsigned src = (L.hm[d] >> 24) & 3u;
+          const unsigned off = in_off(a, L.idx, d, src) + nx * (unsigned)a.RX;
+          L.ht[d] = src_t(a, src)[off];
+          pos = src_p(a, src)[off];
+        }
       }
       L.hm[d] = (L.hm[d] & 0xFF0000FFu) | (nx << 8) | (pos << 16);
     }
@@ -523,55 +648,54 @@ __device__ __forceinline__ bool lane_step(const KArgs& a, Lane<G>& L, unsigned& 
   {
     Classes<G> C;
     C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
-    L.lam = fold_lambda<G>(C, a.rate);
+    L.lam = fold_lambda<G>(C, PT);
   }
   if (ev) {
     // next pair of the list; the unused remainder carries over
     ++L.n;
     double U;
-    draw_pair(a.seed, L.gid, L.n, U, L.V);
+    draw_pair(a.seed, gid, L.n, U, L.V);
     L.R = expvar(U);
   }
   L.tc = cand_time(L.ts, L.R, L.lam);
   return true;
 }
 
+// Publish a finished region: diff its new edge histories against the latest
+// ones (statement (c)), flip the changed edges' slots in a new
+// selector word, mark the neighbours across changed edges dirty, and write
+// the tentative end-of-window state.
 template <class G>
-__device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& changed, bool& overflow) {
+__device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, unsigned& n_cmp, bool& changed,
+                                            bool& overflow) {
   const int idx = L.idx;
   const int r = idx / a.RX, c = idx - r * a.RX;
   const unsigned K = a.it_K;
   unsigned chmask = 0;
-  unsigned long long word = L.vown & 0xFFFFFFFFull;
+  unsigned long long word = 0;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const unsigned oc = L.om[e] & 0xFFu, pc = (L.om[e] >> 8) & 0xFFu, ps = (L.om[e] >> 16) & 1u;
-    bool dve = (L.om[e] >> 17) & 1u;
     if ((int)oc > a.K) overflow = true;
-    const EdgeView& Pold = ps ? a.ed[1] : a.ed[0];
-    const EdgeView& Pnew = ps ? a.ed[0] : a.ed[1];
-    if (!dve && oc != pc) {
-      // new history is a strict prefix of the latest one: copy it over
+    bool diff = oc != pc;
+    if (!diff && oc > 0) {
+      const EdgeView& Pold = ps ? a.ed[1] : a.ed[0];
+      const EdgeView& Pnew = ps ? a.ed[0] : a.ed[1];
       const unsigned base = (unsigned)((long long)e * a.tstride + ((long long)r * a.K) * a.RX + c);
-      for (unsigned q = 0; q < oc && (int)q < a.K; ++q) {
+      for (unsigned q = 0; q < oc; ++q) {
         const unsigned o = base + q * (unsigned)a.RX;
-        Pnew.t[o] = Pold.t[o];
-        Pnew.pos[o] = Pold.pos[o];
+        diff |= __double_as_longlong(Pold.t[o]) != __double_as_longlong(Pnew.t[o]) || Pold.pos[o] != Pnew.pos[o];
       }
-      dve = true;
+      n_cmp += oc;
     }
-    if (dve) {
-      chmask |= 1u << e;
-      const unsigned nc = (int)oc < a.K ? oc : (unsigned)a.K;
-      word = (word & ~((unsigned long long)CNT_MAX << (4 + CNT_BITS * e))) |
-             ((unsigned long long)nc << (4 + CNT_BITS * e));
-    }
+    const unsigned slot = diff ? ps ^ 1u : ps;
+    const unsigned cnt = diff ? ((int)oc < a.K ? oc : (unsigned)a.K) : pc;
+    chmask |= (diff ? 1u : 0u) << e;
+    word |= ((unsigned long long)slot << e) | ((unsigned long long)cnt << (4 + CNT_BITS * e));
   }
   if (chmask) {
     changed = true;
-    // new word: changed edges move to the other slot with their new counts
-    word = ((unsigned long long)K << 32) | ((word & 0xFFFFFFF0ull) | ((word ^ chmask) & 0xFull));
-    a.sel[2 * (long long)idx + L.whalf] = word;
+    a.sel[2 * (long long)idx + L.whalf] = ((unsigned long long)K << 32) | word;
     // neighbours across changed edges must be recomputed next iteration
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -592,12 +716,15 @@ __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& ch
 }
 
 template <int BX, int BY, bool LOG>
-__global__ void __launch_bounds__(128) region_kernel(const KArgs a) {
+__global__ void __launch_bounds__(NT) region_kernel(const KArgs a) {
   using G = Geo<BX, BY>;
   __shared__ unsigned q_next;
+  __shared__ Stage S;
+  __shared__ ProdTable<G> PT;
   const int tile_begin = blockIdx.x * a.tile;
   const int tile_n = min(a.tile, a.n_work - tile_begin);
   if (threadIdx.x == 0) q_next = blockDim.x;  // the first blockDim items are taken statically
+  fill_prod<G>(PT, a.rate);
   __syncthreads();
 
   unsigned n_ev = 0, n_out = 0, n_in = 0, n_cmp = 0, n_bev = 0, n_reg = 0;
@@ -608,13 +735,13 @@ __global__ void __launch_bounds__(128) region_kernel(const KArgs a) {
   // together, so the (memory-heavy) load/publish path runs converged.
   constexpr int REFILL = 12;
   bool active = false, pending = false, exhausted = false;
-  int item = threadIdx.x;  // the first blockDim items are taken statically
+  int item = threadIdx.x;
   for (;;) {
     const unsigned idle = __ballot_sync(0xffffffffu, !active);
     if (__popc(idle) >= REFILL || idle == 0xffffffffu) {
       if (!active) {
         if (pending) {
-          if (!LOG) lane_finish<G>(a, L, changed, overflow);
+          if (!LOG) lane_finish<G>(a, L, n_cmp, changed, overflow);
           n_ev += L.n_ev;
           n_bev = max(n_bev, L.bev);
           pending = false;
@@ -623,7 +750,7 @@ __global__ void __launch_bounds__(128) region_kernel(const KArgs a) {
           if (item < 0) item = (int)atomicAdd(&q_next, 1u);
           if (item < tile_n) {
             const int idx = a.wl_in ? (int)a.wl_in[tile_begin + item] : tile_begin + item;
-            lane_load<G, LOG>(a, L, idx);
+            lane_load<G, LOG>(a, L, idx, S, PT);
             n_in += (L.hm[0] & 0xFFu) + (L.hm[1] & 0xFFu) + (L.hm[2] & 0xFFu) + (L.hm[3] & 0xFFu);
             ++n_reg;
             active = pending = true;
@@ -635,7 +762,7 @@ __global__ void __launch_bounds__(128) region_kernel(const KArgs a) {
       }
       if (__all_sync(0xffffffffu, exhausted && !active)) break;
     }
-    if (active && !lane_step<G, LOG>(a, L, n_out, n_cmp, overflow)) active = false;
+    if (active && !lane_step<G, LOG>(a, L, S, PT, n_out, overflow)) active = false;
   }
 
   if (!LOG) {
