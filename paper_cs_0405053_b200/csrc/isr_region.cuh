@@ -339,16 +339,20 @@ __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000
 // longer idles while its slowest region finishes (region histories have
 // Poisson-distributed lengths).
 // ---------------------------------------------------------------------------
-// Per-lane shared-memory stage of the incoming histories: up to CI entries
-// per direction are copied global -> shared with cp.async when a region is
-// loaded (one memory latency per refill batch, many loads in flight), so
-// the break-point merge inside the step loop reads shared memory only.
+// Per-lane shared-memory stage of the histories a region reads: up to CI
+// entries of each incoming direction and of each of its own latest edge
+// histories are copied global -> shared with cp.async when the region is
+// loaded (one memory latency per refill batch, many loads in flight).  The
+// break-point merge and the diff against the latest own history then read
+// shared memory only.
 constexpr int NT = 128;  // threads per block of K1
-constexpr int CI = 4;    // staged entries per incoming direction
+constexpr int CI = 3;    // staged entries per history
 
 struct Stage {
-  double t[4][CI][NT];
-  uint32_t p[4][CI][NT];  // 4-byte word holding the position byte, then the byte itself
+  double in_t[4][CI][NT];
+  uint32_t in_p[4][CI][NT];   // 4-byte word holding the position byte, then the byte itself
+  double own_t[4][CI][NT];
+  uint32_t own_p[4][CI][NT];
 };
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -377,17 +381,13 @@ struct Lane {
   // (source 0/1 = slot, 2/3 = ghost row above/below; bit 28 = staged in smem)
   unsigned hm[4];
   double ht[4];
-  // own edges: new count | latest count << 8 | latest slot << 16
+  // own edges: new count | latest count << 8 | latest slot << 16 |
+  // diverged << 17 | latest staged in smem << 18
   unsigned om[4];
   int whalf;      // selector word to overwrite on change
   unsigned n_ev;  // events of this region (log offset)
   unsigned bev;   // own boundary events of this region
 };
-
-__device__ __forceinline__ uint32_t region_gid(const KArgs& a, int idx) {
-  const int r = idx / a.RX, c = idx - r * a.RX;
-  return (uint32_t)((a.row0 + r) * a.RX + c);
-}
 
 // element offset of entry 0 of the history that direction d reads
 __device__ __forceinline__ unsigned in_off(const KArgs& a, int idx, int d, unsigned src) {
@@ -442,6 +442,15 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
       }
     }
   }
+  // own latest histories: slot and count per edge
+  unsigned long long vown = 0ull;
+  L.whalf = 0;
+  if (!LOG) {
+    const int li = latest_index(wp_own, K);
+    const unsigned long long v = li ? wp_own.y : wp_own.x;
+    vown = word_valid(v, K0) ? v : (v & 0xFull);  // outside the window: slots only, counts 0
+    L.whalf = li ^ 1;                             // overwrite the older word
+  }
   // committed state (the old tau_m becomes tau_0)
   L.spins = (M)((const typename G::ST*)a.in.spins)[idx];
   expand_halo<G>((unsigned long long)((const typename G::HT*)a.in.halo)[idx], L.gN, L.gS, L.gW, L.gE);
@@ -449,7 +458,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   L.R = a.in.R[idx];
   L.n = a.in.n[idx];
   L.dig = a.digest ? a.in.dig[idx] : 0ull;
-  // stage the incoming histories (or, above CI entries, read them lazily)
+  // stage incoming histories (above CI entries: read lazily from global)
   bool staged_any = false;
 #pragma unroll
   for (int d = 0; d < 4; ++d) {
@@ -466,8 +475,8 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
         for (int q = 0; q < CI; ++q) {
           if (q < (int)cnt[d]) {
             const unsigned o = off + (unsigned)q * (unsigned)a.RX;
-            cp_async8(&S.t[d][q][lane], T + o);
-            cp_async4(&S.p[d][q][lane], P + (o & ~3u));
+            cp_async8(&S.in_t[d][q][lane], T + o);
+            cp_async4(&S.in_p[d][q][lane], P + (o & ~3u));
           }
         }
       } else {
@@ -477,6 +486,27 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
     }
     L.hm[d] = cnt[d] | (src[d] << 24) | flags;
   }
+  // stage own latest histories for the diff
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const unsigned pc = word_count(vown, e), ps = (unsigned)word_slot(vown, e);
+    unsigned st = 0;
+    if (!LOG && pc > 0 && pc <= (unsigned)CI) {
+      st = 1;
+      staged_any = true;
+      const EdgeView& E = ps ? a.ed[1] : a.ed[0];
+      const unsigned base = (unsigned)(e * a.tstride) + L.obase;
+#pragma unroll
+      for (int q = 0; q < CI; ++q) {
+        if (q < (int)pc) {
+          const unsigned o = base + (unsigned)q * (unsigned)a.RX;
+          cp_async8(&S.own_t[e][q][lane], E.t + o);
+          cp_async4(&S.own_p[e][q][lane], E.pos + (o & ~3u));
+        }
+      }
+    }
+    L.om[e] = (pc << 8) | (ps << 16) | (st << 18);
+  }
   if (staged_any) {
     cp_async_wait_all();
 #pragma unroll
@@ -485,26 +515,25 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
       const unsigned off = in_off(a, idx, d, src[d]);
 #pragma unroll
       for (int q = 0; q < CI; ++q)
-        if (q < (int)cnt[d]) {
+        if (q < (int)(L.hm[d] & 0xFFu)) {
           const unsigned o = off + (unsigned)q * (unsigned)a.RX;
-          S.p[d][q][lane] = (S.p[d][q][lane] >> (8u * (o & 3u))) & 0xFFu;
+          S.in_p[d][q][lane] = (S.in_p[d][q][lane] >> (8u * (o & 3u))) & 0xFFu;
         }
-      L.ht[d] = S.t[d][0][lane];
-      L.hm[d] |= S.p[d][0][lane] << 16;
+      L.ht[d] = S.in_t[d][0][lane];
+      L.hm[d] |= S.in_p[d][0][lane] << 16;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (!((L.om[e] >> 18) & 1u)) continue;
+      const unsigned base = (unsigned)(e * a.tstride) + L.obase;
+#pragma unroll
+      for (int q = 0; q < CI; ++q)
+        if (q < (int)((L.om[e] >> 8) & 0xFFu)) {
+          const unsigned o = base + (unsigned)q * (unsigned)a.RX;
+          S.own_p[e][q][lane] = (S.own_p[e][q][lane] >> (8u * (o & 3u))) & 0xFFu;
+        }
     }
   }
-  // own latest histories: slot and count per edge (fused diff at finish)
-  unsigned long long vown = 0ull;
-  L.whalf = 0;
-  if (!LOG) {
-    const int li = latest_index(wp_own, K);
-    const unsigned long long v = li ? wp_own.y : wp_own.x;
-    vown = word_valid(v, K0) ? v : (v & 0xFull);  // outside the window: slots only, counts 0
-    L.whalf = li ^ 1;                             // overwrite the older word
-  }
-#pragma unroll
-  for (int e = 0; e < 4; ++e)
-    L.om[e] = (word_count(vown, e) << 8) | ((unsigned)word_slot(vown, e) << 16);
   // pair n: U already spent into R (carried), V selects the next atom
   double U;
   draw_pair(a.seed, L.gid, L.n, U, L.V);
@@ -514,9 +543,6 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   L.tc = cand_time(L.ts, L.R, L.lam);
 }
 
-// One step of the region's history: the earliest of its own candidate event
-// and the pending break points.  Returns false when the region has reached
-// the window end.
 // neighbour id in direction d (only needed to order exactly equal times)
 __device__ __forceinline__ uint32_t neighbour_id(const KArgs& a, uint32_t gid, int d) {
   const int c = (int)(gid % (uint32_t)a.RX);
@@ -527,17 +553,13 @@ __device__ __forceinline__ uint32_t neighbour_id(const KArgs& a, uint32_t gid, i
                      : (uint32_t)(gr * a.RX + (c + 1) % a.RX);
 }
 
-template <class G, bool LOG>
-__device__ __forceinline__ bool lane_step(const KArgs& a, Lane<G>& L, const Stage& S, const ProdTable<G>& PT,
-                                          unsigned& n_out, bool& overflow) {
-  constexpr int BX = G::BX, BY = G::BY;
-  const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
-  const int lane = threadIdx.x;
-  const uint32_t gid = L.gid;
-  // earliest pending break point, (time, neighbour id) order (R10);
-  // ids are computed only for exactly equal times
+// Earliest pending break point that precedes the candidate event, in
+// (time, region id) order (R10); ids only for exactly equal times.
+// Returns its direction or -1.
+template <class G>
+__device__ __forceinline__ int next_bp_before_event(const KArgs& a, const Lane<G>& L, double& tb) {
   int dstar = -1;
-  double tb = dinf();
+  tb = dinf();
   bool tie = false;
 #pragma unroll
   for (int d = 0; d < 4; ++d) {
@@ -551,123 +573,150 @@ __device__ __forceinline__ bool lane_step(const KArgs& a, Lane<G>& L, const Stag
       }
     }
   }
-  uint32_t nb = dstar >= 0 ? 0u : 0xffffffffu;
-  if (tie || (dstar >= 0 && tb == L.tc)) {
-    // rare: resolve exact ties by region id
-    nb = 0xffffffffu;
-    dstar = -1;
+  if (dstar < 0) return -1;
+  if (tb < L.tc && !tie) return dstar;
+  if (tb > L.tc) return -1;
+  // rare: equal times, resolve by region id
+  uint32_t nb = 0xffffffffu;
+  dstar = -1;
 #pragma unroll
-    for (int d = 0; d < 4; ++d) {
-      const bool pend = ((L.hm[d] >> 8) & 0xFFu) < (L.hm[d] & 0xFFu);
-      if (pend && L.ht[d] == tb) {
-        const uint32_t nid = neighbour_id(a, gid, d);
-        if (nid < nb) {
-          dstar = d;
-          nb = nid;
-        }
+  for (int d = 0; d < 4; ++d) {
+    const bool pend = ((L.hm[d] >> 8) & 0xFFu) < (L.hm[d] & 0xFFu);
+    if (pend && L.ht[d] == tb) {
+      const uint32_t nid = neighbour_id(a, L.gid, d);
+      if (nid < nb) {
+        dstar = d;
+        nb = nid;
       }
     }
   }
-  const bool bp = dstar >= 0 && (tb < L.tc || (tb == L.tc && nb < gid));
-  const bool ev = !bp && L.tc < a.t_w;
-  if (!bp && !ev) return false;
-  if (ev) {
-    // ---- own event at tc ----
-    int site;
-    {
-      Classes<G> C;
-      C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
-      site = select_site<G>(C, PT, a.rate, L.V, L.lam);
-    }
-    L.spins ^= G::ONE << site;
-    const int sr = site / BX, sc = site - sr * BX;
-    if (a.digest)
-      L.dig = mix64(mix64(L.dig ^ (unsigned long long)__double_as_longlong(L.tc)) ^ (unsigned long long)site);
-    if (LOG) {
-      const unsigned long long o = a.log_off[L.idx] + L.n_ev;
-      a.log_t[o] = L.tc;
-      a.log_region[o] = gid;
-      a.log_site[o] = (uint16_t)site;
-    } else {
-      // own boundary history, written to the free slot;
-      // compared with the latest one when the region finishes
-      bool on_edge = false;
+  return (tb < L.tc || nb < L.gid) ? dstar : -1;
+}
+
+// Break point at tb from direction dstar (eqs. lambdataua..newtau,
+// P:638-674): consume the budget at the old rate, flip the ghost spin,
+// advance the cursor, refold Lambda, new candidate.
+template <class G>
+__device__ __forceinline__ void lane_bp(const KArgs& a, Lane<G>& L, const Stage& S, const ProdTable<G>& PT, int dstar,
+                                        double tb) {
+  constexpr int BX = G::BX, BY = G::BY;
+  const int lane = threadIdx.x;
+  const double Rn = __dsub_rn(L.R, __dmul_rn(L.lam, __dsub_rn(tb, L.ts)));
+  L.R = Rn < 0.0 ? 0.0 : Rn;
+  L.ts = tb;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const bool on = e == EDGE_N ? (!wrapY && sr == 0)
-                      : e == EDGE_S ? (!wrapY && sr == BY - 1)
-                      : e == EDGE_W ? (!wrapX && sc == 0)
-                                    : (!wrapX && sc == BX - 1);
-        if (!on) continue;
-        on_edge = true;
-        const unsigned k = L.om[e] & 0xFFu;
-        if ((int)k < a.K) {
-          const unsigned o = (unsigned)(e * a.tstride) + L.obase + k * (unsigned)a.RX;
-          const EdgeView& Pnew = ((L.om[e] >> 16) & 1u) ? a.ed[0] : a.ed[1];
-          Pnew.t[o] = L.tc;
-          Pnew.pos[o] = (uint8_t)(e < 2 ? sc : sr);
-          ++n_out;
-        } else {
-          overflow = true;
-        }
-        if (k < 255u) L.om[e] += 1u;
+  for (int d = 0; d < 4; ++d) {
+    if (d != dstar) continue;
+    const int p = (int)((L.hm[d] >> 16) & 0xFFu);
+    if (d == EDGE_N) L.gN ^= G::ONE << p;
+    else if (d == EDGE_S) L.gS ^= G::ONE << ((BY - 1) * BX + p);
+    else if (d == EDGE_W) L.gW ^= G::ONE << (p * BX);
+    else L.gE ^= G::ONE << (p * BX + BX - 1);
+    const unsigned nx = ((L.hm[d] >> 8) & 0xFFu) + 1;
+    unsigned pos = 0;
+    if (nx < (L.hm[d] & 0xFFu)) {
+      if (L.hm[d] & (1u << 28)) {
+        L.ht[d] = S.in_t[d][nx][lane];
+        pos = S.in_p[d][nx][lane];
+      } else {
+        const unsigned src = (L.hm[d] >> 24) & 3u;
+        const unsigned off = in_off(a, L.idx, d, src) + nx * (unsigned)a.RX;
+        L.ht[d] = src_t(a, src)[off];
+        pos = src_p(a, src)[off];
       }
-      L.bev += on_edge ? 1u : 0u;
     }
-    ++L.n_ev;
-    L.ts = L.tc;
+    L.hm[d] = (L.hm[d] & 0xFF0000FFu) | (nx << 8) | (pos << 16);
+  }
+  Classes<G> C;
+  C.build(L.spins, L.gN, L.gS, L.gW, L.gE, a.RX == 1, a.RYg == 1);
+  L.lam = fold_lambda<G>(C, PT);
+  L.tc = cand_time(L.ts, L.R, L.lam);
+}
+
+// Own event at tc: select the atom, flip it, record it in the
+// boundary histories (diffed against the staged latest ones on the fly),
+// the digest or the log; draw the next pair of the list.
+template <class G, bool LOG>
+__device__ __forceinline__ void lane_event(const KArgs& a, Lane<G>& L, const Stage& S, const ProdTable<G>& PT,
+                                           unsigned& n_out, bool& overflow) {
+  constexpr int BX = G::BX, BY = G::BY;
+  const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
+  const int lane = threadIdx.x;
+  int site;
+  {
+    Classes<G> C;
+    C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
+    site = select_site<G>(C, PT, a.rate, L.V, L.lam);
+  }
+  L.spins ^= G::ONE << site;
+  const int sr = site / BX, sc = site - sr * BX;
+  if (a.digest)
+    L.dig = mix64(mix64(L.dig ^ (unsigned long long)__double_as_longlong(L.tc)) ^ (unsigned long long)site);
+  if (LOG) {
+    const unsigned long long o = a.log_off[L.idx] + L.n_ev;
+    a.log_t[o] = L.tc;
+    a.log_region[o] = L.gid;
+    a.log_site[o] = (uint16_t)site;
   } else {
-    // ---- break point at tb (eqs. lambdataua..newtau) ----
-    const double Rn = __dsub_rn(L.R, __dmul_rn(L.lam, __dsub_rn(tb, L.ts)));
-    L.R = Rn < 0.0 ? 0.0 : Rn;
-    L.ts = tb;
+    // own boundary history, written to the free slot
+    bool on_edge = false;
 #pragma unroll
-    for (int d = 0; d < 4; ++d) {
-      if (d != dstar) continue;
-      const int p = (int)((L.hm[d] >> 16) & 0xFFu);
-      if (d == EDGE_N) L.gN ^= G::ONE << p;
-      else if (d == EDGE_S) L.gS ^= G::ONE << ((BY - 1) * BX + p);
-      else if (d == EDGE_W) L.gW ^= G::ONE << (p * BX);
-      else L.gE ^= G::ONE << (p * BX + BX - 1);
-      const unsigned nx = ((L.hm[d] >> 8) & 0xFFu) + 1;
-      unsigned pos = 0;
-      if (nx < (L.hm[d] & 0xFFu)) {
-        if (L.hm[d] & (1u << 28)) {
-          L.ht[d] = S.t[d][nx][lane];
-          pos = S.p[d][nx][lane];
-        } else {
-          const unsigned src = (L.hm[d] >> 24) & 3u;
-          const unsigned off = in_off(a, L.idx, d, src) + nx * (unsigned)a.RX;
-          L.ht[d] = src_t(a, src)[off];
-          pos = src_p(a, src)[off];
+    for (int e = 0; e < 4; ++e) {
+      const bool on = e == EDGE_N ? (!wrapY && sr == 0)
+                    : e == EDGE_S ? (!wrapY && sr == BY - 1)
+                    : e == EDGE_W ? (!wrapX && sc == 0)
+                                  : (!wrapX && sc == BX - 1);
+      if (!on) continue;
+      on_edge = true;
+      const unsigned k = L.om[e] & 0xFFu, pc = (L.om[e] >> 8) & 0xFFu;
+      const unsigned ps = (L.om[e] >> 16) & 1u;
+      const uint8_t p = (uint8_t)(e < 2 ? sc : sr);
+      unsigned dv = (L.om[e] >> 17) & 1u;
+      if ((int)k < a.K) {
+        const unsigned o = (unsigned)(e * a.tstride) + L.obase + k * (unsigned)a.RX;
+        const EdgeView& Pnew = ps ? a.ed[0] : a.ed[1];
+        Pnew.t[o] = L.tc;
+        Pnew.pos[o] = p;
+        ++n_out;
+        if (!dv) {
+          if (k >= pc) {
+            dv = 1;
+          } else if ((L.om[e] >> 18) & 1u) {
+            dv = (__double_as_longlong(S.own_t[e][k][lane]) != __double_as_longlong(L.tc) ||
+                  S.own_p[e][k][lane] != p) ? 1u : 0u;
+          } else {
+            const EdgeView& Pold = ps ? a.ed[1] : a.ed[0];
+            dv = (__double_as_longlong(Pold.t[o]) != __double_as_longlong(L.tc) || Pold.pos[o] != p) ? 1u : 0u;
+          }
         }
+      } else {
+        overflow = true;
       }
-      L.hm[d] = (L.hm[d] & 0xFF0000FFu) | (nx << 8) | (pos << 16);
+      L.om[e] = (L.om[e] & ~((1u << 17) | 0xFFu)) | (dv << 17) | (k < 255u ? k + 1 : 255u);
     }
+    L.bev += on_edge ? 1u : 0u;
   }
+  ++L.n_ev;
+  L.ts = L.tc;
   {
     Classes<G> C;
     C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
     L.lam = fold_lambda<G>(C, PT);
   }
-  if (ev) {
-    // next pair of the list; the unused remainder carries over
-    ++L.n;
-    double U;
-    draw_pair(a.seed, gid, L.n, U, L.V);
-    L.R = expvar(U);
-  }
+  ++L.n;
+  double U;
+  draw_pair(a.seed, L.gid, L.n, U, L.V);
+  L.R = expvar(U);
   L.tc = cand_time(L.ts, L.R, L.lam);
-  return true;
 }
 
-// Publish a finished region: diff its new edge histories against the latest
-// ones (statement (c)), flip the changed edges' slots in a new
-// selector word, mark the neighbours across changed edges dirty, and write
-// the tentative end-of-window state.
+// Publish a finished region: an edge changed iff its history diverged from
+// the latest one or has a different length (statement (c));
+// changed edges move to the other slot in a new selector word, neighbours
+// across them are marked dirty, and the tentative end-of-window state is
+// written.
 template <class G>
-__device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, unsigned& n_cmp, bool& changed,
-                                            bool& overflow) {
+__device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& changed, bool& overflow) {
   const int idx = L.idx;
   const int r = idx / a.RX, c = idx - r * a.RX;
   const unsigned K = a.it_K;
@@ -677,17 +726,7 @@ __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, unsigned
   for (int e = 0; e < 4; ++e) {
     const unsigned oc = L.om[e] & 0xFFu, pc = (L.om[e] >> 8) & 0xFFu, ps = (L.om[e] >> 16) & 1u;
     if ((int)oc > a.K) overflow = true;
-    bool diff = oc != pc;
-    if (!diff && oc > 0) {
-      const EdgeView& Pold = ps ? a.ed[1] : a.ed[0];
-      const EdgeView& Pnew = ps ? a.ed[0] : a.ed[1];
-      const unsigned base = (unsigned)((long long)e * a.tstride + ((long long)r * a.K) * a.RX + c);
-      for (unsigned q = 0; q < oc; ++q) {
-        const unsigned o = base + q * (unsigned)a.RX;
-        diff |= __double_as_longlong(Pold.t[o]) != __double_as_longlong(Pnew.t[o]) || Pold.pos[o] != Pnew.pos[o];
-      }
-      n_cmp += oc;
-    }
+    const bool diff = ((L.om[e] >> 17) & 1u) || oc != pc;
     const unsigned slot = diff ? ps ^ 1u : ps;
     const unsigned cnt = diff ? ((int)oc < a.K ? oc : (unsigned)a.K) : pc;
     chmask |= (diff ? 1u : 0u) << e;
@@ -741,7 +780,7 @@ __global__ void __launch_bounds__(NT) region_kernel(const KArgs a) {
     if (__popc(idle) >= REFILL || idle == 0xffffffffu) {
       if (!active) {
         if (pending) {
-          if (!LOG) lane_finish<G>(a, L, n_cmp, changed, overflow);
+          if (!LOG) lane_finish<G>(a, L, changed, overflow);
           n_ev += L.n_ev;
           n_bev = max(n_bev, L.bev);
           pending = false;
@@ -752,6 +791,8 @@ __global__ void __launch_bounds__(NT) region_kernel(const KArgs a) {
             const int idx = a.wl_in ? (int)a.wl_in[tile_begin + item] : tile_begin + item;
             lane_load<G, LOG>(a, L, idx, S, PT);
             n_in += (L.hm[0] & 0xFFu) + (L.hm[1] & 0xFFu) + (L.hm[2] & 0xFFu) + (L.hm[3] & 0xFFu);
+            n_cmp += ((L.om[0] >> 8) & 0xFFu) + ((L.om[1] >> 8) & 0xFFu) + ((L.om[2] >> 8) & 0xFFu) +
+                     ((L.om[3] >> 8) & 0xFFu);  // latest own entries read for the diff
             ++n_reg;
             active = pending = true;
           } else {
@@ -762,7 +803,14 @@ __global__ void __launch_bounds__(NT) region_kernel(const KArgs a) {
       }
       if (__all_sync(0xffffffffu, exhausted && !active)) break;
     }
-    if (active && !lane_step<G, LOG>(a, L, S, PT, n_out, overflow)) active = false;
+    if (active) {
+      // drain the break points that precede the next event, then the event
+      double tb;
+      int d;
+      while ((d = next_bp_before_event<G>(a, L, tb)) >= 0) lane_bp<G>(a, L, S, PT, d, tb);
+      if (L.tc < a.t_w) lane_event<G, LOG>(a, L, S, PT, n_out, overflow);
+      else active = false;
+    }
   }
 
   if (!LOG) {
