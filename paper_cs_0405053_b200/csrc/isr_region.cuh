@@ -95,6 +95,7 @@ struct KArgs {
   const uint32_t* wl_in;   // regions to recompute (nullptr: all regions)
   int n_work;              // number of regions to recompute
   int tile;                // work items per block (lane-persistent scheduling)
+  int refill;              // idle lanes per warp that trigger a batched refill
   uint32_t* wl_out;        // worklist of the next iteration
   unsigned* wl_out_count;
   uint32_t* dirty;         // per region: last stamp it was queued for
@@ -381,6 +382,7 @@ struct Lane {
   // (source 0/1 = slot, 2/3 = ghost row above/below; bit 28 = staged in smem)
   unsigned hm[4];
   double ht[4];
+  unsigned hoff[4];  // element offset of entry 0 of each incoming history
   // own edges: new count | latest count << 8 | latest slot << 16 |
   // diverged << 17 | latest staged in smem << 18
   unsigned om[4];
@@ -390,8 +392,7 @@ struct Lane {
 };
 
 // element offset of entry 0 of the history that direction d reads
-__device__ __forceinline__ unsigned in_off(const KArgs& a, int idx, int d, unsigned src) {
-  const int r = idx / a.RX, c = idx - r * a.RX;
+__device__ __forceinline__ unsigned in_off(const KArgs& a, int r, int c, int d, unsigned src) {
   if (src >= 2) return (unsigned)c;
   const int nr = d == EDGE_N ? (r - 1 + a.RYl) % a.RYl : d == EDGE_S ? (r + 1) % a.RYl : r;
   const int nc = d == EDGE_W ? (c - 1 + a.RX) % a.RX : d == EDGE_E ? (c + 1) % a.RX : c;
@@ -463,9 +464,11 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
 #pragma unroll
   for (int d = 0; d < 4; ++d) {
     L.ht[d] = dinf();
+    L.hoff[d] = 0;
     unsigned flags = 0;
     if (cnt[d] > 0) {
-      const unsigned off = in_off(a, idx, d, src[d]);
+      const unsigned off = in_off(a, r, c, d, src[d]);
+      L.hoff[d] = off;
       const double* T = src_t(a, src[d]);
       const uint8_t* P = src_p(a, src[d]);
       if (cnt[d] <= (unsigned)CI) {
@@ -512,7 +515,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
       if (!(L.hm[d] & (1u << 28))) continue;
-      const unsigned off = in_off(a, idx, d, src[d]);
+      const unsigned off = L.hoff[d];
 #pragma unroll
       for (int q = 0; q < CI; ++q)
         if (q < (int)(L.hm[d] & 0xFFu)) {
@@ -620,7 +623,7 @@ __device__ __forceinline__ void lane_bp(const KArgs& a, Lane<G>& L, const Stage&
         pos = S.in_p[d][nx][lane];
       } else {
         const unsigned src = (L.hm[d] >> 24) & 3u;
-        const unsigned off = in_off(a, L.idx, d, src) + nx * (unsigned)a.RX;
+        const unsigned off = L.hoff[d] + nx * (unsigned)a.RX;
         L.ht[d] = src_t(a, src)[off];
         pos = src_p(a, src)[off];
       }
@@ -772,7 +775,7 @@ __global__ void __launch_bounds__(NT) region_kernel(const KArgs a) {
   // Refill in batches: lanes whose region reached the window end wait until
   // at least REFILL lanes of the warp are idle, then publish and reload
   // together, so the (memory-heavy) load/publish path runs converged.
-  constexpr int REFILL = 12;
+  const int REFILL = a.refill;
   bool active = false, pending = false, exhausted = false;
   int item = threadIdx.x;
   for (;;) {

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -195,6 +196,7 @@ struct ising_sr_ctx {
   double win_bytes = 0.0;
   int win_f = 0;
   long long launches = 0;
+  int refill = 24;  // K1 batched-refill threshold (env ISING_SR_REFILL for tuning)
   ising_sr_stats stats;
 };
 
@@ -323,6 +325,7 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   a.seed = c->cfg.seed;
   for (int k = 0; k < 10; ++k) a.rate[k] = c->cfg.rate[k];
   a.dirty = c->dirty;
+  a.refill = c->refill;
   a.flags = c->d_flags;
   a.stats = c->d_stats;
   return a;
@@ -541,6 +544,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   c->row0 = cfg->rank * c->RYl;
   c->nreg = c->RX * c->RYl;
   std::memset(&c->stats, 0, sizeof c->stats);
+  if (const char* e = std::getenv("ISING_SR_REFILL")) c->refill = std::max(1, std::min(32, std::atoi(e)));
 
   auto bail = [&](ising_sr_status s) {
     ising_sr_destroy(c);
