@@ -71,7 +71,7 @@ struct EdgeView {
 // A ghost row received from a neighbouring strip (world > 1):
 // cnt[RX], stamp[RX] (global iteration of the last change), t/pos[K][RX].
 struct GhostView {
-  uint8_t* cnt;
+  uint16_t* cnt;
   uint32_t* stamp;
   double* t;
   uint8_t* pos;
@@ -874,7 +874,7 @@ __global__ void pack_kernel(const KArgs a, GhostView send_up, GhostView send_dow
       g.pos[(long long)q * a.RX + c] = E.pos[base + (long long)q * a.RX];
     }
   }
-  g.cnt[c] = (uint8_t)cnt;
+  g.cnt[c] = (uint16_t)cnt;
   // changed in this iteration: the word was rewritten now and edge e moved
   // slot relative to the previous latest word (the other one)
   const unsigned long long other = latest_index(wp, a.it_K + 1) ? wp.x : wp.y;

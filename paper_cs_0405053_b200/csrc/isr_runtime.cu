@@ -18,6 +18,7 @@
 
 #include "../../include/ising_sr.h"
 #include "isr_region.cuh"
+#include "isr_warp.cuh"
 
 namespace {
 
@@ -33,11 +34,16 @@ constexpr int kThreads = 128;
 // ---------------------------------------------------------------------------
 struct ShapeOps {
   int bx, by;
+  bool warp;         // warp-per-region form (regions > 64 sites)
   size_t spin_bytes, halo_bytes;
+  int sel_words;     // selector words per region (2: packed per region; 8: pair per edge)
+  int cnt_max;       // largest history length the selector can record
+  double sel_read_bytes;  // selector bytes read per recomputation (own + neighbours)
   void (*region)(const KArgs&, int nreg, cudaStream_t);
   void (*replay)(const KArgs&, int nreg, cudaStream_t);
   void (*init)(const uint8_t*, int, int, int, int, unsigned long long, StateView, cudaStream_t);
   void (*unpack)(StateView, int, int, int, uint8_t*, cudaStream_t);
+  void (*pack)(const KArgs&, GhostView, GhostView, int RX, cudaStream_t);
 };
 
 template <int BX, int BY>
@@ -46,8 +52,12 @@ ShapeOps make_ops() {
   ShapeOps o;
   o.bx = BX;
   o.by = BY;
+  o.warp = false;
   o.spin_bytes = sizeof(typename G::ST);
   o.halo_bytes = sizeof(typename G::HT);
+  o.sel_words = 2;
+  o.cnt_max = isr::CNT_MAX;
+  o.sel_read_bytes = 5 * 16.0;
   o.region = [](const KArgs& a, int n, cudaStream_t s) {
     const int grid = (n + a.tile - 1) / a.tile;
     isr::region_kernel<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
@@ -65,12 +75,58 @@ ShapeOps make_ops() {
     const long long n = (long long)RYl * BY * Lx;
     isr::unpack_kernel<BX, BY><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(st, Lx, RX, RYl, out);
   };
+  o.pack = [](const KArgs& a, GhostView up, GhostView down, int RX, cudaStream_t s) {
+    isr::pack_kernel<<<(2 * RX + 127) / 128, 128, 0, s>>>(a, up, down);
+  };
+  return o;
+}
+
+template <int BX, int BY>
+ShapeOps make_ops_w() {
+  ShapeOps o;
+  o.bx = BX;
+  o.by = BY;
+  o.warp = true;
+  o.spin_bytes = (size_t)BY * 4;
+  o.halo_bytes = 16;
+  o.sel_words = 8;
+  o.cnt_max = 65535;
+  o.sel_read_bytes = 8 * 16.0;
+  auto launch = [](const KArgs& a, int n, cudaStream_t s, bool log) {
+    const int warps_per_block = kThreads / 32;
+    const int grid = std::max(1, std::min((n + warps_per_block - 1) / warps_per_block, 148 * 16));
+    if (log) isr::region_kernel_w<BX, BY, true><<<grid, kThreads, 0, s>>>(a);
+    else isr::region_kernel_w<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
+  };
+  o.region = [](const KArgs& a, int n, cudaStream_t s) {
+    const int grid = std::max(1, std::min((n + 3) / 4, 148 * 16));
+    isr::region_kernel_w<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
+  };
+  o.replay = [](const KArgs& a, int n, cudaStream_t s) {
+    const int grid = std::max(1, std::min((n + 3) / 4, 148 * 16));
+    isr::region_kernel_w<BX, BY, true><<<grid, kThreads, 0, s>>>(a);
+  };
+  (void)launch;
+  o.init = [](const uint8_t* buf, int Lx, int RX, int RYl, int row0, unsigned long long seed, StateView st,
+              cudaStream_t s) {
+    const int n = RX * RYl;
+    isr::init_kernel_w<BX, BY><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(buf, Lx, RX, RYl, row0, seed, st);
+  };
+  o.unpack = [](StateView st, int Lx, int RX, int RYl, uint8_t* out, cudaStream_t s) {
+    const long long n = (long long)RYl * BY * Lx;
+    isr::unpack_kernel_w<BX, BY><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(st, Lx, RX, RYl, out);
+  };
+  o.pack = [](const KArgs& a, GhostView up, GhostView down, int RX, cudaStream_t s) {
+    isr::pack_kernel_w<<<(2 * RX + 127) / 128, 128, 0, s>>>(a, up, down);
+  };
   return o;
 }
 
 const ShapeOps* find_ops(int bx, int by) {
-  static const ShapeOps table[] = {make_ops<1, 1>(), make_ops<2, 2>(), make_ops<4, 4>(), make_ops<8, 8>(),
-                                   make_ops<4, 2>(), make_ops<2, 4>(), make_ops<8, 4>(), make_ops<4, 8>()};
+  static const ShapeOps table[] = {make_ops<1, 1>(),    make_ops<2, 2>(),    make_ops<4, 4>(),    make_ops<8, 8>(),
+                                   make_ops<4, 2>(),    make_ops<2, 4>(),    make_ops<8, 4>(),    make_ops<4, 8>(),
+                                   make_ops_w<16, 16>(), make_ops_w<32, 32>(), make_ops_w<16, 32>(), make_ops_w<32, 16>(),
+                                   make_ops_w<16, 8>(),  make_ops_w<8, 16>()};
   for (const auto& o : table)
     if (o.bx == bx && o.by == by) return &o;
   return nullptr;
@@ -253,7 +309,7 @@ ising_sr_status alloc_edges(ising_sr_ctx* c, int K) {
   if (c->cfg.world > 1) {
     const size_t RX = (size_t)c->RX;
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
-    c->gchunk[0] = RX;
+    c->gchunk[0] = RX * 2;
     c->gchunk[1] = RX * 4;
     c->gchunk[2] = RX * (size_t)K * 8;
     c->gchunk[3] = RX * (size_t)K;
@@ -267,7 +323,7 @@ ising_sr_status alloc_edges(ising_sr_ctx* c, int K) {
     GhostView* views[4] = {&c->gsend[0], &c->gsend[1], &c->grecv[0], &c->grecv[1]};
     for (int i = 0; i < 4; ++i) {
       char* b = (char*)c->gbuf + i * one;
-      views[i]->cnt = (uint8_t*)b;
+      views[i]->cnt = (uint16_t*)b;
       b += al(c->gchunk[0]);
       views[i]->stamp = (uint32_t*)b;
       b += al(c->gchunk[1]);
@@ -279,14 +335,14 @@ ising_sr_status alloc_edges(ising_sr_ctx* c, int K) {
   return ISING_SR_OK;
 }
 
-int auto_capacity(const ising_sr_config& cfg) {
+int auto_capacity(const ising_sr_config& cfg, int cnt_max) {
   // expected boundary events per edge per window at the largest rate, with a
   // generous Poisson tail margin; overflow is detected and retried anyway
   double rmax = 0.0;
   for (double r : cfg.rate) rmax = std::max(rmax, r);
   const double mu = std::max(cfg.bx, cfg.by) * rmax * cfg.W;
   const int K = (int)std::ceil(mu + 6.0 * std::sqrt(mu) + 8.0);
-  return std::min(std::max(K, 8), isr::CNT_MAX);
+  return std::min(std::max(K, 8), cnt_max);
 }
 
 ising_sr_status check(const ising_sr_ctx* c) {
@@ -339,7 +395,7 @@ double iteration_bytes(const ising_sr_ctx* c, const unsigned long long* s) {
   const double S = (double)c->ops->spin_bytes + (double)c->ops->halo_bytes + 8 + 8 + 4 +
                    ((c->cfg.flags & ISING_SR_FLAG_DIGEST) ? 8 : 0);
   const double regions = (double)s[5];
-  return regions * (2.0 * S + 5 * 16.0 + 8.0) + 9.0 * ((double)s[1] + (double)s[2] + (double)s[3]);
+  return regions * (2.0 * S + c->ops->sel_read_bytes + 8.0) + 9.0 * ((double)s[1] + (double)s[2] + (double)s[3]);
 }
 
 ising_sr_status compact_worklist(ising_sr_ctx* c) {
@@ -373,7 +429,7 @@ ising_sr_status launch_iteration(ising_sr_ctx* c) {
   }
   CK(c, cudaEventRecord(c->kev1, c->stream));
   if (c->cfg.world > 1) {
-    isr::pack_kernel<<<(2 * c->RX + 127) / 128, 128, 0, c->stream>>>(a, c->gsend[0], c->gsend[1]);
+    c->ops->pack(a, c->gsend[0], c->gsend[1], c->RX, c->stream);
     ++c->launches;
     CK(c, cudaGetLastError());
   } else {
@@ -433,8 +489,8 @@ void fill_halo(ising_sr_ctx* c, ising_sr_halo* h) {
 }
 
 ising_sr_status grow_capacity(ising_sr_ctx* c) {
-  if (c->K >= isr::CNT_MAX) return ISING_SR_E_CAPACITY;
-  const int K = std::min(isr::CNT_MAX, c->K * 2);
+  if (c->K >= c->ops->cnt_max) return ISING_SR_E_CAPACITY;
+  const int K = std::min(c->ops->cnt_max, c->K * 2);
   ising_sr_status s = alloc_edges(c, K);
   if (s != ISING_SR_OK) return s;
   c->stats.overflow_retries++;
@@ -564,7 +620,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
         dmalloc(&s.R, n) != cudaSuccess || dmalloc(&s.n, n) != cudaSuccess || dmalloc(&s.dig, n) != cudaSuccess)
       return bail(ISING_SR_E_OOM);
   }
-  if (dmalloc(&c->sel, 2 * n) != cudaSuccess || dmalloc(&c->dirty, n) != cudaSuccess ||
+  if (dmalloc(&c->sel, (size_t)ops->sel_words * n) != cudaSuccess || dmalloc(&c->dirty, n) != cudaSuccess ||
       dmalloc(&c->wl[0], n) != cudaSuccess || dmalloc(&c->wl[1], n) != cudaSuccess ||
       dmalloc(&c->d_wlc, 2) != cudaSuccess || dmalloc(&c->d_flags, 4) != cudaSuccess ||
       dmalloc(&c->d_stats, 8) != cudaSuccess ||
@@ -574,13 +630,13 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
       dmalloc(&c->d_off, n) != cudaSuccess || dmalloc(&c->d_bsum, (n + kThreads - 1) / kThreads) != cudaSuccess ||
       dmalloc(&c->d_total, 1) != cudaSuccess)
     return bail(ISING_SR_E_OOM);
-  if (cudaMemsetAsync(c->sel, 0, n * 16, c->stream) != cudaSuccess ||
+  if (cudaMemsetAsync(c->sel, 0, n * 8 * (size_t)ops->sel_words, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->dirty, 0, n * 4, c->stream) != cudaSuccess)
     return bail(ISING_SR_E_CUDA);
   if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
       cudaEventCreate(&c->kev0) != cudaSuccess || cudaEventCreate(&c->kev1) != cudaSuccess)
     return bail(ISING_SR_E_CUDA);
-  const int K0 = cfg->hist_capacity > 0 ? std::min(cfg->hist_capacity, isr::CNT_MAX) : auto_capacity(*cfg);
+  const int K0 = cfg->hist_capacity > 0 ? std::min(cfg->hist_capacity, ops->cnt_max) : auto_capacity(*cfg, ops->cnt_max);
   ising_sr_status s = alloc_edges(c, K0);
   if (s != ISING_SR_OK) return bail(s);
   c->stats.hist_capacity = c->K;

@@ -173,3 +173,42 @@ def test_c4_full_lattice_prefix():
     assert np.array_equal(gpu["count"], ref["count"])
     assert np.array_equal(gpu["digest"], ref["digest"])
     assert np.array_equal(gpu["spins"], ref["spins"])
+
+
+# ---------------------------------------------------------------------------
+# warp-per-region form (regions of more than 64 sites: c3 16x16, c5 32x32)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("geom", [
+    # Lx, Ly, bx, by, T, H, W, t_end, init
+    (64, 64, 16, 16, 2.269, 0.0, 0.5, 3.0, "random"),
+    (64, 64, 32, 32, 4.0, 0.0, 1.0, 3.0, "random"),
+    (96, 64, 32, 32, 2.269, 0.0, 4.0, 8.0, "random"),
+    (64, 96, 16, 32, 1.0, 0.1, 2.0, 10.0, "random"),
+    (96, 48, 32, 16, 3.0, -0.2, 0.7, 4.0, "random"),
+    (32, 48, 16, 8, 2.0, 0.0, 0.6, 5.0, "random"),
+    (48, 32, 8, 16, 2.0, 0.0, 0.6, 5.0, "random"),
+    (32, 32, 32, 32, 2.0, 0.0, 1.0, 6.0, "random"),   # one region: wraps both ways, g == 1
+    (64, 32, 32, 32, 2.0, 0.0, 1.0, 6.0, "random"),   # two regions per row: W and E neighbour coincide
+])
+def test_warp_form_bit_exact(geom):
+    Lx, Ly, bx, by, T, H, W, t_end, init = geom
+    w = workloads.Workload("w", Lx, Ly, bx, by, T=T, H=H, W=W, t_end=t_end, init=init, seed=5)
+    ref, gpu = check_against_oracle(w)
+    if Lx == bx and Ly == by:
+        assert set(gpu["g"]) == {1}
+
+
+def test_c3_prefix_bit_exact():
+    """BASELINE config 3 at full size (4096^2, 16x16 regions, T=1, H=0.1,
+    W=2) on the prefix t < 4 (the bulk of its events)."""
+    w = workloads.get("c3", t_end=4.0)
+    check_against_oracle(w, logs=False)
+
+
+def test_c5_geometry_sample_bit_exact():
+    """c5 dynamics (H=0, 32x32 regions, T in {1, 2.269, 4}, W in {.25,1,4})
+    on a 512^2 lattice."""
+    for T in (1.0, 2.269, 4.0):
+        for W in (0.25, 4.0):
+            w = workloads.Workload("c5s", 512, 512, 32, 32, T=T, W=W, t_end=4.0, seed=1)
+            check_against_oracle(w, logs=False)
