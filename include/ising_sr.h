@@ -161,7 +161,8 @@ ising_sr_status ising_sr_get_events(ising_sr_ctx* ctx, double* t, uint32_t* regi
                                     int64_t cap, int64_t* n);
 
 /* Per own region (region-id order): digest chain over all committed events,
- * h <- mix64(mix64(h ^ tau_bits) ^ site) (requires FLAG_DIGEST), and the
+ * h <- (h ^ tau_bits) * 0x9E3779B97F4A7C15 + site + 1 mod 2^64 (requires
+ * FLAG_DIGEST; R27), and the
  * committed event count n.  Either pointer may be NULL. */
 ising_sr_status ising_sr_get_digests(ising_sr_ctx* ctx, uint64_t* digest, uint64_t* count);
 

@@ -103,10 +103,12 @@ uint64_t orc_mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+/* per-region digest chain (R27): h <- (h ^ tau_bits) * K + site + 1
+ * mod 2^64, K = 0x9E3779B97F4A7C15 (odd: a bijection of h) */
 static uint64_t digest_step(uint64_t h, double tau, uint32_t site) {
   uint64_t tb;
   memcpy(&tb, &tau, 8);
-  return orc_mix64(orc_mix64(h ^ tb) ^ (uint64_t)site);
+  return (h ^ tb) * 0x9E3779B97F4A7C15ULL + (uint64_t)site + 1u;
 }
 
 /* ------------------------------------------------------------------------ */

@@ -41,8 +41,8 @@ void orc_pair(uint64_t seed, uint32_t stream, uint64_t n, double* U, double* V);
  * the exponential variate of eq. nextau. */
 double orc_expvar(double U);
 
-/* 64-bit mixer used by the per-region digest chain:
- * h <- mix64(mix64(h ^ tau_bits) ^ site). */
+/* splitmix64 finalizer (kept for tests; the per-region digest chain is
+ * h <- (h ^ tau_bits) * 0x9E3779B97F4A7C15 + site + 1, R27). */
 uint64_t orc_mix64(uint64_t z);
 
 typedef struct {

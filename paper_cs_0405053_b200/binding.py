@@ -14,7 +14,7 @@ from typing import Callable, Dict, Optional, Sequence, Tuple
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libising_sr.so")
+LIB_PATH = os.environ.get("ISING_SR_LIB") or os.path.join(_PKG, "libising_sr.so")
 
 FLAG_LOG_EVENTS = 0x1
 FLAG_DIGEST = 0x2

@@ -9,6 +9,10 @@
 #pragma once
 #include <cstdint>
 
+#ifndef ISR_PHILOX_WIDE
+#define ISR_PHILOX_WIDE 0
+#endif
+
 namespace isr {
 
 // ---------------------------------------------------------------------------
@@ -23,15 +27,22 @@ struct U4 {
 __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    const uint32_t lo0 = 0xD2511F53u * c.x;
-    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x);
-    const uint32_t lo1 = 0xCD9E8D57u * c.z;
-    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z);
+#if ISR_PHILOX_WIDE
+    // one 32x32->64 multiply each (IMAD.WIDE.U32): hi and lo words together
+    const unsigned long long p0 = (unsigned long long)0xD2511F53u * c.x;
+    const unsigned long long p1 = (unsigned long long)0xCD9E8D57u * c.z;
     U4 n;
-    n.x = hi1 ^ c.y ^ k0;
-    n.y = lo1;
-    n.z = hi0 ^ c.w ^ k1;
-    n.w = lo0;
+    n.x = (uint32_t)(p1 >> 32) ^ c.y ^ k0;
+    n.y = (uint32_t)p1;
+    n.z = (uint32_t)(p0 >> 32) ^ c.w ^ k1;
+    n.w = (uint32_t)p0;
+#else
+    U4 n;
+    n.x = __umulhi(0xCD9E8D57u, c.z) ^ c.y ^ k0;
+    n.y = 0xCD9E8D57u * c.z;
+    n.z = __umulhi(0xD2511F53u, c.x) ^ c.w ^ k1;
+    n.w = 0xD2511F53u * c.x;
+#endif
     c = n;
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
@@ -96,10 +107,22 @@ __device__ __forceinline__ double cand_time(double t, double R, double lam) {
   return tau == t ? __longlong_as_double(__double_as_longlong(t) + 1) : tau;
 }
 
-__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+// Per-region event digest step (R27): h <- (h ^ tau_bits) * K + site + 1,
+// a bijection of h for fixed (tau, site), so a difference in any event of a
+// sequence survives to the final digest.
+#ifndef ISR_DIGEST_OLD
+#define ISR_DIGEST_OLD 0
+#endif
+__device__ __forceinline__ unsigned long long mix64_(unsigned long long z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
   z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
   return z ^ (z >> 31);
+}
+__device__ __forceinline__ unsigned long long digest_step(unsigned long long h, double tau, int site) {
+#if ISR_DIGEST_OLD
+  return mix64_(mix64_(h ^ (unsigned long long)__double_as_longlong(tau)) ^ (unsigned long long)site);
+#endif
+  return (h ^ (unsigned long long)__double_as_longlong(tau)) * 0x9E3779B97F4A7C15ULL + (unsigned long long)(site + 1);
 }
 
 }  // namespace isr

@@ -95,6 +95,8 @@ struct KArgs {
   const uint32_t* wl_in;   // regions to recompute (nullptr: all regions)
   int n_work;              // number of regions to recompute
   int tile;                // work items per block (lane-persistent scheduling)
+  unsigned rx_M;           // idx / RX == (idx * rx_M) >> rx_k for idx < 2^31 (host-computed)
+  int rx_k;
   int refill;              // idle lanes per warp that trigger a batched refill
   uint32_t* wl_out;        // worklist of the next iteration
   unsigned* wl_out_count;
@@ -228,6 +230,13 @@ __device__ __forceinline__ int nth_bit(M x, int j) {
   return pos;
 }
 
+#if ISR_CSUM
+#define LAMBDA_FOLD(C, PT, S, lane) fold_lambda_cs<G>(C, PT, &S.csum[0][lane])
+#else
+#define LAMBDA_FOLD(C, PT, S, lane) fold_lambda<G>(C, PT)
+#endif
+constexpr int NT_CS = 128;  // column stride of the per-lane partial-sum table (= K1 block size)
+
 // Products fl(N * r_k) for N = 0..NS, one table per block in shared memory:
 // the fold below adds exactly the values __dmul_rn((double)N_k, r_k) would
 // give, so the result is bit-identical to multiplying in place.
@@ -252,6 +261,47 @@ __device__ __forceinline__ double fold_lambda(const Classes<G>& C, const ProdTab
 #pragma unroll
   for (int k = 0; k < 10; ++k) c = __dadd_rn(c, T.at(k, popc_m(C.mask(k))));
   return c;
+}
+
+// The same fold, also keeping the partial sums c_k (one column of a
+// per-lane shared-memory table) for the next atom selection.
+template <class G>
+__device__ __forceinline__ double fold_lambda_cs(const Classes<G>& C, const ProdTable<G>& T, double* cs) {
+  double c = 0.0;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    c = __dadd_rn(c, T.at(k, popc_m(C.mask(k))));
+    cs[k * NT_CS] = c;
+  }
+  return c;
+}
+
+// Phases 2-3 from the stored partial sums: k* = first k with x <= c_k by
+// binary search over the non-decreasing c_0..c_9 (c_9 = Lambda >= x).
+template <class G>
+__device__ __forceinline__ int select_site_cs(const Classes<G>& C, const double* cs, const double* rate, double V,
+                                              double lam) {
+  const double x = __dmul_rn(V, lam);
+  int lo = 0, hi = 9;
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int mid = (lo + hi) >> 1;
+    if (lo < hi) {
+      if (x <= cs[mid * NT_CS]) hi = mid;
+      else lo = mid + 1;
+    }
+  }
+  const int ks = lo;
+  const double cprev = ks > 0 ? cs[(ks - 1) * NT_CS] : 0.0;
+  const typename G::M mk = C.mask(ks);
+  const int nk = popc_m(mk);
+  const double aq = __dsub_rn(x, cprev);
+  const double rk = rate[ks];
+  const double q = rk == 1.0 ? aq : __ddiv_rn(aq, rk);  // aq / 1.0 == aq exactly
+  long long j = (long long)floor(q);
+  if (j > nk - 1) j = nk - 1;
+  if (j < 0) j = 0;
+  return nth_bit<typename G::M, G::NS>(mk, (int)j);
 }
 
 // Phases 2-3 of atom selection (eqs. Wsum, Wstop, nores, vindex)
@@ -324,6 +374,15 @@ __device__ __forceinline__ unsigned long long compress_halo(typename G::M gN, ty
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
+// region row of a shard-local index without an integer division
+__device__ __forceinline__ int div_rx(const KArgs& a, int idx) {
+#if ISR_MAGICDIV
+  return (int)(((unsigned long long)(unsigned)idx * a.rx_M) >> a.rx_k);
+#else
+  return idx / a.RX;
+#endif
+}
+
 // ---------------------------------------------------------------------------
 // K1: one relaxation iteration for the regions of the worklist (all regions
 // in the window's first iteration), or the commit-time replay that writes
@@ -346,14 +405,37 @@ __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000
 // loaded (one memory latency per refill batch, many loads in flight).  The
 // break-point merge and the diff against the latest own history then read
 // shared memory only.
-constexpr int NT = 128;  // threads per block of K1
-constexpr int CI = 3;    // staged entries per history
+#ifndef ISR_CI
+#define ISR_CI 3
+#endif
+#ifndef ISR_MINB
+#define ISR_MINB 0   // 0: no minimum-blocks hint (ptxas default register heuristics)
+#endif
+#if ISR_MINB > 0
+#define ISR_LAUNCH_BOUNDS __launch_bounds__(NT, ISR_MINB)
+#else
+#define ISR_LAUNCH_BOUNDS __launch_bounds__(NT)
+#endif
+#ifndef ISR_CSUM
+#define ISR_CSUM 0   // atom selection from the stored partial sums of the last fold
+#endif
+#ifndef ISR_MAGICDIV
+#define ISR_MAGICDIV 1
+#endif
+#ifndef ISR_BPCACHE
+#define ISR_BPCACHE 0  // cache the earliest pending break point
+#endif
+constexpr int NT = 128;      // threads per block of K1
+constexpr int CI = ISR_CI;   // staged entries per history
 
 struct Stage {
   double in_t[4][CI][NT];
   uint32_t in_p[4][CI][NT];   // 4-byte word holding the position byte, then the byte itself
   double own_t[4][CI][NT];
   uint32_t own_p[4][CI][NT];
+#if ISR_CSUM
+  double csum[10][NT];  // partial sums c_k of the last Lambda fold
+#endif
 };
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -383,6 +465,8 @@ struct Lane {
   unsigned hm[4];
   double ht[4];
   unsigned hoff[4];  // element offset of entry 0 of each incoming history
+  double tbn;        // earliest pending break-point time (cached)
+  int bdir;          // its direction, -1 if none; bit 8: another head has the same time
   // own edges: new count | latest count << 8 | latest slot << 16 |
   // diverged << 17 | latest staged in smem << 18
   unsigned om[4];
@@ -412,7 +496,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
   const unsigned K = a.it_K, K0 = a.it_K0;
   const int lane = threadIdx.x;
-  const int r = idx / a.RX, c = idx - r * a.RX;
+  const int r = div_rx(a, idx), c = idx - r * a.RX;
   L.idx = idx;
   L.gid = (uint32_t)((a.row0 + r) * a.RX + c);
   L.obase = (unsigned)(((long long)r * a.K) * a.RX + c);
@@ -542,8 +626,9 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   draw_pair(a.seed, L.gid, L.n, U, L.V);
   Classes<G> C;
   C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
-  L.lam = fold_lambda<G>(C, PT);
+  L.lam = LAMBDA_FOLD(C, PT, S, lane);
   L.tc = cand_time(L.ts, L.R, L.lam);
+  if (ISR_BPCACHE) refresh_bp(L);
 }
 
 // neighbour id in direction d (only needed to order exactly equal times)
@@ -560,7 +645,34 @@ __device__ __forceinline__ uint32_t neighbour_id(const KArgs& a, uint32_t gid, i
 // (time, region id) order (R10); ids only for exactly equal times.
 // Returns its direction or -1.
 template <class G>
+__device__ __forceinline__ void refresh_bp(Lane<G>& L) {
+  int dstar = -1;
+  double tb = dinf();
+  bool tie = false;
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    const bool pend = ((L.hm[d] >> 8) & 0xFFu) < (L.hm[d] & 0xFFu);
+    if (pend) {
+      if (L.ht[d] < tb) {
+        dstar = d;
+        tb = L.ht[d];
+      } else if (L.ht[d] == tb) {
+        tie = true;
+      }
+    }
+  }
+  L.tbn = tb;
+  L.bdir = dstar | (tie ? 0x100 : 0);
+}
+
+template <class G>
 __device__ __forceinline__ int next_bp_before_event(const KArgs& a, const Lane<G>& L, double& tb) {
+#if ISR_BPCACHE
+  int dstar = L.bdir & 0xFF;
+  tb = L.tbn;
+  const bool tie = (L.bdir & 0x100) != 0;
+  if (L.bdir < 0) return -1;
+#else
   int dstar = -1;
   tb = dinf();
   bool tie = false;
@@ -577,6 +689,7 @@ __device__ __forceinline__ int next_bp_before_event(const KArgs& a, const Lane<G
     }
   }
   if (dstar < 0) return -1;
+#endif
   if (tb < L.tc && !tie) return dstar;
   if (tb > L.tc) return -1;
   // rare: equal times, resolve by region id
@@ -600,7 +713,7 @@ __device__ __forceinline__ int next_bp_before_event(const KArgs& a, const Lane<G
 // P:638-674): consume the budget at the old rate, flip the ghost spin,
 // advance the cursor, refold Lambda, new candidate.
 template <class G>
-__device__ __forceinline__ void lane_bp(const KArgs& a, Lane<G>& L, const Stage& S, const ProdTable<G>& PT, int dstar,
+__device__ __forceinline__ void lane_bp(const KArgs& a, Lane<G>& L, Stage& S, const ProdTable<G>& PT, int dstar,
                                         double tb) {
   constexpr int BX = G::BX, BY = G::BY;
   const int lane = threadIdx.x;
@@ -632,15 +745,16 @@ __device__ __forceinline__ void lane_bp(const KArgs& a, Lane<G>& L, const Stage&
   }
   Classes<G> C;
   C.build(L.spins, L.gN, L.gS, L.gW, L.gE, a.RX == 1, a.RYg == 1);
-  L.lam = fold_lambda<G>(C, PT);
+  L.lam = LAMBDA_FOLD(C, PT, S, lane);
   L.tc = cand_time(L.ts, L.R, L.lam);
+  if (ISR_BPCACHE) refresh_bp(L);
 }
 
 // Own event at tc: select the atom, flip it, record it in the
 // boundary histories (diffed against the staged latest ones on the fly),
 // the digest or the log; draw the next pair of the list.
 template <class G, bool LOG>
-__device__ __forceinline__ void lane_event(const KArgs& a, Lane<G>& L, const Stage& S, const ProdTable<G>& PT,
+__device__ __forceinline__ void lane_event(const KArgs& a, Lane<G>& L, Stage& S, const ProdTable<G>& PT,
                                            unsigned& n_out, bool& overflow) {
   constexpr int BX = G::BX, BY = G::BY;
   const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
@@ -649,12 +763,16 @@ __device__ __forceinline__ void lane_event(const KArgs& a, Lane<G>& L, const Sta
   {
     Classes<G> C;
     C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
+#if ISR_CSUM
+    site = select_site_cs<G>(C, &S.csum[0][lane], a.rate, L.V, L.lam);
+#else
     site = select_site<G>(C, PT, a.rate, L.V, L.lam);
+#endif
   }
   L.spins ^= G::ONE << site;
   const int sr = site / BX, sc = site - sr * BX;
   if (a.digest)
-    L.dig = mix64(mix64(L.dig ^ (unsigned long long)__double_as_longlong(L.tc)) ^ (unsigned long long)site);
+    L.dig = digest_step(L.dig, L.tc, site);
   if (LOG) {
     const unsigned long long o = a.log_off[L.idx] + L.n_ev;
     a.log_t[o] = L.tc;
@@ -704,7 +822,7 @@ __device__ __forceinline__ void lane_event(const KArgs& a, Lane<G>& L, const Sta
   {
     Classes<G> C;
     C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
-    L.lam = fold_lambda<G>(C, PT);
+    L.lam = LAMBDA_FOLD(C, PT, S, lane);
   }
   ++L.n;
   double U;
@@ -721,7 +839,7 @@ __device__ __forceinline__ void lane_event(const KArgs& a, Lane<G>& L, const Sta
 template <class G>
 __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& changed, bool& overflow) {
   const int idx = L.idx;
-  const int r = idx / a.RX, c = idx - r * a.RX;
+  const int r = div_rx(a, idx), c = idx - r * a.RX;
   const unsigned K = a.it_K;
   unsigned chmask = 0;
   unsigned long long word = 0;
@@ -758,7 +876,7 @@ __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& ch
 }
 
 template <int BX, int BY, bool LOG>
-__global__ void __launch_bounds__(NT) region_kernel(const KArgs a) {
+__global__ void ISR_LAUNCH_BOUNDS region_kernel(const KArgs a) {
   using G = Geo<BX, BY>;
   __shared__ unsigned q_next;
   __shared__ Stage S;

@@ -382,6 +382,14 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   for (int k = 0; k < 10; ++k) a.rate[k] = c->cfg.rate[k];
   a.dirty = c->dirty;
   a.refill = c->refill;
+  {
+    // magic division by RX: k = 31 + ceil(log2 RX), M = ceil(2^k / RX) < 2^32;
+    // exact for every index below 2^31 (M * RX - 2^k < RX <= 2^(k - 31))
+    int l = 0;
+    while ((1ll << l) < c->RX) ++l;
+    a.rx_k = 31 + l;
+    a.rx_M = (unsigned)(((1ull << a.rx_k) + (unsigned long long)c->RX - 1) / (unsigned long long)c->RX);
+  }
   a.flags = c->d_flags;
   a.stats = c->d_stats;
   return a;

@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
         const int sr = site / BX, sc = site - sr * BX;
         if (lane == sr) row ^= 1u << sc;
         if (a.digest)
-          dig = mix64(mix64(dig ^ (unsigned long long)__double_as_longlong(tc)) ^ (unsigned long long)site);
+          dig = digest_step(dig, tc, site);
         if (LOG) {
           if (lane == 0) {
             const unsigned long long o = a.log_off[idx] + n_ev_r;
