@@ -338,6 +338,45 @@ __device__ __forceinline__ int select_site(const Classes<G>& C, const ProdTable<
   return nth_bit<typename G::M, G::NS>(mk, (int)j);
 }
 
+// The same selection in one pass: the fold's partial sums are compared with
+// x as they are formed, and the class mask of k* is captured on the way (no
+// dynamically indexed class mask, no second scan).  Identical decisions.
+template <class G>
+__device__ __forceinline__ int select_site2(const Classes<G>& C, const ProdTable<G>& T, const double* rate,
+                                            double V, double lam) {
+  using M = typename G::M;
+  const double x = __dmul_rn(V, lam);
+  double c = 0.0, cprev = 0.0;
+  int ks = -1, lastnz = 0;
+  M mk = 0, mlast = C.mask(0);
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    const M m = C.mask(k);
+    const int nk = popc_m(m);
+    const double cn = __dadd_rn(c, T.at(k, nk));
+    const bool hit = ks < 0 && x <= cn;
+    ks = hit ? k : ks;
+    cprev = hit ? c : cprev;
+    mk = hit ? m : mk;
+    lastnz = nk > 0 ? k : lastnz;
+    mlast = nk > 0 ? m : mlast;
+    c = cn;
+  }
+  if (ks < 0) {  // unreachable for V < 1 (x <= Lambda = c_9)
+    ks = lastnz;
+    mk = mlast;
+    cprev = 0.0;
+  }
+  const int nk = popc_m(mk);
+  const double aq = __dsub_rn(x, cprev);
+  const double rk = rate[ks];
+  const double q = rk == 1.0 ? aq : __ddiv_rn(aq, rk);  // aq / 1.0 == aq exactly
+  long long j = __double2ll_rd(q);                         // floor
+  j = j > nk - 1 ? nk - 1 : j;
+  j = j < 0 ? 0 : j;
+  return nth_bit<M, G::NS>(mk, (int)j);
+}
+
 // Expand/compress the stored ghost bits (N[BX] S[BX] W[BY] E[BY]) to/from
 // site-position masks (bit of the in-region site adjacent to the ghost).
 template <class G>
@@ -371,6 +410,10 @@ __device__ __forceinline__ unsigned long long compress_halo(typename G::M gN, ty
   }
   return h;
 }
+
+// periodic neighbour row/column index without an integer division
+__device__ __forceinline__ int wdec(int v, int n) { return v == 0 ? n - 1 : v - 1; }
+__device__ __forceinline__ int winc(int v, int n) { return v == n - 1 ? 0 : v + 1; }
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
@@ -425,6 +468,19 @@ __device__ __forceinline__ int div_rx(const KArgs& a, int idx) {
 #ifndef ISR_BPCACHE
 #define ISR_BPCACHE 0  // cache the earliest pending break point
 #endif
+#ifndef ISR_SEL2
+#define ISR_SEL2 1     // one-pass atom selection (select_site2)
+#endif
+#ifndef ISR_HIST2
+#define ISR_HIST2 1    // per-axis (not per-edge) own-history writes
+#endif
+#ifndef ISR_BP2
+#define ISR_BP2 1      // branch-free break-point step, exhausted heads read as +inf
+#endif
+#ifndef ISR_UNIFIED
+#define ISR_UNIFIED 2  // 0: drain break points, then the event; 1: one step per round;
+                       // 2: one step per round sharing the refold/candidate code
+#endif
 constexpr int NT = 128;      // threads per block of K1
 constexpr int CI = ISR_CI;   // staged entries per history
 
@@ -478,8 +534,8 @@ struct Lane {
 // element offset of entry 0 of the history that direction d reads
 __device__ __forceinline__ unsigned in_off(const KArgs& a, int r, int c, int d, unsigned src) {
   if (src >= 2) return (unsigned)c;
-  const int nr = d == EDGE_N ? (r - 1 + a.RYl) % a.RYl : d == EDGE_S ? (r + 1) % a.RYl : r;
-  const int nc = d == EDGE_W ? (c - 1 + a.RX) % a.RX : d == EDGE_E ? (c + 1) % a.RX : c;
+  const int nr = d == EDGE_N ? wdec(r, a.RYl) : d == EDGE_S ? winc(r, a.RYl) : r;
+  const int nc = d == EDGE_W ? wdec(c, a.RX) : d == EDGE_E ? winc(c, a.RX) : c;
   return (unsigned)((long long)(d ^ 1) * a.tstride + ((long long)nr * a.K) * a.RX + nc);
 }
 
@@ -517,8 +573,8 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
       cnt[d] = (d == EDGE_N ? a.gh_up : a.gh_down).cnt[c];
       src[d] = d == EDGE_N ? 2u : 3u;
     } else {
-      const int nr = d == EDGE_N ? (r - 1 + a.RYl) % a.RYl : d == EDGE_S ? (r + 1) % a.RYl : r;
-      const int nc = d == EDGE_W ? (c - 1 + a.RX) % a.RX : d == EDGE_E ? (c + 1) % a.RX : c;
+      const int nr = d == EDGE_N ? wdec(r, a.RYl) : d == EDGE_S ? winc(r, a.RYl) : r;
+      const int nc = d == EDGE_W ? wdec(c, a.RX) : d == EDGE_E ? winc(c, a.RX) : c;
       const ulonglong2 wp = __ldcg(reinterpret_cast<const ulonglong2*>(a.sel) + ((long long)nr * a.RX + nc));
       const unsigned long long v = latest_word(wp, K);
       if (word_valid(v, K0)) {
@@ -637,8 +693,8 @@ __device__ __forceinline__ uint32_t neighbour_id(const KArgs& a, uint32_t gid, i
   const int gr = (int)(gid / (uint32_t)a.RX);
   return d == EDGE_N ? (uint32_t)(((gr - 1 + a.RYg) % a.RYg) * a.RX + c)
        : d == EDGE_S ? (uint32_t)(((gr + 1) % a.RYg) * a.RX + c)
-       : d == EDGE_W ? (uint32_t)(gr * a.RX + (c - 1 + a.RX) % a.RX)
-                     : (uint32_t)(gr * a.RX + (c + 1) % a.RX);
+       : d == EDGE_W ? (uint32_t)(gr * a.RX + wdec(c, a.RX))
+                     : (uint32_t)(gr * a.RX + winc(c, a.RX));
 }
 
 // Earliest pending break point that precedes the candidate event, in
@@ -861,8 +917,8 @@ __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& ch
     for (int e = 0; e < 4; ++e) {
       if (!((chmask >> e) & 1u)) continue;
       if (a.world > 1 && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
-      const int nr = e == EDGE_N ? (r - 1 + a.RYl) % a.RYl : e == EDGE_S ? (r + 1) % a.RYl : r;
-      const int nc = e == EDGE_W ? (c - 1 + a.RX) % a.RX : e == EDGE_E ? (c + 1) % a.RX : c;
+      const int nr = e == EDGE_N ? wdec(r, a.RYl) : e == EDGE_S ? winc(r, a.RYl) : r;
+      const int nc = e == EDGE_W ? wdec(c, a.RX) : e == EDGE_E ? winc(c, a.RX) : c;
       a.dirty[nr * a.RX + nc] = K + 1;  // same value from every writer: a plain store suffices
     }
   }
@@ -873,6 +929,182 @@ __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& ch
   a.out.R[idx] = L.R;
   a.out.n[idx] = L.n;
   if (a.digest) a.out.dig[idx] = L.dig;
+}
+
+
+// ---------------------------------------------------------------------------
+// Step variants (ISR_BP2 / ISR_HIST2 / ISR_UNIFIED): the same decisions and
+// IEEE operations as next_bp_before_event / lane_bp / lane_event above,
+// arranged so that lanes on different kinds of step share instructions.
+// An incoming head whose history is exhausted reads as +inf.
+// ---------------------------------------------------------------------------
+template <class G>
+__device__ __forceinline__ int next_bp2(const KArgs& a, const Lane<G>& L, double& tb) {
+  const double m01 = fmin(L.ht[0], L.ht[1]), m23 = fmin(L.ht[2], L.ht[3]);
+  tb = fmin(m01, m23);
+  if (!(tb <= L.tc) || tb == dinf()) return -1;
+  const int neq = (L.ht[0] == tb) + (L.ht[1] == tb) + (L.ht[2] == tb) + (L.ht[3] == tb);
+  const int dstar = L.ht[0] == tb ? 0 : L.ht[1] == tb ? 1 : L.ht[2] == tb ? 2 : 3;
+  if (tb < L.tc && neq == 1) return dstar;
+  // rare: equal times, resolve by region id (R10)
+  uint32_t nb = 0xffffffffu;
+  int dm = -1;
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    if (L.ht[d] == tb) {
+      const uint32_t nid = neighbour_id(a, L.gid, d);
+      if (nid < nb) {
+        dm = d;
+        nb = nid;
+      }
+    }
+  }
+  return (tb < L.tc || nb < L.gid) ? dm : -1;
+}
+
+// break point at tb from direction dstar, up to (not including) the refold
+template <class G>
+__device__ __forceinline__ void bp_pre2(const KArgs& a, Lane<G>& L, Stage& S, int dstar, double tb) {
+  constexpr int BX = G::BX, BY = G::BY;
+  using M = typename G::M;
+  const int lane = threadIdx.x;
+  const double Rn = __dsub_rn(L.R, __dmul_rn(L.lam, __dsub_rn(tb, L.ts)));
+  L.R = Rn < 0.0 ? 0.0 : Rn;
+  L.ts = tb;
+  const unsigned hmd = dstar == 0 ? L.hm[0] : dstar == 1 ? L.hm[1] : dstar == 2 ? L.hm[2] : L.hm[3];
+  const int p = (int)((hmd >> 16) & 0xFFu);
+  L.gN ^= dstar == EDGE_N ? (M)(G::ONE << p) : (M)0;
+  L.gS ^= dstar == EDGE_S ? (M)(G::ONE << ((BY - 1) * BX + p)) : (M)0;
+  L.gW ^= dstar == EDGE_W ? (M)(G::ONE << (p * BX)) : (M)0;
+  L.gE ^= dstar == EDGE_E ? (M)(G::ONE << (p * BX + BX - 1)) : (M)0;
+  const unsigned nx = ((hmd >> 8) & 0xFFu) + 1;
+  double tn = dinf();
+  unsigned pos = 0;
+  if (nx < (hmd & 0xFFu)) {
+    if (hmd & (1u << 28)) {
+      tn = S.in_t[dstar][nx][lane];
+      pos = S.in_p[dstar][nx][lane];
+    } else {
+      const unsigned src = (hmd >> 24) & 3u;
+      const unsigned hoff = dstar == 0 ? L.hoff[0] : dstar == 1 ? L.hoff[1] : dstar == 2 ? L.hoff[2] : L.hoff[3];
+      const unsigned off = hoff + nx * (unsigned)a.RX;
+      tn = src_t(a, src)[off];
+      pos = src_p(a, src)[off];
+    }
+  }
+  const unsigned hn = (hmd & 0xFF0000FFu) | (nx << 8) | (pos << 16);
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    L.hm[d] = d == dstar ? hn : L.hm[d];
+    L.ht[d] = d == dstar ? tn : L.ht[d];
+  }
+}
+
+// one own-history entry on edge e (EDGE_*), diffed against the latest one
+__device__ __forceinline__ unsigned hist_put(const KArgs& a, unsigned om, int e, unsigned obase, double tc, uint8_t p,
+                                             const Stage& S, unsigned& n_out, bool& overflow) {
+  const int lane = threadIdx.x;
+  const unsigned k = om & 0xFFu, pc = (om >> 8) & 0xFFu;
+  const unsigned ps = (om >> 16) & 1u;
+  unsigned dv = (om >> 17) & 1u;
+  if ((int)k < a.K) {
+    const unsigned o = (unsigned)(e * a.tstride) + obase + k * (unsigned)a.RX;
+    double* Tn = ps ? a.ed[0].t : a.ed[1].t;
+    uint8_t* Pn = ps ? a.ed[0].pos : a.ed[1].pos;
+    Tn[o] = tc;
+    Pn[o] = p;
+    ++n_out;
+    if (!dv) {
+      if (k >= pc) {
+        dv = 1;
+      } else if ((om >> 18) & 1u) {
+        dv = (__double_as_longlong(S.own_t[e][k][lane]) != __double_as_longlong(tc) || S.own_p[e][k][lane] != p)
+                 ? 1u : 0u;
+      } else {
+        const double* To = ps ? a.ed[1].t : a.ed[0].t;
+        const uint8_t* Po = ps ? a.ed[1].pos : a.ed[0].pos;
+        dv = (__double_as_longlong(To[o]) != __double_as_longlong(tc) || Po[o] != p) ? 1u : 0u;
+      }
+    }
+  } else {
+    overflow = true;
+  }
+  return (om & ~((1u << 17) | 0xFFu)) | (dv << 17) | (k < 255u ? k + 1 : 255u);
+}
+
+// own event at tc, up to (not including) the refold; draws the next pair
+template <class G, bool LOG>
+__device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, Stage& S, const ProdTable<G>& PT,
+                                        unsigned& n_out, bool& overflow) {
+  constexpr int BX = G::BX, BY = G::BY;
+  const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
+  int site;
+  {
+    Classes<G> C;
+    C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
+#if ISR_SEL2
+    site = select_site2<G>(C, PT, a.rate, L.V, L.lam);
+#else
+    site = select_site<G>(C, PT, a.rate, L.V, L.lam);
+#endif
+  }
+  L.spins ^= G::ONE << site;
+  const int sr = site / BX, sc = site - sr * BX;
+  if (a.digest) L.dig = digest_step(L.dig, L.tc, site);
+  if (LOG) {
+    const unsigned long long o = a.log_off[L.idx] + L.n_ev;
+    a.log_t[o] = L.tc;
+    a.log_region[o] = L.gid;
+    a.log_site[o] = (uint16_t)site;
+  } else if (ISR_HIST2 && BX > 1 && BY > 1) {
+    // a site lies on at most one vertical (N/S) and one horizontal (W/E) edge
+    const bool onV = !wrapY && (sr == 0 || sr == BY - 1);
+    const bool onH = !wrapX && (sc == 0 || sc == BX - 1);
+    if (onV) {
+      const bool n = sr == 0;
+      const unsigned om = hist_put(a, n ? L.om[EDGE_N] : L.om[EDGE_S], n ? EDGE_N : EDGE_S, L.obase, L.tc,
+                                   (uint8_t)sc, S, n_out, overflow);
+      L.om[EDGE_N] = n ? om : L.om[EDGE_N];
+      L.om[EDGE_S] = n ? L.om[EDGE_S] : om;
+    }
+    if (onH) {
+      const bool w = sc == 0;
+      const unsigned om = hist_put(a, w ? L.om[EDGE_W] : L.om[EDGE_E], w ? EDGE_W : EDGE_E, L.obase, L.tc,
+                                   (uint8_t)sr, S, n_out, overflow);
+      L.om[EDGE_W] = w ? om : L.om[EDGE_W];
+      L.om[EDGE_E] = w ? L.om[EDGE_E] : om;
+    }
+    L.bev += (onV || onH) ? 1u : 0u;
+  } else {
+    bool on_edge = false;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const bool on = e == EDGE_N ? (!wrapY && sr == 0)
+                    : e == EDGE_S ? (!wrapY && sr == BY - 1)
+                    : e == EDGE_W ? (!wrapX && sc == 0)
+                                  : (!wrapX && sc == BX - 1);
+      if (!on) continue;
+      on_edge = true;
+      L.om[e] = hist_put(a, L.om[e], e, L.obase, L.tc, (uint8_t)(e < 2 ? sc : sr), S, n_out, overflow);
+    }
+    L.bev += on_edge ? 1u : 0u;
+  }
+  ++L.n_ev;
+  L.ts = L.tc;
+  ++L.n;
+  double U;
+  draw_pair(a.seed, L.gid, L.n, U, L.V);
+  L.R = expvar(U);
+}
+
+template <class G>
+__device__ __forceinline__ void refold(const KArgs& a, Lane<G>& L, Stage& S, const ProdTable<G>& PT) {
+  const int lane = threadIdx.x;
+  (void)lane;
+  Classes<G> C;
+  C.build(L.spins, L.gN, L.gS, L.gW, L.gE, a.RX == 1, a.RYg == 1);
+  L.lam = LAMBDA_FOLD(C, PT, S, lane);
+  L.tc = cand_time(L.ts, L.R, L.lam);
 }
 
 template <int BX, int BY, bool LOG>
@@ -925,12 +1157,43 @@ __global__ void ISR_LAUNCH_BOUNDS region_kernel(const KArgs a) {
       if (__all_sync(0xffffffffu, exhausted && !active)) break;
     }
     if (active) {
+#if ISR_UNIFIED == 0
       // drain the break points that precede the next event, then the event
       double tb;
       int d;
       while ((d = next_bp_before_event<G>(a, L, tb)) >= 0) lane_bp<G>(a, L, S, PT, d, tb);
       if (L.tc < a.t_w) lane_event<G, LOG>(a, L, S, PT, n_out, overflow);
       else active = false;
+#else
+      // one step per round: the earliest of (next break point, own event)
+      double tb;
+#if ISR_BP2
+      const int d = next_bp2<G>(a, L, tb);
+#else
+      const int d = next_bp_before_event<G>(a, L, tb);
+#endif
+      if (d < 0 && !(L.tc < a.t_w)) {
+        active = false;
+      } else {
+#if ISR_UNIFIED == 1
+        if (d >= 0) {
+#if ISR_BP2
+          bp_pre2<G>(a, L, S, d, tb);
+          refold<G>(a, L, S, PT);
+#else
+          lane_bp<G>(a, L, S, PT, d, tb);
+#endif
+        } else {
+          ev_pre2<G, LOG>(a, L, S, PT, n_out, overflow);
+          refold<G>(a, L, S, PT);
+        }
+#else
+        if (d >= 0) bp_pre2<G>(a, L, S, d, tb);
+        else ev_pre2<G, LOG>(a, L, S, PT, n_out, overflow);
+        refold<G>(a, L, S, PT);  // shared by both kinds of step
+#endif
+      }
+#endif
     }
   }
 

@@ -171,8 +171,8 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
         hsrc[d] = d == EDGE_N ? 2u : 3u;
         hoff[d] = (unsigned)c;
       } else {
-        const int nr = d == EDGE_N ? (r - 1 + a.RYl) % a.RYl : d == EDGE_S ? (r + 1) % a.RYl : r;
-        const int nc = d == EDGE_W ? (c - 1 + a.RX) % a.RX : d == EDGE_E ? (c + 1) % a.RX : c;
+        const int nr = d == EDGE_N ? wdec(r, a.RYl) : d == EDGE_S ? winc(r, a.RYl) : r;
+        const int nc = d == EDGE_W ? wdec(c, a.RX) : d == EDGE_E ? winc(c, a.RX) : c;
         const unsigned long long v = latest_edge_word(a.sel, ((long long)nr * a.RX + nc) * 4 + (d ^ 1), K);
         if (word_valid(v, K0)) {
           hcnt[d] = ew_count(v);
@@ -333,8 +333,8 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
           for (int e = 0; e < 4; ++e) {
             if (!((chmask >> e) & 1u)) continue;
             if (a.world > 1 && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
-            const int nr = e == EDGE_N ? (r - 1 + a.RYl) % a.RYl : e == EDGE_S ? (r + 1) % a.RYl : r;
-            const int nc = e == EDGE_W ? (c - 1 + a.RX) % a.RX : e == EDGE_E ? (c + 1) % a.RX : c;
+            const int nr = e == EDGE_N ? wdec(r, a.RYl) : e == EDGE_S ? winc(r, a.RYl) : r;
+            const int nc = e == EDGE_W ? wdec(c, a.RX) : e == EDGE_E ? winc(c, a.RX) : c;
             a.dirty[nr * a.RX + nc] = K + 1;
           }
         }
