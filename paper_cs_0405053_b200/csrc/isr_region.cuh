@@ -94,6 +94,8 @@ struct KArgs {
   double rate[10];
   const uint32_t* wl_in;   // regions to recompute (nullptr: all regions)
   int n_work;              // number of regions to recompute
+  const unsigned* n_work_dev;  // if set: the number is read here on the device (pool kernel)
+  unsigned* work_ctr;          // if set: global work queue (persistent pool kernel), zeroed per launch
   int tile;                // work items per block (lane-persistent scheduling)
   unsigned rx_M;           // idx / RX == (idx * rx_M) >> rx_k for idx < 2^31 (host-computed)
   int rx_k;
@@ -230,12 +232,6 @@ __device__ __forceinline__ int nth_bit(M x, int j) {
   return pos;
 }
 
-#if ISR_CSUM
-#define LAMBDA_FOLD(C, PT, S, lane) fold_lambda_cs<G>(C, PT, &S.csum[0][lane])
-#else
-#define LAMBDA_FOLD(C, PT, S, lane) fold_lambda<G>(C, PT)
-#endif
-constexpr int NT_CS = 128;  // column stride of the per-lane partial-sum table (= K1 block size)
 
 // Products fl(N * r_k) for N = 0..NS, one table per block in shared memory:
 // the fold below adds exactly the values __dmul_rn((double)N_k, r_k) would
@@ -261,47 +257,6 @@ __device__ __forceinline__ double fold_lambda(const Classes<G>& C, const ProdTab
 #pragma unroll
   for (int k = 0; k < 10; ++k) c = __dadd_rn(c, T.at(k, popc_m(C.mask(k))));
   return c;
-}
-
-// The same fold, also keeping the partial sums c_k (one column of a
-// per-lane shared-memory table) for the next atom selection.
-template <class G>
-__device__ __forceinline__ double fold_lambda_cs(const Classes<G>& C, const ProdTable<G>& T, double* cs) {
-  double c = 0.0;
-#pragma unroll
-  for (int k = 0; k < 10; ++k) {
-    c = __dadd_rn(c, T.at(k, popc_m(C.mask(k))));
-    cs[k * NT_CS] = c;
-  }
-  return c;
-}
-
-// Phases 2-3 from the stored partial sums: k* = first k with x <= c_k by
-// binary search over the non-decreasing c_0..c_9 (c_9 = Lambda >= x).
-template <class G>
-__device__ __forceinline__ int select_site_cs(const Classes<G>& C, const double* cs, const double* rate, double V,
-                                              double lam) {
-  const double x = __dmul_rn(V, lam);
-  int lo = 0, hi = 9;
-#pragma unroll
-  for (int it = 0; it < 4; ++it) {
-    const int mid = (lo + hi) >> 1;
-    if (lo < hi) {
-      if (x <= cs[mid * NT_CS]) hi = mid;
-      else lo = mid + 1;
-    }
-  }
-  const int ks = lo;
-  const double cprev = ks > 0 ? cs[(ks - 1) * NT_CS] : 0.0;
-  const typename G::M mk = C.mask(ks);
-  const int nk = popc_m(mk);
-  const double aq = __dsub_rn(x, cprev);
-  const double rk = rate[ks];
-  const double q = rk == 1.0 ? aq : __ddiv_rn(aq, rk);  // aq / 1.0 == aq exactly
-  long long j = (long long)floor(q);
-  if (j > nk - 1) j = nk - 1;
-  if (j < 0) j = 0;
-  return nth_bit<typename G::M, G::NS>(mk, (int)j);
 }
 
 // Phases 2-3 of atom selection (eqs. Wsum, Wstop, nores, vindex)
@@ -459,9 +414,6 @@ __device__ __forceinline__ int div_rx(const KArgs& a, int idx) {
 #else
 #define ISR_LAUNCH_BOUNDS __launch_bounds__(NT)
 #endif
-#ifndef ISR_CSUM
-#define ISR_CSUM 0   // atom selection from the stored partial sums of the last fold
-#endif
 #ifndef ISR_MAGICDIV
 #define ISR_MAGICDIV 1
 #endif
@@ -484,15 +436,18 @@ __device__ __forceinline__ int div_rx(const KArgs& a, int idx) {
 constexpr int NT = 128;      // threads per block of K1
 constexpr int CI = ISR_CI;   // staged entries per history
 
-struct Stage {
-  double in_t[4][CI][NT];
-  uint32_t in_p[4][CI][NT];   // 4-byte word holding the position byte, then the byte itself
-  double own_t[4][CI][NT];
-  uint32_t own_p[4][CI][NT];
-#if ISR_CSUM
-  double csum[10][NT];  // partial sums c_k of the last Lambda fold
-#endif
+// Staged history entries, column si per region in flight: incoming
+// histories (and, with OWN, the region's own latest ones for the diff).
+template <int NC, bool OWN, int NCI = CI>
+struct StageT {
+  static constexpr bool HAS_OWN = OWN;
+  static constexpr int CIN = NCI;  // staged entries per history
+  double in_t[4][NCI][NC];
+  uint32_t in_p[4][NCI][NC];   // 4-byte word holding the position byte, then the byte itself
+  double own_t[4][OWN ? NCI : 1][OWN ? NC : 1];
+  uint32_t own_p[4][OWN ? NCI : 1][OWN ? NC : 1];
 };
+using Stage = StageT<NT, true>;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -531,27 +486,36 @@ struct Lane {
   unsigned bev;   // own boundary events of this region
 };
 
-// element offset of entry 0 of the history that direction d reads
+// element offset of entry 0 of the history that direction d reads, within
+// its edge array (edge d ^ 1 of the neighbour; < 2^32, checked at allocation)
 __device__ __forceinline__ unsigned in_off(const KArgs& a, int r, int c, int d, unsigned src) {
   if (src >= 2) return (unsigned)c;
   const int nr = d == EDGE_N ? wdec(r, a.RYl) : d == EDGE_S ? winc(r, a.RYl) : r;
   const int nc = d == EDGE_W ? wdec(c, a.RX) : d == EDGE_E ? winc(c, a.RX) : c;
-  return (unsigned)((long long)(d ^ 1) * a.tstride + ((long long)nr * a.K) * a.RX + nc);
+  return ((unsigned)nr * (unsigned)a.K) * (unsigned)a.RX + (unsigned)nc;
 }
 
-__device__ __forceinline__ const double* src_t(const KArgs& a, unsigned src) {
-  return src == 0 ? a.ed[0].t : src == 1 ? a.ed[1].t : src == 2 ? a.gh_up.t : a.gh_down.t;
+// base of edge e's array in slot `src` (0/1), or of a ghost row (2 = above, 3 = below)
+__device__ __forceinline__ const double* src_t(const KArgs& a, unsigned src, int e) {
+  return src == 0 ? a.ed[0].t + e * a.tstride : src == 1 ? a.ed[1].t + e * a.tstride
+       : src == 2 ? a.gh_up.t : a.gh_down.t;
 }
-__device__ __forceinline__ const uint8_t* src_p(const KArgs& a, unsigned src) {
-  return src == 0 ? a.ed[0].pos : src == 1 ? a.ed[1].pos : src == 2 ? a.gh_up.pos : a.gh_down.pos;
+__device__ __forceinline__ const uint8_t* src_p(const KArgs& a, unsigned src, int e) {
+  return src == 0 ? a.ed[0].pos + e * a.tstride : src == 1 ? a.ed[1].pos + e * a.tstride
+       : src == 2 ? a.gh_up.pos : a.gh_down.pos;
 }
+__device__ __forceinline__ const void* word_of(const uint8_t* p) {
+  return (const void*)((size_t)p & ~(size_t)3);
+}
+__device__ __forceinline__ unsigned byte_shift(const uint8_t* p) { return 8u * (unsigned)((size_t)p & 3); }
 
-template <class G, bool LOG>
-__device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, Stage& S, const ProdTable<G>& PT) {
+template <class G, bool LOG, class SG>
+__device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, SG& S, const ProdTable<G>& PT,
+                                          int si) {
   using M = typename G::M;
   const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
   const unsigned K = a.it_K, K0 = a.it_K0;
-  const int lane = threadIdx.x;
+  const int lane = si;
   const int r = div_rx(a, idx), c = idx - r * a.RX;
   L.idx = idx;
   L.gid = (uint32_t)((a.row0 + r) * a.RX + c);
@@ -609,17 +573,17 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
     if (cnt[d] > 0) {
       const unsigned off = in_off(a, r, c, d, src[d]);
       L.hoff[d] = off;
-      const double* T = src_t(a, src[d]);
-      const uint8_t* P = src_p(a, src[d]);
-      if (cnt[d] <= (unsigned)CI) {
+      const double* T = src_t(a, src[d], d ^ 1);
+      const uint8_t* P = src_p(a, src[d], d ^ 1);
+      if (cnt[d] <= (unsigned)SG::CIN) {
         flags = 1u << 28;
         staged_any = true;
 #pragma unroll
-        for (int q = 0; q < CI; ++q) {
+        for (int q = 0; q < SG::CIN; ++q) {
           if (q < (int)cnt[d]) {
             const unsigned o = off + (unsigned)q * (unsigned)a.RX;
             cp_async8(&S.in_t[d][q][lane], T + o);
-            cp_async4(&S.in_p[d][q][lane], P + (o & ~3u));
+            cp_async4(&S.in_p[d][q][lane], word_of(P + o));
           }
         }
       } else {
@@ -634,17 +598,17 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   for (int e = 0; e < 4; ++e) {
     const unsigned pc = word_count(vown, e), ps = (unsigned)word_slot(vown, e);
     unsigned st = 0;
-    if (!LOG && pc > 0 && pc <= (unsigned)CI) {
+    if (SG::HAS_OWN && !LOG && pc > 0 && pc <= (unsigned)SG::CIN) {
       st = 1;
       staged_any = true;
-      const EdgeView& E = ps ? a.ed[1] : a.ed[0];
-      const unsigned base = (unsigned)(e * a.tstride) + L.obase;
+      const double* Et = src_t(a, ps, e);
+      const uint8_t* Ep = src_p(a, ps, e);
 #pragma unroll
-      for (int q = 0; q < CI; ++q) {
+      for (int q = 0; q < SG::CIN; ++q) {
         if (q < (int)pc) {
-          const unsigned o = base + (unsigned)q * (unsigned)a.RX;
-          cp_async8(&S.own_t[e][q][lane], E.t + o);
-          cp_async4(&S.own_p[e][q][lane], E.pos + (o & ~3u));
+          const unsigned o = L.obase + (unsigned)q * (unsigned)a.RX;
+          cp_async8(&S.own_t[e][q][lane], Et + o);
+          cp_async4(&S.own_p[e][q][lane], word_of(Ep + o));
         }
       }
     }
@@ -656,11 +620,12 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
     for (int d = 0; d < 4; ++d) {
       if (!(L.hm[d] & (1u << 28))) continue;
       const unsigned off = L.hoff[d];
+      const uint8_t* P = src_p(a, (L.hm[d] >> 24) & 3u, d ^ 1);
 #pragma unroll
-      for (int q = 0; q < CI; ++q)
+      for (int q = 0; q < SG::CIN; ++q)
         if (q < (int)(L.hm[d] & 0xFFu)) {
           const unsigned o = off + (unsigned)q * (unsigned)a.RX;
-          S.in_p[d][q][lane] = (S.in_p[d][q][lane] >> (8u * (o & 3u))) & 0xFFu;
+          S.in_p[d][q][lane] = (S.in_p[d][q][lane] >> byte_shift(P + o)) & 0xFFu;
         }
       L.ht[d] = S.in_t[d][0][lane];
       L.hm[d] |= S.in_p[d][0][lane] << 16;
@@ -668,12 +633,12 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       if (!((L.om[e] >> 18) & 1u)) continue;
-      const unsigned base = (unsigned)(e * a.tstride) + L.obase;
+      const uint8_t* Ep = src_p(a, (L.om[e] >> 16) & 1u, e);
 #pragma unroll
-      for (int q = 0; q < CI; ++q)
+      for (int q = 0; q < SG::CIN; ++q)
         if (q < (int)((L.om[e] >> 8) & 0xFFu)) {
-          const unsigned o = base + (unsigned)q * (unsigned)a.RX;
-          S.own_p[e][q][lane] = (S.own_p[e][q][lane] >> (8u * (o & 3u))) & 0xFFu;
+          const unsigned o = L.obase + (unsigned)q * (unsigned)a.RX;
+          S.own_p[e][q][lane] = (S.own_p[e][q][lane] >> byte_shift(Ep + o)) & 0xFFu;
         }
     }
   }
@@ -682,7 +647,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   draw_pair(a.seed, L.gid, L.n, U, L.V);
   Classes<G> C;
   C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
-  L.lam = LAMBDA_FOLD(C, PT, S, lane);
+  L.lam = fold_lambda<G>(C, PT);
   L.tc = cand_time(L.ts, L.R, L.lam);
   if (ISR_BPCACHE) refresh_bp(L);
 }
@@ -768,11 +733,11 @@ __device__ __forceinline__ int next_bp_before_event(const KArgs& a, const Lane<G
 // Break point at tb from direction dstar (eqs. lambdataua..newtau,
 // P:638-674): consume the budget at the old rate, flip the ghost spin,
 // advance the cursor, refold Lambda, new candidate.
-template <class G>
-__device__ __forceinline__ void lane_bp(const KArgs& a, Lane<G>& L, Stage& S, const ProdTable<G>& PT, int dstar,
+template <class G, class SG>
+__device__ __forceinline__ void lane_bp(const KArgs& a, Lane<G>& L, SG& S, const ProdTable<G>& PT, int si, int dstar,
                                         double tb) {
   constexpr int BX = G::BX, BY = G::BY;
-  const int lane = threadIdx.x;
+  const int lane = si;
   const double Rn = __dsub_rn(L.R, __dmul_rn(L.lam, __dsub_rn(tb, L.ts)));
   L.R = Rn < 0.0 ? 0.0 : Rn;
   L.ts = tb;
@@ -793,15 +758,15 @@ __device__ __forceinline__ void lane_bp(const KArgs& a, Lane<G>& L, Stage& S, co
       } else {
         const unsigned src = (L.hm[d] >> 24) & 3u;
         const unsigned off = L.hoff[d] + nx * (unsigned)a.RX;
-        L.ht[d] = src_t(a, src)[off];
-        pos = src_p(a, src)[off];
+        L.ht[d] = src_t(a, src, d ^ 1)[off];
+        pos = src_p(a, src, d ^ 1)[off];
       }
     }
     L.hm[d] = (L.hm[d] & 0xFF0000FFu) | (nx << 8) | (pos << 16);
   }
   Classes<G> C;
   C.build(L.spins, L.gN, L.gS, L.gW, L.gE, a.RX == 1, a.RYg == 1);
-  L.lam = LAMBDA_FOLD(C, PT, S, lane);
+  L.lam = fold_lambda<G>(C, PT);
   L.tc = cand_time(L.ts, L.R, L.lam);
   if (ISR_BPCACHE) refresh_bp(L);
 }
@@ -809,21 +774,17 @@ __device__ __forceinline__ void lane_bp(const KArgs& a, Lane<G>& L, Stage& S, co
 // Own event at tc: select the atom, flip it, record it in the
 // boundary histories (diffed against the staged latest ones on the fly),
 // the digest or the log; draw the next pair of the list.
-template <class G, bool LOG>
-__device__ __forceinline__ void lane_event(const KArgs& a, Lane<G>& L, Stage& S, const ProdTable<G>& PT,
+template <class G, bool LOG, class SG>
+__device__ __forceinline__ void lane_event(const KArgs& a, Lane<G>& L, SG& S, const ProdTable<G>& PT, int si,
                                            unsigned& n_out, bool& overflow) {
   constexpr int BX = G::BX, BY = G::BY;
   const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
-  const int lane = threadIdx.x;
+  const int lane = si;
   int site;
   {
     Classes<G> C;
     C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
-#if ISR_CSUM
-    site = select_site_cs<G>(C, &S.csum[0][lane], a.rate, L.V, L.lam);
-#else
     site = select_site<G>(C, PT, a.rate, L.V, L.lam);
-#endif
   }
   L.spins ^= G::ONE << site;
   const int sr = site / BX, sc = site - sr * BX;
@@ -850,10 +811,10 @@ __device__ __forceinline__ void lane_event(const KArgs& a, Lane<G>& L, Stage& S,
       const uint8_t p = (uint8_t)(e < 2 ? sc : sr);
       unsigned dv = (L.om[e] >> 17) & 1u;
       if ((int)k < a.K) {
-        const unsigned o = (unsigned)(e * a.tstride) + L.obase + k * (unsigned)a.RX;
+        const unsigned o = L.obase + k * (unsigned)a.RX;
         const EdgeView& Pnew = ps ? a.ed[0] : a.ed[1];
-        Pnew.t[o] = L.tc;
-        Pnew.pos[o] = p;
+        Pnew.t[e * a.tstride + o] = L.tc;
+        Pnew.pos[e * a.tstride + o] = p;
         ++n_out;
         if (!dv) {
           if (k >= pc) {
@@ -863,7 +824,8 @@ __device__ __forceinline__ void lane_event(const KArgs& a, Lane<G>& L, Stage& S,
                   S.own_p[e][k][lane] != p) ? 1u : 0u;
           } else {
             const EdgeView& Pold = ps ? a.ed[1] : a.ed[0];
-            dv = (__double_as_longlong(Pold.t[o]) != __double_as_longlong(L.tc) || Pold.pos[o] != p) ? 1u : 0u;
+            dv = (__double_as_longlong(Pold.t[e * a.tstride + o]) != __double_as_longlong(L.tc) ||
+                  Pold.pos[e * a.tstride + o] != p) ? 1u : 0u;
           }
         }
       } else {
@@ -878,7 +840,7 @@ __device__ __forceinline__ void lane_event(const KArgs& a, Lane<G>& L, Stage& S,
   {
     Classes<G> C;
     C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
-    L.lam = LAMBDA_FOLD(C, PT, S, lane);
+    L.lam = fold_lambda<G>(C, PT);
   }
   ++L.n;
   double U;
@@ -892,8 +854,11 @@ __device__ __forceinline__ void lane_event(const KArgs& a, Lane<G>& L, Stage& S,
 // changed edges move to the other slot in a new selector word, neighbours
 // across them are marked dirty, and the tentative end-of-window state is
 // written.
-template <class G>
-__device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& changed, bool& overflow) {
+// DEFER: the entry-by-entry diff was not done while writing; compare the
+// new history (slot ps ^ 1) with the latest one (slot ps) here.
+template <class G, bool DEFER = false>
+__device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& changed, bool& overflow,
+                                            unsigned* n_cmp = nullptr) {
   const int idx = L.idx;
   const int r = div_rx(a, idx), c = idx - r * a.RX;
   const unsigned K = a.it_K;
@@ -903,7 +868,18 @@ __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& ch
   for (int e = 0; e < 4; ++e) {
     const unsigned oc = L.om[e] & 0xFFu, pc = (L.om[e] >> 8) & 0xFFu, ps = (L.om[e] >> 16) & 1u;
     if ((int)oc > a.K) overflow = true;
-    const bool diff = ((L.om[e] >> 17) & 1u) || oc != pc;
+    bool diff = ((L.om[e] >> 17) & 1u) || oc != pc;
+    if (DEFER && !diff && oc > 0 && (int)oc <= a.K) {
+      const double* Tn = src_t(a, ps ^ 1u, e);
+      const double* To = src_t(a, ps, e);
+      const uint8_t* Pn = src_p(a, ps ^ 1u, e);
+      const uint8_t* Po = src_p(a, ps, e);
+      for (unsigned q = 0; q < oc && !diff; ++q) {
+        const unsigned o = L.obase + q * (unsigned)a.RX;
+        diff = __double_as_longlong(__ldcg(Tn + o)) != __double_as_longlong(__ldcg(To + o)) || Pn[o] != Po[o];
+      }
+      if (n_cmp) *n_cmp += oc;
+    }
     const unsigned slot = diff ? ps ^ 1u : ps;
     const unsigned cnt = diff ? ((int)oc < a.K ? oc : (unsigned)a.K) : pc;
     chmask |= (diff ? 1u : 0u) << e;
@@ -963,11 +939,11 @@ __device__ __forceinline__ int next_bp2(const KArgs& a, const Lane<G>& L, double
 }
 
 // break point at tb from direction dstar, up to (not including) the refold
-template <class G>
-__device__ __forceinline__ void bp_pre2(const KArgs& a, Lane<G>& L, Stage& S, int dstar, double tb) {
+template <class G, class SG>
+__device__ __forceinline__ void bp_pre2(const KArgs& a, Lane<G>& L, SG& S, int si, int dstar, double tb) {
   constexpr int BX = G::BX, BY = G::BY;
   using M = typename G::M;
-  const int lane = threadIdx.x;
+  const int lane = si;
   const double Rn = __dsub_rn(L.R, __dmul_rn(L.lam, __dsub_rn(tb, L.ts)));
   L.R = Rn < 0.0 ? 0.0 : Rn;
   L.ts = tb;
@@ -988,8 +964,8 @@ __device__ __forceinline__ void bp_pre2(const KArgs& a, Lane<G>& L, Stage& S, in
       const unsigned src = (hmd >> 24) & 3u;
       const unsigned hoff = dstar == 0 ? L.hoff[0] : dstar == 1 ? L.hoff[1] : dstar == 2 ? L.hoff[2] : L.hoff[3];
       const unsigned off = hoff + nx * (unsigned)a.RX;
-      tn = src_t(a, src)[off];
-      pos = src_p(a, src)[off];
+      tn = src_t(a, src, dstar ^ 1)[off];
+      pos = src_p(a, src, dstar ^ 1)[off];
     }
   }
   const unsigned hn = (hmd & 0xFF0000FFu) | (nx << 8) | (pos << 16);
@@ -1001,28 +977,31 @@ __device__ __forceinline__ void bp_pre2(const KArgs& a, Lane<G>& L, Stage& S, in
 }
 
 // one own-history entry on edge e (EDGE_*), diffed against the latest one
+// DEFER: no diff here (lane_finish compares the histories in global memory)
+template <bool DEFER, class SG>
 __device__ __forceinline__ unsigned hist_put(const KArgs& a, unsigned om, int e, unsigned obase, double tc, uint8_t p,
-                                             const Stage& S, unsigned& n_out, bool& overflow) {
-  const int lane = threadIdx.x;
+                                             const SG& S, int si, unsigned& n_out, bool& overflow) {
+  const int lane = si;
   const unsigned k = om & 0xFFu, pc = (om >> 8) & 0xFFu;
   const unsigned ps = (om >> 16) & 1u;
   unsigned dv = (om >> 17) & 1u;
   if ((int)k < a.K) {
-    const unsigned o = (unsigned)(e * a.tstride) + obase + k * (unsigned)a.RX;
-    double* Tn = ps ? a.ed[0].t : a.ed[1].t;
-    uint8_t* Pn = ps ? a.ed[0].pos : a.ed[1].pos;
+    const unsigned o = obase + k * (unsigned)a.RX;
+    double* Tn = (ps ? a.ed[0].t : a.ed[1].t) + e * a.tstride;
+    uint8_t* Pn = (ps ? a.ed[0].pos : a.ed[1].pos) + e * a.tstride;
     Tn[o] = tc;
     Pn[o] = p;
     ++n_out;
-    if (!dv) {
+    if (DEFER) {
+    } else if (!dv) {
       if (k >= pc) {
         dv = 1;
-      } else if ((om >> 18) & 1u) {
+      } else if (SG::HAS_OWN && ((om >> 18) & 1u)) {
         dv = (__double_as_longlong(S.own_t[e][k][lane]) != __double_as_longlong(tc) || S.own_p[e][k][lane] != p)
                  ? 1u : 0u;
       } else {
-        const double* To = ps ? a.ed[1].t : a.ed[0].t;
-        const uint8_t* Po = ps ? a.ed[1].pos : a.ed[0].pos;
+        const double* To = (ps ? a.ed[1].t : a.ed[0].t) + e * a.tstride;
+        const uint8_t* Po = (ps ? a.ed[1].pos : a.ed[0].pos) + e * a.tstride;
         dv = (__double_as_longlong(To[o]) != __double_as_longlong(tc) || Po[o] != p) ? 1u : 0u;
       }
     }
@@ -1033,8 +1012,8 @@ __device__ __forceinline__ unsigned hist_put(const KArgs& a, unsigned om, int e,
 }
 
 // own event at tc, up to (not including) the refold; draws the next pair
-template <class G, bool LOG>
-__device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, Stage& S, const ProdTable<G>& PT,
+template <class G, bool LOG, bool DEFER, class SG>
+__device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const ProdTable<G>& PT, int si,
                                         unsigned& n_out, bool& overflow) {
   constexpr int BX = G::BX, BY = G::BY;
   const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
@@ -1062,15 +1041,15 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, Stage& S, co
     const bool onH = !wrapX && (sc == 0 || sc == BX - 1);
     if (onV) {
       const bool n = sr == 0;
-      const unsigned om = hist_put(a, n ? L.om[EDGE_N] : L.om[EDGE_S], n ? EDGE_N : EDGE_S, L.obase, L.tc,
-                                   (uint8_t)sc, S, n_out, overflow);
+      const unsigned om = hist_put<DEFER>(a, n ? L.om[EDGE_N] : L.om[EDGE_S], n ? EDGE_N : EDGE_S, L.obase, L.tc,
+                                   (uint8_t)sc, S, si, n_out, overflow);
       L.om[EDGE_N] = n ? om : L.om[EDGE_N];
       L.om[EDGE_S] = n ? L.om[EDGE_S] : om;
     }
     if (onH) {
       const bool w = sc == 0;
-      const unsigned om = hist_put(a, w ? L.om[EDGE_W] : L.om[EDGE_E], w ? EDGE_W : EDGE_E, L.obase, L.tc,
-                                   (uint8_t)sr, S, n_out, overflow);
+      const unsigned om = hist_put<DEFER>(a, w ? L.om[EDGE_W] : L.om[EDGE_E], w ? EDGE_W : EDGE_E, L.obase, L.tc,
+                                   (uint8_t)sr, S, si, n_out, overflow);
       L.om[EDGE_W] = w ? om : L.om[EDGE_W];
       L.om[EDGE_E] = w ? L.om[EDGE_E] : om;
     }
@@ -1085,7 +1064,7 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, Stage& S, co
                                   : (!wrapX && sc == BX - 1);
       if (!on) continue;
       on_edge = true;
-      L.om[e] = hist_put(a, L.om[e], e, L.obase, L.tc, (uint8_t)(e < 2 ? sc : sr), S, n_out, overflow);
+      L.om[e] = hist_put<DEFER>(a, L.om[e], e, L.obase, L.tc, (uint8_t)(e < 2 ? sc : sr), S, si, n_out, overflow);
     }
     L.bev += on_edge ? 1u : 0u;
   }
@@ -1098,12 +1077,10 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, Stage& S, co
 }
 
 template <class G>
-__device__ __forceinline__ void refold(const KArgs& a, Lane<G>& L, Stage& S, const ProdTable<G>& PT) {
-  const int lane = threadIdx.x;
-  (void)lane;
+__device__ __forceinline__ void refold(const KArgs& a, Lane<G>& L, const ProdTable<G>& PT) {
   Classes<G> C;
   C.build(L.spins, L.gN, L.gS, L.gW, L.gE, a.RX == 1, a.RYg == 1);
-  L.lam = LAMBDA_FOLD(C, PT, S, lane);
+  L.lam = fold_lambda<G>(C, PT);
   L.tc = cand_time(L.ts, L.R, L.lam);
 }
 
@@ -1142,7 +1119,7 @@ __global__ void ISR_LAUNCH_BOUNDS region_kernel(const KArgs a) {
           if (item < 0) item = (int)atomicAdd(&q_next, 1u);
           if (item < tile_n) {
             const int idx = a.wl_in ? (int)a.wl_in[tile_begin + item] : tile_begin + item;
-            lane_load<G, LOG>(a, L, idx, S, PT);
+            lane_load<G, LOG>(a, L, idx, S, PT, threadIdx.x);
             n_in += (L.hm[0] & 0xFFu) + (L.hm[1] & 0xFFu) + (L.hm[2] & 0xFFu) + (L.hm[3] & 0xFFu);
             n_cmp += ((L.om[0] >> 8) & 0xFFu) + ((L.om[1] >> 8) & 0xFFu) + ((L.om[2] >> 8) & 0xFFu) +
                      ((L.om[3] >> 8) & 0xFFu);  // latest own entries read for the diff
@@ -1161,8 +1138,8 @@ __global__ void ISR_LAUNCH_BOUNDS region_kernel(const KArgs a) {
       // drain the break points that precede the next event, then the event
       double tb;
       int d;
-      while ((d = next_bp_before_event<G>(a, L, tb)) >= 0) lane_bp<G>(a, L, S, PT, d, tb);
-      if (L.tc < a.t_w) lane_event<G, LOG>(a, L, S, PT, n_out, overflow);
+      while ((d = next_bp_before_event<G>(a, L, tb)) >= 0) lane_bp<G>(a, L, S, PT, threadIdx.x, d, tb);
+      if (L.tc < a.t_w) lane_event<G, LOG>(a, L, S, PT, threadIdx.x, n_out, overflow);
       else active = false;
 #else
       // one step per round: the earliest of (next break point, own event)
@@ -1178,19 +1155,19 @@ __global__ void ISR_LAUNCH_BOUNDS region_kernel(const KArgs a) {
 #if ISR_UNIFIED == 1
         if (d >= 0) {
 #if ISR_BP2
-          bp_pre2<G>(a, L, S, d, tb);
-          refold<G>(a, L, S, PT);
+          bp_pre2<G>(a, L, S, threadIdx.x, d, tb);
+          refold<G>(a, L, PT);
 #else
-          lane_bp<G>(a, L, S, PT, d, tb);
+          lane_bp<G>(a, L, S, PT, threadIdx.x, d, tb);
 #endif
         } else {
-          ev_pre2<G, LOG>(a, L, S, PT, n_out, overflow);
-          refold<G>(a, L, S, PT);
+          ev_pre2<G, LOG, false>(a, L, S, PT, threadIdx.x, n_out, overflow);
+          refold<G>(a, L, PT);
         }
 #else
-        if (d >= 0) bp_pre2<G>(a, L, S, d, tb);
-        else ev_pre2<G, LOG>(a, L, S, PT, n_out, overflow);
-        refold<G>(a, L, S, PT);  // shared by both kinds of step
+        if (d >= 0) bp_pre2<G>(a, L, S, threadIdx.x, d, tb);
+        else ev_pre2<G, LOG, false>(a, L, S, PT, threadIdx.x, n_out, overflow);
+        refold<G>(a, L, PT);  // shared by both kinds of step
 #endif
       }
 #endif

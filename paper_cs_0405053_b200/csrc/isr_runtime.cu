@@ -19,6 +19,7 @@
 #include "../../include/ising_sr.h"
 #include "isr_region.cuh"
 #include "isr_warp.cuh"
+#include "isr_pool.cuh"
 
 namespace {
 
@@ -28,6 +29,7 @@ using isr::KArgs;
 using isr::StateView;
 
 constexpr int kThreads = 128;
+constexpr int kBatch = 8;  // max iterations in flight per host sync
 
 // ---------------------------------------------------------------------------
 // per-shape kernel table (lane-per-region forms)
@@ -40,6 +42,8 @@ struct ShapeOps {
   int cnt_max;       // largest history length the selector can record
   double sel_read_bytes;  // selector bytes read per recomputation (own + neighbours)
   void (*region)(const KArgs&, int nreg, cudaStream_t);
+  void (*region_pool)(const KArgs&, int nreg, cudaStream_t);  // slot-pool form (lane shapes), or null
+  void (*region_pool_persistent)(const KArgs&, cudaStream_t);  // same, one resident grid, global queue
   void (*replay)(const KArgs&, int nreg, cudaStream_t);
   void (*init)(const uint8_t*, int, int, int, int, unsigned long long, StateView, cudaStream_t);
   void (*unpack)(StateView, int, int, int, uint8_t*, cudaStream_t);
@@ -66,6 +70,31 @@ ShapeOps make_ops() {
     const int grid = (n + a.tile - 1) / a.tile;
     isr::region_kernel<BX, BY, true><<<grid, kThreads, 0, s>>>(a);
   };
+  o.region_pool = [](const KArgs& a, int n, cudaStream_t s) {
+    constexpr int S = ISR_POOL_S;
+    constexpr size_t bytes = isr::pool_smem_bytes<G, S>();
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(isr::region_kernel_pool<BX, BY, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      attr = true;
+    }
+    const int grid = (n + a.tile - 1) / a.tile;
+    isr::region_kernel_pool<BX, BY, S><<<grid, isr::PW * 32, bytes, s>>>(a);
+  };
+  o.region_pool_persistent = [](const KArgs& a, cudaStream_t s) {
+    constexpr int S = ISR_POOL_S;
+    constexpr size_t bytes = isr::pool_smem_bytes<G, S>();
+    static int grid = 0;
+    if (!grid) {
+      cudaFuncSetAttribute(isr::region_kernel_pool<BX, BY, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      int dev = 0, sms = 148, per = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, isr::region_kernel_pool<BX, BY, S>, isr::PW * 32, bytes);
+      grid = sms * std::max(per, 1);
+    }
+    isr::region_kernel_pool<BX, BY, S><<<grid, isr::PW * 32, bytes, s>>>(a);
+  };
   o.init = [](const uint8_t* buf, int Lx, int RX, int RYl, int row0, unsigned long long seed, StateView st,
               cudaStream_t s) {
     const int n = RX * RYl;
@@ -91,6 +120,8 @@ ShapeOps make_ops_w() {
   o.halo_bytes = 16;
   o.sel_words = 8;
   o.cnt_max = 65535;
+  o.region_pool = nullptr;
+  o.region_pool_persistent = nullptr;
   o.sel_read_bytes = 8 * 16.0;
   auto launch = [](const KArgs& a, int n, cudaStream_t s, bool log) {
     const int warps_per_block = kThreads / 32;
@@ -222,10 +253,11 @@ struct ising_sr_ctx {
   GhostView gsend[2] = {}, grecv[2] = {};  // [0] = up, [1] = down  (world > 1)
   void* gbuf = nullptr;
   size_t gchunk[4] = {0, 0, 0, 0};
-  int* d_flags = nullptr;                 // [4]
-  unsigned long long* d_stats = nullptr;  // [8]
-  int* h_flags = nullptr;                 // pinned mirror [4]
-  unsigned long long* h_stats = nullptr;  // pinned mirror [8]
+  int* d_flags = nullptr;                 // [kBatch][4] (one slot per iteration in flight)
+  unsigned long long* d_stats = nullptr;  // [kBatch][8]
+  unsigned* d_wctr = nullptr;             // [kBatch] global work-queue counters
+  int* h_flags = nullptr;                 // pinned mirror
+  unsigned long long* h_stats = nullptr;  // pinned mirror
   unsigned* h_wlc = nullptr;              // pinned mirror [2]
   // log
   double* log_t = nullptr;
@@ -237,6 +269,8 @@ struct ising_sr_ctx {
   unsigned long long* d_total = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t kev0 = nullptr, kev1 = nullptr;  // around each region-kernel launch
+  cudaEvent_t bev[2 * 8] = {};                 // batched iterations: around launch j (2j, 2j+1)
+  int batch = 4;  // iterations enqueued per host sync (world == 1, pool K1; env ISING_SR_BATCH)
 
   // window state
   long long w = 0;
@@ -253,6 +287,8 @@ struct ising_sr_ctx {
   int win_f = 0;
   long long launches = 0;
   int refill = 24;  // K1 batched-refill threshold (env ISING_SR_REFILL for tuning)
+  bool pool = true;     // slot-pool K1 for lane shapes (env ISING_SR_POOL=0: lane-persistent K1)
+  int pool_refill = ISR_POOL_S / 2;  // free slots that trigger a pool refill (env ISING_SR_POOL_REFILL)
   ising_sr_stats stats;
 };
 
@@ -298,7 +334,7 @@ ising_sr_status alloc_edges(ising_sr_ctx* c, int K) {
   c->K = K;
   const size_t cn = (size_t)4 * c->RYl * c->RX;
   const size_t tn = cn * (size_t)K;
-  if (tn >= (1ull << 32)) return ISING_SR_E_CAPACITY;  // kernel offsets are 32-bit
+  if (tn / 4 >= (1ull << 32)) return ISING_SR_E_CAPACITY;  // offsets within one edge array are 32-bit
   for (auto& e : c->ed) {
     if (dmalloc(&e.t, tn) != cudaSuccess || dmalloc(&e.pos, tn) != cudaSuccess) {
       cudaGetLastError();
@@ -354,6 +390,14 @@ ising_sr_status check(const ising_sr_ctx* c) {
 int tile_for(int n) {
   const int per = std::max(1, std::min(16, n / (kThreads * 148 * 4)));
   return kThreads * per;
+}
+
+// slot-pool K1: a block holds PW * S regions at a time; >= 2 blocks' worth of
+// tiles per SM slot (3 resident blocks), at most 32 pool generations per tile
+int tile_for_pool(int n) {
+  const int slots = isr::PW * ISR_POOL_S;
+  const int per = std::max(1, std::min(32, n / (slots * 148 * 3 * 2)));
+  return slots * per;
 }
 
 KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
@@ -426,12 +470,15 @@ ising_sr_status launch_iteration(ising_sr_ctx* c) {
   KArgs a = base_args(c, K, first);
   a.wl_in = first ? nullptr : c->wl[K & 1];
   a.n_work = nw;
-  a.tile = tile_for(nw);
+  const bool pool = c->pool && c->ops->region_pool;
+  a.tile = pool ? tile_for_pool(nw) : tile_for(nw);
+  if (pool) a.refill = c->pool_refill;
   a.wl_out = c->wl[(K + 1) & 1];
   a.wl_out_count = c->d_wlc + ((K + 1) & 1);
   CK(c, cudaEventRecord(c->kev0, c->stream));
   if (nw > 0) {
-    c->ops->region(a, nw, c->stream);
+    if (pool) c->ops->region_pool(a, nw, c->stream);
+    else c->ops->region(a, nw, c->stream);
     ++c->launches;
     CK(c, cudaGetLastError());
   }
@@ -458,6 +505,18 @@ ising_sr_status mark_ghosts(ising_sr_ctx* c) {
   return compact_worklist(c);
 }
 
+void account_iteration(ising_sr_ctx* c, float kms, const unsigned long long* s) {
+  const double ib = iteration_bytes(c, s);
+  c->stats.region_launches++;
+  c->stats.region_ms += kms;
+  c->stats.region_bytes += ib;
+  c->stats.iterations_total++;
+  c->stats.recomputations_total += (long long)s[5];
+  c->win_bytes += ib;
+  c->win_events += s[0];  // events of the recomputed regions (see commit)
+  c->win_f = std::max(c->win_f, (int)s[4]);
+}
+
 ising_sr_status read_flags(ising_sr_ctx* c) {
   const unsigned K = c->Kglob;
   CK(c, cudaMemcpyAsync(c->h_flags, c->d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -467,18 +526,11 @@ ising_sr_status read_flags(ising_sr_ctx* c) {
   CK(c, cudaStreamSynchronize(c->stream));
   float kms = 0.f;
   CK(c, cudaEventElapsedTime(&kms, c->kev0, c->kev1));
-  const double ib = iteration_bytes(c, c->h_stats);
-  c->stats.region_launches++;
-  c->stats.region_ms += kms;
-  c->stats.region_bytes += ib;
-  c->stats.iterations_total++;
-  c->stats.recomputations_total += (long long)c->h_stats[5];
-  c->win_bytes += ib;
-  c->win_events += c->h_stats[0];  // events of the recomputed regions (see commit)
-  c->win_f = std::max(c->win_f, (int)c->h_stats[4]);
+  account_iteration(c, kms, c->h_stats);
   c->n_work = (int)c->h_wlc[0];
   return ISING_SR_OK;
 }
+
 
 void fill_halo(ising_sr_ctx* c, ising_sr_halo* h) {
   std::memset(h, 0, sizeof *h);
@@ -519,6 +571,83 @@ void start_window(ising_sr_ctx* c) {
   c->win_events = 0;
   c->win_bytes = 0.0;
   c->win_f = 0;
+}
+
+// ---------------------------------------------------------------------------
+// Batched relaxation (world == 1, slot-pool K1): `batch` iterations are
+// enqueued back to back -- K1 reads its worklist length on the device and
+// takes work from a global queue, so no host round trip is needed between
+// iterations -- and their flags are read with one synchronisation.  An
+// iteration enqueued after the converged one finds an empty worklist (no
+// region was marked dirty) and changes nothing, so g and every result are
+// those of the one-iteration-per-sync loop.
+// ---------------------------------------------------------------------------
+ising_sr_status enqueue_iteration(ising_sr_ctx* c, int j) {
+  ++c->it;
+  const unsigned K = ++c->Kglob;
+  const bool first = c->it == 1;
+  CK(c, cudaMemsetAsync(c->d_flags + 4 * j, 0, 4 * sizeof(int), c->stream));
+  CK(c, cudaMemsetAsync(c->d_stats + 8 * j, 0, 8 * sizeof(unsigned long long), c->stream));
+  CK(c, cudaMemsetAsync(c->d_wctr + j, 0, sizeof(unsigned), c->stream));
+  CK(c, cudaMemsetAsync(c->d_wlc + ((K + 1) & 1), 0, sizeof(unsigned), c->stream));
+  KArgs a = base_args(c, K, first);
+  a.flags = c->d_flags + 4 * j;
+  a.stats = c->d_stats + 8 * j;
+  a.wl_in = first ? nullptr : c->wl[K & 1];
+  a.n_work = c->nreg;
+  a.n_work_dev = first ? nullptr : c->d_wlc + (K & 1);
+  a.work_ctr = c->d_wctr + j;
+  a.tile = 0;
+  a.refill = c->pool_refill;
+  a.wl_out = c->wl[(K + 1) & 1];
+  a.wl_out_count = c->d_wlc + ((K + 1) & 1);
+  CK(c, cudaEventRecord(c->bev[2 * j], c->stream));
+  c->ops->region_pool_persistent(a, c->stream);
+  ++c->launches;
+  CK(c, cudaGetLastError());
+  CK(c, cudaEventRecord(c->bev[2 * j + 1], c->stream));
+  return compact_worklist(c);
+}
+
+ising_sr_status run_window_batched(ising_sr_ctx* c) {
+  ising_sr_status s;
+  for (;;) {
+    const int it0 = c->it;
+    const int B = std::max(1, std::min(c->batch, c->cfg.max_iterations - it0));
+    for (int j = 0; j < B; ++j)
+      if ((s = enqueue_iteration(c, j))) return s;
+    CK(c, cudaMemcpyAsync(c->h_flags, c->d_flags, 4 * B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaMemcpyAsync(c->h_stats, c->d_stats, 8 * B * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    bool restart = false, conv = false;
+    for (int j = 0; j < B; ++j) {
+      float kms = 0.f;
+      CK(c, cudaEventElapsedTime(&kms, c->bev[2 * j], c->bev[2 * j + 1]));
+      account_iteration(c, kms, c->h_stats + 8 * j);
+      if (c->h_flags[4 * j + 1]) {  // history capacity overflow: grow and restart the window
+        if ((s = grow_capacity(c))) return s;
+        start_window(c);
+        restart = true;
+        break;
+      }
+      if (!c->h_flags[4 * j]) {
+        conv = true;
+        c->g = it0 + j + 1;
+        break;
+      }
+    }
+    if (restart) continue;
+    if (conv) {
+      c->it = c->g;
+      c->converged = true;
+      return ISING_SR_OK;
+    }
+    if (c->it >= c->cfg.max_iterations) {
+      c->in_window = false;
+      return ISING_SR_E_DIVERGED;
+    }
+  }
 }
 
 }  // namespace
@@ -563,6 +692,9 @@ void ising_sr_destroy(ising_sr_ctx* c) {
   cudaFree(c->d_wlc);
   cudaFree(c->d_flags);
   cudaFree(c->d_stats);
+  cudaFree(c->d_wctr);
+  for (auto& e : c->bev)
+    if (e) cudaEventDestroy(e);
   cudaFreeHost(c->h_flags);
   cudaFreeHost(c->h_stats);
   cudaFreeHost(c->h_wlc);
@@ -609,6 +741,9 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   c->nreg = c->RX * c->RYl;
   std::memset(&c->stats, 0, sizeof c->stats);
   if (const char* e = std::getenv("ISING_SR_REFILL")) c->refill = std::max(1, std::min(32, std::atoi(e)));
+  if (const char* e = std::getenv("ISING_SR_POOL")) c->pool = std::atoi(e) != 0;
+  if (const char* e = std::getenv("ISING_SR_POOL_REFILL"))
+    c->pool_refill = std::max(1, std::min(ISR_POOL_S, std::atoi(e)));
 
   auto bail = [&](ising_sr_status s) {
     ising_sr_destroy(c);
@@ -630,10 +765,10 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   }
   if (dmalloc(&c->sel, (size_t)ops->sel_words * n) != cudaSuccess || dmalloc(&c->dirty, n) != cudaSuccess ||
       dmalloc(&c->wl[0], n) != cudaSuccess || dmalloc(&c->wl[1], n) != cudaSuccess ||
-      dmalloc(&c->d_wlc, 2) != cudaSuccess || dmalloc(&c->d_flags, 4) != cudaSuccess ||
-      dmalloc(&c->d_stats, 8) != cudaSuccess ||
-      cudaMallocHost((void**)&c->h_flags, 4 * sizeof(int)) != cudaSuccess ||
-      cudaMallocHost((void**)&c->h_stats, 8 * sizeof(unsigned long long)) != cudaSuccess ||
+      dmalloc(&c->d_wlc, 2) != cudaSuccess || dmalloc(&c->d_flags, 4 * kBatch) != cudaSuccess ||
+      dmalloc(&c->d_stats, 8 * kBatch) != cudaSuccess || dmalloc(&c->d_wctr, kBatch) != cudaSuccess ||
+      cudaMallocHost((void**)&c->h_flags, 4 * kBatch * sizeof(int)) != cudaSuccess ||
+      cudaMallocHost((void**)&c->h_stats, 8 * kBatch * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMallocHost((void**)&c->h_wlc, 2 * sizeof(unsigned)) != cudaSuccess ||
       dmalloc(&c->d_off, n) != cudaSuccess || dmalloc(&c->d_bsum, (n + kThreads - 1) / kThreads) != cudaSuccess ||
       dmalloc(&c->d_total, 1) != cudaSuccess)
@@ -644,6 +779,9 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
       cudaEventCreate(&c->kev0) != cudaSuccess || cudaEventCreate(&c->kev1) != cudaSuccess)
     return bail(ISING_SR_E_CUDA);
+  for (auto& e : c->bev)
+    if (cudaEventCreate(&e) != cudaSuccess) return bail(ISING_SR_E_CUDA);
+  if (const char* e = std::getenv("ISING_SR_BATCH")) c->batch = std::max(1, std::min(kBatch, std::atoi(e)));
   const int K0 = cfg->hist_capacity > 0 ? std::min(cfg->hist_capacity, ops->cnt_max) : auto_capacity(*cfg, ops->cnt_max);
   ising_sr_status s = alloc_edges(c, K0);
   if (s != ISING_SR_OK) return bail(s);
@@ -737,6 +875,11 @@ ising_sr_status ising_sr_run_window(ising_sr_ctx* c, int32_t* g_out) {
   ising_sr_status s = check(c);
   if (s) return s;
   if ((s = ising_sr_begin_window(c))) return s;
+  if (c->cfg.world <= 1 && c->pool && c->ops->region_pool_persistent && c->batch > 1) {
+    if ((s = run_window_batched(c))) return s;
+    if (g_out) *g_out = c->g;
+    return ISING_SR_OK;
+  }
   for (;;) {
     if ((s = launch_iteration(c))) return s;
     if (c->cfg.world > 1) {

@@ -177,12 +177,12 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
         if (word_valid(v, K0)) {
           hcnt[d] = ew_count(v);
           hsrc[d] = ew_slot(v);
-          hoff[d] = (unsigned)((long long)(d ^ 1) * a.tstride + ((long long)nr * a.K) * a.RX + nc);
+          hoff[d] = ((unsigned)nr * (unsigned)a.K) * (unsigned)a.RX + (unsigned)nc;
         }
       }
       if (hcnt[d] > 0) {
-        ht[d] = src_t(a, hsrc[d])[hoff[d]];
-        hpos[d] = src_p(a, hsrc[d])[hoff[d]];
+        ht[d] = src_t(a, hsrc[d], d ^ 1)[hoff[d]];
+        hpos[d] = src_p(a, hsrc[d], d ^ 1)[hoff[d]];
       }
       n_in += hcnt[d];
     }
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
             const unsigned k = oc[e];
             const uint8_t p = (uint8_t)(e < 2 ? sc : sr);
             if ((int)k < a.K) {
-              const unsigned o = (unsigned)(e * a.tstride) + obase + k * (unsigned)a.RX;
+              const long long o = e * a.tstride + (long long)(obase + k * (unsigned)a.RX);
               if (lane == 0) {
                 const EdgeView& Pnew = ps[e] ? a.ed[0] : a.ed[1];
                 Pnew.t[o] = tc;
@@ -293,8 +293,8 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
           const unsigned nx = ++hidx[d];
           if (nx < hcnt[d]) {
             const unsigned off = hoff[d] + nx * (unsigned)a.RX;
-            ht[d] = src_t(a, hsrc[d])[off];
-            hpos[d] = src_p(a, hsrc[d])[off];
+            ht[d] = src_t(a, hsrc[d], d ^ 1)[off];
+            hpos[d] = src_p(a, hsrc[d], d ^ 1)[off];
           }
         }
       }

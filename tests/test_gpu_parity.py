@@ -212,3 +212,25 @@ def test_c5_geometry_sample_bit_exact():
         for W in (0.25, 4.0):
             w = workloads.Workload("c5s", 512, 512, 32, 32, T=T, W=W, t_end=4.0, seed=1)
             check_against_oracle(w, logs=False)
+
+
+# ---------------------------------------------------------------------------
+# both schedules of the lane-form K1 (slot pool: default; lane-persistent:
+# ISING_SR_POOL=0) and extreme refill thresholds give the oracle's bits
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("env", [
+    {"ISING_SR_POOL": "0"},
+    {"ISING_SR_POOL": "0", "ISING_SR_REFILL": "1"},
+    {"ISING_SR_POOL": "1", "ISING_SR_POOL_REFILL": "1"},
+    {"ISING_SR_POOL": "1", "ISING_SR_POOL_REFILL": "64"},
+    {"ISING_SR_POOL": "1", "ISING_SR_BATCH": "1"},
+    {"ISING_SR_POOL": "1", "ISING_SR_BATCH": "8"},
+])
+def test_k1_schedules_bit_exact(env, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    check_against_oracle(workloads.get("c1"))
+    for Lx, Ly, bx, by, T, W in [(64, 64, 4, 4, 2.0, 0.5), (32, 32, 8, 8, 2.269, 1.0), (16, 16, 1, 1, 2.0, 0.5),
+                                 (24, 24, 2, 2, 1.5, 2.0)]:
+        w = workloads.Workload("sched", Lx, Ly, bx, by, T=T, W=W, t_end=4.0, seed=9)
+        check_against_oracle(w, logs=False)

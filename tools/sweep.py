@@ -1,0 +1,119 @@
+#!/usr/bin/env python
+"""Per-config reports: committed events/s, iterations per window g (vs ln N),
+f, recomputations per region per window, and (with --oracle) the oracle's
+events/s and bit-exact parity on the same full run.
+
+  python tools/sweep.py --configs c1,c2,c3 --oracle --out profiles/r01_configs.jsonl
+  python tools/sweep.py --c5 [--only b32] --out profiles/r01_c5_sweep.jsonl [--csv profiles/r01_c5_sweep.csv]
+
+Device time = CUDA events around the run_window + commit calls (inputs
+resident); g, f and recomputations come from ising_sr_stats.
+"""
+import argparse
+import csv
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import workloads  # noqa: E402
+from paper_cs_0405053_b200 import FLAG_DIGEST, IsingSR  # noqa: E402
+
+
+def run_one(w, digest=True):
+    stream = torch.cuda.current_stream()
+    sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed, J=w.J, H=w.H, T=w.T,
+                  flags=FLAG_DIGEST if digest else 0, stream=stream.cuda_stream)
+    gs, fs, evs = [], [], []
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(w.n_windows()):
+        gs.append(sim.run_window())
+        evs.append(sim.commit())
+        fs.append(sim.stats()["f_last"])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ms = e0.elapsed_time(e1)
+    st = sim.stats()
+    out = {"sim": sim, "g": gs, "f": fs, "events": evs, "ms": ms, "wall_s": wall, "stats": st}
+    return out
+
+
+def record(w, r):
+    g = np.array(r["g"])
+    N = w.n_regions
+    bd = 1 if (w.bx == 1 and w.by == 1) else 2 * (w.bx + w.by) - 4
+    tot = int(sum(r["events"]))
+    st = r["stats"]
+    return {
+        "config": w.name, "Lx": w.Lx, "Ly": w.Ly, "bx": w.bx, "by": w.by, "T": w.T, "H": w.H, "W": w.W,
+        "t_end": w.t_end, "regions": N, "ln_N": math.log(N), "windows": len(g),
+        "events": tot, "device_s": r["ms"] / 1e3, "events_per_s": tot / (r["ms"] / 1e3),
+        "wall_events_per_s": tot / r["wall_s"],
+        "g_mean": float(g.mean()), "g_p50": float(np.percentile(g, 50)), "g_p99": float(np.percentile(g, 99)),
+        "g_max": int(g.max()), "f_mean": float(np.mean(r["f"])), "f_max": int(max(r["f"])),
+        "recomputations_per_region_window": st["recomputations_total"] / (N * len(g)),
+        "events_per_region_window": tot / (N * len(g)),
+        "paper_T_max": math.log(N) / bd,  # T_max = ln N / (lambda |dG|), lambda = 1
+        "hist_capacity": st["hist_capacity"], "overflow_retries": st["overflow_retries"],
+        "gpu": torch.cuda.get_device_name(0),
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="")
+    ap.add_argument("--c5", action="store_true")
+    ap.add_argument("--only", default="")
+    ap.add_argument("--oracle", action="store_true", help="also run the CPU oracle (test infrastructure) for parity")
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--csv", default="")
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    ws = [workloads.get(c) for c in args.configs.split(",") if c]
+    if args.c5:
+        ws += [p for p in workloads.c5_points() if args.only in p.name]
+    rows = []
+    with open(args.out, "a") as fo:
+        for w in ws:
+            r = run_one(w)
+            rec = record(w, r)
+            if args.oracle:
+                import oracle
+                dig, cnt = r["sim"].digests()
+                spins = r["sim"].spins()
+                t0 = time.perf_counter()
+                ref = oracle.des_workload(w)
+                dt = time.perf_counter() - t0
+                rec["oracle_events_per_s"] = ref["n_events"] / dt
+                rec["oracle_cores"] = 1
+                rec["parity_bit_exact"] = bool(ref["n_events"] == rec["events"] and np.array_equal(cnt, ref["count"])
+                                               and np.array_equal(spins, ref["spins"])
+                                               and np.array_equal(dig, ref["digest"]))
+            r["sim"].close()
+            rows.append(rec)
+            fo.write(json.dumps(rec) + "\n")
+            fo.flush()
+            print(json.dumps(rec), flush=True)
+    if args.csv:
+        keys = list(rows[0].keys())
+        with open(args.csv, "w", newline="") as f:
+            wr = csv.DictWriter(f, fieldnames=keys)
+            wr.writeheader()
+            for r in rows:
+                wr.writerow(r)
+
+
+if __name__ == "__main__":
+    main()
