@@ -43,6 +43,12 @@ struct PoolSlots {
   double ht[4][S];
   uint32_t hoff[4][S];
   uint32_t om[4][S];
+#if ISR_PREPAIR
+  double Rn[S], Vn[S];
+#endif
+#if ISR_PSUM
+  double cs[9][S];
+#endif
 };
 
 template <class G, int S>
@@ -93,6 +99,25 @@ __device__ __forceinline__ void slot_get(const KArgs& a, const PoolSlots<G, S>& 
     L.hoff[d] = P.hoff[d][s];
     L.om[d] = P.om[d][s];
   }
+#if ISR_PREPAIR
+  L.Rn = P.Rn[s];
+  L.Vn = P.Vn[s];
+#endif
+#if ISR_PSUM
+#pragma unroll
+  for (int k = 0; k < 9; ++k) L.cs[k] = P.cs[k][s];
+#endif
+}
+
+// the fields a step (event or break point) and its refold change
+template <class G, int S>
+__device__ __forceinline__ void slot_put_step(PoolSlots<G, S>& P, int s, const Lane<G>& L) {
+  P.lam[s] = L.lam;
+  P.tc[s] = L.tc;
+#if ISR_PSUM
+#pragma unroll
+  for (int k = 0; k < 9; ++k) P.cs[k][s] = L.cs[k];
+#endif
 }
 
 template <class G, int S>
@@ -120,6 +145,11 @@ __device__ __forceinline__ void slot_put_all(PoolSlots<G, S>& P, int s, const La
     P.hoff[d][s] = L.hoff[d];
     P.om[d][s] = L.om[d];
   }
+#if ISR_PREPAIR
+  P.Rn[s] = L.Rn;
+  P.Vn[s] = L.Vn;
+#endif
+  slot_put_step<G, S>(P, s, L);
 }
 
 template <int BX, int BY, int S>
@@ -244,8 +274,11 @@ __global__ void __launch_bounds__(PW * 32) region_kernel_pool(const KArgs a) {
         P.ts[s] = L.ts;
         P.R[s] = L.R;
         P.V[s] = L.V;
-        P.lam[s] = L.lam;
-        P.tc[s] = L.tc;
+#if ISR_PREPAIR
+        P.Rn[s] = L.Rn;
+        P.Vn[s] = L.Vn;
+#endif
+        slot_put_step<G, S>(P, s, L);
         P.n[s] = L.n;
         P.nev[s] = L.n_ev;
         P.bev[s] = L.bev;
@@ -272,8 +305,7 @@ __global__ void __launch_bounds__(PW * 32) region_kernel_pool(const KArgs a) {
         P.ge[s] = L.gE;
         P.ts[s] = L.ts;
         P.R[s] = L.R;
-        P.lam[s] = L.lam;
-        P.tc[s] = L.tc;
+        slot_put_step<G, S>(P, s, L);
         P.hm[d][s] = d == 0 ? L.hm[0] : d == 1 ? L.hm[1] : d == 2 ? L.hm[2] : L.hm[3];
         P.ht[d][s] = d == 0 ? L.ht[0] : d == 1 ? L.ht[1] : d == 2 ? L.ht[2] : L.ht[3];
       }

@@ -102,7 +102,8 @@ struct KArgs {
   int refill;              // idle lanes per warp that trigger a batched refill
   uint32_t* wl_out;        // worklist of the next iteration
   unsigned* wl_out_count;
-  uint32_t* dirty;         // per region: last stamp it was queued for
+  uint32_t* dirty;         // dirty-region bitmaps [2][dwords], parity of the iteration they are for
+  int dwords;              // 32-bit words per bitmap
   int* flags;                   // [0] changed, [1] overflow
   unsigned long long* stats;    // [0] events [1] entries out [2] entries in [3] entries cmp [4] f max [5] regions
   // log replay
@@ -262,40 +263,8 @@ __device__ __forceinline__ double fold_lambda(const Classes<G>& C, const ProdTab
 // Phases 2-3 of atom selection (eqs. Wsum, Wstop, nores, vindex)
 // in x = V*Lambda space: k* = first k with x <= c_k,
 // j = min(floor((x - c_{k*-1}) / r_k*), N_k* - 1); returns the local site.
-template <class G>
-__device__ __forceinline__ int select_site(const Classes<G>& C, const ProdTable<G>& T, const double* rate,
-                                           double V, double lam) {
-  const double x = __dmul_rn(V, lam);
-  double c = 0.0, cprev = 0.0;
-  int ks = -1;
-#pragma unroll
-  for (int k = 0; k < 10; ++k) {
-    const double cn = __dadd_rn(c, T.at(k, popc_m(C.mask(k))));
-    if (ks < 0 && x <= cn) {
-      ks = k;
-      cprev = c;
-    }
-    c = cn;
-  }
-  if (ks < 0) {  // unreachable for V < 1 (x <= Lambda = c_9)
-    ks = 9;
-    while (ks > 0 && popc_m(C.mask(ks)) == 0) --ks;
-    cprev = 0.0;
-  }
-  const typename G::M mk = C.mask(ks);
-  const int nk = popc_m(mk);
-  const double a = __dsub_rn(x, cprev);
-  const double rk = rate[ks];
-  const double q = rk == 1.0 ? a : __ddiv_rn(a, rk);  // a / 1.0 == a exactly
-  long long j = (long long)floor(q);
-  if (j > nk - 1) j = nk - 1;
-  if (j < 0) j = 0;
-  return nth_bit<typename G::M, G::NS>(mk, (int)j);
-}
-
-// The same selection in one pass: the fold's partial sums are compared with
-// x as they are formed, and the class mask of k* is captured on the way (no
-// dynamically indexed class mask, no second scan).  Identical decisions.
+// One pass: the fold's partial sums are compared with x as they are formed,
+// and the class mask of k* is captured on the way.
 template <class G>
 __device__ __forceinline__ int select_site2(const Classes<G>& C, const ProdTable<G>& T, const double* rate,
                                             double V, double lam) {
@@ -327,6 +296,56 @@ __device__ __forceinline__ int select_site2(const Classes<G>& C, const ProdTable
   const double rk = rate[ks];
   const double q = rk == 1.0 ? aq : __ddiv_rn(aq, rk);  // aq / 1.0 == aq exactly
   long long j = __double2ll_rd(q);                         // floor
+  j = j > nk - 1 ? nk - 1 : j;
+  j = j < 0 ? 0 : j;
+  return nth_bit<M, G::NS>(mk, (int)j);
+}
+
+// eq. biglambda keeping the partial sums c_0..c_8 (the same additions as fold_lambda)
+template <class G>
+__device__ __forceinline__ double fold_lambda_ps(const Classes<G>& C, const ProdTable<G>& T, double* cs) {
+  double c = 0.0;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    c = __dadd_rn(c, T.at(k, popc_m(C.mask(k))));
+    if (k < 9) cs[k] = c;
+  }
+  return c;
+}
+
+// select_site2 from the stored partial sums of the current state (no refold):
+// the same c_k values, so the same k*, c_{k*-1} and site
+template <class G>
+__device__ __forceinline__ int select_site_ps(const Classes<G>& C, const double* cs, const double* rate, double V,
+                                             double lam) {
+  using M = typename G::M;
+  const double x = __dmul_rn(V, lam);
+  int ks = -1, lastnz = 0;
+  double cprev = 0.0, cp = 0.0;
+  M mk = 0, mlast = C.mask(0);
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    const M m = C.mask(k);
+    const double ck = k < 9 ? cs[k] : lam;
+    const bool hit = ks < 0 && x <= ck;
+    ks = hit ? k : ks;
+    cprev = hit ? cp : cprev;
+    mk = hit ? m : mk;
+    const bool nz = m != 0;
+    lastnz = nz ? k : lastnz;
+    mlast = nz ? m : mlast;
+    cp = ck;
+  }
+  if (ks < 0) {  // unreachable for V < 1 (x <= Lambda = c_9)
+    ks = lastnz;
+    mk = mlast;
+    cprev = 0.0;
+  }
+  const int nk = popc_m(mk);
+  const double aq = __dsub_rn(x, cprev);
+  const double rk = rate[ks];
+  const double q = rk == 1.0 ? aq : __ddiv_rn(aq, rk);
+  long long j = __double2ll_rd(q);
   j = j > nk - 1 ? nk - 1 : j;
   j = j < 0 ? 0 : j;
   return nth_bit<M, G::NS>(mk, (int)j);
@@ -417,21 +436,14 @@ __device__ __forceinline__ int div_rx(const KArgs& a, int idx) {
 #ifndef ISR_MAGICDIV
 #define ISR_MAGICDIV 1
 #endif
-#ifndef ISR_BPCACHE
-#define ISR_BPCACHE 0  // cache the earliest pending break point
-#endif
-#ifndef ISR_SEL2
-#define ISR_SEL2 1     // one-pass atom selection (select_site2)
-#endif
 #ifndef ISR_HIST2
 #define ISR_HIST2 1    // per-axis (not per-edge) own-history writes
 #endif
-#ifndef ISR_BP2
-#define ISR_BP2 1      // branch-free break-point step, exhausted heads read as +inf
+#ifndef ISR_PREPAIR
+#define ISR_PREPAIR 0  // draw the next event's pair one event ahead (measured slower: registers)
 #endif
-#ifndef ISR_UNIFIED
-#define ISR_UNIFIED 2  // 0: drain break points, then the event; 1: one step per round;
-                       // 2: one step per round sharing the refold/candidate code
+#ifndef ISR_PSUM
+#define ISR_PSUM 0     // keep the fold's partial sums c_0..c_8 for the next selection (measured slower)
 #endif
 constexpr int NT = 128;      // threads per block of K1
 constexpr int CI = ISR_CI;   // staged entries per history
@@ -469,6 +481,12 @@ struct Lane {
   unsigned obase;  // (r * K) * RX + c: own-edge history offset without the edge term
   M spins, gN, gS, gW, gE;
   double ts, R, V, lam, tc;
+#if ISR_PREPAIR
+  double Rn, Vn;  // E(U) and V of the pair after the current one (drawn ahead)
+#endif
+#if ISR_PSUM
+  double cs[9];   // partial sums c_0..c_8 of the last Lambda fold (c_9 = lam)
+#endif
   uint32_t n;
   unsigned long long dig;
   // incoming history cursors: cnt | idx << 8 | pos << 16 | source << 24
@@ -476,8 +494,6 @@ struct Lane {
   unsigned hm[4];
   double ht[4];
   unsigned hoff[4];  // element offset of entry 0 of each incoming history
-  double tbn;        // earliest pending break-point time (cached)
-  int bdir;          // its direction, -1 if none; bit 8: another head has the same time
   // own edges: new count | latest count << 8 | latest slot << 16 |
   // diverged << 17 | latest staged in smem << 18
   unsigned om[4];
@@ -645,11 +661,26 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   // pair n: U already spent into R (carried), V selects the next atom
   double U;
   draw_pair(a.seed, L.gid, L.n, U, L.V);
+#if ISR_PREPAIR
+  {
+    double U1;
+    draw_pair(a.seed, L.gid, L.n + 1, U1, L.Vn);
+    L.Rn = expvar(U1);
+  }
+#endif
   Classes<G> C;
   C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
+#if ISR_PSUM
+  L.lam = fold_lambda_ps<G>(C, PT, L.cs);
+#else
   L.lam = fold_lambda<G>(C, PT);
+#endif
   L.tc = cand_time(L.ts, L.R, L.lam);
-  if (ISR_BPCACHE) refresh_bp(L);
+}
+
+// queue region i for the iteration with stamp `stamp` (bitmap of its parity)
+__device__ __forceinline__ void mark_dirty(const KArgs& a, int i, unsigned stamp) {
+  atomicOr(a.dirty + (size_t)(stamp & 1u) * (size_t)a.dwords + (i >> 5), 1u << (i & 31));
 }
 
 // neighbour id in direction d (only needed to order exactly equal times)
@@ -662,198 +693,6 @@ __device__ __forceinline__ uint32_t neighbour_id(const KArgs& a, uint32_t gid, i
                      : (uint32_t)(gr * a.RX + winc(c, a.RX));
 }
 
-// Earliest pending break point that precedes the candidate event, in
-// (time, region id) order (R10); ids only for exactly equal times.
-// Returns its direction or -1.
-template <class G>
-__device__ __forceinline__ void refresh_bp(Lane<G>& L) {
-  int dstar = -1;
-  double tb = dinf();
-  bool tie = false;
-#pragma unroll
-  for (int d = 0; d < 4; ++d) {
-    const bool pend = ((L.hm[d] >> 8) & 0xFFu) < (L.hm[d] & 0xFFu);
-    if (pend) {
-      if (L.ht[d] < tb) {
-        dstar = d;
-        tb = L.ht[d];
-      } else if (L.ht[d] == tb) {
-        tie = true;
-      }
-    }
-  }
-  L.tbn = tb;
-  L.bdir = dstar | (tie ? 0x100 : 0);
-}
-
-template <class G>
-__device__ __forceinline__ int next_bp_before_event(const KArgs& a, const Lane<G>& L, double& tb) {
-#if ISR_BPCACHE
-  int dstar = L.bdir & 0xFF;
-  tb = L.tbn;
-  const bool tie = (L.bdir & 0x100) != 0;
-  if (L.bdir < 0) return -1;
-#else
-  int dstar = -1;
-  tb = dinf();
-  bool tie = false;
-#pragma unroll
-  for (int d = 0; d < 4; ++d) {
-    const bool pend = ((L.hm[d] >> 8) & 0xFFu) < (L.hm[d] & 0xFFu);
-    if (pend) {
-      if (L.ht[d] < tb) {
-        dstar = d;
-        tb = L.ht[d];
-      } else if (L.ht[d] == tb) {
-        tie = true;
-      }
-    }
-  }
-  if (dstar < 0) return -1;
-#endif
-  if (tb < L.tc && !tie) return dstar;
-  if (tb > L.tc) return -1;
-  // rare: equal times, resolve by region id
-  uint32_t nb = 0xffffffffu;
-  dstar = -1;
-#pragma unroll
-  for (int d = 0; d < 4; ++d) {
-    const bool pend = ((L.hm[d] >> 8) & 0xFFu) < (L.hm[d] & 0xFFu);
-    if (pend && L.ht[d] == tb) {
-      const uint32_t nid = neighbour_id(a, L.gid, d);
-      if (nid < nb) {
-        dstar = d;
-        nb = nid;
-      }
-    }
-  }
-  return (tb < L.tc || nb < L.gid) ? dstar : -1;
-}
-
-// Break point at tb from direction dstar (eqs. lambdataua..newtau,
-// P:638-674): consume the budget at the old rate, flip the ghost spin,
-// advance the cursor, refold Lambda, new candidate.
-template <class G, class SG>
-__device__ __forceinline__ void lane_bp(const KArgs& a, Lane<G>& L, SG& S, const ProdTable<G>& PT, int si, int dstar,
-                                        double tb) {
-  constexpr int BX = G::BX, BY = G::BY;
-  const int lane = si;
-  const double Rn = __dsub_rn(L.R, __dmul_rn(L.lam, __dsub_rn(tb, L.ts)));
-  L.R = Rn < 0.0 ? 0.0 : Rn;
-  L.ts = tb;
-#pragma unroll
-  for (int d = 0; d < 4; ++d) {
-    if (d != dstar) continue;
-    const int p = (int)((L.hm[d] >> 16) & 0xFFu);
-    if (d == EDGE_N) L.gN ^= G::ONE << p;
-    else if (d == EDGE_S) L.gS ^= G::ONE << ((BY - 1) * BX + p);
-    else if (d == EDGE_W) L.gW ^= G::ONE << (p * BX);
-    else L.gE ^= G::ONE << (p * BX + BX - 1);
-    const unsigned nx = ((L.hm[d] >> 8) & 0xFFu) + 1;
-    unsigned pos = 0;
-    if (nx < (L.hm[d] & 0xFFu)) {
-      if (L.hm[d] & (1u << 28)) {
-        L.ht[d] = S.in_t[d][nx][lane];
-        pos = S.in_p[d][nx][lane];
-      } else {
-        const unsigned src = (L.hm[d] >> 24) & 3u;
-        const unsigned off = L.hoff[d] + nx * (unsigned)a.RX;
-        L.ht[d] = src_t(a, src, d ^ 1)[off];
-        pos = src_p(a, src, d ^ 1)[off];
-      }
-    }
-    L.hm[d] = (L.hm[d] & 0xFF0000FFu) | (nx << 8) | (pos << 16);
-  }
-  Classes<G> C;
-  C.build(L.spins, L.gN, L.gS, L.gW, L.gE, a.RX == 1, a.RYg == 1);
-  L.lam = fold_lambda<G>(C, PT);
-  L.tc = cand_time(L.ts, L.R, L.lam);
-  if (ISR_BPCACHE) refresh_bp(L);
-}
-
-// Own event at tc: select the atom, flip it, record it in the
-// boundary histories (diffed against the staged latest ones on the fly),
-// the digest or the log; draw the next pair of the list.
-template <class G, bool LOG, class SG>
-__device__ __forceinline__ void lane_event(const KArgs& a, Lane<G>& L, SG& S, const ProdTable<G>& PT, int si,
-                                           unsigned& n_out, bool& overflow) {
-  constexpr int BX = G::BX, BY = G::BY;
-  const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
-  const int lane = si;
-  int site;
-  {
-    Classes<G> C;
-    C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
-    site = select_site<G>(C, PT, a.rate, L.V, L.lam);
-  }
-  L.spins ^= G::ONE << site;
-  const int sr = site / BX, sc = site - sr * BX;
-  if (a.digest)
-    L.dig = digest_step(L.dig, L.tc, site);
-  if (LOG) {
-    const unsigned long long o = a.log_off[L.idx] + L.n_ev;
-    a.log_t[o] = L.tc;
-    a.log_region[o] = L.gid;
-    a.log_site[o] = (uint16_t)site;
-  } else {
-    // own boundary history, written to the free slot
-    bool on_edge = false;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const bool on = e == EDGE_N ? (!wrapY && sr == 0)
-                    : e == EDGE_S ? (!wrapY && sr == BY - 1)
-                    : e == EDGE_W ? (!wrapX && sc == 0)
-                                  : (!wrapX && sc == BX - 1);
-      if (!on) continue;
-      on_edge = true;
-      const unsigned k = L.om[e] & 0xFFu, pc = (L.om[e] >> 8) & 0xFFu;
-      const unsigned ps = (L.om[e] >> 16) & 1u;
-      const uint8_t p = (uint8_t)(e < 2 ? sc : sr);
-      unsigned dv = (L.om[e] >> 17) & 1u;
-      if ((int)k < a.K) {
-        const unsigned o = L.obase + k * (unsigned)a.RX;
-        const EdgeView& Pnew = ps ? a.ed[0] : a.ed[1];
-        Pnew.t[e * a.tstride + o] = L.tc;
-        Pnew.pos[e * a.tstride + o] = p;
-        ++n_out;
-        if (!dv) {
-          if (k >= pc) {
-            dv = 1;
-          } else if ((L.om[e] >> 18) & 1u) {
-            dv = (__double_as_longlong(S.own_t[e][k][lane]) != __double_as_longlong(L.tc) ||
-                  S.own_p[e][k][lane] != p) ? 1u : 0u;
-          } else {
-            const EdgeView& Pold = ps ? a.ed[1] : a.ed[0];
-            dv = (__double_as_longlong(Pold.t[e * a.tstride + o]) != __double_as_longlong(L.tc) ||
-                  Pold.pos[e * a.tstride + o] != p) ? 1u : 0u;
-          }
-        }
-      } else {
-        overflow = true;
-      }
-      L.om[e] = (L.om[e] & ~((1u << 17) | 0xFFu)) | (dv << 17) | (k < 255u ? k + 1 : 255u);
-    }
-    L.bev += on_edge ? 1u : 0u;
-  }
-  ++L.n_ev;
-  L.ts = L.tc;
-  {
-    Classes<G> C;
-    C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
-    L.lam = fold_lambda<G>(C, PT);
-  }
-  ++L.n;
-  double U;
-  draw_pair(a.seed, L.gid, L.n, U, L.V);
-  L.R = expvar(U);
-  L.tc = cand_time(L.ts, L.R, L.lam);
-}
-
-// Publish a finished region: an edge changed iff its history diverged from
-// the latest one or has a different length (statement (c));
-// changed edges move to the other slot in a new selector word, neighbours
-// across them are marked dirty, and the tentative end-of-window state is
-// written.
 // DEFER: the entry-by-entry diff was not done while writing; compare the
 // new history (slot ps ^ 1) with the latest one (slot ps) here.
 template <class G, bool DEFER = false>
@@ -895,7 +734,7 @@ __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& ch
       if (a.world > 1 && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
       const int nr = e == EDGE_N ? wdec(r, a.RYl) : e == EDGE_S ? winc(r, a.RYl) : r;
       const int nc = e == EDGE_W ? wdec(c, a.RX) : e == EDGE_E ? winc(c, a.RX) : c;
-      a.dirty[nr * a.RX + nc] = K + 1;  // same value from every writer: a plain store suffices
+      mark_dirty(a, nr * a.RX + nc, K + 1);
     }
   }
   // tentative end-of-window state (committed by pointer swap at commit)
@@ -909,10 +748,10 @@ __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& ch
 
 
 // ---------------------------------------------------------------------------
-// Step variants (ISR_BP2 / ISR_HIST2 / ISR_UNIFIED): the same decisions and
-// IEEE operations as next_bp_before_event / lane_bp / lane_event above,
-// arranged so that lanes on different kinds of step share instructions.
-// An incoming head whose history is exhausted reads as +inf.
+// One step of a region: the earliest of its next break point and its own
+// event.  Both kinds share the refold/candidate code (refold), so lanes on
+// different kinds of step share those instructions.  An incoming head whose
+// history is exhausted reads as +inf.
 // ---------------------------------------------------------------------------
 template <class G>
 __device__ __forceinline__ int next_bp2(const KArgs& a, const Lane<G>& L, double& tb) {
@@ -1021,10 +860,10 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const
   {
     Classes<G> C;
     C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
-#if ISR_SEL2
-    site = select_site2<G>(C, PT, a.rate, L.V, L.lam);
+#if ISR_PSUM
+    site = select_site_ps<G>(C, L.cs, a.rate, L.V, L.lam);
 #else
-    site = select_site<G>(C, PT, a.rate, L.V, L.lam);
+    site = select_site2<G>(C, PT, a.rate, L.V, L.lam);
 #endif
   }
   L.spins ^= G::ONE << site;
@@ -1071,16 +910,30 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const
   ++L.n_ev;
   L.ts = L.tc;
   ++L.n;
+#if ISR_PREPAIR
+  L.R = L.Rn;  // pair n (drawn one event ago)
+  L.V = L.Vn;
+  {
+    double U1;  // pair n + 1, needed only at the next event
+    draw_pair(a.seed, L.gid, L.n + 1, U1, L.Vn);
+    L.Rn = expvar(U1);
+  }
+#else
   double U;
   draw_pair(a.seed, L.gid, L.n, U, L.V);
   L.R = expvar(U);
+#endif
 }
 
 template <class G>
 __device__ __forceinline__ void refold(const KArgs& a, Lane<G>& L, const ProdTable<G>& PT) {
   Classes<G> C;
   C.build(L.spins, L.gN, L.gS, L.gW, L.gE, a.RX == 1, a.RYg == 1);
+#if ISR_PSUM
+  L.lam = fold_lambda_ps<G>(C, PT, L.cs);
+#else
   L.lam = fold_lambda<G>(C, PT);
+#endif
   L.tc = cand_time(L.ts, L.R, L.lam);
 }
 
@@ -1090,8 +943,13 @@ __global__ void ISR_LAUNCH_BOUNDS region_kernel(const KArgs a) {
   __shared__ unsigned q_next;
   __shared__ Stage S;
   __shared__ ProdTable<G> PT;
-  const int tile_begin = blockIdx.x * a.tile;
-  const int tile_n = min(a.tile, a.n_work - tile_begin);
+  // work: a static tile per block (lanes take items from a block queue), or
+  // (work_ctr set) the whole worklist as a global queue served to a
+  // persistent grid in per-warp chunks, its length read on the device
+  const bool global_q = a.work_ctr != nullptr;
+  const int n_all = a.n_work_dev ? (int)__ldcg(a.n_work_dev) : a.n_work;
+  const int tile_begin = global_q ? 0 : blockIdx.x * a.tile;
+  const int tile_n = global_q ? n_all : min(a.tile, n_all - tile_begin);
   if (threadIdx.x == 0) q_next = blockDim.x;  // the first blockDim items are taken statically
   fill_prod<G>(PT, a.rate);
   __syncthreads();
@@ -1104,10 +962,38 @@ __global__ void ISR_LAUNCH_BOUNDS region_kernel(const KArgs a) {
   // together, so the (memory-heavy) load/publish path runs converged.
   const int REFILL = a.refill;
   bool active = false, pending = false, exhausted = false;
-  int item = threadIdx.x;
+  int item = global_q ? -1 : (int)threadIdx.x;
+  const unsigned lane_lt = (1u << (threadIdx.x & 31)) - 1u;
+  constexpr int CHUNK = 256;        // items per global-queue claim of a warp
+  int wc_cur = 0, wc_end = 0;       // the warp's current chunk (warp-uniform)
+  bool wq_done = !global_q;         // global queue exhausted for this warp
   for (;;) {
     const unsigned idle = __ballot_sync(0xffffffffu, !active);
     if (__popc(idle) >= REFILL || idle == 0xffffffffu) {
+      if (global_q) {
+        // deal the next items of the warp's chunk to the idle lanes, claiming
+        // new chunks from the global queue as needed (warp-uniform)
+        unsigned rem = __ballot_sync(0xffffffffu, !active && !exhausted);
+        while (rem && !wq_done) {
+          if (wc_cur >= wc_end) {
+            unsigned b = 0;
+            if ((threadIdx.x & 31) == 0) b = atomicAdd(a.work_ctr, (unsigned)CHUNK);
+            b = __shfl_sync(0xffffffffu, b, 0);
+            if ((int)b >= n_all) {
+              wq_done = true;
+              break;
+            }
+            wc_cur = (int)b;
+            wc_end = min((int)b + CHUNK, n_all);
+          }
+          const int take = min(__popc(rem), wc_end - wc_cur);
+          const int rank = __popc(rem & lane_lt);
+          const bool mine = ((rem >> (threadIdx.x & 31)) & 1u) && rank < take;
+          if (mine) item = wc_cur + rank;
+          rem &= ~__ballot_sync(0xffffffffu, mine);
+          wc_cur += take;
+        }
+      }
       if (!active) {
         if (pending) {
           if (!LOG) lane_finish<G>(a, L, changed, overflow);
@@ -1116,8 +1002,8 @@ __global__ void ISR_LAUNCH_BOUNDS region_kernel(const KArgs a) {
           pending = false;
         }
         if (!exhausted) {
-          if (item < 0) item = (int)atomicAdd(&q_next, 1u);
-          if (item < tile_n) {
+          if (item < 0 && !global_q) item = (int)atomicAdd(&q_next, 1u);
+          if (item >= 0 && item < tile_n) {
             const int idx = a.wl_in ? (int)a.wl_in[tile_begin + item] : tile_begin + item;
             lane_load<G, LOG>(a, L, idx, S, PT, threadIdx.x);
             n_in += (L.hm[0] & 0xFFu) + (L.hm[1] & 0xFFu) + (L.hm[2] & 0xFFu) + (L.hm[3] & 0xFFu);
@@ -1134,43 +1020,16 @@ __global__ void ISR_LAUNCH_BOUNDS region_kernel(const KArgs a) {
       if (__all_sync(0xffffffffu, exhausted && !active)) break;
     }
     if (active) {
-#if ISR_UNIFIED == 0
-      // drain the break points that precede the next event, then the event
-      double tb;
-      int d;
-      while ((d = next_bp_before_event<G>(a, L, tb)) >= 0) lane_bp<G>(a, L, S, PT, threadIdx.x, d, tb);
-      if (L.tc < a.t_w) lane_event<G, LOG>(a, L, S, PT, threadIdx.x, n_out, overflow);
-      else active = false;
-#else
       // one step per round: the earliest of (next break point, own event)
       double tb;
-#if ISR_BP2
       const int d = next_bp2<G>(a, L, tb);
-#else
-      const int d = next_bp_before_event<G>(a, L, tb);
-#endif
       if (d < 0 && !(L.tc < a.t_w)) {
         active = false;
       } else {
-#if ISR_UNIFIED == 1
-        if (d >= 0) {
-#if ISR_BP2
-          bp_pre2<G>(a, L, S, threadIdx.x, d, tb);
-          refold<G>(a, L, PT);
-#else
-          lane_bp<G>(a, L, S, PT, threadIdx.x, d, tb);
-#endif
-        } else {
-          ev_pre2<G, LOG, false>(a, L, S, PT, threadIdx.x, n_out, overflow);
-          refold<G>(a, L, PT);
-        }
-#else
         if (d >= 0) bp_pre2<G>(a, L, S, threadIdx.x, d, tb);
         else ev_pre2<G, LOG, false>(a, L, S, PT, threadIdx.x, n_out, overflow);
         refold<G>(a, L, PT);  // shared by both kinds of step
-#endif
       }
-#endif
     }
   }
 
@@ -1251,33 +1110,50 @@ __global__ void mark_kernel(const KArgs a, GhostView up, GhostView down) {
   if (g.stamp[c] != a.it_K) return;
   const int r = isup ? 0 : a.RYl - 1;
   const int nidx = r * a.RX + c;
-  a.dirty[nidx] = a.it_K + 1;
+  mark_dirty(a, nidx, a.it_K + 1);
 }
 
-// Ordered worklist of the next iteration: regions whose dirty stamp equals
-// `stamp`, compacted in region order within each 256-region block (one
-// atomic per block), so the next iteration's loads stay coalesced.
-__global__ void __launch_bounds__(256) compact_kernel(const uint32_t* dirty, int n, uint32_t stamp, uint32_t* wl,
+// Ordered worklist of the next iteration from its dirty bitmap (one word =
+// 32 regions per thread), compacted in region order within each block of
+// 8192 regions (one atomic per block); the bitmap is cleared for reuse two
+// iterations later.
+__global__ void __launch_bounds__(256) compact_kernel(uint32_t* bm, int nwords, int n, uint32_t* wl,
                                                       unsigned* count) {
   __shared__ unsigned wsum[8];
   __shared__ unsigned base;
   const int i = blockIdx.x * 256 + threadIdx.x;
-  const bool take = i < n && dirty[i] == stamp;
+  uint32_t w = 0;
+  if (i < nwords) {
+    w = bm[i];
+    if (w) bm[i] = 0u;
+  }
+  const int c = __popc(w);
   const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const unsigned m = __ballot_sync(0xffffffffu, take);
-  if (lane == 0) wsum[wid] = __popc(m);
+  int x = c;  // inclusive warp scan of the counts
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, x, o);
+    if ((int)lane >= o) x += t;
+  }
+  if (lane == 31) wsum[wid] = (unsigned)x;
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned s = 0;
-    for (int w = 0; w < 8; ++w) {
-      const unsigned t = wsum[w];
-      wsum[w] = s;
+    for (int q = 0; q < 8; ++q) {
+      const unsigned t = wsum[q];
+      wsum[q] = s;
       s += t;
     }
     base = s ? atomicAdd(count, s) : 0u;
   }
   __syncthreads();
-  if (take) wl[base + wsum[wid] + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
+  unsigned o = base + wsum[wid] + (unsigned)(x - c);
+  while (w) {
+    const int b = __ffs(w) - 1;
+    w &= w - 1u;
+    const int r = i * 32 + b;
+    if (r < n) wl[o++] = (uint32_t)r;
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -44,6 +44,7 @@ struct ShapeOps {
   void (*region)(const KArgs&, int nreg, cudaStream_t);
   void (*region_pool)(const KArgs&, int nreg, cudaStream_t);  // slot-pool form (lane shapes), or null
   void (*region_pool_persistent)(const KArgs&, cudaStream_t);  // same, one resident grid, global queue
+  void (*region_persistent)(const KArgs&, cudaStream_t);       // lane K1, one resident grid, global queue
   void (*replay)(const KArgs&, int nreg, cudaStream_t);
   void (*init)(const uint8_t*, int, int, int, int, unsigned long long, StateView, cudaStream_t);
   void (*unpack)(StateView, int, int, int, uint8_t*, cudaStream_t);
@@ -80,6 +81,17 @@ ShapeOps make_ops() {
     }
     const int grid = (n + a.tile - 1) / a.tile;
     isr::region_kernel_pool<BX, BY, S><<<grid, isr::PW * 32, bytes, s>>>(a);
+  };
+  o.region_persistent = [](const KArgs& a, cudaStream_t s) {
+    static int grid = 0;
+    if (!grid) {
+      int dev = 0, sms = 148, per = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, isr::region_kernel<BX, BY, false>, kThreads, 0);
+      grid = sms * std::max(per, 1);
+    }
+    isr::region_kernel<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
   };
   o.region_pool_persistent = [](const KArgs& a, cudaStream_t s) {
     constexpr int S = ISR_POOL_S;
@@ -122,6 +134,7 @@ ShapeOps make_ops_w() {
   o.cnt_max = 65535;
   o.region_pool = nullptr;
   o.region_pool_persistent = nullptr;
+  o.region_persistent = nullptr;
   o.sel_read_bytes = 8 * 16.0;
   auto launch = [](const KArgs& a, int n, cudaStream_t s, bool log) {
     const int warps_per_block = kThreads / 32;
@@ -247,7 +260,8 @@ struct ising_sr_ctx {
   int comm = 0;  // index of the committed state
   EdgeView ed[2] = {};
   unsigned long long* sel = nullptr;  // per region selector word
-  uint32_t* dirty = nullptr;          // per region: last stamp queued for
+  uint32_t* dirty = nullptr;          // dirty-region bitmaps [2][dwords] (iteration parity)
+  int dwords = 0;
   uint32_t* wl[2] = {nullptr, nullptr};
   unsigned* d_wlc = nullptr;          // [2] worklist counts
   GhostView gsend[2] = {}, grecv[2] = {};  // [0] = up, [1] = down  (world > 1)
@@ -270,7 +284,7 @@ struct ising_sr_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t kev0 = nullptr, kev1 = nullptr;  // around each region-kernel launch
   cudaEvent_t bev[2 * 8] = {};                 // batched iterations: around launch j (2j, 2j+1)
-  int batch = 4;  // iterations enqueued per host sync (world == 1, pool K1; env ISING_SR_BATCH)
+  int batch = 1;  // iterations enqueued per host sync (world == 1; env ISING_SR_BATCH; measured: 1 is fastest)
 
   // window state
   long long w = 0;
@@ -287,7 +301,7 @@ struct ising_sr_ctx {
   int win_f = 0;
   long long launches = 0;
   int refill = 24;  // K1 batched-refill threshold (env ISING_SR_REFILL for tuning)
-  bool pool = true;     // slot-pool K1 for lane shapes (env ISING_SR_POOL=0: lane-persistent K1)
+  bool pool = false;    // slot-pool K1 for lane shapes (env ISING_SR_POOL=1; measured slower so far)
   int pool_refill = ISR_POOL_S / 2;  // free slots that trigger a pool refill (env ISING_SR_POOL_REFILL)
   ising_sr_stats stats;
 };
@@ -425,6 +439,7 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   a.seed = c->cfg.seed;
   for (int k = 0; k < 10; ++k) a.rate[k] = c->cfg.rate[k];
   a.dirty = c->dirty;
+  a.dwords = c->dwords;
   a.refill = c->refill;
   {
     // magic division by RX: k = 31 + ceil(log2 RX), M = ceil(2^k / RX) < 2^32;
@@ -452,7 +467,8 @@ double iteration_bytes(const ising_sr_ctx* c, const unsigned long long* s) {
 
 ising_sr_status compact_worklist(ising_sr_ctx* c) {
   const unsigned K = c->Kglob;
-  isr::compact_kernel<<<(c->nreg + 255) / 256, 256, 0, c->stream>>>(c->dirty, c->nreg, K + 1, c->wl[(K + 1) & 1],
+  isr::compact_kernel<<<(c->dwords + 255) / 256, 256, 0, c->stream>>>(c->dirty + (size_t)((K + 1) & 1) * c->dwords,
+                                                                       c->dwords, c->nreg, c->wl[(K + 1) & 1],
                                                                      c->d_wlc + ((K + 1) & 1));
   ++c->launches;
   CK(c, cudaGetLastError());
@@ -598,11 +614,12 @@ ising_sr_status enqueue_iteration(ising_sr_ctx* c, int j) {
   a.n_work_dev = first ? nullptr : c->d_wlc + (K & 1);
   a.work_ctr = c->d_wctr + j;
   a.tile = 0;
-  a.refill = c->pool_refill;
+  a.refill = c->pool ? c->pool_refill : c->refill;
   a.wl_out = c->wl[(K + 1) & 1];
   a.wl_out_count = c->d_wlc + ((K + 1) & 1);
   CK(c, cudaEventRecord(c->bev[2 * j], c->stream));
-  c->ops->region_pool_persistent(a, c->stream);
+  if (c->pool) c->ops->region_pool_persistent(a, c->stream);
+  else c->ops->region_persistent(a, c->stream);
   ++c->launches;
   CK(c, cudaGetLastError());
   CK(c, cudaEventRecord(c->bev[2 * j + 1], c->stream));
@@ -739,6 +756,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   c->RYl = RY / world;
   c->row0 = cfg->rank * c->RYl;
   c->nreg = c->RX * c->RYl;
+  c->dwords = (c->nreg + 31) / 32;
   std::memset(&c->stats, 0, sizeof c->stats);
   if (const char* e = std::getenv("ISING_SR_REFILL")) c->refill = std::max(1, std::min(32, std::atoi(e)));
   if (const char* e = std::getenv("ISING_SR_POOL")) c->pool = std::atoi(e) != 0;
@@ -763,7 +781,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
         dmalloc(&s.R, n) != cudaSuccess || dmalloc(&s.n, n) != cudaSuccess || dmalloc(&s.dig, n) != cudaSuccess)
       return bail(ISING_SR_E_OOM);
   }
-  if (dmalloc(&c->sel, (size_t)ops->sel_words * n) != cudaSuccess || dmalloc(&c->dirty, n) != cudaSuccess ||
+  if (dmalloc(&c->sel, (size_t)ops->sel_words * n) != cudaSuccess || dmalloc(&c->dirty, 2 * ((n + 31) / 32)) != cudaSuccess ||
       dmalloc(&c->wl[0], n) != cudaSuccess || dmalloc(&c->wl[1], n) != cudaSuccess ||
       dmalloc(&c->d_wlc, 2) != cudaSuccess || dmalloc(&c->d_flags, 4 * kBatch) != cudaSuccess ||
       dmalloc(&c->d_stats, 8 * kBatch) != cudaSuccess || dmalloc(&c->d_wctr, kBatch) != cudaSuccess ||
@@ -774,7 +792,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
       dmalloc(&c->d_total, 1) != cudaSuccess)
     return bail(ISING_SR_E_OOM);
   if (cudaMemsetAsync(c->sel, 0, n * 8 * (size_t)ops->sel_words, c->stream) != cudaSuccess ||
-      cudaMemsetAsync(c->dirty, 0, n * 4, c->stream) != cudaSuccess)
+      cudaMemsetAsync(c->dirty, 0, 2 * ((n + 31) / 32) * 4, c->stream) != cudaSuccess)
     return bail(ISING_SR_E_CUDA);
   if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
       cudaEventCreate(&c->kev0) != cudaSuccess || cudaEventCreate(&c->kev1) != cudaSuccess)
@@ -875,7 +893,7 @@ ising_sr_status ising_sr_run_window(ising_sr_ctx* c, int32_t* g_out) {
   ising_sr_status s = check(c);
   if (s) return s;
   if ((s = ising_sr_begin_window(c))) return s;
-  if (c->cfg.world <= 1 && c->pool && c->ops->region_pool_persistent && c->batch > 1) {
+  if (c->cfg.world <= 1 && c->ops->region_persistent && c->batch > 1) {
     if ((s = run_window_batched(c))) return s;
     if (g_out) *g_out = c->g;
     return ISING_SR_OK;

@@ -89,25 +89,26 @@ __device__ __forceinline__ int wselect(const WClasses& C, const int N[10], const
   const int lane = threadIdx.x & 31;
   const double x = __dmul_rn(V, lam);
   double c = 0.0, cprev = 0.0;
-  int ks = -1;
+  int ks = -1, nk = 0, lastnz = 0, nlast = N[0];
 #pragma unroll
   for (int k = 0; k < 10; ++k) {
     const double cn = __dadd_rn(c, __dmul_rn((double)N[k], rate[k]));
-    if (ks < 0 && x <= cn) {
-      ks = k;
-      cprev = c;
-    }
+    const bool hit = ks < 0 && x <= cn;
+    ks = hit ? k : ks;
+    cprev = hit ? c : cprev;
+    nk = hit ? N[k] : nk;
+    lastnz = N[k] > 0 ? k : lastnz;
+    nlast = N[k] > 0 ? N[k] : nlast;
     c = cn;
   }
-  if (ks < 0) {
-    ks = 9;
-    while (ks > 0 && N[ks] == 0) --ks;
+  if (ks < 0) {  // unreachable for V < 1
+    ks = lastnz;
+    nk = nlast;
     cprev = 0.0;
   }
-  const int nk = N[ks];
   const double aq = __dsub_rn(x, cprev);
   const double rk = rate[ks];
-  long long j = (long long)floor(rk == 1.0 ? aq : __ddiv_rn(aq, rk));
+  long long j = __double2ll_rd(rk == 1.0 ? aq : __ddiv_rn(aq, rk));
   if (j > nk - 1) j = nk - 1;
   if (j < 0) j = 0;
   // rank-select across rows: exclusive prefix of per-row counts
@@ -157,9 +158,12 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
     unsigned n_ev_r = 0, bev = 0;
 
     // ---- incoming histories (uniform cursors) ----
+    // lane q caches entry 32 * floor(hidx / 32) + q of each incoming history
+    // (lt, lp), so a break point reads its successor with a shuffle
     unsigned hcnt[4], hidx[4], hsrc[4], hoff[4];
-    double ht[4];
+    double ht[4], lt[4];
     int hpos[4];
+    unsigned lp = 0;  // byte d: cached position of direction d
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
       hcnt[d] = 0; hidx[d] = 0; hsrc[d] = 0; hoff[d] = 0; ht[d] = dinf(); hpos[d] = 0;
@@ -180,9 +184,15 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
           hoff[d] = ((unsigned)nr * (unsigned)a.K) * (unsigned)a.RX + (unsigned)nc;
         }
       }
+      lt[d] = dinf();
       if (hcnt[d] > 0) {
-        ht[d] = src_t(a, hsrc[d], d ^ 1)[hoff[d]];
-        hpos[d] = src_p(a, hsrc[d], d ^ 1)[hoff[d]];
+        if ((unsigned)lane < hcnt[d]) {
+          const unsigned off = hoff[d] + (unsigned)lane * (unsigned)a.RX;
+          lt[d] = src_t(a, hsrc[d], d ^ 1)[off];
+          lp |= (unsigned)src_p(a, hsrc[d], d ^ 1)[off] << (8 * d);
+        }
+        ht[d] = __shfl_sync(0xffffffffu, lt[d], 0);
+        hpos[d] = (int)((__shfl_sync(0xffffffffu, lp, 0) >> (8 * d)) & 0xFFu);
       }
       n_in += hcnt[d];
     }
@@ -261,14 +271,6 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
                 Pnew.pos[o] = p;
               }
               ++n_out;
-              if (!dv[e]) {
-                if (k >= pc[e]) {
-                  dv[e] = 1;
-                } else {
-                  const EdgeView& Pold = ps[e] ? a.ed[1] : a.ed[0];
-                  dv[e] = (__double_as_longlong(Pold.t[o]) != __double_as_longlong(tc) || Pold.pos[o] != p) ? 1u : 0u;
-                }
-              }
             } else {
               overflow = true;
             }
@@ -292,9 +294,16 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
           else { if (lane == p) gEb ^= 1u; }
           const unsigned nx = ++hidx[d];
           if (nx < hcnt[d]) {
-            const unsigned off = hoff[d] + nx * (unsigned)a.RX;
-            ht[d] = src_t(a, hsrc[d], d ^ 1)[off];
-            hpos[d] = src_p(a, hsrc[d], d ^ 1)[off];
+            if ((nx & 31u) == 0) {  // next chunk of 32 entries
+              lp &= ~(0xFFu << (8 * d));
+              if (nx + (unsigned)lane < hcnt[d]) {
+                const unsigned off = hoff[d] + (nx + (unsigned)lane) * (unsigned)a.RX;
+                lt[d] = src_t(a, hsrc[d], d ^ 1)[off];
+                lp |= (unsigned)src_p(a, hsrc[d], d ^ 1)[off] << (8 * d);
+              }
+            }
+            ht[d] = __shfl_sync(0xffffffffu, lt[d], (int)(nx & 31u));
+            hpos[d] = (int)((__shfl_sync(0xffffffffu, lp, (int)(nx & 31u)) >> (8 * d)) & 0xFFu);
           }
         }
       }
@@ -312,6 +321,27 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
     fmax = max(fmax, bev);
 
     if (!LOG) {
+      // statement (c): compare each new edge history with the latest one,
+      // 32 entries per warp step (the new entries were stored by lane 0)
+      __syncwarp();
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (oc[e] != pc[e] || oc[e] == 0 || (int)oc[e] > a.K) continue;
+        const double* Tn = src_t(a, ps[e] ^ 1u, e);
+        const double* To = src_t(a, ps[e], e);
+        const uint8_t* Pn = src_p(a, ps[e] ^ 1u, e);
+        const uint8_t* Po = src_p(a, ps[e], e);
+        for (unsigned q0 = 0; q0 < oc[e] && !dv[e]; q0 += 32) {
+          bool df = false;
+          const unsigned q = q0 + (unsigned)lane;
+          if (q < oc[e]) {
+            const unsigned o = obase + q * (unsigned)a.RX;
+            df = __double_as_longlong(__ldcg(Tn + o)) != __double_as_longlong(__ldcg(To + o)) ||
+                 __ldcg(Pn + o) != __ldcg(Po + o);
+          }
+          dv[e] = __any_sync(0xffffffffu, df) ? 1u : 0u;
+        }
+      }
       unsigned chmask = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -335,7 +365,7 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
             if (a.world > 1 && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
             const int nr = e == EDGE_N ? wdec(r, a.RYl) : e == EDGE_S ? winc(r, a.RYl) : r;
             const int nc = e == EDGE_W ? wdec(c, a.RX) : e == EDGE_E ? winc(c, a.RX) : c;
-            a.dirty[nr * a.RX + nc] = K + 1;
+            mark_dirty(a, nr * a.RX + nc, K + 1);
           }
         }
       }

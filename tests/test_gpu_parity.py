@@ -220,6 +220,7 @@ def test_c5_geometry_sample_bit_exact():
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("env", [
     {"ISING_SR_POOL": "0"},
+    {"ISING_SR_POOL": "0", "ISING_SR_BATCH": "1"},
     {"ISING_SR_POOL": "0", "ISING_SR_REFILL": "1"},
     {"ISING_SR_POOL": "1", "ISING_SR_POOL_REFILL": "1"},
     {"ISING_SR_POOL": "1", "ISING_SR_POOL_REFILL": "64"},
