@@ -1,0 +1,511 @@
+// isr_big.cuh -- region-trajectory kernel (K1), lane-per-region form for
+// regions of more than 64 sites (8x16 .. 32x32: BASELINE c3 16x16, c5 32x32).
+//
+// One thread owns one region for one relaxation iteration, exactly like the
+// small-region lane kernel (isr_region.cuh), so a warp advances 32 regions
+// per step instead of one (the warp form, isr_warp.cuh, spends a whole warp
+// on one region).  What changes with the region size:
+//   * the spins live in shared memory, one 32-bit row mask per region row;
+//   * the n-fold-way class counts N_k (eq. nidef) are exact
+//     integers updated incrementally: a flip changes the class of the
+//     flipped site (spin) and of its in-region neighbours (up-neighbour
+//     count +-1); a break point changes the class of the one site next to
+//     the flipped halo spin.  Lambda (eq. biglambda) is still re-folded from
+//     the counts in the fixed order after every change (R3);
+//   * per-row class counts (4 rows per 32-bit word, one byte each) let the
+//     atom selection (eqs. Wsum..vindex; j-th site of class k* in
+//     local row-major order, R6) skip to the right row and build
+//     only that row's class mask;
+//   * incoming history entries are read from global memory one ahead (the
+//     entry after the head is always in flight), own entries are diffed
+//     against the latest history at write time with the old entry read one
+//     ahead as well.
+// State, selector and history layouts are those of the warp form, so the two
+// are interchangeable (ISING_SR_BIG=0 selects the warp form) and bit-identical.
+#pragma once
+#include "isr_warp.cuh"
+
+namespace isr {
+
+constexpr int BNT = 64;  // threads per block of the big-region lane kernel
+
+template <int BX, int BY>
+struct BigSmem {
+  static constexpr int RQ = (BY + 3) / 4;  // row-count words per class
+  uint32_t rows[BY][BNT];                  // spins, bit c of rows[r] = site (r, c)
+  uint32_t rc[10][RQ][BNT];                // per-row class counts, byte (r & 3) of word r >> 2
+};
+
+template <int BX, int BY>
+struct BigRegion {
+  static constexpr uint32_t ROWM = BX == 32 ? 0xffffffffu : ((1u << BX) - 1u);
+  BigSmem<BX, BY>& S;
+  int t;                 // column (thread index)
+  bool wrapX, wrapY;
+  uint32_t gN, gS, gW, gE;  // ghost row above / below (bit = column), ghost columns (bit = row)
+  uint32_t Nw[5];           // class counts: N_k in half-word k & 1 of Nw[k >> 1]
+
+  __device__ __forceinline__ uint32_t row(int r) const { return S.rows[r][t]; }
+  __device__ __forceinline__ uint32_t above(int r) const {
+    return r > 0 ? row(r - 1) : (wrapY ? row(BY - 1) : gN);
+  }
+  __device__ __forceinline__ uint32_t below(int r) const {
+    return r < BY - 1 ? row(r + 1) : (wrapY ? row(0) : gS);
+  }
+  // neighbour-is-up bit of the column to the west / east of the row's ends
+  __device__ __forceinline__ uint32_t wbit(int r, uint32_t rw) const {
+    return wrapX ? (rw >> (BX - 1)) & 1u : (gW >> r) & 1u;
+  }
+  __device__ __forceinline__ uint32_t ebit(int r, uint32_t rw) const { return wrapX ? rw & 1u : (gE >> r) & 1u; }
+
+  // class mask of class k in row r (sites of the row whose class is k)
+  __device__ __forceinline__ uint32_t class_mask(int r, int k) const {
+    const uint32_t rw = row(r);
+    const uint32_t nN = above(r), nS = below(r);
+    const uint32_t nW = ((rw << 1) | wbit(r, rw)) & ROWM;
+    const uint32_t nE = (rw >> 1) | (ebit(r, rw) << (BX - 1));
+    const uint32_t s1 = nN ^ nS, c1 = nN & nS, s2 = nW ^ nE, c2 = nW & nE;
+    const uint32_t p0 = s1 ^ s2, kk = s1 & s2, p1 = c1 ^ c2 ^ kk, p2 = (c1 & c2) | (kk & (c1 ^ c2));
+    const int u = k >= 5 ? k - 5 : k;
+    const uint32_t mu = u == 0 ? ~(p0 | p1 | p2) : u == 1 ? (p0 & ~p1) : u == 2 ? (~p0 & p1) : u == 3 ? (p0 & p1) : p2;
+    return (k >= 5 ? rw : ~rw) & mu & ROWM;
+  }
+  // all ten class masks of row r
+  __device__ __forceinline__ void class_masks(int r, uint32_t* m) const {
+    const uint32_t rw = row(r);
+    const uint32_t nN = above(r), nS = below(r);
+    const uint32_t nW = ((rw << 1) | wbit(r, rw)) & ROWM;
+    const uint32_t nE = (rw >> 1) | (ebit(r, rw) << (BX - 1));
+    const uint32_t s1 = nN ^ nS, c1 = nN & nS, s2 = nW ^ nE, c2 = nW & nE;
+    const uint32_t p0 = s1 ^ s2, kk = s1 & s2, p1 = c1 ^ c2 ^ kk, p2 = (c1 & c2) | (kk & (c1 ^ c2));
+    const uint32_t mu[5] = {~(p0 | p1 | p2), p0 & ~p1, ~p0 & p1, p0 & p1, p2};
+#pragma unroll
+    for (int k = 0; k < 10; ++k) m[k] = (k >= 5 ? rw : ~rw) & mu[k >= 5 ? k - 5 : k] & ROWM;
+  }
+  // class of site (r, c) = 5 * s + u (u = number of up neighbours)
+  __device__ __forceinline__ int site_class(int r, int c) const {
+    const uint32_t rw = row(r);
+    const uint32_t s = (rw >> c) & 1u;
+    const uint32_t un = (above(r) >> c) & 1u, us = (below(r) >> c) & 1u;
+    const uint32_t uw = c > 0 ? (rw >> (c - 1)) & 1u : wbit(r, rw);
+    const uint32_t ue = c < BX - 1 ? (rw >> (c + 1)) & 1u : ebit(r, rw);
+    return (int)(5u * s + un + us + uw + ue);
+  }
+  __device__ __forceinline__ int N(int k) const { return (int)((Nw[k >> 1] >> (16 * (k & 1))) & 0xFFFFu); }
+  // N_k += d and the row count of class k in row r += d (d = +-1)
+  __device__ __forceinline__ void add(int k, int r, int d) {
+    const uint32_t inc = (uint32_t)d << (16 * (k & 1));
+#pragma unroll
+    for (int i = 0; i < 5; ++i) Nw[i] += (k >> 1) == i ? inc : 0u;
+    S.rc[k][r >> 2][t] += (uint32_t)d << (8 * (r & 3));
+  }
+  // a site whose up-neighbour count changes by du (spin unchanged)
+  __device__ __forceinline__ void neighbour_changed(int r, int c, int du_after_flip) {
+    const int k = site_class(r, c);  // class after the flip
+    add(k, r, 1);
+    add(k - du_after_flip, r, -1);
+  }
+};
+
+// eq. biglambda, fixed fold order: c_k = c_{k-1} + fl(N_k r_k)
+template <class BR>
+__device__ __forceinline__ double big_fold(const BR& B, const double* rate) {
+  double c = 0.0;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) c = __dadd_rn(c, __dmul_rn((double)B.N(k), rate[k]));
+  return c;
+}
+
+// atom selection: returns the local site index r * BX + c
+template <int BX, int BY>
+__device__ __forceinline__ int big_select(const BigRegion<BX, BY>& B, const double* rate, double V, double lam) {
+  const double x = __dmul_rn(V, lam);
+  double c = 0.0, cprev = 0.0;
+  int ks = -1, nk = 0, lastnz = 0, nlast = B.N(0);
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    const int n = B.N(k);
+    const double cn = __dadd_rn(c, __dmul_rn((double)n, rate[k]));
+    const bool hit = ks < 0 && x <= cn;
+    ks = hit ? k : ks;
+    cprev = hit ? c : cprev;
+    nk = hit ? n : nk;
+    lastnz = n > 0 ? k : lastnz;
+    nlast = n > 0 ? n : nlast;
+    c = cn;
+  }
+  if (ks < 0) {  // unreachable for V < 1 (x <= Lambda = c_9)
+    ks = lastnz;
+    nk = nlast;
+    cprev = 0.0;
+  }
+  const double aq = __dsub_rn(x, cprev);
+  const double rk = rate[ks];
+  long long j = __double2ll_rd(rk == 1.0 ? aq : __ddiv_rn(aq, rk));
+  if (j > nk - 1) j = nk - 1;
+  if (j < 0) j = 0;
+  int jj = (int)j;
+  // skip whole groups of 4 rows, then rows, using the per-row counts
+  int r = 0;
+  constexpr int RQ = BigSmem<BX, BY>::RQ;
+  for (int q = 0; q < RQ; ++q) {
+    const uint32_t w = B.S.rc[ks][q][B.t];
+    const int s = (int)((w * 0x01010101u) >> 24);  // sum of the 4 byte counts (<= 128)
+    if (jj < s) {
+      int c0 = (int)(w & 0xFFu);
+      r = 4 * q;
+      if (jj >= c0) {
+        jj -= c0;
+        ++r;
+        c0 = (int)((w >> 8) & 0xFFu);
+        if (jj >= c0) {
+          jj -= c0;
+          ++r;
+          c0 = (int)((w >> 16) & 0xFFu);
+          if (jj >= c0) {
+            jj -= c0;
+            ++r;
+          }
+        }
+      }
+      break;
+    }
+    jj -= s;
+  }
+  return r * BX + nth_bit<uint32_t, 32>(B.class_mask(r, ks), jj);
+}
+
+template <int BX, int BY, bool LOG>
+__global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
+  using BR = BigRegion<BX, BY>;
+  static_assert(BX <= 32 && BY <= 32 && BX >= 3 && BY >= 3, "rows of up to 32 sites");
+  __shared__ BigSmem<BX, BY> SM;
+  const int t = threadIdx.x;
+  const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
+  const unsigned K = a.it_K, K0 = a.it_K0;
+  unsigned long long n_ev = 0, n_out = 0, n_in = 0, n_cmp = 0, n_reg = 0;
+  unsigned fmax = 0;
+  bool changed = false, overflow = false;
+  const int stride = gridDim.x * BNT;
+
+  for (int item = blockIdx.x * BNT + t; item < a.n_work; item += stride) {
+    const int idx = a.wl_in ? (int)a.wl_in[item] : item;
+    const int r = idx / a.RX, c = idx - r * a.RX;
+    const uint32_t gid = (uint32_t)((a.row0 + r) * a.RX + c);
+    ++n_reg;
+    BR B{SM, t, wrapX, wrapY, 0u, 0u, 0u, 0u, {0u, 0u, 0u, 0u, 0u}};
+    // ---- committed state ----
+    {
+      const uint32_t* src = (const uint32_t*)a.in.spins + (long long)idx * BY;
+#pragma unroll
+      for (int q = 0; q < BY; ++q) SM.rows[q][t] = src[q];
+      const uint4 h = ((const uint4*)a.in.halo)[idx];
+      B.gN = h.x;
+      B.gS = h.y;
+      B.gW = h.z;
+      B.gE = h.w;
+    }
+    double ts = a.in.ts[idx], R = a.in.R[idx];
+    uint32_t n = a.in.n[idx];
+    unsigned long long dig = a.digest ? a.in.dig[idx] : 0ull;
+    unsigned n_ev_r = 0, bev = 0;
+    // class counts and per-row class counts of the committed state
+    for (int q = 0; q < BigSmem<BX, BY>::RQ; ++q) {
+      uint32_t w[10];
+#pragma unroll
+      for (int k = 0; k < 10; ++k) w[k] = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int rr = 4 * q + i;
+        if (rr < BY) {
+          uint32_t m[10];
+          B.class_masks(rr, m);
+#pragma unroll
+          for (int k = 0; k < 10; ++k) w[k] |= (uint32_t)__popc(m[k]) << (8 * i);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 10; ++k) {
+        SM.rc[k][q][t] = w[k];
+        B.Nw[k >> 1] += ((w[k] * 0x01010101u) >> 24) << (16 * (k & 1));
+      }
+    }
+
+    // ---- incoming histories: head entry + the next one in flight ----
+    unsigned hcnt[4], hidx[4], hsrc[4], hoff[4];
+    double ht[4], hn[4];
+    unsigned hp = 0, hq = 0;  // byte d: position of the head / next entry of direction d
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      hcnt[d] = 0; hidx[d] = 0; hsrc[d] = 0; hoff[d] = 0; ht[d] = dinf(); hn[d] = dinf();
+      const bool axis_off = (d < 2) ? wrapY : wrapX;
+      if (a.first || axis_off) continue;
+      const bool ghost = a.world > 1 && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
+      if (ghost) {
+        hcnt[d] = (d == EDGE_N ? a.gh_up : a.gh_down).cnt[c];
+        hsrc[d] = d == EDGE_N ? 2u : 3u;
+        hoff[d] = (unsigned)c;
+      } else {
+        const int nr = d == EDGE_N ? wdec(r, a.RYl) : d == EDGE_S ? winc(r, a.RYl) : r;
+        const int nc = d == EDGE_W ? wdec(c, a.RX) : d == EDGE_E ? winc(c, a.RX) : c;
+        const unsigned long long v = latest_edge_word(a.sel, ((long long)nr * a.RX + nc) * 4 + (d ^ 1), K);
+        if (word_valid(v, K0)) {
+          hcnt[d] = ew_count(v);
+          hsrc[d] = ew_slot(v);
+          hoff[d] = ((unsigned)nr * (unsigned)a.K) * (unsigned)a.RX + (unsigned)nc;
+        }
+      }
+      if (hcnt[d] > 0) {
+        const double* T = src_t(a, hsrc[d], d ^ 1);
+        const uint8_t* P = src_p(a, hsrc[d], d ^ 1);
+        ht[d] = T[hoff[d]];
+        hp |= (unsigned)P[hoff[d]] << (8 * d);
+        if (hcnt[d] > 1) {
+          hn[d] = T[hoff[d] + (unsigned)a.RX];
+          hq |= (unsigned)P[hoff[d] + (unsigned)a.RX] << (8 * d);
+        }
+      }
+      n_in += hcnt[d];
+    }
+    // ---- own latest histories (diff at write time, old entry read ahead) ----
+    unsigned oc[4], pc[4], ps[4], dv[4], wh[4];
+    double ot[4];
+    unsigned op = 0;  // byte e: position of the old entry at index oc[e]
+    const unsigned obase = (unsigned)(((long long)r * a.K) * a.RX + c);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      oc[e] = 0; pc[e] = 0; ps[e] = 0; dv[e] = 0; wh[e] = 0; ot[e] = 0.0;
+      if (LOG) continue;
+      const ulonglong2 wp = reinterpret_cast<const ulonglong2*>(a.sel)[(long long)idx * 4 + e];
+      const int li = latest_index(wp, K);
+      const unsigned long long v = li ? wp.y : wp.x;
+      ps[e] = ew_slot(v);
+      pc[e] = word_valid(v, K0) ? ew_count(v) : 0u;
+      wh[e] = (unsigned)(li ^ 1);
+      n_cmp += pc[e];
+      if (pc[e] > 0) {
+        ot[e] = src_t(a, ps[e], e)[obase];
+        op |= (unsigned)src_p(a, ps[e], e)[obase] << (8 * e);
+      }
+    }
+
+    double U, V;
+    draw_pair(a.seed, gid, n, U, V);
+    double lam = big_fold(B, a.rate);
+    double tc = cand_time(ts, R, lam);
+
+    for (;;) {
+      int dstar = -1;
+      double tb = dinf();
+#pragma unroll
+      for (int d = 0; d < 4; ++d) {
+        if (ht[d] < tb) {
+          tb = ht[d];
+          dstar = d;
+        }
+      }
+      bool bp = false;
+      if (dstar >= 0) {
+        if (tb < tc) {
+          bp = true;
+          // exactly equal head times in two directions: smallest neighbour id first
+          uint32_t nb = 0xffffffffu;
+#pragma unroll
+          for (int d = 0; d < 4; ++d) {
+            if (ht[d] == tb) {
+              const uint32_t nid = neighbour_id(a, gid, d);
+              if (nid < nb) {
+                nb = nid;
+                dstar = d;
+              }
+            }
+          }
+        } else if (tb == tc) {
+          uint32_t nb = 0xffffffffu;
+#pragma unroll
+          for (int d = 0; d < 4; ++d) {
+            if (ht[d] == tb) {
+              const uint32_t nid = neighbour_id(a, gid, d);
+              if (nid < nb) {
+                nb = nid;
+                dstar = d;
+              }
+            }
+          }
+          bp = nb < gid;
+        }
+      }
+      if (!bp && !(tc < a.t_w)) break;
+      if (bp) {
+        // break point (eqs. lambdataua..newtau): budget at the old rate
+        const double Rn = __dsub_rn(R, __dmul_rn(lam, __dsub_rn(tb, ts)));
+        R = Rn < 0.0 ? 0.0 : Rn;
+        ts = tb;
+        const int p = (int)((hp >> (8 * dstar)) & 0xFFu);
+        // the in-region site next to the flipped halo spin and its change of
+        // up-neighbour count
+        int sr, sc;
+        uint32_t was;
+        if (dstar == EDGE_N) { sr = 0; sc = p; was = (B.gN >> p) & 1u; B.gN ^= 1u << p; }
+        else if (dstar == EDGE_S) { sr = BY - 1; sc = p; was = (B.gS >> p) & 1u; B.gS ^= 1u << p; }
+        else if (dstar == EDGE_W) { sr = p; sc = 0; was = (B.gW >> p) & 1u; B.gW ^= 1u << p; }
+        else { sr = p; sc = BX - 1; was = (B.gE >> p) & 1u; B.gE ^= 1u << p; }
+        B.neighbour_changed(sr, sc, was ? -1 : 1);
+        // advance the cursor: the next entry becomes the head, read the one after
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+          if (d != dstar) continue;
+          const unsigned nx = ++hidx[d];
+          double h1 = dinf();
+          unsigned p1 = 0;
+          if (nx + 1 < hcnt[d]) {
+            const unsigned off = hoff[d] + (nx + 1) * (unsigned)a.RX;
+            h1 = src_t(a, hsrc[d], d ^ 1)[off];
+            p1 = src_p(a, hsrc[d], d ^ 1)[off];
+          }
+          ht[d] = nx < hcnt[d] ? hn[d] : dinf();
+          hp = (hp & ~(0xFFu << (8 * d))) | (((hq >> (8 * d)) & 0xFFu) << (8 * d));
+          hn[d] = h1;
+          hq = (hq & ~(0xFFu << (8 * d))) | (p1 << (8 * d));
+        }
+      } else {
+        // own event at tc
+        const int site = big_select<BX, BY>(B, a.rate, V, lam);
+        const int sr = site / BX, sc = site - sr * BX;
+        {
+          const int k0 = B.site_class(sr, sc);
+          const uint32_t s = (uint32_t)(k0 >= 5);
+          // flip: the site changes spin, its in-region neighbours' up-count moves by du
+          const int du = s ? -1 : 1;
+          B.add(k0, sr, -1);
+          SM.rows[sr][t] ^= 1u << sc;
+          B.add(s ? k0 - 5 : k0 + 5, sr, 1);
+          if (sr > 0) B.neighbour_changed(sr - 1, sc, du);
+          else if (wrapY) B.neighbour_changed(BY - 1, sc, du);
+          if (sr < BY - 1) B.neighbour_changed(sr + 1, sc, du);
+          else if (wrapY) B.neighbour_changed(0, sc, du);
+          if (sc > 0) B.neighbour_changed(sr, sc - 1, du);
+          else if (wrapX) B.neighbour_changed(sr, BX - 1, du);
+          if (sc < BX - 1) B.neighbour_changed(sr, sc + 1, du);
+          else if (wrapX) B.neighbour_changed(sr, 0, du);
+        }
+        if (a.digest) dig = digest_step(dig, tc, site);
+        if (LOG) {
+          const unsigned long long o = a.log_off[idx] + n_ev_r;
+          a.log_t[o] = tc;
+          a.log_region[o] = gid;
+          a.log_site[o] = (uint16_t)site;
+        } else {
+          bool on_edge = false;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const bool on = e == EDGE_N ? (!wrapY && sr == 0)
+                          : e == EDGE_S ? (!wrapY && sr == BY - 1)
+                          : e == EDGE_W ? (!wrapX && sc == 0)
+                                        : (!wrapX && sc == BX - 1);
+            if (!on) continue;
+            on_edge = true;
+            const unsigned k = oc[e];
+            const uint8_t p = (uint8_t)(e < 2 ? sc : sr);
+            if ((int)k < a.K) {
+              const unsigned o = obase + k * (unsigned)a.RX;
+              (ps[e] ? a.ed[0].t : a.ed[1].t)[e * a.tstride + o] = tc;
+              (ps[e] ? a.ed[0].pos : a.ed[1].pos)[e * a.tstride + o] = p;
+              ++n_out;
+              if (!dv[e]) {
+                if (k >= pc[e]) {
+                  dv[e] = 1;
+                } else {
+                  dv[e] = (__double_as_longlong(ot[e]) != __double_as_longlong(tc) ||
+                           ((op >> (8 * e)) & 0xFFu) != p) ? 1u : 0u;
+                  if (!dv[e] && k + 1 < pc[e]) {  // read the next old entry ahead
+                    const unsigned o1 = o + (unsigned)a.RX;
+                    ot[e] = src_t(a, ps[e], e)[o1];
+                    op = (op & ~(0xFFu << (8 * e))) | ((unsigned)src_p(a, ps[e], e)[o1] << (8 * e));
+                  }
+                }
+              }
+            } else {
+              overflow = true;
+            }
+            oc[e] = k + 1;
+          }
+          bev += on_edge ? 1u : 0u;
+        }
+        ++n_ev_r;
+        ts = tc;
+        ++n;
+        draw_pair(a.seed, gid, n, U, V);
+        R = expvar(U);
+      }
+      lam = big_fold(B, a.rate);
+      tc = cand_time(ts, R, lam);
+    }
+    n_ev += n_ev_r;
+    fmax = max(fmax, bev);
+
+    if (!LOG) {
+      unsigned chmask = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if ((int)oc[e] > a.K) overflow = true;
+        const bool diff = dv[e] || oc[e] != pc[e];
+        if (diff) {
+          chmask |= 1u << e;
+          const unsigned cnt = (int)oc[e] < a.K ? oc[e] : (unsigned)a.K;
+          a.sel[((long long)idx * 4 + e) * 2 + wh[e]] =
+              ((unsigned long long)K << 32) | ((unsigned long long)cnt << 1) | (ps[e] ^ 1u);
+        }
+      }
+      if (chmask) {
+        changed = true;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (!((chmask >> e) & 1u)) continue;
+          if (a.world > 1 && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
+          const int nr = e == EDGE_N ? wdec(r, a.RYl) : e == EDGE_S ? winc(r, a.RYl) : r;
+          const int nc = e == EDGE_W ? wdec(c, a.RX) : e == EDGE_E ? winc(c, a.RX) : c;
+          mark_dirty(a, nr * a.RX + nc, K + 1);
+        }
+      }
+      uint32_t* dst = (uint32_t*)a.out.spins + (long long)idx * BY;
+#pragma unroll
+      for (int q = 0; q < BY; ++q) dst[q] = SM.rows[q][t];
+      ((uint4*)a.out.halo)[idx] = make_uint4(B.gN, B.gS, B.gW, B.gE);
+      a.out.ts[idx] = ts;
+      a.out.R[idx] = R;
+      a.out.n[idx] = n;
+      if (a.digest) a.out.dig[idx] = dig;
+    }
+  }
+
+  if (!LOG) {
+    const unsigned full = 0xffffffffu;
+    const unsigned anych = __ballot_sync(full, changed);
+    const unsigned anyov = __ballot_sync(full, overflow);
+    unsigned long long v0 = n_ev, v1 = n_out, v2 = n_in, v3 = n_cmp, v5 = n_reg;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v0 += __shfl_xor_sync(full, v0, o);
+      v1 += __shfl_xor_sync(full, v1, o);
+      v2 += __shfl_xor_sync(full, v2, o);
+      v3 += __shfl_xor_sync(full, v3, o);
+      v5 += __shfl_xor_sync(full, v5, o);
+      fmax = max(fmax, __shfl_xor_sync(full, fmax, o));
+    }
+    if ((t & 31) == 0) {
+      if (anych) atomicOr(&a.flags[0], 1);
+      if (anyov) atomicOr(&a.flags[1], 1);
+      if (v5) {
+        atomicAdd(&a.stats[0], v0);
+        atomicAdd(&a.stats[1], v1);
+        atomicAdd(&a.stats[2], v2);
+        atomicAdd(&a.stats[3], v3);
+        atomicMax(&a.stats[4], (unsigned long long)fmax);
+        atomicAdd(&a.stats[5], v5);
+      }
+    }
+  }
+}
+
+}  // namespace isr

@@ -20,6 +20,7 @@
 #include "isr_region.cuh"
 #include "isr_warp.cuh"
 #include "isr_pool.cuh"
+#include "isr_big.cuh"
 
 namespace {
 
@@ -122,6 +123,14 @@ ShapeOps make_ops() {
   return o;
 }
 
+bool big_enabled() {
+  static const int v = [] {
+    const char* e = std::getenv("ISING_SR_BIG");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 template <int BX, int BY>
 ShapeOps make_ops_w() {
   ShapeOps o;
@@ -142,13 +151,24 @@ ShapeOps make_ops_w() {
     if (log) isr::region_kernel_w<BX, BY, true><<<grid, kThreads, 0, s>>>(a);
     else isr::region_kernel_w<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
   };
+  // lane-per-region K1 for big regions (isr_big.cuh); ISING_SR_BIG=0: warp form
   o.region = [](const KArgs& a, int n, cudaStream_t s) {
-    const int grid = std::max(1, std::min((n + 3) / 4, 148 * 16));
-    isr::region_kernel_w<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
+    if (big_enabled()) {
+      const int grid = std::max(1, std::min((n + isr::BNT - 1) / isr::BNT, 148 * 32));
+      isr::region_kernel_big<BX, BY, false><<<grid, isr::BNT, 0, s>>>(a);
+    } else {
+      const int grid = std::max(1, std::min((n + 3) / 4, 148 * 16));
+      isr::region_kernel_w<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
+    }
   };
   o.replay = [](const KArgs& a, int n, cudaStream_t s) {
-    const int grid = std::max(1, std::min((n + 3) / 4, 148 * 16));
-    isr::region_kernel_w<BX, BY, true><<<grid, kThreads, 0, s>>>(a);
+    if (big_enabled()) {
+      const int grid = std::max(1, std::min((n + isr::BNT - 1) / isr::BNT, 148 * 32));
+      isr::region_kernel_big<BX, BY, true><<<grid, isr::BNT, 0, s>>>(a);
+    } else {
+      const int grid = std::max(1, std::min((n + 3) / 4, 148 * 16));
+      isr::region_kernel_w<BX, BY, true><<<grid, kThreads, 0, s>>>(a);
+    }
   };
   (void)launch;
   o.init = [](const uint8_t* buf, int Lx, int RX, int RYl, int row0, unsigned long long seed, StateView st,
@@ -191,6 +211,15 @@ __global__ void scan_block_sums(const uint32_t* n1, const uint32_t* n0, int N, u
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
     bsum[blockIdx.x] = s;
   }
+}
+
+// sum of e_i = n1[i] - n0[i] (the window's committed events) without offsets
+__global__ void __launch_bounds__(256) count_events(const uint32_t* n1, const uint32_t* n0, int N,
+                                                    unsigned long long* total) {
+  unsigned long long v = 0;
+  for (int i = blockIdx.x * 256 + threadIdx.x; i < N; i += gridDim.x * 256) v += (unsigned long long)(n1[i] - n0[i]);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(total, v);
 }
 
 __global__ void scan_top(unsigned long long* bsum, int nb, unsigned long long* total) {
@@ -934,11 +963,18 @@ ising_sr_status ising_sr_commit(ising_sr_ctx* c, int64_t* events_out) {
   const StateView& s0 = c->st[c->comm];
   const StateView& s1 = c->st[c->comm ^ 1];
   const int nb = (c->nreg + kThreads - 1) / kThreads;
-  // e_i = n_next - n_comm: scan for the log offsets and the window's total
-  scan_block_sums<<<nb, kThreads, 0, c->stream>>>(s1.n, s0.n, c->nreg, c->d_bsum);
-  scan_top<<<1, 1024, 0, c->stream>>>(c->d_bsum, nb, c->d_total);
-  c->launches += 2;
+  // e_i = n_next - n_comm: the window's total, and (event log) the scan for the log offsets
   const bool log = (c->cfg.flags & ISING_SR_FLAG_LOG_EVENTS) != 0;
+  if (!log) {
+    CK(c, cudaMemsetAsync(c->d_total, 0, sizeof(unsigned long long), c->stream));
+    count_events<<<std::max(1, std::min((c->nreg + 255) / 256, 148 * 8)), 256, 0, c->stream>>>(s1.n, s0.n, c->nreg,
+                                                                                             c->d_total);
+    c->launches++;
+  } else {
+    scan_block_sums<<<nb, kThreads, 0, c->stream>>>(s1.n, s0.n, c->nreg, c->d_bsum);
+    scan_top<<<1, 1024, 0, c->stream>>>(c->d_bsum, nb, c->d_total);
+    c->launches += 2;
+  }
   if (log) {
     scan_apply<<<nb, kThreads, 0, c->stream>>>(s1.n, s0.n, c->nreg, c->d_bsum, c->d_off);
     c->launches++;
