@@ -246,8 +246,18 @@ def run_ising(args):
         return 0
     peak, peak_kind = _peaks()
     achieved = (region_bytes / (region_ms * 1e-3)) / 1e9 if region_ms > 0 else 0.0
+    # DRAM bytes per K1 launch from the committed ncu capture of one c4 window
+    # (tools/ncu_traffic.py); scaled to this run's launches by the measured
+    # DRAM/algorithmic ratio of that window
+    traffic, traffic_src = None, None
+    tp = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if args.config == "c4" and os.path.exists(tp):
+        t = json.load(open(tp))
+        traffic = t["dram_over_alg"] * region_bytes / max(nlaunch, 1)
+        traffic_src = (f"profiles/k1_traffic.json: ncu --set full of all {t['launches']} K1 launches of c4 window "
+                       f"{t['window']}, DRAM/alg = {t['dram_over_alg']:.2f}")
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+            "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src, "peak_kind": peak_kind,
             "kernel": "region_kernel<4,4> (K1 trajectory + fused diff)",
             "bytes_per_launch": region_bytes / max(nlaunch, 1),
             "ms_per_launch": region_ms / max(nlaunch, 1),

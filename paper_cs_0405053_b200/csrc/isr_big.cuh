@@ -187,8 +187,9 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
   unsigned fmax = 0;
   bool changed = false, overflow = false;
   const int stride = gridDim.x * BNT;
+  const int n_all = a.n_work_dev ? (int)__ldcg(a.n_work_dev) : a.n_work;
 
-  for (int item = blockIdx.x * BNT + t; item < a.n_work; item += stride) {
+  for (int item = blockIdx.x * BNT + t; item < n_all; item += stride) {
     const int idx = a.wl_in ? (int)a.wl_in[item] : item;
     const int r = idx / a.RX, c = idx - r * a.RX;
     const uint32_t gid = (uint32_t)((a.row0 + r) * a.RX + c);

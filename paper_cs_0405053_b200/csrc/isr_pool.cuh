@@ -37,6 +37,7 @@ struct PoolSlots {
   M sp[S], gn[S], gs[S], gw[S], ge[S];
   double ts[S], R[S], V[S], lam[S], tc[S];
   uint32_t n[S], nev[S], bev[S];
+  int site[S];     // atom of the next event (ISR_SELAHEAD)
   uint32_t fl[S];  // bit 0: selector word to overwrite; bits 4-5: direction of the next break point
   unsigned long long dig[S];
   uint32_t hm[4][S];
@@ -91,6 +92,7 @@ __device__ __forceinline__ void slot_get(const KArgs& a, const PoolSlots<G, S>& 
   L.n_ev = P.nev[s];
   L.bev = P.bev[s];
   L.whalf = (int)(P.fl[s] & 1u);
+  L.site = P.site[s];
   L.dig = P.dig[s];
 #pragma unroll
   for (int d = 0; d < 4; ++d) {
@@ -114,6 +116,7 @@ template <class G, int S>
 __device__ __forceinline__ void slot_put_step(PoolSlots<G, S>& P, int s, const Lane<G>& L) {
   P.lam[s] = L.lam;
   P.tc[s] = L.tc;
+  P.site[s] = L.site;
 #if ISR_PSUM
 #pragma unroll
   for (int k = 0; k < 9; ++k) P.cs[k][s] = L.cs[k];

@@ -240,6 +240,7 @@ __device__ __forceinline__ int nth_bit(M x, int j) {
 template <class G>
 struct ProdTable {
   double v[10][G::NS + 1];
+  double rinv[10];  // fl(1 / r_k): screens floor((x - c_{k-1}) / r_k) (exact fallback near integers)
   __device__ __forceinline__ double at(int k, int n) const { return v[k][n]; }
 };
 
@@ -249,6 +250,18 @@ __device__ __forceinline__ void fill_prod(ProdTable<G>& T, const double* rate) {
     const int k = i / (G::NS + 1), n = i - k * (G::NS + 1);
     T.v[k][n] = __dmul_rn((double)n, rate[k]);
   }
+  if (threadIdx.x < 10) T.rinv[threadIdx.x] = __ddiv_rn(1.0, rate[threadIdx.x]);
+}
+
+// j = floor(fl(aq / rk)) for aq > 0, q = aq / rk <= 64: a product with the
+// rounded reciprocal is within 1e-13 of the correctly rounded quotient, so it
+// decides the floor unless the quotient is that close to an integer; then
+// the IEEE division decides (bit-identical to always dividing)
+__device__ __forceinline__ long long floor_div(double aq, double rk, double rinv) {
+  if (rk == 1.0) return __double2ll_rd(aq);  // aq / 1.0 == aq exactly
+  const double qa = __dmul_rn(aq, rinv);
+  const long long jl = __double2ll_rd(__dsub_rn(qa, 1e-12)), jh = __double2ll_rd(__dadd_rn(qa, 1e-12));
+  return jl == jh ? jl : __double2ll_rd(__ddiv_rn(aq, rk));
 }
 
 // eq. biglambda, fixed fold order (R3): c_k = c_{k-1} + N_k r_k
@@ -351,6 +364,49 @@ __device__ __forceinline__ int select_site_ps(const Classes<G>& C, const double*
   return nth_bit<M, G::NS>(mk, (int)j);
 }
 
+// eq. biglambda followed at once by the atom selection for the next event
+// (eqs. Wsum..vindex) on the same state: the partial sums c_k are still in
+// registers, so the selection needs no second fold.  Identical decisions to
+// select_site2 on this state; returns the site (any value when Lambda = 0,
+// then no event can happen: the candidate time is +inf).
+template <class G>
+__device__ __forceinline__ int fold_select(const Classes<G>& C, const ProdTable<G>& T, const double* rate, double V,
+                                           double& lam) {
+  using M = typename G::M;
+  double cs[10];
+  double c = 0.0;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    c = __dadd_rn(c, T.at(k, popc_m(C.mask(k))));
+    cs[k] = c;
+  }
+  lam = c;
+  const double x = __dmul_rn(V, lam);
+  int ks = -1, lastnz = 0;
+  double cprev = 0.0;
+  M mk = 0, mlast = C.mask(0);
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    const M m = C.mask(k);
+    const bool hit = ks < 0 && x <= cs[k];
+    ks = hit ? k : ks;
+    cprev = hit ? (k > 0 ? cs[k - 1] : 0.0) : cprev;
+    mk = hit ? m : mk;
+    lastnz = m != 0 ? k : lastnz;
+    mlast = m != 0 ? m : mlast;
+  }
+  if (ks < 0) {  // unreachable for V < 1 (x <= Lambda = c_9)
+    ks = lastnz;
+    mk = mlast;
+    cprev = 0.0;
+  }
+  const int nk = popc_m(mk);
+  long long j = floor_div(__dsub_rn(x, cprev), rate[ks], T.rinv[ks]);
+  j = j > nk - 1 ? nk - 1 : j;
+  j = j < 0 ? 0 : j;
+  return nth_bit<M, G::NS>(mk, (int)j);
+}
+
 // Expand/compress the stored ghost bits (N[BX] S[BX] W[BY] E[BY]) to/from
 // site-position masks (bit of the in-region site adjacent to the ghost).
 template <class G>
@@ -442,6 +498,9 @@ __device__ __forceinline__ int div_rx(const KArgs& a, int idx) {
 #ifndef ISR_PREPAIR
 #define ISR_PREPAIR 0  // draw the next event's pair one event ahead (measured slower: registers)
 #endif
+#ifndef ISR_SELAHEAD
+#define ISR_SELAHEAD 1  // select the next event's atom right after each refold (fold_select)
+#endif
 #ifndef ISR_PSUM
 #define ISR_PSUM 0     // keep the fold's partial sums c_0..c_8 for the next selection (measured slower)
 #endif
@@ -481,6 +540,7 @@ struct Lane {
   unsigned obase;  // (r * K) * RX + c: own-edge history offset without the edge term
   M spins, gN, gS, gW, gE;
   double ts, R, V, lam, tc;
+  int site;       // ISR_SELAHEAD: atom of the next event on the current state
 #if ISR_PREPAIR
   double Rn, Vn;  // E(U) and V of the pair after the current one (drawn ahead)
 #endif
@@ -670,7 +730,9 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
 #endif
   Classes<G> C;
   C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
-#if ISR_PSUM
+#if ISR_SELAHEAD
+  L.site = fold_select<G>(C, PT, a.rate, L.V, L.lam);
+#elif ISR_PSUM
   L.lam = fold_lambda_ps<G>(C, PT, L.cs);
 #else
   L.lam = fold_lambda<G>(C, PT);
@@ -857,6 +919,9 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const
   constexpr int BX = G::BX, BY = G::BY;
   const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
   int site;
+#if ISR_SELAHEAD
+  site = L.site;
+#else
   {
     Classes<G> C;
     C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
@@ -866,6 +931,7 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const
     site = select_site2<G>(C, PT, a.rate, L.V, L.lam);
 #endif
   }
+#endif
   L.spins ^= G::ONE << site;
   const int sr = site / BX, sc = site - sr * BX;
   if (a.digest) L.dig = digest_step(L.dig, L.tc, site);
@@ -929,7 +995,9 @@ template <class G>
 __device__ __forceinline__ void refold(const KArgs& a, Lane<G>& L, const ProdTable<G>& PT) {
   Classes<G> C;
   C.build(L.spins, L.gN, L.gS, L.gW, L.gE, a.RX == 1, a.RYg == 1);
-#if ISR_PSUM
+#if ISR_SELAHEAD
+  L.site = fold_select<G>(C, PT, a.rate, L.V, L.lam);
+#elif ISR_PSUM
   L.lam = fold_lambda_ps<G>(C, PT, L.cs);
 #else
   L.lam = fold_lambda<G>(C, PT);
@@ -937,7 +1005,9 @@ __device__ __forceinline__ void refold(const KArgs& a, Lane<G>& L, const ProdTab
   L.tc = cand_time(L.ts, L.R, L.lam);
 }
 
-template <int BX, int BY, bool LOG>
+// GQ (persistent launch): the worklist is one global queue (a.work_ctr) and
+// its length is read on the device; otherwise each block owns a static tile.
+template <int BX, int BY, bool LOG, bool GQ = false>
 __global__ void ISR_LAUNCH_BOUNDS region_kernel(const KArgs a) {
   using G = Geo<BX, BY>;
   __shared__ unsigned q_next;
@@ -946,8 +1016,8 @@ __global__ void ISR_LAUNCH_BOUNDS region_kernel(const KArgs a) {
   // work: a static tile per block (lanes take items from a block queue), or
   // (work_ctr set) the whole worklist as a global queue served to a
   // persistent grid in per-warp chunks, its length read on the device
-  const bool global_q = a.work_ctr != nullptr;
-  const int n_all = a.n_work_dev ? (int)__ldcg(a.n_work_dev) : a.n_work;
+  constexpr bool global_q = GQ;
+  const int n_all = GQ && a.n_work_dev ? (int)__ldcg(a.n_work_dev) : a.n_work;
   const int tile_begin = global_q ? 0 : blockIdx.x * a.tile;
   const int tile_n = global_q ? n_all : min(a.tile, n_all - tile_begin);
   if (threadIdx.x == 0) q_next = blockDim.x;  // the first blockDim items are taken statically

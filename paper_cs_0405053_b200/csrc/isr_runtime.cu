@@ -89,10 +89,10 @@ ShapeOps make_ops() {
       int dev = 0, sms = 148, per = 1;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, isr::region_kernel<BX, BY, false>, kThreads, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, isr::region_kernel<BX, BY, false, true>, kThreads, 0);
       grid = sms * std::max(per, 1);
     }
-    isr::region_kernel<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
+    isr::region_kernel<BX, BY, false, true><<<grid, kThreads, 0, s>>>(a);
   };
   o.region_pool_persistent = [](const KArgs& a, cudaStream_t s) {
     constexpr int S = ISR_POOL_S;
@@ -143,7 +143,11 @@ ShapeOps make_ops_w() {
   o.cnt_max = 65535;
   o.region_pool = nullptr;
   o.region_pool_persistent = nullptr;
-  o.region_persistent = nullptr;
+  // one resident grid striding over the worklist, its length read on the device
+  o.region_persistent = [](const KArgs& a, cudaStream_t s) {
+    if (big_enabled()) isr::region_kernel_big<BX, BY, false><<<148 * 8, isr::BNT, 0, s>>>(a);
+    else isr::region_kernel_w<BX, BY, false><<<148 * 16, kThreads, 0, s>>>(a);
+  };
   o.sel_read_bytes = 8 * 16.0;
   auto launch = [](const KArgs& a, int n, cudaStream_t s, bool log) {
     const int warps_per_block = kThreads / 32;
@@ -314,6 +318,8 @@ struct ising_sr_ctx {
   cudaEvent_t kev0 = nullptr, kev1 = nullptr;  // around each region-kernel launch
   cudaEvent_t bev[2 * 8] = {};                 // batched iterations: around launch j (2j, 2j+1)
   int batch = 1;  // iterations enqueued per host sync (world == 1; env ISING_SR_BATCH; measured: 1 is fastest)
+  int tail_batch = 8;      // ... once fewer than tail_n regions are left (env ISING_SR_TAIL_BATCH; 1 = off)
+  int tail_n = 1 << 15;    // env ISING_SR_TAIL_N
 
   // window state
   long long w = 0;
@@ -655,11 +661,11 @@ ising_sr_status enqueue_iteration(ising_sr_ctx* c, int j) {
   return compact_worklist(c);
 }
 
-ising_sr_status run_window_batched(ising_sr_ctx* c) {
+ising_sr_status run_window_batched(ising_sr_ctx* c, int bmax) {
   ising_sr_status s;
   for (;;) {
     const int it0 = c->it;
-    const int B = std::max(1, std::min(c->batch, c->cfg.max_iterations - it0));
+    const int B = std::max(1, std::min(bmax, c->cfg.max_iterations - it0));
     for (int j = 0; j < B; ++j)
       if ((s = enqueue_iteration(c, j))) return s;
     CK(c, cudaMemcpyAsync(c->h_flags, c->d_flags, 4 * B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -829,6 +835,8 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   for (auto& e : c->bev)
     if (cudaEventCreate(&e) != cudaSuccess) return bail(ISING_SR_E_CUDA);
   if (const char* e = std::getenv("ISING_SR_BATCH")) c->batch = std::max(1, std::min(kBatch, std::atoi(e)));
+  if (const char* e = std::getenv("ISING_SR_TAIL_BATCH")) c->tail_batch = std::max(1, std::min(kBatch, std::atoi(e)));
+  if (const char* e = std::getenv("ISING_SR_TAIL_N")) c->tail_n = std::max(0, std::atoi(e));
   const int K0 = cfg->hist_capacity > 0 ? std::min(cfg->hist_capacity, ops->cnt_max) : auto_capacity(*cfg, ops->cnt_max);
   ising_sr_status s = alloc_edges(c, K0);
   if (s != ISING_SR_OK) return bail(s);
@@ -922,8 +930,10 @@ ising_sr_status ising_sr_run_window(ising_sr_ctx* c, int32_t* g_out) {
   ising_sr_status s = check(c);
   if (s) return s;
   if ((s = ising_sr_begin_window(c))) return s;
-  if (c->cfg.world <= 1 && c->ops->region_persistent && c->batch > 1) {
-    if ((s = run_window_batched(c))) return s;
+  const bool can_batch = c->cfg.world <= 1 && c->ops->region_persistent &&
+                         (!c->pool || c->ops->region_pool_persistent);
+  if (can_batch && c->batch > 1) {
+    if ((s = run_window_batched(c, c->batch))) return s;
     if (g_out) *g_out = c->g;
     return ISING_SR_OK;
   }
@@ -950,6 +960,12 @@ ising_sr_status ising_sr_run_window(ising_sr_ctx* c, int32_t* g_out) {
     if (c->it >= c->cfg.max_iterations) {
       c->in_window = false;
       return ISING_SR_E_DIVERGED;
+    }
+    // the tail of the relaxation (few regions left): several iterations per
+    // host synchronisation, the worklist length read on the device
+    if (can_batch && c->tail_batch > 1 && c->n_work < c->tail_n) {
+      if ((s = run_window_batched(c, c->tail_batch))) return s;
+      break;
     }
   }
   if (g_out) *g_out = c->g;

@@ -142,7 +142,8 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
   unsigned fmax = 0;
   bool changed = false, overflow = false;
 
-  for (int item = warp; item < a.n_work; item += nwarps) {
+  const int n_all = a.n_work_dev ? (int)__ldcg(a.n_work_dev) : a.n_work;
+  for (int item = warp; item < n_all; item += nwarps) {
     const int idx = a.wl_in ? (int)a.wl_in[item] : item;
     const int r = idx / a.RX, c = idx - r * a.RX;
     const uint32_t gid = (uint32_t)((a.row0 + r) * a.RX + c);

@@ -226,12 +226,15 @@ def test_c5_geometry_sample_bit_exact():
     {"ISING_SR_POOL": "1", "ISING_SR_POOL_REFILL": "64"},
     {"ISING_SR_POOL": "1", "ISING_SR_BATCH": "1"},
     {"ISING_SR_POOL": "1", "ISING_SR_BATCH": "8"},
+    {"ISING_SR_TAIL_BATCH": "1"},
+    {"ISING_SR_TAIL_N": "1000000000", "ISING_SR_TAIL_BATCH": "3"},
+    {"ISING_SR_BIG": "0", "ISING_SR_TAIL_N": "1000000000"},
 ])
 def test_k1_schedules_bit_exact(env, monkeypatch):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     check_against_oracle(workloads.get("c1"))
     for Lx, Ly, bx, by, T, W in [(64, 64, 4, 4, 2.0, 0.5), (32, 32, 8, 8, 2.269, 1.0), (16, 16, 1, 1, 2.0, 0.5),
-                                 (24, 24, 2, 2, 1.5, 2.0)]:
+                                 (24, 24, 2, 2, 1.5, 2.0), (64, 64, 16, 16, 2.269, 1.0), (64, 64, 32, 32, 4.0, 0.5)]:
         w = workloads.Workload("sched", Lx, Ly, bx, by, T=T, W=W, t_end=4.0, seed=9)
         check_against_oracle(w, logs=False)
