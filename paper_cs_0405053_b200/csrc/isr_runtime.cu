@@ -55,6 +55,7 @@ struct ShapeOps {
 template <int BX, int BY>
 ShapeOps make_ops() {
   using G = isr::Geo<BX, BY>;
+  constexpr bool kMB = BX * BY > 32;  // 64-bit site masks: launch bounds for 5 blocks (isr_region.cuh)
   ShapeOps o;
   o.bx = BX;
   o.by = BY;
@@ -66,11 +67,13 @@ ShapeOps make_ops() {
   o.sel_read_bytes = 5 * 16.0;
   o.region = [](const KArgs& a, int n, cudaStream_t s) {
     const int grid = (n + a.tile - 1) / a.tile;
-    isr::region_kernel<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
+    if constexpr (kMB) isr::region_kernel_mb<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
+    else isr::region_kernel<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
   };
   o.replay = [](const KArgs& a, int n, cudaStream_t s) {
     const int grid = (n + a.tile - 1) / a.tile;
-    isr::region_kernel<BX, BY, true><<<grid, kThreads, 0, s>>>(a);
+    if constexpr (kMB) isr::region_kernel_mb<BX, BY, true><<<grid, kThreads, 0, s>>>(a);
+    else isr::region_kernel<BX, BY, true><<<grid, kThreads, 0, s>>>(a);
   };
   o.region_pool = [](const KArgs& a, int n, cudaStream_t s) {
     constexpr int S = ISR_POOL_S;
@@ -318,7 +321,8 @@ struct ising_sr_ctx {
   cudaEvent_t kev0 = nullptr, kev1 = nullptr;  // around each region-kernel launch
   cudaEvent_t bev[2 * 8] = {};                 // batched iterations: around launch j (2j, 2j+1)
   int batch = 1;  // iterations enqueued per host sync (world == 1; env ISING_SR_BATCH; measured: 1 is fastest)
-  int tail_batch = 8;      // ... once fewer than tail_n regions are left (env ISING_SR_TAIL_BATCH; 1 = off)
+  int tail_batch = 1;      // ... once fewer than tail_n regions are left (env ISING_SR_TAIL_BATCH; measured
+                           // slower on c4 and c5, so off: the persistent grid costs more than the syncs)
   int tail_n = 1 << 15;    // env ISING_SR_TAIL_N
 
   // window state
