@@ -500,6 +500,9 @@ __device__ __forceinline__ int div_rx(const KArgs& a, int idx) {
 #ifndef ISR_SELAHEAD
 #define ISR_SELAHEAD 1  // select the next event's atom right after each refold (fold_select)
 #endif
+#ifndef ISR_FRESH
+#define ISR_FRESH 1  // a freshly loaded region's first pair and refold run in the shared step code
+#endif
 #ifndef ISR_PSUM
 #define ISR_PSUM 0     // keep the fold's partial sums c_0..c_8 for the next selection (measured slower)
 #endif
@@ -584,7 +587,9 @@ __device__ __forceinline__ const void* word_of(const uint8_t* p) {
 }
 __device__ __forceinline__ unsigned byte_shift(const uint8_t* p) { return 8u * (unsigned)((size_t)p & 3); }
 
-template <class G, bool LOG, class SG>
+// FULL = false: stop after the state and histories are in; the caller draws
+// the pair and refolds (sharing that code with the step)
+template <class G, bool LOG, class SG, bool FULL = true>
 __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, SG& S, const ProdTable<G>& PT,
                                           int si) {
   using M = typename G::M;
@@ -717,6 +722,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
         }
     }
   }
+  if (!FULL) return;
   // pair n: U already spent into R (carried), V selects the next atom
   double U;
   draw_pair(a.seed, L.gid, L.n, U, L.V);
@@ -912,7 +918,8 @@ __device__ __forceinline__ unsigned hist_put(const KArgs& a, unsigned om, int e,
 }
 
 // own event at tc, up to (not including) the refold; draws the next pair
-template <class G, bool LOG, bool DEFER, class SG>
+// DRAW = false: leave drawing the next pair to the caller (shared code)
+template <class G, bool LOG, bool DEFER, class SG, bool DRAW = true>
 __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const ProdTable<G>& PT, int si,
                                         unsigned& n_out, bool& overflow) {
   constexpr int BX = G::BX, BY = G::BY;
@@ -975,6 +982,7 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const
   ++L.n_ev;
   L.ts = L.tc;
   ++L.n;
+  if (!DRAW) return;
 #if ISR_PREPAIR
   L.R = L.Rn;  // pair n (drawn one event ago)
   L.V = L.Vn;
@@ -1030,7 +1038,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
   // at least REFILL lanes of the warp are idle, then publish and reload
   // together, so the (memory-heavy) load/publish path runs converged.
   const int REFILL = a.refill;
-  bool active = false, pending = false, exhausted = false;
+  bool active = false, pending = false, exhausted = false, fresh = false;
   int item = global_q ? -1 : (int)threadIdx.x;
   const unsigned lane_lt = (1u << (threadIdx.x & 31)) - 1u;
   constexpr int CHUNK = 256;        // items per global-queue claim of a warp
@@ -1074,7 +1082,8 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
           if (item < 0 && !global_q) item = (int)atomicAdd(&q_next, 1u);
           if (item >= 0 && item < tile_n) {
             const int idx = a.wl_in ? (int)a.wl_in[tile_begin + item] : tile_begin + item;
-            lane_load<G, LOG>(a, L, idx, S, PT, threadIdx.x);
+            lane_load<G, LOG, Stage, !(ISR_FRESH && !ISR_PREPAIR)>(a, L, idx, S, PT, threadIdx.x);
+            fresh = true;
             n_in += (L.hm[0] & 0xFFu) + (L.hm[1] & 0xFFu) + (L.hm[2] & 0xFFu) + (L.hm[3] & 0xFFu);
             n_cmp += ((L.om[0] >> 8) & 0xFFu) + ((L.om[1] >> 8) & 0xFFu) + ((L.om[2] >> 8) & 0xFFu) +
                      ((L.om[3] >> 8) & 0xFFu);  // latest own entries read for the diff
@@ -1089,16 +1098,32 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
       if (__all_sync(0xffffffffu, exhausted && !active)) break;
     }
     if (active) {
-      // one step per round: the earliest of (next break point, own event)
-      double tb;
-      const int d = next_bp2<G>(a, L, tb);
-      if (d < 0 && !(L.tc < a.t_w)) {
-        active = false;
-      } else {
-        if (d >= 0) bp_pre2<G>(a, L, S, threadIdx.x, d, tb);
-        else ev_pre2<G, LOG, false>(a, L, S, PT, threadIdx.x, n_out, overflow);
+      // one step per round: the earliest of (next break point, own event);
+      // a region loaded in this round only draws its pair and refolds
+      constexpr bool SHARE = ISR_FRESH && !ISR_PREPAIR;
+      bool go = true, ev = false;
+      if (!SHARE || !fresh) {
+        double tb;
+        const int d = next_bp2<G>(a, L, tb);
+        if (d < 0 && !(L.tc < a.t_w)) {
+          active = false;
+          go = false;
+        } else if (d >= 0) {
+          bp_pre2<G>(a, L, S, threadIdx.x, d, tb);
+        } else {
+          ev_pre2<G, LOG, false, Stage, !SHARE>(a, L, S, PT, threadIdx.x, n_out, overflow);
+          ev = true;
+        }
+      }
+      if (go) {
+        if (SHARE && (ev || fresh)) {  // pair n: V picks the next atom, E(U) its budget
+          double U;
+          draw_pair(a.seed, L.gid, L.n, U, L.V);
+          if (ev) L.R = expvar(U);
+        }
         refold<G>(a, L, PT);  // shared by both kinds of step
       }
+      fresh = false;
     }
   }
 

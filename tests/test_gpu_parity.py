@@ -238,3 +238,16 @@ def test_k1_schedules_bit_exact(env, monkeypatch):
                                  (24, 24, 2, 2, 1.5, 2.0), (64, 64, 16, 16, 2.269, 1.0), (64, 64, 32, 32, 4.0, 0.5)]:
         w = workloads.Workload("sched", Lx, Ly, bx, by, T=T, W=W, t_end=4.0, seed=9)
         check_against_oracle(w, logs=False)
+
+
+@pytest.mark.parametrize("b,T,t_end", [(8, 2.269, 0.05), (32, 4.0, 0.05), (2, 1.0, 0.02)])
+def test_c5_full_lattice_prefix(b, T, t_end):
+    """c5 at its full size (8192^2) for b x b regions on a prefix of the run:
+    every region's event count and digest, and all spins."""
+    w = workloads.Workload(f"c5_b{b}", 8192, 8192, b, b, T=T, W=0.25, t_end=t_end, seed=1)
+    ref = oracle.des_workload(w)
+    gpu = run_gpu(w, flags=FLAG_DIGEST)
+    assert gpu["events"] == ref["n_events"] > 10**5
+    assert np.array_equal(gpu["count"], ref["count"])
+    assert np.array_equal(gpu["digest"], ref["digest"])
+    assert np.array_equal(gpu["spins"], ref["spins"])
