@@ -60,6 +60,12 @@ typedef enum {
 /* cfg.flags */
 #define ISING_SR_FLAG_LOG_EVENTS 0x1u /* commit writes the window's compact event log (get_events) */
 #define ISING_SR_FLAG_DIGEST 0x2u     /* maintain per-region event digests (get_digests) */
+/* The paper's alternate approach to subsequent steps: at every
+ * committed time t_c = fl(w W), w >= 1, each region discards its pending
+ * budget and restarts at t_c with pair n of random-number generation w
+ * (Philox counter word 2 = w).  Unbiased (memorylessness), but the
+ * trajectory then depends on W.  Default off (the carried budget of P:726-742). */
+#define ISING_SR_FLAG_FRESH_WINDOW 0x4u
 
 /* Halo exchange between strips (world > 1).  Rank q owns a band of region
  * rows; "up" is toward region row 0 (rank q-1, periodic), "down" toward rank
@@ -184,6 +190,20 @@ ising_sr_status ising_sr_iterate(ising_sr_ctx* ctx, int32_t flags_out[2]);
 ising_sr_status ising_sr_halo_get(ising_sr_ctx* ctx, ising_sr_halo* out);
 ising_sr_status ising_sr_exchange_done(ising_sr_ctx* ctx);
 ising_sr_status ising_sr_end_iterations(ising_sr_ctx* ctx, int32_t g);
+
+/* Checkpoint / resume at a committed time (the committed state is
+ * the whole state of the simulation; the next window starts from the
+ * canonical assumption, so no boundary history is saved).  checkpoint_size
+ * gives the bytes of this rank's checkpoint; checkpoint_save writes them to a
+ * caller-owned host buffer of `cap` bytes (E_INVALID_ARG if too small);
+ * checkpoint_load restores a checkpoint into a ctx created with the same
+ * configuration (lattice, regions, rates, seed, W, flags, rank/world;
+ * E_INVALID_ARG on any mismatch or a corrupted buffer).  Both are allowed
+ * only between windows (E_STATE inside one).  A resumed run is bit-identical
+ * to the uninterrupted one. */
+ising_sr_status ising_sr_checkpoint_size(const ising_sr_ctx* ctx, int64_t* bytes);
+ising_sr_status ising_sr_checkpoint_save(ising_sr_ctx* ctx, void* buf, int64_t cap);
+ising_sr_status ising_sr_checkpoint_load(ising_sr_ctx* ctx, const void* buf, int64_t len);
 
 /* Number of kernel launches issued by this ctx so far (instrumentation). */
 int64_t ising_sr_launch_count(const ising_sr_ctx* ctx);

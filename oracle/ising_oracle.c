@@ -51,7 +51,11 @@ static double unit_from_words(uint32_t hi, uint32_t lo) {
 }
 
 void orc_pair(uint64_t seed, uint32_t stream, uint64_t n, double* U, double* V) {
-  uint32_t ctr[4] = {(uint32_t)n, (uint32_t)(n >> 32), 0u, (uint32_t)(seed >> 32)};
+  orc_pair_g(seed, stream, n, 0u, U, V);
+}
+
+void orc_pair_g(uint64_t seed, uint32_t stream, uint64_t n, uint32_t g, double* U, double* V) {
+  uint32_t ctr[4] = {(uint32_t)n, (uint32_t)(n >> 32), g, (uint32_t)(seed >> 32)};
   uint32_t key[2] = {stream, (uint32_t)seed};
   uint32_t x[4];
   orc_philox4x32_10(ctr, key, x);
@@ -383,9 +387,33 @@ int orc_des_run(const orc_cfg* cfg, const uint8_t* spins0, uint8_t* spins_out, o
   for (int32_t i = 0; i < NR; ++i) { H.h[i] = i; H.pos[i] = i; }
   for (int i = NR / 2 - 1; i >= 0; --i) heap_down(&H, i);
 
+  /* alternate approach to subsequent steps: generation of the
+   * random numbers in use and the next committed time at which every region
+   * starts afresh */
+  uint32_t gen = 0;
+  int64_t w_next = 1;
+  double t_next = cfg->fresh_W > 0.0 ? (double)w_next * cfg->fresh_W : INFINITY;
+
   for (;;) {
     int32_t r = H.h[0];
     double tau = tc[r];
+    if (t_next < cfg->t_end && !(tau < t_next)) {
+      /* wipe the slate at t_c = t_next: pending budgets are discarded, each
+       * region draws pair n of generation w (taken later than any so far) */
+      gen = (uint32_t)w_next;
+      for (int32_t q = 0; q < NR; ++q) {
+        double U, V;
+        orc_pair_g(cfg->seed, (uint32_t)q, nev[q], gen, &U, &V);
+        Rb[q] = orc_expvar(U);
+        Vv[q] = V;
+        ts[q] = t_next;
+        tc[q] = cand_time(t_next, Rb[q], lam[q]);
+      }
+      for (int i = NR / 2 - 1; i >= 0; --i) heap_down(&H, i);
+      w_next++;
+      t_next = (double)w_next * cfg->fresh_W;
+      continue;
+    }
     if (!(tau < cfg->t_end)) break;
     obs_advance(&O, cfg, out, tau);
 
@@ -418,7 +446,7 @@ int orc_des_run(const orc_cfg* cfg, const uint8_t* spins0, uint8_t* spins_out, o
     /* renew region r: next pair of its list */
     {
       double U, V;
-      orc_pair(cfg->seed, (uint32_t)r, nev[r], &U, &V);
+      orc_pair_g(cfg->seed, (uint32_t)r, nev[r], gen, &U, &V);
       Rb[r] = orc_expvar(U);
       Vv[r] = V;
       ts[r] = tau;

@@ -36,6 +36,9 @@ void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t ou
  * U from (x0,x1), V from (x2,x3): a = ((x_hi<<32)|x_lo)>>12,
  * value = ((double)a + 0.5) * 2^-52, in [2^-53, 1-2^-53]. */
 void orc_pair(uint64_t seed, uint32_t stream, uint64_t n, double* U, double* V);
+/* pair n of generation g (counter word 2 = g): the "fresh" random numbers of
+ * the alternate approach to subsequent steps; g = 0 is orc_pair */
+void orc_pair_g(uint64_t seed, uint32_t stream, uint64_t n, uint32_t g, double* U, double* V);
 
 /* E(U) = -log U evaluated with IEEE +,-,*,/ only (SURVEY §8c.3 "E(U)"),
  * the exponential variate of eq. nextau. */
@@ -53,6 +56,9 @@ typedef struct {
   double   t_end;          /* process events with tau < t_end                    */
   double   t_obs0;         /* time averages accumulate over [t_obs0, t_end)      */
   int32_t  check;          /* 1: verify incremental (B, M, N_k) after every event */
+  double   fresh_W;        /* > 0: alternate approach to subsequent steps: at
+                              every t_c = fl(w fresh_W), w >= 1, each region discards its
+                              pending budget and restarts at t_c with pair (n, generation w) */
 } orc_cfg;
 
 typedef struct {

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("ISING_SR_LIB") or os.path.join(_PKG, "libising_sr.so"
 
 FLAG_LOG_EVENTS = 0x1
 FLAG_DIGEST = 0x2
+FLAG_FRESH_WINDOW = 0x4  # alternate approach to subsequent steps
 
 STATUS = {
     0: "OK", -1: "E_INVALID_ARG", -2: "E_DIMENSION", -3: "E_PARTITION", -4: "E_DIVERGED",
@@ -72,6 +73,7 @@ EXPORTS = ["ising_sr_init", "ising_sr_run_window", "ising_sr_commit", "ising_sr_
            "ising_sr_stats_get", "ising_sr_get_spins", "ising_sr_get_events", "ising_sr_get_digests",
            "ising_sr_begin_window", "ising_sr_iterate", "ising_sr_halo_get", "ising_sr_exchange_done",
            "ising_sr_end_iterations",
+           "ising_sr_checkpoint_size", "ising_sr_checkpoint_save", "ising_sr_checkpoint_load",
            "ising_sr_launch_count", "ising_sr_destroy", "ising_sr_strerror"]
 
 
@@ -98,6 +100,9 @@ def load_library(path: str = LIB_PATH):
     L.ising_sr_halo_get.argtypes = [vp, ctypes.POINTER(Halo)]
     L.ising_sr_exchange_done.argtypes = [vp]
     L.ising_sr_end_iterations.argtypes = [vp, i32]
+    L.ising_sr_checkpoint_size.argtypes = [vp, ctypes.POINTER(i64)]
+    L.ising_sr_checkpoint_save.argtypes = [vp, vp, i64]
+    L.ising_sr_checkpoint_load.argtypes = [vp, vp, i64]
     L.ising_sr_launch_count.argtypes = [vp]
     L.ising_sr_launch_count.restype = i64
     L.ising_sr_destroy.argtypes = [vp]
@@ -237,6 +242,19 @@ class IsingSR:
         _check(self._L.ising_sr_get_digests(self._h, d.ctypes.data if want_d else None, c.ctypes.data),
                "ising_sr_get_digests")
         return (d if want_d else None), c
+
+    def checkpoint(self) -> bytes:
+        """The committed state at the current committed time (between windows)."""
+        n = ctypes.c_int64()
+        _check(self._L.ising_sr_checkpoint_size(self._h, ctypes.byref(n)), "ising_sr_checkpoint_size")
+        buf = ctypes.create_string_buffer(n.value)
+        _check(self._L.ising_sr_checkpoint_save(self._h, buf, n.value), "ising_sr_checkpoint_save")
+        return buf.raw
+
+    def restore(self, data: bytes):
+        """Resume from checkpoint() of a ctx with the same configuration."""
+        buf = ctypes.create_string_buffer(data, len(data))
+        _check(self._L.ising_sr_checkpoint_load(self._h, buf, len(data)), "ising_sr_checkpoint_load")
 
     def launch_count(self) -> int:
         return int(self._L.ising_sr_launch_count(self._h))

@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
       B.gW = h.z;
       B.gE = h.w;
     }
-    double ts = a.in.ts[idx], R = a.in.R[idx];
+    double ts = a.fresh_w ? a.t_c : a.in.ts[idx], R = a.in.R[idx];
     uint32_t n = a.in.n[idx];
     unsigned long long dig = a.digest ? a.in.dig[idx] : 0ull;
     unsigned n_ev_r = 0, bev = 0;
@@ -291,7 +291,8 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
     }
 
     double U, V;
-    draw_pair(a.seed, gid, n, U, V);
+    draw_pair(a.seed, gid, n, U, V, a.gen);
+    if (a.fresh_w) R = expvar(U);  // the slate is wiped at t_c
     double lam = big_fold(B, a.rate);
     double tc = cand_time(ts, R, lam);
 
@@ -436,7 +437,7 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
         ++n_ev_r;
         ts = tc;
         ++n;
-        draw_pair(a.seed, gid, n, U, V);
+        draw_pair(a.seed, gid, n, U, V, a.gen);
         R = expvar(U);
       }
       lam = big_fold(B, a.rate);

@@ -56,9 +56,11 @@ __device__ __forceinline__ double unit52(uint32_t hi, uint32_t lo) {
   return __dmul_rn(__dadd_rn(__ull2double_rn(a), 0.5), 0x1p-52);
 }
 
+// gen: generation of the random numbers (counter word 2), 0 except in the
+// alternate approach to subsequent steps, where window w uses w
 __device__ __forceinline__ void draw_pair(unsigned long long seed, uint32_t region, uint32_t n,
-                                          double& U, double& V) {
-  U4 c{n, 0u, 0u, (uint32_t)(seed >> 32)};
+                                          double& U, double& V, uint32_t gen = 0u) {
+  U4 c{n, 0u, gen, (uint32_t)(seed >> 32)};
   const U4 x = philox4x32_10(c, region, (uint32_t)seed);
   U = unit52(x.x, x.y);
   V = unit52(x.z, x.w);

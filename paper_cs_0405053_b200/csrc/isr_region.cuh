@@ -90,6 +90,9 @@ struct KArgs {
   int first;          // window's first iteration: canonical assumption
   int digest;
   double t_w;         // window end
+  double t_c;         // window start (committed time)
+  int fresh_w;        // alternate approach: every region restarts at t_c with fresh numbers
+  unsigned gen;       // generation of the random numbers in use (window index if fresh_w, else 0)
   unsigned long long seed;
   double rate[10];
   const uint32_t* wl_in;   // regions to recompute (nullptr: all regions)
@@ -639,7 +642,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   // committed state (the old tau_m becomes tau_0)
   L.spins = (M)((const typename G::ST*)a.in.spins)[idx];
   expand_halo<G>((unsigned long long)((const typename G::HT*)a.in.halo)[idx], L.gN, L.gS, L.gW, L.gE);
-  L.ts = a.in.ts[idx];
+  L.ts = a.fresh_w ? a.t_c : a.in.ts[idx];  // fresh_w: every region starts afresh at t_c
   L.R = a.in.R[idx];
   L.n = a.in.n[idx];
   L.dig = a.digest ? a.in.dig[idx] : 0ull;
@@ -725,11 +728,12 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   if (!FULL) return;
   // pair n: U already spent into R (carried), V selects the next atom
   double U;
-  draw_pair(a.seed, L.gid, L.n, U, L.V);
+  draw_pair(a.seed, L.gid, L.n, U, L.V, a.gen);
+  if (a.fresh_w) L.R = expvar(U);  // the slate is wiped at t_c: the budget restarts from pair n
 #if ISR_PREPAIR
   {
     double U1;
-    draw_pair(a.seed, L.gid, L.n + 1, U1, L.Vn);
+    draw_pair(a.seed, L.gid, L.n + 1, U1, L.Vn, a.gen);
     L.Rn = expvar(U1);
   }
 #endif
@@ -988,12 +992,12 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const
   L.V = L.Vn;
   {
     double U1;  // pair n + 1, needed only at the next event
-    draw_pair(a.seed, L.gid, L.n + 1, U1, L.Vn);
+    draw_pair(a.seed, L.gid, L.n + 1, U1, L.Vn, a.gen);
     L.Rn = expvar(U1);
   }
 #else
   double U;
-  draw_pair(a.seed, L.gid, L.n, U, L.V);
+  draw_pair(a.seed, L.gid, L.n, U, L.V, a.gen);
   L.R = expvar(U);
 #endif
 }
@@ -1118,8 +1122,8 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
       if (go) {
         if (SHARE && (ev || fresh)) {  // pair n: V picks the next atom, E(U) its budget
           double U;
-          draw_pair(a.seed, L.gid, L.n, U, L.V);
-          if (ev) L.R = expvar(U);
+          draw_pair(a.seed, L.gid, L.n, U, L.V, a.gen);
+          if (ev || a.fresh_w) L.R = expvar(U);  // (fresh_w: a loaded region restarts its budget at t_c)
         }
         refold<G>(a, L, PT);  // shared by both kinds of step
       }

@@ -339,7 +339,7 @@ struct ising_sr_ctx {
   double win_bytes = 0.0;
   int win_f = 0;
   long long launches = 0;
-  int refill = 24;  // K1 batched-refill threshold (env ISING_SR_REFILL for tuning)
+  int refill = 28;  // K1 batched-refill threshold (env ISING_SR_REFILL; 28 measured best after the shared fresh-load step)
   bool pool = false;    // slot-pool K1 for lane shapes (env ISING_SR_POOL=1; measured slower so far)
   int pool_refill = ISR_POOL_S / 2;  // free slots that trigger a pool refill (env ISING_SR_POOL_REFILL)
   ising_sr_stats stats;
@@ -475,6 +475,9 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   a.first = first ? 1 : 0;
   a.digest = (c->cfg.flags & ISING_SR_FLAG_DIGEST) ? 1 : 0;
   a.t_w = c->t_w;
+  a.t_c = c->t_c;
+  a.fresh_w = (c->cfg.flags & ISING_SR_FLAG_FRESH_WINDOW) ? 1 : 0;
+  a.gen = a.fresh_w ? (unsigned)c->w : 0u;
   a.seed = c->cfg.seed;
   for (int k = 0; k < 10; ++k) a.rate[k] = c->cfg.rate[k];
   a.dirty = c->dirty;
@@ -1127,6 +1130,119 @@ ising_sr_status ising_sr_get_digests(ising_sr_ctx* c, uint64_t* digest, uint64_t
     for (size_t i = 0; i < tmp.size(); ++i) count[i] = tmp[i];
   }
   CK(c, cudaStreamSynchronize(c->stream));
+  return ISING_SR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// checkpoint / resume: header + the committed state arrays of this rank
+// ---------------------------------------------------------------------------
+namespace {
+struct CkptHeader {
+  char magic[8];  // "ISRCKPT1"
+  int32_t Lx, Ly, bx, by, rank, world;
+  uint32_t flags, pad;
+  uint64_t seed;
+  double W, t_end, rate[10];
+  int64_t w;  // committed windows: t_c = fl(w W)
+  int64_t windows, events_total;
+  int64_t nreg;
+  int64_t bytes[6];  // spins, halo, ts, R, n, dig
+  uint64_t checksum;  // FNV-1a over the arrays
+};
+
+void state_bytes(const ising_sr_ctx* c, int64_t b[6]) {
+  const int64_t n = c->nreg;
+  b[0] = n * (int64_t)c->ops->spin_bytes;
+  b[1] = n * (int64_t)c->ops->halo_bytes;
+  b[2] = n * 8;
+  b[3] = n * 8;
+  b[4] = n * 4;
+  b[5] = n * 8;
+}
+
+uint64_t fnv1a(const unsigned char* p, int64_t n, uint64_t h) {
+  for (int64_t i = 0; i < n; ++i) h = (h ^ p[i]) * 0x100000001b3ULL;
+  return h;
+}
+}  // namespace
+
+ising_sr_status ising_sr_checkpoint_size(const ising_sr_ctx* c, int64_t* bytes) {
+  if (!c || !bytes) return ISING_SR_E_INVALID_ARG;
+  int64_t b[6];
+  state_bytes(c, b);
+  *bytes = (int64_t)sizeof(CkptHeader) + b[0] + b[1] + b[2] + b[3] + b[4] + b[5];
+  return c->sticky;
+}
+
+ising_sr_status ising_sr_checkpoint_save(ising_sr_ctx* c, void* buf, int64_t cap) {
+  ising_sr_status s = check(c);
+  if (s) return s;
+  if (!buf) return ISING_SR_E_INVALID_ARG;
+  if (c->in_window) return ISING_SR_E_STATE;
+  int64_t need = 0;
+  ising_sr_checkpoint_size(c, &need);
+  if (cap < need) return ISING_SR_E_INVALID_ARG;
+  CkptHeader h;
+  std::memset(&h, 0, sizeof h);
+  std::memcpy(h.magic, "ISRCKPT1", 8);
+  h.Lx = c->cfg.Lx; h.Ly = c->cfg.Ly; h.bx = c->cfg.bx; h.by = c->cfg.by;
+  h.rank = c->cfg.rank; h.world = c->cfg.world;
+  h.flags = c->cfg.flags;
+  h.seed = c->cfg.seed;
+  h.W = c->cfg.W; h.t_end = c->cfg.t_end;
+  for (int k = 0; k < 10; ++k) h.rate[k] = c->cfg.rate[k];
+  h.w = c->w;
+  h.windows = c->stats.windows;
+  h.events_total = c->stats.events_total;
+  h.nreg = c->nreg;
+  state_bytes(c, h.bytes);
+  unsigned char* p = (unsigned char*)buf + sizeof(CkptHeader);
+  const StateView& st = c->st[c->comm];
+  void* src[6] = {st.spins, st.halo, st.ts, st.R, st.n, st.dig};
+  unsigned char* q = p;
+  for (int i = 0; i < 6; ++i) {
+    CK(c, cudaMemcpyAsync(q, src[i], (size_t)h.bytes[i], cudaMemcpyDeviceToHost, c->stream));
+    q += h.bytes[i];
+  }
+  CK(c, cudaStreamSynchronize(c->stream));
+  h.checksum = fnv1a(p, need - (int64_t)sizeof(CkptHeader), 0xcbf29ce484222325ULL);
+  std::memcpy(buf, &h, sizeof h);
+  return ISING_SR_OK;
+}
+
+ising_sr_status ising_sr_checkpoint_load(ising_sr_ctx* c, const void* buf, int64_t len) {
+  ising_sr_status s = check(c);
+  if (s) return s;
+  if (!buf || len < (int64_t)sizeof(CkptHeader)) return ISING_SR_E_INVALID_ARG;
+  if (c->in_window) return ISING_SR_E_STATE;
+  CkptHeader h;
+  std::memcpy(&h, buf, sizeof h);
+  int64_t b[6], need = 0;
+  state_bytes(c, b);
+  ising_sr_checkpoint_size(c, &need);
+  bool ok = std::memcmp(h.magic, "ISRCKPT1", 8) == 0 && len >= need && h.Lx == c->cfg.Lx && h.Ly == c->cfg.Ly &&
+            h.bx == c->cfg.bx && h.by == c->cfg.by && h.rank == c->cfg.rank && h.world == c->cfg.world &&
+            h.flags == c->cfg.flags && h.seed == c->cfg.seed && h.W == c->cfg.W && h.nreg == c->nreg &&
+            h.w >= 0;
+  for (int k = 0; k < 10 && ok; ++k) ok = h.rate[k] == c->cfg.rate[k];
+  for (int i = 0; i < 6 && ok; ++i) ok = h.bytes[i] == b[i];
+  const unsigned char* p = (const unsigned char*)buf + sizeof(CkptHeader);
+  if (ok) ok = fnv1a(p, need - (int64_t)sizeof(CkptHeader), 0xcbf29ce484222325ULL) == h.checksum;
+  if (!ok) return ISING_SR_E_INVALID_ARG;
+  const StateView& st = c->st[c->comm];
+  void* dst[6] = {st.spins, st.halo, st.ts, st.R, st.n, st.dig};
+  for (int i = 0; i < 6; ++i) {
+    CK(c, cudaMemcpyAsync(dst[i], p, (size_t)b[i], cudaMemcpyHostToDevice, c->stream));
+    p += b[i];
+  }
+  CK(c, cudaStreamSynchronize(c->stream));
+  c->w = h.w;
+  c->t_c = (double)c->w * c->cfg.W;
+  c->in_window = false;
+  c->converged = false;
+  c->stats.windows = h.windows;
+  c->stats.events_total = h.events_total;
+  c->stats.t_c = c->t_c < c->cfg.t_end ? c->t_c : c->cfg.t_end;
   return ISING_SR_OK;
 }
 

@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
     const uint4 h = ((const uint4*)a.in.halo)[idx];  // gN, gS, gW (bit per row), gE
     uint32_t gN = h.x, gS = h.y;
     uint32_t gWb = lane < BY ? (h.z >> lane) & 1u : 0u, gEb = lane < BY ? (h.w >> lane) & 1u : 0u;
-    double ts = a.in.ts[idx], R = a.in.R[idx];
+    double ts = a.fresh_w ? a.t_c : a.in.ts[idx], R = a.in.R[idx];
     uint32_t n = a.in.n[idx];
     unsigned long long dig = a.digest ? a.in.dig[idx] : 0ull;
     unsigned n_ev_r = 0, bev = 0;
@@ -214,7 +214,8 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
     const unsigned obase = (unsigned)(((long long)r * a.K) * a.RX + c);
 
     double U, V;
-    draw_pair(a.seed, gid, n, U, V);
+    draw_pair(a.seed, gid, n, U, V, a.gen);
+    if (a.fresh_w) R = expvar(U);  // the slate is wiped at t_c
     WClasses C = wbuild<BX, BY>(row, gN, gS, gWb, gEb, wrapX, wrapY);
     int N[10];
     wcounts(C, N);
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
       lam = wfold(N, a.rate);
       if (ev) {
         ++n;
-        draw_pair(a.seed, gid, n, U, V);
+        draw_pair(a.seed, gid, n, U, V, a.gen);
         R = expvar(U);
       }
       tc = cand_time(ts, R, lam);

@@ -251,3 +251,71 @@ def test_c5_full_lattice_prefix(b, T, t_end):
     assert np.array_equal(gpu["count"], ref["count"])
     assert np.array_equal(gpu["digest"], ref["digest"])
     assert np.array_equal(gpu["spins"], ref["spins"])
+
+
+# ---------------------------------------------------------------------------
+# the alternate approach to subsequent steps: every window starts
+# afresh with random numbers of a new generation; the oracle implements the
+# same rule (fresh_W), every K1 form must match it bit for bit
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("geom", [
+    (32, 32, 4, 4, 2.269, 0.5, 4.0),
+    (16, 16, 1, 1, 2.0, 0.3, 2.0),
+    (64, 64, 8, 8, 1.5, 0.7, 4.0),
+    (64, 64, 16, 16, 2.269, 1.0, 4.0),
+    (64, 64, 32, 32, 4.0, 0.25, 2.0),
+])
+@pytest.mark.parametrize("env", [{}, {"ISING_SR_BIG": "0", "ISING_SR_POOL": "1"}])
+def test_fresh_window_variant_bit_exact(geom, env, monkeypatch):
+    from paper_cs_0405053_b200 import FLAG_FRESH_WINDOW
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    Lx, Ly, bx, by, T, W, t_end = geom
+    w = workloads.Workload("fw", Lx, Ly, bx, by, T=T, W=W, t_end=t_end, seed=4)
+    ref = oracle.des_workload(w, fresh_W=W)
+    gpu = run_gpu(w, flags=FLAG_DIGEST | FLAG_FRESH_WINDOW)
+    assert gpu["events"] == ref["n_events"]
+    assert np.array_equal(gpu["count"], ref["count"])
+    assert np.array_equal(gpu["spins"], ref["spins"])
+    assert np.array_equal(gpu["digest"], ref["digest"])
+    base = oracle.des_workload(w)
+    assert not np.array_equal(base["digest"], ref["digest"])  # the variant changes the trajectory
+
+
+def test_checkpoint_resume_bit_exact():
+    """A run checkpointed at a committed time and resumed in a fresh ctx is
+    bit-identical to the uninterrupted run; a corrupted checkpoint or one of
+    another configuration is refused."""
+    from paper_cs_0405053_b200 import FLAG_FRESH_WINDOW
+    for flags in (FLAG_DIGEST, FLAG_DIGEST | FLAG_FRESH_WINDOW):
+        w = workloads.Workload("ck", 64, 64, 4, 4, T=2.269, W=0.5, t_end=4.0, seed=6)
+        full = run_gpu(w, flags=flags)
+        a = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed, flags=flags)
+        for _ in range(3):
+            a.run_window()
+            a.commit()
+        ck = a.checkpoint()
+        a.close()
+        b = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed, flags=flags)
+        b.restore(ck)
+        ev = 0
+        while True:
+            try:
+                b.run_window()
+            except IsingSRError as e:
+                assert e.status == -9
+                break
+            ev += b.commit()
+        dig, cnt = b.digests()
+        assert np.array_equal(dig, full["digest"]) and np.array_equal(cnt, full["count"])
+        assert np.array_equal(b.spins(), full["spins"])
+        assert b.stats()["events_total"] == full["events"]
+        bad = bytearray(ck)
+        bad[-1] ^= 1
+        with pytest.raises(IsingSRError):
+            b.restore(bytes(bad))
+        b.close()
+        other = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed + 1, flags=flags)
+        with pytest.raises(IsingSRError):
+            other.restore(ck)
+        other.close()

@@ -181,3 +181,56 @@ def test_no_interaction_union_of_independent_runs():
         sel = r["log_region"] == q
         assert np.array_equal(r["log_t"][sel], one["log_t"])
         assert np.array_equal(r["log_site"][sel], one["log_site"])
+
+
+# ---------------------------------------------------------------------------
+# the alternate approach to subsequent steps: at every committed
+# time t_c = w W every region discards its pending budget and starts afresh
+# with random numbers of a new generation.  Unbiased by memorylessness of the
+# Poisson process (the paper's claim), so the equilibrium and the T = inf
+# relaxation are unchanged while the trajectory is not.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("bx,by", [(1, 1), (3, 3)])
+def test_fresh_window_boltzmann_3x3(bx, by):
+    T = 2.0
+    ex = boltzmann_averages(3, 3, T)
+    rates = workloads.rate_table(T)
+    vals = {"E": [], "absM": [], "M2": []}
+    for seed in range(1, 17):
+        s0 = workloads.initial_spins(3, 3, "random", seed=seed)
+        r = oracle.des_run(3, 3, bx, by, rates, seed, s0, 50000.0, t_obs0=20.0, fresh_W=0.37)
+        dt, Bi, Mi, aMi, M2i = r["obs"]
+        vals["E"].append(-Bi / dt)
+        vals["absM"].append(aMi / dt)
+        vals["M2"].append(M2i / dt)
+    for q in vals:
+        a = np.array(vals[q])
+        se = a.std(ddof=1) / math.sqrt(len(a))
+        assert abs(a.mean() - ex[q]) < 4 * se + 1e-9, (q, a.mean(), ex[q], se)
+
+
+def test_fresh_window_infinite_temperature_closed_form():
+    L, b = 64, 4
+    N = L * L
+    ts = [0.1, 0.25, 0.5, 1.0]
+    ms = []
+    for seed in range(1, 9):
+        s0 = workloads.initial_spins(L, L, "up")
+        r = oracle.des_run(L, L, b, b, [1.0] * 10, seed, s0, 1.0, sample_t=ts, fresh_W=0.15)
+        ms.append(r["sample_M"] / N)
+    ms = np.array(ms)
+    for i, t in enumerate(ts):
+        sd = math.sqrt((1 - math.exp(-4 * t)) / N / ms.shape[0])
+        assert abs(ms[:, i].mean() - math.exp(-2 * t)) < 4.5 * sd
+
+
+def test_fresh_window_identity_and_effect():
+    w = workloads.Workload("fw", 32, 32, 4, 4, T=2.269, W=0.5, t_end=3.0, seed=3)
+    base = oracle.des_workload(w)
+    # no committed time before t_end: nothing is wiped, bit-identical
+    same = oracle.des_workload(w, fresh_W=5.0)
+    assert np.array_equal(same["digest"], base["digest"]) and same["n_events"] == base["n_events"]
+    # wiping at t_c = 0.5, 1.0, ... changes the trajectory
+    fresh = oracle.des_workload(w, fresh_W=0.5)
+    assert not np.array_equal(fresh["digest"], base["digest"])
+    assert fresh["check_failures"] == 0
