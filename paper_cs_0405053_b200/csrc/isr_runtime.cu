@@ -7,6 +7,7 @@
 // convergence commits the window by swapping the committed and tentative
 // state buffers.  Device memory layout: DESIGN.md §5.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys / ncu --nvtx
 
 #include <algorithm>
 #include <cmath>
@@ -23,6 +24,12 @@
 #include "isr_big.cuh"
 
 namespace {
+
+// NVTX range for the lifetime of a scope (window / iteration / commit)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 using isr::EdgeView;
 using isr::GhostView;
@@ -518,6 +525,7 @@ ising_sr_status compact_worklist(ising_sr_ctx* c) {
 }
 
 ising_sr_status launch_iteration(ising_sr_ctx* c) {
+  NvtxRange nv("isr iteration");
   ++c->it;
   const unsigned K = ++c->Kglob;
   const bool first = c->it == 1;
@@ -641,6 +649,7 @@ void start_window(ising_sr_ctx* c) {
 // those of the one-iteration-per-sync loop.
 // ---------------------------------------------------------------------------
 ising_sr_status enqueue_iteration(ising_sr_ctx* c, int j) {
+  NvtxRange nv("isr iteration (batched)");
   ++c->it;
   const unsigned K = ++c->Kglob;
   const bool first = c->it == 1;
@@ -934,6 +943,7 @@ ising_sr_status ising_sr_end_iterations(ising_sr_ctx* c, int32_t g) {
 }
 
 ising_sr_status ising_sr_run_window(ising_sr_ctx* c, int32_t* g_out) {
+  NvtxRange nv("isr window");
   ising_sr_status s = check(c);
   if (s) return s;
   if ((s = ising_sr_begin_window(c))) return s;
@@ -980,6 +990,7 @@ ising_sr_status ising_sr_run_window(ising_sr_ctx* c, int32_t* g_out) {
 }
 
 ising_sr_status ising_sr_commit(ising_sr_ctx* c, int64_t* events_out) {
+  NvtxRange nv("isr commit");
   ising_sr_status s = check(c);
   if (s) return s;
   if (!c->in_window || !c->converged) return ISING_SR_E_STATE;
