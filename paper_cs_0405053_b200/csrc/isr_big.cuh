@@ -210,6 +210,134 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
     uint32_t n = a.in.n[idx];
     unsigned long long dig = a.digest ? a.in.dig[idx] : 0ull;
     unsigned n_ev_r = 0, bev = 0;
+    // ---- incoming histories: head entry + the next one in flight ----
+    unsigned hcnt[4], hidx[4], hsrc[4], hoff[4];
+    double ht[4], hn[4];
+    unsigned hp = 0, hq = 0;  // byte d: position of the head / next entry of direction d
+    unsigned chg = 0;         // bit d: incoming history d changed in the previous iteration
+    unsigned qd[4];           // ... its first changed entry
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      hcnt[d] = 0; hidx[d] = 0; hsrc[d] = 0; hoff[d] = 0; ht[d] = dinf(); hn[d] = dinf(); qd[d] = 0;
+      const bool axis_off = (d < 2) ? wrapY : wrapX;
+      if (a.first || axis_off) continue;
+      const bool ghost = a.world > 1 && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
+      if (ghost) {
+        const GhostView& gv = d == EDGE_N ? a.gh_up : a.gh_down;
+        hcnt[d] = gv.cnt[c];
+        hsrc[d] = d == EDGE_N ? 2u : 3u;
+        hoff[d] = (unsigned)c;
+        if (gv.stamp[c] == K - 1) chg |= 1u << d;  // first changed entry unknown: 0
+      } else {
+        const int nr = d == EDGE_N ? wdec(r, a.RYl) : d == EDGE_S ? winc(r, a.RYl) : r;
+        const int nc = d == EDGE_W ? wdec(c, a.RX) : d == EDGE_E ? winc(c, a.RX) : c;
+        const unsigned long long v = latest_edge_word(a.sel, ((long long)nr * a.RX + nc) * 4 + (d ^ 1), K);
+        if (word_valid(v, K0)) {
+          hcnt[d] = ew_count(v);
+          hsrc[d] = ew_slot(v);
+          hoff[d] = ((unsigned)nr * (unsigned)a.K) * (unsigned)a.RX + (unsigned)nc;
+          if ((unsigned)(v >> 32) == K - 1) {
+            chg |= 1u << d;
+            qd[d] = ew_fd(v);
+          }
+        }
+      }
+      n_in += hcnt[d];
+    }
+
+    // ---- own latest histories ----
+    unsigned oc[4], pc[4], ps[4], dv[4], wh[4], k0[4], fdk[4];
+    double ot[4];
+    unsigned op = 0;  // byte e: position of the old entry at index oc[e]
+    const unsigned obase = (unsigned)(((long long)r * a.K) * a.RX + c);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      oc[e] = 0; pc[e] = 0; ps[e] = 0; dv[e] = 0; wh[e] = 0; ot[e] = 0.0; k0[e] = 0; fdk[e] = 0;
+      if (LOG) continue;
+      const ulonglong2 wp = reinterpret_cast<const ulonglong2*>(a.sel)[(long long)idx * 4 + e];
+      const int li = latest_index(wp, K);
+      const unsigned long long v = li ? wp.y : wp.x;
+      ps[e] = ew_slot(v);
+      pc[e] = word_valid(v, K0) ? ew_count(v) : 0u;
+      wh[e] = (unsigned)(li ^ 1);
+      n_cmp += pc[e];
+    }
+
+    // ---- resume: the trajectory of the region's last recomputation in this
+    // window (its step log) is unchanged up to the first changed incoming
+    // entry; replay that prefix instead of re-simulating it ----
+    const long long lb = (long long)idx * a.LC;
+    unsigned lpos = 0;  // steps of this recomputation (log length)
+    if (!LOG && a.resume && !a.first && chg) {
+      const uint2 meta = a.lg_meta[idx];
+      if (meta.x >= K0 && meta.y != 0xffffffffu) {
+        const unsigned len = meta.y;
+        // earliest time at which an input differs: the new entry q_d ...
+        double tst = dinf();
+#pragma unroll
+        for (int d = 0; d < 4; ++d)
+          if (((chg >> d) & 1u) && qd[d] < hcnt[d])
+            tst = fmin(tst, src_t(a, hsrc[d], d ^ 1)[hoff[d] + qd[d] * (unsigned)a.RX]);
+        // ... or the old entry q_d, consumed as that direction's q_d-th break point
+        unsigned cntd = 0;  // byte d: break points of direction d so far
+        unsigned i = 0;
+        for (; i < len; ++i) {
+          const double ti = a.lg_t[lb + i];
+          if (!(ti < tst)) break;
+          const unsigned code = a.lg_c[lb + i];
+          if (code & 0x8000u) {
+            const int d = (int)((code >> 12) & 3u);
+            const unsigned kd = (cntd >> (8 * d)) & 0xFFu;
+            if (((chg >> d) & 1u) && kd == qd[d]) {
+              tst = ti;
+              break;
+            }
+            if (kd < 255u) cntd += 1u << (8 * d);
+          }
+        }
+        while (i > 0 && !(a.lg_t[lb + i - 1] < tst)) --i;  // steps at time tst are re-simulated
+        // replay steps [0, i): flips, cursors, own-history counts, digest
+        for (unsigned j = 0; j < i; ++j) {
+          const unsigned code = a.lg_c[lb + j];
+          if (code & 0x8000u) {
+            const int d = (int)((code >> 12) & 3u);
+            const int p = (int)(code & 0xFFu);
+            if (d == EDGE_N) B.gN ^= 1u << p;
+            else if (d == EDGE_S) B.gS ^= 1u << p;
+            else if (d == EDGE_W) B.gW ^= 1u << p;
+            else B.gE ^= 1u << p;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) hidx[q] += q == d ? 1u : 0u;
+          } else {
+            const int site = (int)code;
+            const int sr = site / BX, sc = site - sr * BX;
+            SM.rows[sr][t] ^= 1u << sc;
+            if (a.digest) dig = digest_step(dig, a.lg_t[lb + j], site);
+            ++n_ev_r;
+            bool on_edge = false;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const bool on = e == EDGE_N ? (!wrapY && sr == 0)
+                            : e == EDGE_S ? (!wrapY && sr == BY - 1)
+                            : e == EDGE_W ? (!wrapX && sc == 0)
+                                          : (!wrapX && sc == BX - 1);
+              oc[e] += on ? 1u : 0u;
+              on_edge |= on;
+            }
+            bev += on_edge ? 1u : 0u;
+          }
+        }
+        if (i > 0) {
+          ts = a.lg_t[lb + i - 1];
+          R = a.lg_R[lb + i - 1];
+        }
+        n += n_ev_r;
+        lpos = i;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) k0[e] = oc[e];  // own-history prefix == the latest history's
+      }
+    }
+
     // class counts and per-row class counts of the committed state
     for (int q = 0; q < BigSmem<BX, BY>::RQ; ++q) {
       uint32_t w[10];
@@ -232,61 +360,27 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
       }
     }
 
-    // ---- incoming histories: head entry + the next one in flight ----
-    unsigned hcnt[4], hidx[4], hsrc[4], hoff[4];
-    double ht[4], hn[4];
-    unsigned hp = 0, hq = 0;  // byte d: position of the head / next entry of direction d
+    // incoming heads at the cursors: the head entry and the next one in flight
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
-      hcnt[d] = 0; hidx[d] = 0; hsrc[d] = 0; hoff[d] = 0; ht[d] = dinf(); hn[d] = dinf();
-      const bool axis_off = (d < 2) ? wrapY : wrapX;
-      if (a.first || axis_off) continue;
-      const bool ghost = a.world > 1 && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
-      if (ghost) {
-        hcnt[d] = (d == EDGE_N ? a.gh_up : a.gh_down).cnt[c];
-        hsrc[d] = d == EDGE_N ? 2u : 3u;
-        hoff[d] = (unsigned)c;
-      } else {
-        const int nr = d == EDGE_N ? wdec(r, a.RYl) : d == EDGE_S ? winc(r, a.RYl) : r;
-        const int nc = d == EDGE_W ? wdec(c, a.RX) : d == EDGE_E ? winc(c, a.RX) : c;
-        const unsigned long long v = latest_edge_word(a.sel, ((long long)nr * a.RX + nc) * 4 + (d ^ 1), K);
-        if (word_valid(v, K0)) {
-          hcnt[d] = ew_count(v);
-          hsrc[d] = ew_slot(v);
-          hoff[d] = ((unsigned)nr * (unsigned)a.K) * (unsigned)a.RX + (unsigned)nc;
-        }
-      }
-      if (hcnt[d] > 0) {
+      const unsigned x = hidx[d];
+      if (x < hcnt[d]) {
         const double* T = src_t(a, hsrc[d], d ^ 1);
         const uint8_t* P = src_p(a, hsrc[d], d ^ 1);
-        ht[d] = T[hoff[d]];
-        hp |= (unsigned)P[hoff[d]] << (8 * d);
-        if (hcnt[d] > 1) {
-          hn[d] = T[hoff[d] + (unsigned)a.RX];
-          hq |= (unsigned)P[hoff[d] + (unsigned)a.RX] << (8 * d);
+        ht[d] = T[hoff[d] + x * (unsigned)a.RX];
+        hp |= (unsigned)P[hoff[d] + x * (unsigned)a.RX] << (8 * d);
+        if (x + 1 < hcnt[d]) {
+          hn[d] = T[hoff[d] + (x + 1) * (unsigned)a.RX];
+          hq |= (unsigned)P[hoff[d] + (x + 1) * (unsigned)a.RX] << (8 * d);
         }
       }
-      n_in += hcnt[d];
     }
-    // ---- own latest histories (diff at write time, old entry read ahead) ----
-    unsigned oc[4], pc[4], ps[4], dv[4], wh[4];
-    double ot[4];
-    unsigned op = 0;  // byte e: position of the old entry at index oc[e]
-    const unsigned obase = (unsigned)(((long long)r * a.K) * a.RX + c);
+    // the old own entry at each edge's write position, read ahead for the diff
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      oc[e] = 0; pc[e] = 0; ps[e] = 0; dv[e] = 0; wh[e] = 0; ot[e] = 0.0;
-      if (LOG) continue;
-      const ulonglong2 wp = reinterpret_cast<const ulonglong2*>(a.sel)[(long long)idx * 4 + e];
-      const int li = latest_index(wp, K);
-      const unsigned long long v = li ? wp.y : wp.x;
-      ps[e] = ew_slot(v);
-      pc[e] = word_valid(v, K0) ? ew_count(v) : 0u;
-      wh[e] = (unsigned)(li ^ 1);
-      n_cmp += pc[e];
-      if (pc[e] > 0) {
-        ot[e] = src_t(a, ps[e], e)[obase];
-        op |= (unsigned)src_p(a, ps[e], e)[obase] << (8 * e);
+      if (!LOG && oc[e] < pc[e]) {
+        ot[e] = src_t(a, ps[e], e)[obase + oc[e] * (unsigned)a.RX];
+        op |= (unsigned)src_p(a, ps[e], e)[obase + oc[e] * (unsigned)a.RX] << (8 * e);
       }
     }
 
@@ -338,12 +432,14 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
         }
       }
       if (!bp && !(tc < a.t_w)) break;
+      unsigned code = 0;  // step log code: site, or 0x8000 | direction << 12 | position
       if (bp) {
         // break point (eqs. lambdataua..newtau): budget at the old rate
         const double Rn = __dsub_rn(R, __dmul_rn(lam, __dsub_rn(tb, ts)));
         R = Rn < 0.0 ? 0.0 : Rn;
         ts = tb;
         const int p = (int)((hp >> (8 * dstar)) & 0xFFu);
+        code = 0x8000u | ((unsigned)dstar << 12) | (unsigned)p;
         // the in-region site next to the flipped halo spin and its change of
         // up-neighbour count
         int sr, sc;
@@ -374,6 +470,7 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
         // own event at tc
         const int site = big_select<BX, BY>(B, a.rate, V, lam);
         const int sr = site / BX, sc = site - sr * BX;
+        code = (unsigned)site;
         {
           const int k0 = B.site_class(sr, sc);
           const uint32_t s = (uint32_t)(k0 >= 5);
@@ -415,6 +512,7 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
               (ps[e] ? a.ed[0].pos : a.ed[1].pos)[e * a.tstride + o] = p;
               ++n_out;
               if (!dv[e]) {
+                fdk[e] = k;  // first differing entry, if it differs here
                 if (k >= pc[e]) {
                   dv[e] = 1;
                 } else {
@@ -440,11 +538,20 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
         draw_pair(a.seed, gid, n, U, V, a.gen);
         R = expvar(U);
       }
+      if (!LOG && a.resume) {  // step log: time, budget after the step, code
+        if (lpos < (unsigned)a.LC) {
+          a.lg_t[lb + lpos] = ts;
+          a.lg_R[lb + lpos] = R;
+          a.lg_c[lb + lpos] = (uint16_t)code;
+        }
+        ++lpos;
+      }
       lam = big_fold(B, a.rate);
       tc = cand_time(ts, R, lam);
     }
     n_ev += n_ev_r;
     fmax = max(fmax, bev);
+    if (!LOG && a.resume) a.lg_meta[idx] = make_uint2(K, lpos <= (unsigned)a.LC ? lpos : 0xffffffffu);
 
     if (!LOG) {
       unsigned chmask = 0;
@@ -455,8 +562,23 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
         if (diff) {
           chmask |= 1u << e;
           const unsigned cnt = (int)oc[e] < a.K ? oc[e] : (unsigned)a.K;
-          a.sel[((long long)idx * 4 + e) * 2 + wh[e]] =
-              ((unsigned long long)K << 32) | ((unsigned long long)cnt << 1) | (ps[e] ^ 1u);
+          // a resumed recomputation wrote only the entries after its replayed
+          // prefix: complete the new history with the (identical) prefix
+          if (k0[e] > 0 && (int)k0[e] <= a.K) {
+            const double* To = src_t(a, ps[e], e);
+            const uint8_t* Po = src_p(a, ps[e], e);
+            double* Tn = const_cast<double*>(src_t(a, ps[e] ^ 1u, e));
+            uint8_t* Pn = const_cast<uint8_t*>(src_p(a, ps[e] ^ 1u, e));
+            for (unsigned q = 0; q < k0[e]; ++q) {
+              const unsigned o = obase + q * (unsigned)a.RX;
+              Tn[o] = To[o];
+              Pn[o] = Po[o];
+            }
+          }
+          const unsigned fd = min(dv[e] ? fdk[e] : min(oc[e], pc[e]), 0x7FFFu);
+          a.sel[((long long)idx * 4 + e) * 2 + wh[e]] = ((unsigned long long)K << 32) |
+                                                       ((unsigned long long)fd << 17) |
+                                                       ((unsigned long long)cnt << 1) | (ps[e] ^ 1u);
         }
       }
       if (chmask) {

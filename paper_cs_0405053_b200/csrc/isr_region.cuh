@@ -95,6 +95,15 @@ struct KArgs {
   unsigned gen;       // generation of the random numbers in use (window index if fresh_w, else 0)
   unsigned long long seed;
   double rate[10];
+  // big-region kernel: step log of each region's last recomputation in this
+  // window (time, budget after the step, step code), so a recomputation can
+  // resume just before the first changed incoming entry (isr_big.cuh)
+  double* lg_t;
+  double* lg_R;
+  uint16_t* lg_c;
+  uint2* lg_meta;          // per region: {stamp of the recomputation that wrote the log, length}
+  int LC;                  // log capacity (steps) per region
+  int resume;
   const uint32_t* wl_in;   // regions to recompute (nullptr: all regions)
   int n_work;              // number of regions to recompute
   const unsigned* n_work_dev;  // if set: the number is read here on the device (pool kernel)

@@ -303,6 +303,13 @@ struct ising_sr_ctx {
   int comm = 0;  // index of the committed state
   EdgeView ed[2] = {};
   unsigned long long* sel = nullptr;  // per region selector word
+  // big-region step logs (resume; isr_big.cuh)
+  double* lg_t = nullptr;
+  double* lg_R = nullptr;
+  uint16_t* lg_c = nullptr;
+  uint2* lg_meta = nullptr;
+  int LC = 0;
+  bool resume = true;  // env ISING_SR_RESUME=0 disables
   uint32_t* dirty = nullptr;          // dirty-region bitmaps [2][dwords] (iteration parity)
   int dwords = 0;
   uint32_t* wl[2] = {nullptr, nullptr};
@@ -489,6 +496,12 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   for (int k = 0; k < 10; ++k) a.rate[k] = c->cfg.rate[k];
   a.dirty = c->dirty;
   a.dwords = c->dwords;
+  a.lg_t = c->lg_t;
+  a.lg_R = c->lg_R;
+  a.lg_c = c->lg_c;
+  a.lg_meta = c->lg_meta;
+  a.LC = c->LC;
+  a.resume = (c->resume && c->lg_meta) ? 1 : 0;
   a.refill = c->refill;
   {
     // magic division by RX: k = 31 + ceil(log2 RX), M = ceil(2^k / RX) < 2^32;
@@ -755,6 +768,10 @@ void ising_sr_destroy(ising_sr_ctx* c) {
   free_edges(c);
   cudaFree(c->sel);
   cudaFree(c->dirty);
+  cudaFree(c->lg_t);
+  cudaFree(c->lg_R);
+  cudaFree(c->lg_c);
+  cudaFree(c->lg_meta);
   cudaFree(c->wl[0]);
   cudaFree(c->wl[1]);
   cudaFree(c->d_wlc);
@@ -856,6 +873,31 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   const int K0 = cfg->hist_capacity > 0 ? std::min(cfg->hist_capacity, ops->cnt_max) : auto_capacity(*cfg, ops->cnt_max);
   ising_sr_status s = alloc_edges(c, K0);
   if (s != ISING_SR_OK) return bail(s);
+  if (const char* e = std::getenv("ISING_SR_RESUME")) c->resume = std::atoi(e) != 0;
+  if (ops->warp && big_enabled() && c->resume) {
+    // step log per region: incoming break points (<= 4 K) + events (twice the
+    // expectation at the largest rate) + slack; capped at 48 GB in all (a
+    // region whose log overflows is simply recomputed in full)
+    double rmax = 0.0;
+    for (double r : cfg->rate) rmax = std::max(rmax, r);
+    long long LC = 4LL * K0 + 2LL * (long long)std::ceil((double)cfg->bx * cfg->by * cfg->W * rmax) + 64;
+    LC = std::min<long long>(LC, 32768);
+    const long long cap = (48LL << 30) / (18LL * std::max(1, c->nreg));
+    LC = std::min(LC, cap);
+    if (LC >= 16) {
+      c->LC = (int)LC;
+      const size_t nl = (size_t)c->nreg * (size_t)LC;
+      if (dmalloc(&c->lg_t, nl) != cudaSuccess || dmalloc(&c->lg_R, nl) != cudaSuccess ||
+          dmalloc(&c->lg_c, nl) != cudaSuccess || dmalloc(&c->lg_meta, n) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(c->lg_t); cudaFree(c->lg_R); cudaFree(c->lg_c); cudaFree(c->lg_meta);
+        c->lg_t = nullptr; c->lg_R = nullptr; c->lg_c = nullptr; c->lg_meta = nullptr;
+        c->LC = 0;
+      } else if (cudaMemsetAsync(c->lg_meta, 0, n * sizeof(uint2), c->stream) != cudaSuccess) {
+        return bail(ISING_SR_E_CUDA);
+      }
+    }
+  }
   c->stats.hist_capacity = c->K;
 
   // strip + one halo row above and below (periodic), packed by K0

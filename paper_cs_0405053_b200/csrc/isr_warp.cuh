@@ -25,6 +25,8 @@ __device__ __forceinline__ unsigned long long latest_edge_word(const unsigned lo
 }
 __device__ __forceinline__ unsigned ew_count(unsigned long long v) { return (unsigned)((v >> 1) & 0xFFFFu); }
 __device__ __forceinline__ unsigned ew_slot(unsigned long long v) { return (unsigned)(v & 1ull); }
+// first entry in which this history differs from the edge's previous one (bits 17-31, capped at 32767)
+__device__ __forceinline__ unsigned ew_fd(unsigned long long v) { return (unsigned)((v >> 17) & 0x7FFFu); }
 
 template <int BX, int BY>
 struct WGeo {

@@ -229,6 +229,7 @@ def test_c5_geometry_sample_bit_exact():
     {"ISING_SR_TAIL_BATCH": "1"},
     {"ISING_SR_TAIL_N": "1000000000", "ISING_SR_TAIL_BATCH": "3"},
     {"ISING_SR_BIG": "0", "ISING_SR_TAIL_N": "1000000000"},
+    {"ISING_SR_RESUME": "0"},
 ])
 def test_k1_schedules_bit_exact(env, monkeypatch):
     for k, v in env.items():
