@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
         unsigned cntd = 0;  // byte d: break points of direction d so far
         unsigned i = 0;
         for (; i < len; ++i) {
-          const double ti = a.lg_t[lb + i];
+          const double ti = a.lg_tR[lb + i].x;
           if (!(ti < tst)) break;
           const unsigned code = a.lg_c[lb + i];
           if (code & 0x8000u) {
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
             if (kd < 255u) cntd += 1u << (8 * d);
           }
         }
-        while (i > 0 && !(a.lg_t[lb + i - 1] < tst)) --i;  // steps at time tst are re-simulated
+        while (i > 0 && !(a.lg_tR[lb + i - 1].x < tst)) --i;  // steps at time tst are re-simulated
         // replay steps [0, i): flips, cursors, own-history counts, digest
         for (unsigned j = 0; j < i; ++j) {
           const unsigned code = a.lg_c[lb + j];
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
             const int site = (int)code;
             const int sr = site / BX, sc = site - sr * BX;
             SM.rows[sr][t] ^= 1u << sc;
-            if (a.digest) dig = digest_step(dig, a.lg_t[lb + j], site);
+            if (a.digest) dig = digest_step(dig, a.lg_tR[lb + j].x, site);
             ++n_ev_r;
             bool on_edge = false;
 #pragma unroll
@@ -328,8 +328,9 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
           }
         }
         if (i > 0) {
-          ts = a.lg_t[lb + i - 1];
-          R = a.lg_R[lb + i - 1];
+          const double2 e = a.lg_tR[lb + i - 1];
+          ts = e.x;
+          R = e.y;
         }
         n += n_ev_r;
         lpos = i;
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
 
     double U, V;
     draw_pair(a.seed, gid, n, U, V, a.gen);
-    if (a.fresh_w) R = expvar(U);  // the slate is wiped at t_c
+    if (a.fresh_w && lpos == 0) R = expvar(U);  // the slate is wiped at t_c; a replay restored R
     double lam = big_fold(B, a.rate);
     double tc = cand_time(ts, R, lam);
 
@@ -540,8 +541,7 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
       }
       if (!LOG && a.resume) {  // step log: time, budget after the step, code
         if (lpos < (unsigned)a.LC) {
-          a.lg_t[lb + lpos] = ts;
-          a.lg_R[lb + lpos] = R;
+          a.lg_tR[lb + lpos] = make_double2(ts, R);
           a.lg_c[lb + lpos] = (uint16_t)code;
         }
         ++lpos;

@@ -98,8 +98,7 @@ struct KArgs {
   // big-region kernel: step log of each region's last recomputation in this
   // window (time, budget after the step, step code), so a recomputation can
   // resume just before the first changed incoming entry (isr_big.cuh)
-  double* lg_t;
-  double* lg_R;
+  double2* lg_tR;          // {time, budget after the step}
   uint16_t* lg_c;
   uint2* lg_meta;          // per region: {stamp of the recomputation that wrote the log, length}
   int LC;                  // log capacity (steps) per region

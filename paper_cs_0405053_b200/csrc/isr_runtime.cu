@@ -304,8 +304,7 @@ struct ising_sr_ctx {
   EdgeView ed[2] = {};
   unsigned long long* sel = nullptr;  // per region selector word
   // big-region step logs (resume; isr_big.cuh)
-  double* lg_t = nullptr;
-  double* lg_R = nullptr;
+  double2* lg_tR = nullptr;
   uint16_t* lg_c = nullptr;
   uint2* lg_meta = nullptr;
   int LC = 0;
@@ -496,8 +495,7 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   for (int k = 0; k < 10; ++k) a.rate[k] = c->cfg.rate[k];
   a.dirty = c->dirty;
   a.dwords = c->dwords;
-  a.lg_t = c->lg_t;
-  a.lg_R = c->lg_R;
+  a.lg_tR = c->lg_tR;
   a.lg_c = c->lg_c;
   a.lg_meta = c->lg_meta;
   a.LC = c->LC;
@@ -768,8 +766,7 @@ void ising_sr_destroy(ising_sr_ctx* c) {
   free_edges(c);
   cudaFree(c->sel);
   cudaFree(c->dirty);
-  cudaFree(c->lg_t);
-  cudaFree(c->lg_R);
+  cudaFree(c->lg_tR);
   cudaFree(c->lg_c);
   cudaFree(c->lg_meta);
   cudaFree(c->wl[0]);
@@ -887,11 +884,11 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
     if (LC >= 16) {
       c->LC = (int)LC;
       const size_t nl = (size_t)c->nreg * (size_t)LC;
-      if (dmalloc(&c->lg_t, nl) != cudaSuccess || dmalloc(&c->lg_R, nl) != cudaSuccess ||
-          dmalloc(&c->lg_c, nl) != cudaSuccess || dmalloc(&c->lg_meta, n) != cudaSuccess) {
+      if (dmalloc(&c->lg_tR, nl) != cudaSuccess || dmalloc(&c->lg_c, nl) != cudaSuccess ||
+          dmalloc(&c->lg_meta, n) != cudaSuccess) {
         cudaGetLastError();
-        cudaFree(c->lg_t); cudaFree(c->lg_R); cudaFree(c->lg_c); cudaFree(c->lg_meta);
-        c->lg_t = nullptr; c->lg_R = nullptr; c->lg_c = nullptr; c->lg_meta = nullptr;
+        cudaFree(c->lg_tR); cudaFree(c->lg_c); cudaFree(c->lg_meta);
+        c->lg_tR = nullptr; c->lg_c = nullptr; c->lg_meta = nullptr;
         c->LC = 0;
       } else if (cudaMemsetAsync(c->lg_meta, 0, n * sizeof(uint2), c->stream) != cudaSuccess) {
         return bail(ISING_SR_E_CUDA);
