@@ -281,20 +281,39 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
         // ... or the old entry q_d, consumed as that direction's q_d-th break point
         unsigned cntd = 0;  // byte d: break points of direction d so far
         unsigned i = 0;
-        for (; i < len; ++i) {
-          const double ti = a.lg_tR[lb + i].x;
-          if (!(ti < tst)) break;
-          const unsigned code = a.lg_c[lb + i];
-          if (code & 0x8000u) {
-            const int d = (int)((code >> 12) & 3u);
-            const unsigned kd = (cntd >> (8 * d)) & 0xFFu;
-            if (((chg >> d) & 1u) && kd == qd[d]) {
-              tst = ti;
-              break;
+        bool stop = false;
+        // 4 log entries in flight per round (all inside the region's log)
+        for (unsigned i0 = 0; i0 < len && !stop; i0 += 4) {
+          double tq[4];
+          unsigned cq[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const unsigned iu = min(i0 + (unsigned)u, (unsigned)a.LC - 1u);
+            tq[u] = a.lg_tR[lb + iu].x;
+            cq[u] = a.lg_c[lb + iu];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (stop || i0 + u >= len) continue;
+            i = i0 + u;
+            if (!(tq[u] < tst)) {
+              stop = true;
+              continue;
             }
-            if (kd < 255u) cntd += 1u << (8 * d);
+            const unsigned code = cq[u];
+            if (code & 0x8000u) {
+              const int d = (int)((code >> 12) & 3u);
+              const unsigned kd = (cntd >> (8 * d)) & 0xFFu;
+              if (((chg >> d) & 1u) && kd == qd[d]) {
+                tst = tq[u];
+                stop = true;
+                continue;
+              }
+              if (kd < 255u) cntd += 1u << (8 * d);
+            }
           }
         }
+        if (!stop) i = len;
         while (i > 0 && !(a.lg_tR[lb + i - 1].x < tst)) --i;  // steps at time tst are re-simulated
         // replay steps [0, i): flips, cursors, own-history counts, digest
         for (unsigned j = 0; j < i; ++j) {
