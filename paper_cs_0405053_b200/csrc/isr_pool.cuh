@@ -44,12 +44,6 @@ struct PoolSlots {
   double ht[4][S];
   uint32_t hoff[4][S];
   uint32_t om[4][S];
-#if ISR_PREPAIR
-  double Rn[S], Vn[S];
-#endif
-#if ISR_PSUM
-  double cs[9][S];
-#endif
 };
 
 template <class G, int S>
@@ -101,14 +95,6 @@ __device__ __forceinline__ void slot_get(const KArgs& a, const PoolSlots<G, S>& 
     L.hoff[d] = P.hoff[d][s];
     L.om[d] = P.om[d][s];
   }
-#if ISR_PREPAIR
-  L.Rn = P.Rn[s];
-  L.Vn = P.Vn[s];
-#endif
-#if ISR_PSUM
-#pragma unroll
-  for (int k = 0; k < 9; ++k) L.cs[k] = P.cs[k][s];
-#endif
 }
 
 // the fields a step (event or break point) and its refold change
@@ -117,10 +103,6 @@ __device__ __forceinline__ void slot_put_step(PoolSlots<G, S>& P, int s, const L
   P.lam[s] = L.lam;
   P.tc[s] = L.tc;
   P.site[s] = L.site;
-#if ISR_PSUM
-#pragma unroll
-  for (int k = 0; k < 9; ++k) P.cs[k][s] = L.cs[k];
-#endif
 }
 
 template <class G, int S>
@@ -148,10 +130,6 @@ __device__ __forceinline__ void slot_put_all(PoolSlots<G, S>& P, int s, const La
     P.hoff[d][s] = L.hoff[d];
     P.om[d][s] = L.om[d];
   }
-#if ISR_PREPAIR
-  P.Rn[s] = L.Rn;
-  P.Vn[s] = L.Vn;
-#endif
   slot_put_step<G, S>(P, s, L);
 }
 
@@ -277,10 +255,6 @@ __global__ void __launch_bounds__(PW * 32) region_kernel_pool(const KArgs a) {
         P.ts[s] = L.ts;
         P.R[s] = L.R;
         P.V[s] = L.V;
-#if ISR_PREPAIR
-        P.Rn[s] = L.Rn;
-        P.Vn[s] = L.Vn;
-#endif
         slot_put_step<G, S>(P, s, L);
         P.n[s] = L.n;
         P.nev[s] = L.n_ev;

@@ -325,56 +325,6 @@ __device__ __forceinline__ int select_site2(const Classes<G>& C, const ProdTable
   return nth_bit<M, G::NS>(mk, (int)j);
 }
 
-// eq. biglambda keeping the partial sums c_0..c_8 (the same additions as fold_lambda)
-template <class G>
-__device__ __forceinline__ double fold_lambda_ps(const Classes<G>& C, const ProdTable<G>& T, double* cs) {
-  double c = 0.0;
-#pragma unroll
-  for (int k = 0; k < 10; ++k) {
-    c = __dadd_rn(c, T.at(k, popc_m(C.mask(k))));
-    if (k < 9) cs[k] = c;
-  }
-  return c;
-}
-
-// select_site2 from the stored partial sums of the current state (no refold):
-// the same c_k values, so the same k*, c_{k*-1} and site
-template <class G>
-__device__ __forceinline__ int select_site_ps(const Classes<G>& C, const double* cs, const double* rate, double V,
-                                             double lam) {
-  using M = typename G::M;
-  const double x = __dmul_rn(V, lam);
-  int ks = -1, lastnz = 0;
-  double cprev = 0.0, cp = 0.0;
-  M mk = 0, mlast = C.mask(0);
-#pragma unroll
-  for (int k = 0; k < 10; ++k) {
-    const M m = C.mask(k);
-    const double ck = k < 9 ? cs[k] : lam;
-    const bool hit = ks < 0 && x <= ck;
-    ks = hit ? k : ks;
-    cprev = hit ? cp : cprev;
-    mk = hit ? m : mk;
-    const bool nz = m != 0;
-    lastnz = nz ? k : lastnz;
-    mlast = nz ? m : mlast;
-    cp = ck;
-  }
-  if (ks < 0) {  // unreachable for V < 1 (x <= Lambda = c_9)
-    ks = lastnz;
-    mk = mlast;
-    cprev = 0.0;
-  }
-  const int nk = popc_m(mk);
-  const double aq = __dsub_rn(x, cprev);
-  const double rk = rate[ks];
-  const double q = rk == 1.0 ? aq : __ddiv_rn(aq, rk);
-  long long j = __double2ll_rd(q);
-  j = j > nk - 1 ? nk - 1 : j;
-  j = j < 0 ? 0 : j;
-  return nth_bit<M, G::NS>(mk, (int)j);
-}
-
 // eq. biglambda followed at once by the atom selection for the next event
 // (eqs. Wsum..vindex) on the same state: the partial sums c_k are still in
 // registers, so the selection needs no second fold.  Identical decisions to
@@ -505,17 +455,11 @@ __device__ __forceinline__ int div_rx(const KArgs& a, int idx) {
 #ifndef ISR_HIST2
 #define ISR_HIST2 1    // per-axis (not per-edge) own-history writes
 #endif
-#ifndef ISR_PREPAIR
-#define ISR_PREPAIR 0  // draw the next event's pair one event ahead (measured slower: registers)
-#endif
 #ifndef ISR_SELAHEAD
 #define ISR_SELAHEAD 1  // select the next event's atom right after each refold (fold_select)
 #endif
 #ifndef ISR_FRESH
 #define ISR_FRESH 1  // a freshly loaded region's first pair and refold run in the shared step code
-#endif
-#ifndef ISR_PSUM
-#define ISR_PSUM 0     // keep the fold's partial sums c_0..c_8 for the next selection (measured slower)
 #endif
 constexpr int NT = 128;      // threads per block of K1
 constexpr int CI = ISR_CI;   // staged entries per history
@@ -554,12 +498,6 @@ struct Lane {
   M spins, gN, gS, gW, gE;
   double ts, R, V, lam, tc;
   int site;       // ISR_SELAHEAD: atom of the next event on the current state
-#if ISR_PREPAIR
-  double Rn, Vn;  // E(U) and V of the pair after the current one (drawn ahead)
-#endif
-#if ISR_PSUM
-  double cs[9];   // partial sums c_0..c_8 of the last Lambda fold (c_9 = lam)
-#endif
   uint32_t n;
   unsigned long long dig;
   // incoming history cursors: cnt | idx << 8 | pos << 16 | source << 24
@@ -738,19 +676,10 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   double U;
   draw_pair(a.seed, L.gid, L.n, U, L.V, a.gen);
   if (a.fresh_w) L.R = expvar(U);  // the slate is wiped at t_c: the budget restarts from pair n
-#if ISR_PREPAIR
-  {
-    double U1;
-    draw_pair(a.seed, L.gid, L.n + 1, U1, L.Vn, a.gen);
-    L.Rn = expvar(U1);
-  }
-#endif
   Classes<G> C;
   C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
 #if ISR_SELAHEAD
   L.site = fold_select<G>(C, PT, a.rate, L.V, L.lam);
-#elif ISR_PSUM
-  L.lam = fold_lambda_ps<G>(C, PT, L.cs);
 #else
   L.lam = fold_lambda<G>(C, PT);
 #endif
@@ -943,11 +872,7 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const
   {
     Classes<G> C;
     C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
-#if ISR_PSUM
-    site = select_site_ps<G>(C, L.cs, a.rate, L.V, L.lam);
-#else
     site = select_site2<G>(C, PT, a.rate, L.V, L.lam);
-#endif
   }
 #endif
   L.spins ^= G::ONE << site;
@@ -995,19 +920,9 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const
   L.ts = L.tc;
   ++L.n;
   if (!DRAW) return;
-#if ISR_PREPAIR
-  L.R = L.Rn;  // pair n (drawn one event ago)
-  L.V = L.Vn;
-  {
-    double U1;  // pair n + 1, needed only at the next event
-    draw_pair(a.seed, L.gid, L.n + 1, U1, L.Vn, a.gen);
-    L.Rn = expvar(U1);
-  }
-#else
   double U;
   draw_pair(a.seed, L.gid, L.n, U, L.V, a.gen);
   L.R = expvar(U);
-#endif
 }
 
 template <class G>
@@ -1016,8 +931,6 @@ __device__ __forceinline__ void refold(const KArgs& a, Lane<G>& L, const ProdTab
   C.build(L.spins, L.gN, L.gS, L.gW, L.gE, a.RX == 1, a.RYg == 1);
 #if ISR_SELAHEAD
   L.site = fold_select<G>(C, PT, a.rate, L.V, L.lam);
-#elif ISR_PSUM
-  L.lam = fold_lambda_ps<G>(C, PT, L.cs);
 #else
   L.lam = fold_lambda<G>(C, PT);
 #endif
@@ -1094,7 +1007,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
           if (item < 0 && !global_q) item = (int)atomicAdd(&q_next, 1u);
           if (item >= 0 && item < tile_n) {
             const int idx = a.wl_in ? (int)a.wl_in[tile_begin + item] : tile_begin + item;
-            lane_load<G, LOG, Stage, !(ISR_FRESH && !ISR_PREPAIR)>(a, L, idx, S, PT, threadIdx.x);
+            lane_load<G, LOG, Stage, !ISR_FRESH>(a, L, idx, S, PT, threadIdx.x);
             fresh = true;
             n_in += (L.hm[0] & 0xFFu) + (L.hm[1] & 0xFFu) + (L.hm[2] & 0xFFu) + (L.hm[3] & 0xFFu);
             n_cmp += ((L.om[0] >> 8) & 0xFFu) + ((L.om[1] >> 8) & 0xFFu) + ((L.om[2] >> 8) & 0xFFu) +
@@ -1112,7 +1025,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
     if (active) {
       // one step per round: the earliest of (next break point, own event);
       // a region loaded in this round only draws its pair and refolds
-      constexpr bool SHARE = ISR_FRESH && !ISR_PREPAIR;
+      constexpr bool SHARE = ISR_FRESH;
       bool go = true, ev = false;
       if (!SHARE || !fresh) {
         double tb;
