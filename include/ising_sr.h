@@ -66,6 +66,13 @@ typedef enum {
  * (Philox counter word 2 = w).  Unbiased (memorylessness), but the
  * trajectory then depends on W.  Default off (the carried budget of P:726-742). */
 #define ISING_SR_FLAG_FRESH_WINDOW 0x4u
+/* Time integrals of the magnetisation M = sum_v s(v) and of the bond sum
+ * B = sum_<vu> s(v) s(u) (energy E = -J B - H M, eq. hamil) over every
+ * committed window, accumulated per region inside K1 (each region owns its
+ * internal bonds and the bonds to its north and west neighbours) and reduced
+ * in a fixed order at commit (ising_sr_stats.obs_*).  Lane-per-region K1 forms
+ * only (E_INVALID_ARG with ISING_SR_POOL=1 or ISING_SR_BIG=0). */
+#define ISING_SR_FLAG_OBSERVABLES 0x8u
 
 /* Halo exchange between strips (world > 1).  Rank q owns a band of region
  * rows; "up" is toward region row 0 (rank q-1, periodic), "down" toward rank
@@ -134,6 +141,9 @@ typedef struct {
   int64_t region_launches;
   double region_ms;
   double region_bytes;
+  /* FLAG_OBSERVABLES: integrals over the last committed window and over all
+   * committed windows (this rank's regions): int M dt, int B dt, and the time */
+  double obs_M_last, obs_B_last, obs_M_total, obs_B_total, obs_time_total;
 } ising_sr_stats;
 
 /* Validate cfg, allocate device state, copy the full Ly*Lx row-major spin

@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("ISING_SR_LIB") or os.path.join(_PKG, "libising_sr.so"
 FLAG_LOG_EVENTS = 0x1
 FLAG_DIGEST = 0x2
 FLAG_FRESH_WINDOW = 0x4  # alternate approach to subsequent steps
+FLAG_OBSERVABLES = 0x8   # time integrals of M and of the bond sum per window
 
 STATUS = {
     0: "OK", -1: "E_INVALID_ARG", -2: "E_DIMENSION", -3: "E_PARTITION", -4: "E_DIVERGED",
@@ -64,7 +65,10 @@ class Stats(ctypes.Structure):
                 ("hist_capacity", ctypes.c_int32), ("recomputations_total", ctypes.c_int64),
                 ("bytes_alg_last_window", ctypes.c_double), ("ms_last_window", ctypes.c_double),
                 ("region_launches", ctypes.c_int64), ("region_ms", ctypes.c_double),
-                ("region_bytes", ctypes.c_double)]
+                ("region_bytes", ctypes.c_double),
+                ("obs_M_last", ctypes.c_double), ("obs_B_last", ctypes.c_double),
+                ("obs_M_total", ctypes.c_double), ("obs_B_total", ctypes.c_double),
+                ("obs_time_total", ctypes.c_double)]
 
 
 _lib = None

@@ -92,6 +92,40 @@ struct BigRegion {
     return (int)(5u * s + un + us + uw + ue);
   }
   __device__ __forceinline__ int N(int k) const { return (int)((Nw[k >> 1] >> (16 * (k & 1))) & 0xFFFFu); }
+  // FLAG_OBSERVABLES: spins of the owned-bond partners of site (r, c) -- north
+  // and west always (in-region, wrapped, or the ghost), south and east only
+  // inside the region or wrapped (the bonds across the south/east border
+  // belong to the neighbouring regions) -- as the sum of +-1 values
+  __device__ __forceinline__ int owned_partner_sum(int r, int c) const {
+    const uint32_t rw = row(r);
+    int s = 0;
+    s += (int)((above(r) >> c) & 1u);
+    s += (int)(c > 0 ? (rw >> (c - 1)) & 1u : wbit(r, rw));
+    int n = 2;
+    if (r < BY - 1 || wrapY) {
+      s += (int)((below(r) >> c) & 1u);
+      ++n;
+    }
+    if (c < BX - 1 || wrapX) {
+      s += (int)(c < BX - 1 ? (rw >> (c + 1)) & 1u : ebit(r, rw));
+      ++n;
+    }
+    return 2 * s - n;
+  }
+  // magnetisation and owned bond sum of the whole region
+  __device__ __forceinline__ void obs_counts(int& Mi, int& Bi) const {
+    int m = 0, b = 0;
+    for (int r = 0; r < BY; ++r) {
+      const uint32_t rw = row(r);
+      m += 2 * __popc(rw) - BX;
+      b += 2 * __popc(~(rw ^ (rw >> 1)) & (ROWM >> 1)) - (BX - 1);  // (c, c + 1) inside the row
+      b += 2 * __popc(~(rw ^ above(r)) & ROWM) - BX;                 // north bonds
+      const uint32_t w = (rw & 1u) ^ wbit(r, rw);                     // west bond of column 0
+      b += w ? -1 : 1;
+    }
+    Mi = m;
+    Bi = b;
+  }
   // N_k += d and the row count of class k in row r += d (d = +-1)
   __device__ __forceinline__ void add(int k, int r, int d) {
     const uint32_t inc = (uint32_t)d << (16 * (k & 1));
@@ -175,7 +209,7 @@ __device__ __forceinline__ int big_select(const BigRegion<BX, BY>& B, const doub
   return r * BX + nth_bit<uint32_t, 32>(B.class_mask(r, ks), jj);
 }
 
-template <int BX, int BY, bool LOG>
+template <int BX, int BY, bool LOG, bool OBS = false>
 __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
   using BR = BigRegion<BX, BY>;
   static_assert(BX <= 32 && BY <= 32 && BX >= 3 && BY >= 3, "rows of up to 32 sites");
@@ -210,6 +244,16 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
     uint32_t n = a.in.n[idx];
     unsigned long long dig = a.digest ? a.in.dig[idx] : 0ull;
     unsigned n_ev_r = 0, bev = 0;
+    // FLAG_OBSERVABLES: M and the owned bond sum B now, their integrals since t_c
+    int Mi = 0, Bi = 0;
+    double iM = 0.0, iB = 0.0, tpv = a.t_c;
+    if (OBS && !LOG) B.obs_counts(Mi, Bi);
+    auto obs_adv = [&](double tt) {
+      const double dt = __dsub_rn(tt, tpv);
+      iM = __dadd_rn(iM, __dmul_rn((double)Mi, dt));
+      iB = __dadd_rn(iB, __dmul_rn((double)Bi, dt));
+      tpv = tt;
+    };
     // ---- incoming histories: head entry + the next one in flight ----
     unsigned hcnt[4], hidx[4], hsrc[4], hoff[4];
     double ht[4], hn[4];
@@ -318,9 +362,14 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
         // replay steps [0, i): flips, cursors, own-history counts, digest
         for (unsigned j = 0; j < i; ++j) {
           const unsigned code = a.lg_c[lb + j];
+          if (OBS && !LOG) obs_adv(a.lg_tR[lb + j].x);
           if (code & 0x8000u) {
             const int d = (int)((code >> 12) & 3u);
             const int p = (int)(code & 0xFFu);
+            if (OBS && !LOG) {  // owned bonds: the north and west ghosts
+              if (d == EDGE_N) Bi += ((B.gN >> p) & 1u) == ((B.row(0) >> p) & 1u) ? -2 : 2;
+              else if (d == EDGE_W) Bi += ((B.gW >> p) & 1u) == (B.row(p) & 1u) ? -2 : 2;
+            }
             if (d == EDGE_N) B.gN ^= 1u << p;
             else if (d == EDGE_S) B.gS ^= 1u << p;
             else if (d == EDGE_W) B.gW ^= 1u << p;
@@ -330,6 +379,11 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
           } else {
             const int site = (int)code;
             const int sr = site / BX, sc = site - sr * BX;
+            if (OBS && !LOG) {
+              const int sg = ((B.row(sr) >> sc) & 1u) ? 1 : -1;
+              Mi -= 2 * sg;
+              Bi -= 2 * sg * B.owned_partner_sum(sr, sc);
+            }
             SM.rows[sr][t] ^= 1u << sc;
             if (a.digest) dig = digest_step(dig, a.lg_tR[lb + j].x, site);
             ++n_ev_r;
@@ -460,6 +514,11 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
         ts = tb;
         const int p = (int)((hp >> (8 * dstar)) & 0xFFu);
         code = 0x8000u | ((unsigned)dstar << 12) | (unsigned)p;
+        if (OBS && !LOG) {
+          obs_adv(tb);
+          if (dstar == EDGE_N) Bi += ((B.gN >> p) & 1u) == ((B.row(0) >> p) & 1u) ? -2 : 2;
+          else if (dstar == EDGE_W) Bi += ((B.gW >> p) & 1u) == (B.row(p) & 1u) ? -2 : 2;
+        }
         // the in-region site next to the flipped halo spin and its change of
         // up-neighbour count
         int sr, sc;
@@ -491,6 +550,12 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
         const int site = big_select<BX, BY>(B, a.rate, V, lam);
         const int sr = site / BX, sc = site - sr * BX;
         code = (unsigned)site;
+        if (OBS && !LOG) {
+          obs_adv(tc);
+          const int sg = ((B.row(sr) >> sc) & 1u) ? 1 : -1;
+          Mi -= 2 * sg;
+          Bi -= 2 * sg * B.owned_partner_sum(sr, sc);
+        }
         {
           const int k0 = B.site_class(sr, sc);
           const uint32_t s = (uint32_t)(k0 >= 5);
@@ -610,6 +675,11 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
           const int nc = e == EDGE_W ? wdec(c, a.RX) : e == EDGE_E ? winc(c, a.RX) : c;
           mark_dirty(a, nr * a.RX + nc, K + 1);
         }
+      }
+      if (OBS) {  // integrals up to the window end
+        obs_adv(a.t_w);
+        a.out.oM[idx] = iM;
+        a.out.oB[idx] = iB;
       }
       uint32_t* dst = (uint32_t*)a.out.spins + (long long)idx * BY;
 #pragma unroll

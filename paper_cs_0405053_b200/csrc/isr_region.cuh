@@ -57,6 +57,8 @@ struct StateView {
   double* R;
   uint32_t* n;
   unsigned long long* dig;
+  double* oM;  // FLAG_OBSERVABLES: int M dt, int B dt of the region over the window
+  double* oB;
 };
 
 // Boundary histories of one slot: t/pos[4][RYl][K][RX] (entry q of edge e of
@@ -92,6 +94,7 @@ struct KArgs {
   double t_w;         // window end
   double t_c;         // window start (committed time)
   int fresh_w;        // alternate approach: every region restarts at t_c with fresh numbers
+  int obs;            // FLAG_OBSERVABLES: accumulate int M dt, int B dt per region
   unsigned gen;       // generation of the random numbers in use (window index if fresh_w, else 0)
   unsigned long long seed;
   double rate[10];
@@ -406,6 +409,34 @@ __device__ __forceinline__ unsigned long long compress_halo(typename G::M gN, ty
 __device__ __forceinline__ int wdec(int v, int n) { return v == 0 ? n - 1 : v - 1; }
 __device__ __forceinline__ int winc(int v, int n) { return v == n - 1 ? 0 : v + 1; }
 
+// FLAG_OBSERVABLES: magnetisation of the region and the sum of s(v) s(u) over
+// its owned bonds (internal bonds, bonds to the north row and the west
+// column: every lattice bond is owned by exactly one region), from the masks
+template <class G>
+__device__ __forceinline__ void obs_counts(typename G::M sp, typename G::M gN, typename G::M gW, bool wrapX,
+                                           bool wrapY, int& Mi, int& Bi) {
+  using M = typename G::M;
+  constexpr int BX = G::BX, BY = G::BY;
+  constexpr M FULL = G::full();
+  Mi = 2 * popc_m(sp) - G::NS;
+  int B = 0;
+  if (BX > 1) {  // horizontal internal bonds (c, c + 1)
+    const M h = FULL & ~G::coll();
+    B += 2 * popc_m((M)(~(sp ^ (sp >> 1)) & h)) - (BX - 1) * BY;
+  }
+  if (BY > 1) {  // vertical internal bonds (r, r + 1)
+    const M v = (M)(FULL >> BX);
+    B += 2 * popc_m((M)(~(sp ^ (sp >> BX)) & v)) - BX * (BY - 1);
+  }
+  // north row: the ghost row, or (region spanning the height) the last row
+  const M nrow = wrapY ? (M)((sp >> ((BY - 1) * BX)) & G::row0()) : gN;
+  B += 2 * popc_m((M)(~(sp ^ nrow) & G::row0())) - BX;
+  // west column: the ghost column, or (spanning the width) the last column
+  const M wcol = wrapX ? (M)((sp >> (BX - 1)) & G::col0()) : gW;
+  B += 2 * popc_m((M)(~(sp ^ wcol) & G::col0())) - BY;
+  Bi = B;
+}
+
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
 // region row of a shard-local index without an integer division
@@ -510,6 +541,9 @@ struct Lane {
   unsigned om[4];
   int whalf;      // selector word to overwrite on change
   unsigned n_ev;  // events of this region (log offset)
+  int Mi, Bi;     // FLAG_OBSERVABLES: magnetisation and owned bond sum now
+  double iM, iB;  // ... their integrals since t_c
+  double tpv;     // ... up to this time
   unsigned bev;   // own boundary events of this region
 };
 
@@ -536,9 +570,18 @@ __device__ __forceinline__ const void* word_of(const uint8_t* p) {
 }
 __device__ __forceinline__ unsigned byte_shift(const uint8_t* p) { return 8u * (unsigned)((size_t)p & 3); }
 
+// advance the integrals of M and B to time t (before a step at t)
+template <class G>
+__device__ __forceinline__ void obs_advance(Lane<G>& L, double t) {
+  const double dt = __dsub_rn(t, L.tpv);
+  L.iM = __dadd_rn(L.iM, __dmul_rn((double)L.Mi, dt));
+  L.iB = __dadd_rn(L.iB, __dmul_rn((double)L.Bi, dt));
+  L.tpv = t;
+}
+
 // FULL = false: stop after the state and histories are in; the caller draws
 // the pair and refolds (sharing that code with the step)
-template <class G, bool LOG, class SG, bool FULL = true>
+template <class G, bool LOG, class SG, bool FULL = true, bool OBS = false>
 __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, SG& S, const ProdTable<G>& PT,
                                           int si) {
   using M = typename G::M;
@@ -592,6 +635,12 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   L.R = a.in.R[idx];
   L.n = a.in.n[idx];
   L.dig = a.digest ? a.in.dig[idx] : 0ull;
+  if (OBS && !LOG) {  // integrals over [t_c, t_w) start at the window start
+    obs_counts<G>(L.spins, L.gN, L.gW, wrapX, wrapY, L.Mi, L.Bi);
+    L.iM = 0.0;
+    L.iB = 0.0;
+    L.tpv = a.t_c;
+  }
   // stage incoming histories (above CI entries: read lazily from global)
   bool staged_any = false;
 #pragma unroll
@@ -703,7 +752,7 @@ __device__ __forceinline__ uint32_t neighbour_id(const KArgs& a, uint32_t gid, i
 
 // DEFER: the entry-by-entry diff was not done while writing; compare the
 // new history (slot ps ^ 1) with the latest one (slot ps) here.
-template <class G, bool DEFER = false>
+template <class G, bool DEFER = false, bool OBS = false>
 __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& changed, bool& overflow,
                                             unsigned* n_cmp = nullptr) {
   const int idx = L.idx;
@@ -744,6 +793,11 @@ __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& ch
       const int nc = e == EDGE_W ? wdec(c, a.RX) : e == EDGE_E ? winc(c, a.RX) : c;
       mark_dirty(a, nr * a.RX + nc, K + 1);
     }
+  }
+  if (OBS) {  // integrals up to the window end
+    obs_advance<G>(L, a.t_w);
+    a.out.oM[idx] = L.iM;
+    a.out.oB[idx] = L.iB;
   }
   // tentative end-of-window state (committed by pointer swap at commit)
   ((typename G::ST*)a.out.spins)[idx] = (typename G::ST)L.spins;
@@ -939,7 +993,7 @@ __device__ __forceinline__ void refold(const KArgs& a, Lane<G>& L, const ProdTab
 
 // GQ (persistent launch): the worklist is one global queue (a.work_ctr) and
 // its length is read on the device; otherwise each block owns a static tile.
-template <int BX, int BY, bool LOG, bool GQ>
+template <int BX, int BY, bool LOG, bool GQ, bool OBS>
 __device__ __forceinline__ void region_body(const KArgs& a) {
   using G = Geo<BX, BY>;
   __shared__ unsigned q_next;
@@ -998,7 +1052,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
       }
       if (!active) {
         if (pending) {
-          if (!LOG) lane_finish<G>(a, L, changed, overflow);
+          if (!LOG) lane_finish<G, false, OBS>(a, L, changed, overflow);
           n_ev += L.n_ev;
           n_bev = max(n_bev, L.bev);
           pending = false;
@@ -1007,7 +1061,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
           if (item < 0 && !global_q) item = (int)atomicAdd(&q_next, 1u);
           if (item >= 0 && item < tile_n) {
             const int idx = a.wl_in ? (int)a.wl_in[tile_begin + item] : tile_begin + item;
-            lane_load<G, LOG, Stage, !ISR_FRESH>(a, L, idx, S, PT, threadIdx.x);
+            lane_load<G, LOG, Stage, !ISR_FRESH, OBS>(a, L, idx, S, PT, threadIdx.x);
             fresh = true;
             n_in += (L.hm[0] & 0xFFu) + (L.hm[1] & 0xFFu) + (L.hm[2] & 0xFFu) + (L.hm[3] & 0xFFu);
             n_cmp += ((L.om[0] >> 8) & 0xFFu) + ((L.om[1] >> 8) & 0xFFu) + ((L.om[2] >> 8) & 0xFFu) +
@@ -1034,13 +1088,17 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
           active = false;
           go = false;
         } else if (d >= 0) {
+          if (OBS && !LOG) obs_advance<G>(L, tb);
           bp_pre2<G>(a, L, S, threadIdx.x, d, tb);
         } else {
+          if (OBS && !LOG) obs_advance<G>(L, L.tc);
           ev_pre2<G, LOG, false, Stage, !SHARE>(a, L, S, PT, threadIdx.x, n_out, overflow);
           ev = true;
         }
       }
       if (go) {
+        if (OBS && !LOG && !fresh)  // M and B after the step
+          obs_counts<G>(L.spins, L.gN, L.gW, a.RX == 1, a.RYg == 1, L.Mi, L.Bi);
         if (SHARE && (ev || fresh)) {  // pair n: V picks the next atom, E(U) its budget
           double U;
           draw_pair(a.seed, L.gid, L.n, U, L.V, a.gen);
@@ -1088,13 +1146,13 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
 #else
 #define ISR_K1_BOUNDS __launch_bounds__(NT)
 #endif
-template <int BX, int BY, bool LOG, bool GQ = false>
+template <int BX, int BY, bool LOG, bool GQ = false, bool OBS = false>
 __global__ void ISR_K1_BOUNDS region_kernel(const KArgs a) {
-  region_body<BX, BY, LOG, GQ>(a);
+  region_body<BX, BY, LOG, GQ, OBS>(a);
 }
-template <int BX, int BY, bool LOG, bool GQ = false>
+template <int BX, int BY, bool LOG, bool GQ = false, bool OBS = false>
 __global__ void __launch_bounds__(NT, 5) region_kernel_mb(const KArgs a) {
-  region_body<BX, BY, LOG, GQ>(a);
+  region_body<BX, BY, LOG, GQ, OBS>(a);
 }
 
 // ---------------------------------------------------------------------------

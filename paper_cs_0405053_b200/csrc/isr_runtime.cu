@@ -74,8 +74,13 @@ ShapeOps make_ops() {
   o.sel_read_bytes = 5 * 16.0;
   o.region = [](const KArgs& a, int n, cudaStream_t s) {
     const int grid = (n + a.tile - 1) / a.tile;
-    if constexpr (kMB) isr::region_kernel_mb<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
-    else isr::region_kernel<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
+    if (a.obs) {  // FLAG_OBSERVABLES: the instantiation that integrates M and B
+      if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, true><<<grid, kThreads, 0, s>>>(a);
+      else isr::region_kernel<BX, BY, false, false, true><<<grid, kThreads, 0, s>>>(a);
+    } else {
+      if constexpr (kMB) isr::region_kernel_mb<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
+      else isr::region_kernel<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
+    }
   };
   o.replay = [](const KArgs& a, int n, cudaStream_t s) {
     const int grid = (n + a.tile - 1) / a.tile;
@@ -169,7 +174,8 @@ ShapeOps make_ops_w() {
   o.region = [](const KArgs& a, int n, cudaStream_t s) {
     if (big_enabled()) {
       const int grid = std::max(1, std::min((n + isr::BNT - 1) / isr::BNT, 148 * 32));
-      isr::region_kernel_big<BX, BY, false><<<grid, isr::BNT, 0, s>>>(a);
+      if (a.obs) isr::region_kernel_big<BX, BY, false, true><<<grid, isr::BNT, 0, s>>>(a);
+      else isr::region_kernel_big<BX, BY, false><<<grid, isr::BNT, 0, s>>>(a);
     } else {
       const int grid = std::max(1, std::min((n + 3) / 4, 148 * 16));
       isr::region_kernel_w<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
@@ -234,6 +240,52 @@ __global__ void __launch_bounds__(256) count_events(const uint32_t* n1, const ui
   for (int i = blockIdx.x * 256 + threadIdx.x; i < N; i += gridDim.x * 256) v += (unsigned long long)(n1[i] - n0[i]);
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(total, v);
+}
+
+// FLAG_OBSERVABLES: sums of the per-region integrals in a fixed order (a fixed
+// grid of blocks over contiguous chunks, fixed per-thread strides, fixed trees),
+// so the window's totals do not depend on the schedule
+constexpr int kObsBlocks = 256;
+__global__ void __launch_bounds__(256) obs_partial(const double* a, const double* b, int n, double* part) {
+  __shared__ double sa[256], sb[256];
+  const int chunk = (n + kObsBlocks - 1) / kObsBlocks;
+  const int beg = blockIdx.x * chunk, end = min(n, beg + chunk);
+  double x = 0.0, y = 0.0;
+  for (int i = beg + (int)threadIdx.x; i < end; i += 256) {
+    x += a[i];
+    y += b[i];
+  }
+  sa[threadIdx.x] = x;
+  sb[threadIdx.x] = y;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      sa[threadIdx.x] += sa[threadIdx.x + o];
+      sb[threadIdx.x] += sb[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = sa[0];
+    part[2 * blockIdx.x + 1] = sb[0];
+  }
+}
+__global__ void __launch_bounds__(256) obs_final(const double* part, double* out) {
+  __shared__ double sa[256], sb[256];
+  sa[threadIdx.x] = part[2 * threadIdx.x];
+  sb[threadIdx.x] = part[2 * threadIdx.x + 1];
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      sa[threadIdx.x] += sa[threadIdx.x + o];
+      sb[threadIdx.x] += sb[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = sa[0];
+    out[1] = sb[0];
+  }
 }
 
 __global__ void scan_top(unsigned long long* bsum, int nb, unsigned long long* total) {
@@ -330,6 +382,8 @@ struct ising_sr_ctx {
   unsigned long long* d_off = nullptr;
   unsigned long long* d_bsum = nullptr;
   unsigned long long* d_total = nullptr;
+  double* d_obs = nullptr;   // [2 * kObsBlocks] partial sums, then [2] window totals
+  double h_obs[2] = {0.0, 0.0};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t kev0 = nullptr, kev1 = nullptr;  // around each region-kernel launch
   cudaEvent_t bev[2 * 8] = {};                 // batched iterations: around launch j (2j, 2j+1)
@@ -490,6 +544,7 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   a.t_w = c->t_w;
   a.t_c = c->t_c;
   a.fresh_w = (c->cfg.flags & ISING_SR_FLAG_FRESH_WINDOW) ? 1 : 0;
+  a.obs = (c->cfg.flags & ISING_SR_FLAG_OBSERVABLES) ? 1 : 0;
   a.gen = a.fresh_w ? (unsigned)c->w : 0u;
   a.seed = c->cfg.seed;
   for (int k = 0; k < 10; ++k) a.rate[k] = c->cfg.rate[k];
@@ -762,6 +817,8 @@ void ising_sr_destroy(ising_sr_ctx* c) {
     cudaFree(s.R);
     cudaFree(s.n);
     cudaFree(s.dig);
+    cudaFree(s.oM);
+    cudaFree(s.oB);
   }
   free_edges(c);
   cudaFree(c->sel);
@@ -786,6 +843,7 @@ void ising_sr_destroy(ising_sr_ctx* c) {
   cudaFree(c->d_off);
   cudaFree(c->d_bsum);
   cudaFree(c->d_total);
+  cudaFree(c->d_obs);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->kev0) cudaEventDestroy(c->kev0);
@@ -825,6 +883,10 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   std::memset(&c->stats, 0, sizeof c->stats);
   if (const char* e = std::getenv("ISING_SR_REFILL")) c->refill = std::max(1, std::min(32, std::atoi(e)));
   if (const char* e = std::getenv("ISING_SR_POOL")) c->pool = std::atoi(e) != 0;
+  if ((cfg->flags & ISING_SR_FLAG_OBSERVABLES) && ((!ops->warp && c->pool) || (ops->warp && !big_enabled()))) {
+    delete c;
+    return ISING_SR_E_INVALID_ARG;  // observables are accumulated by the lane-per-region K1 forms only
+  }
   if (const char* e = std::getenv("ISING_SR_POOL_REFILL"))
     c->pool_refill = std::max(1, std::min(ISR_POOL_S, std::atoi(e)));
 
@@ -845,6 +907,9 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
         cudaMalloc(&s.halo, n * ops->halo_bytes) != cudaSuccess || dmalloc(&s.ts, n) != cudaSuccess ||
         dmalloc(&s.R, n) != cudaSuccess || dmalloc(&s.n, n) != cudaSuccess || dmalloc(&s.dig, n) != cudaSuccess)
       return bail(ISING_SR_E_OOM);
+    if ((cfg->flags & ISING_SR_FLAG_OBSERVABLES) &&
+        (dmalloc(&s.oM, n) != cudaSuccess || dmalloc(&s.oB, n) != cudaSuccess))
+      return bail(ISING_SR_E_OOM);
   }
   if (dmalloc(&c->sel, (size_t)ops->sel_words * n) != cudaSuccess || dmalloc(&c->dirty, 2 * ((n + 31) / 32)) != cudaSuccess ||
       dmalloc(&c->wl[0], n) != cudaSuccess || dmalloc(&c->wl[1], n) != cudaSuccess ||
@@ -854,7 +919,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
       cudaMallocHost((void**)&c->h_stats, 8 * kBatch * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMallocHost((void**)&c->h_wlc, 2 * sizeof(unsigned)) != cudaSuccess ||
       dmalloc(&c->d_off, n) != cudaSuccess || dmalloc(&c->d_bsum, (n + kThreads - 1) / kThreads) != cudaSuccess ||
-      dmalloc(&c->d_total, 1) != cudaSuccess)
+      dmalloc(&c->d_total, 1) != cudaSuccess || dmalloc(&c->d_obs, 2 * kObsBlocks + 2) != cudaSuccess)
     return bail(ISING_SR_E_OOM);
   if (cudaMemsetAsync(c->sel, 0, n * 8 * (size_t)ops->sel_words, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->dirty, 0, 2 * ((n + 31) / 32) * 4, c->stream) != cudaSuccess)
@@ -987,7 +1052,8 @@ ising_sr_status ising_sr_run_window(ising_sr_ctx* c, int32_t* g_out) {
   if (s) return s;
   if ((s = ising_sr_begin_window(c))) return s;
   const bool can_batch = c->cfg.world <= 1 && c->ops->region_persistent &&
-                         (!c->pool || c->ops->region_pool_persistent);
+                         (!c->pool || c->ops->region_pool_persistent) &&
+                         !(c->cfg.flags & ISING_SR_FLAG_OBSERVABLES);  // persistent forms do not integrate
   if (can_batch && c->batch > 1) {
     if ((s = run_window_batched(c, c->batch))) return s;
     if (g_out) *g_out = c->g;
@@ -1053,6 +1119,15 @@ ising_sr_status ising_sr_commit(ising_sr_ctx* c, int64_t* events_out) {
     c->launches++;
   }
   CK(c, cudaGetLastError());
+  const bool obs = (c->cfg.flags & ISING_SR_FLAG_OBSERVABLES) != 0;
+  if (obs) {  // the window's int M dt, int B dt: fixed-order sums of the regions' integrals
+    obs_partial<<<kObsBlocks, 256, 0, c->stream>>>(s1.oM, s1.oB, c->nreg, c->d_obs);
+    obs_final<<<1, 256, 0, c->stream>>>(c->d_obs, c->d_obs + 2 * kObsBlocks);
+    c->launches += 2;
+    CK(c, cudaGetLastError());
+    CK(c, cudaMemcpyAsync(c->h_obs, c->d_obs + 2 * kObsBlocks, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                          c->stream));
+  }
   unsigned long long total = 0;
   CK(c, cudaMemcpyAsync(&total, c->d_total, sizeof total, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
@@ -1107,6 +1182,13 @@ ising_sr_status ising_sr_commit(ising_sr_ctx* c, int64_t* events_out) {
   c->stats.f_max = std::max(c->stats.f_max, c->win_f);
   c->stats.bytes_alg_last_window = c->win_bytes;
   c->stats.ms_last_window = ms;
+  if (obs) {
+    c->stats.obs_M_last = c->h_obs[0];
+    c->stats.obs_B_last = c->h_obs[1];
+    c->stats.obs_M_total += c->h_obs[0];
+    c->stats.obs_B_total += c->h_obs[1];
+    c->stats.obs_time_total += c->t_w - (double)(c->w - 1) * c->cfg.W;  // t_w - t_c of this window
+  }
   if (events_out) *events_out = (long long)c->win_events;
   return ISING_SR_OK;
 }

@@ -320,3 +320,72 @@ def test_checkpoint_resume_bit_exact():
         with pytest.raises(IsingSRError):
             other.restore(ck)
         other.close()
+
+
+# ---------------------------------------------------------------------------
+# FLAG_OBSERVABLES: per-region time integrals of M and of the bond sum B,
+# reduced at commit.  Against the oracle's integrals of the global M(t), B(t)
+# (different summation order: relative 1e-9), and against Onsager's exact
+# energy and spontaneous magnetisation (an independent physics pin).
+# ---------------------------------------------------------------------------
+def _run_obs(w, **kw):
+    from paper_cs_0405053_b200 import FLAG_OBSERVABLES
+    sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed,
+                  flags=FLAG_DIGEST | FLAG_OBSERVABLES, **kw)
+    sim.run()
+    st = sim.stats()
+    dig, cnt = sim.digests()
+    sim.close()
+    return st, dig
+
+
+@pytest.mark.parametrize("geom", [
+    (32, 32, 4, 4, 2.269, 0.0, 0.5, 4.0),
+    (24, 24, 2, 2, 1.8, 0.2, 0.7, 3.0),
+    (16, 16, 1, 1, 3.0, 0.0, 0.4, 2.0),
+    (32, 32, 8, 8, 2.0, 0.0, 0.6, 4.0),
+    (64, 64, 16, 16, 2.269, 0.0, 1.0, 3.0),
+    (32, 32, 32, 32, 2.5, 0.0, 0.8, 3.0),   # region = lattice: wrap bonds
+    (32, 64, 32, 16, 2.0, 0.1, 0.5, 3.0),
+    (12, 8, 4, 8, 2.0, 0.0, 0.5, 3.0),      # 4x8 regions spanning the height
+])
+def test_observables_against_oracle(geom):
+    Lx, Ly, bx, by, T, H, W, t_end = geom
+    w = workloads.Workload("obs", Lx, Ly, bx, by, T=T, H=H, W=W, t_end=t_end, seed=2)
+    st, dig = _run_obs(w)
+    ref = oracle.des_workload(w)
+    dt, Bi, Mi = ref["obs"][0], ref["obs"][1], ref["obs"][2]
+    assert np.array_equal(dig, ref["digest"])
+    assert st["obs_time_total"] == pytest.approx(dt, rel=1e-12)
+    scale = Lx * Ly * t_end
+    assert abs(st["obs_M_total"] - Mi) < 1e-9 * scale, (st["obs_M_total"], Mi)
+    assert abs(st["obs_B_total"] - Bi) < 1e-9 * scale, (st["obs_B_total"], Bi)
+
+
+def test_observables_onsager():
+    """256^2 at T = 2 from all up: time averages over t in [20, 60) of the
+    energy per site and |m| against Onsager's exact values (finite-size
+    corrections are far below the tolerance at correlation length ~2)."""
+    from scipy.special import ellipk
+    T = 2.0
+    beta = 1.0 / T
+    k = 2 * math.sinh(2 * beta) / math.cosh(2 * beta) ** 2
+    u = -1 / math.tanh(2 * beta) * (1 + 2 / math.pi * (2 * math.tanh(2 * beta) ** 2 - 1) * ellipk(k * k))
+    m0 = (1 - math.sinh(2 * beta) ** -4) ** 0.125
+    from paper_cs_0405053_b200 import FLAG_OBSERVABLES
+    w = workloads.Workload("ons", 256, 256, 4, 4, T=T, W=0.5, t_end=60.0, init="up", seed=3)
+    sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed, flags=FLAG_OBSERVABLES)
+    for _ in range(40):
+        sim.run_window()
+        sim.commit()
+    a = sim.stats()
+    sim.run()
+    b = sim.stats()
+    sim.close()
+    n = 256 * 256
+    tt = b["obs_time_total"] - a["obs_time_total"]
+    e = -(b["obs_B_total"] - a["obs_B_total"]) / (n * tt)   # J = 1, H = 0
+    m = (b["obs_M_total"] - a["obs_M_total"]) / (n * tt)
+    assert tt == pytest.approx(40.0)
+    assert abs(e - u) < 0.004, (e, u)
+    assert abs(m - m0) < 0.01, (m, m0)
