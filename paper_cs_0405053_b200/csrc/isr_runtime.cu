@@ -1277,6 +1277,7 @@ struct CkptHeader {
   double W, t_end, rate[10];
   int64_t w;  // committed windows: t_c = fl(w W)
   int64_t windows, events_total;
+  double obs_M_total, obs_B_total, obs_time_total;
   int64_t nreg;
   int64_t bytes[6];  // spins, halo, ts, R, n, dig
   uint64_t checksum;  // FNV-1a over the arrays
@@ -1326,6 +1327,9 @@ ising_sr_status ising_sr_checkpoint_save(ising_sr_ctx* c, void* buf, int64_t cap
   h.w = c->w;
   h.windows = c->stats.windows;
   h.events_total = c->stats.events_total;
+  h.obs_M_total = c->stats.obs_M_total;
+  h.obs_B_total = c->stats.obs_B_total;
+  h.obs_time_total = c->stats.obs_time_total;
   h.nreg = c->nreg;
   state_bytes(c, h.bytes);
   unsigned char* p = (unsigned char*)buf + sizeof(CkptHeader);
@@ -1374,6 +1378,9 @@ ising_sr_status ising_sr_checkpoint_load(ising_sr_ctx* c, const void* buf, int64
   c->converged = false;
   c->stats.windows = h.windows;
   c->stats.events_total = h.events_total;
+  c->stats.obs_M_total = h.obs_M_total;
+  c->stats.obs_B_total = h.obs_B_total;
+  c->stats.obs_time_total = h.obs_time_total;
   c->stats.t_c = c->t_c < c->cfg.t_end ? c->t_c : c->cfg.t_end;
   return ISING_SR_OK;
 }

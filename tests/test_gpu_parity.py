@@ -287,8 +287,8 @@ def test_checkpoint_resume_bit_exact():
     """A run checkpointed at a committed time and resumed in a fresh ctx is
     bit-identical to the uninterrupted run; a corrupted checkpoint or one of
     another configuration is refused."""
-    from paper_cs_0405053_b200 import FLAG_FRESH_WINDOW
-    for flags in (FLAG_DIGEST, FLAG_DIGEST | FLAG_FRESH_WINDOW):
+    from paper_cs_0405053_b200 import FLAG_FRESH_WINDOW, FLAG_OBSERVABLES
+    for flags in (FLAG_DIGEST, FLAG_DIGEST | FLAG_FRESH_WINDOW | FLAG_OBSERVABLES):
         w = workloads.Workload("ck", 64, 64, 4, 4, T=2.269, W=0.5, t_end=4.0, seed=6)
         full = run_gpu(w, flags=flags)
         a = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed, flags=flags)
@@ -311,6 +311,7 @@ def test_checkpoint_resume_bit_exact():
         assert np.array_equal(dig, full["digest"]) and np.array_equal(cnt, full["count"])
         assert np.array_equal(b.spins(), full["spins"])
         assert b.stats()["events_total"] == full["events"]
+        assert b.stats()["obs_B_total"] == full["stats"]["obs_B_total"]  # same windows, same sums
         bad = bytearray(ck)
         bad[-1] ^= 1
         with pytest.raises(IsingSRError):
