@@ -260,12 +260,26 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
     unsigned hp = 0, hq = 0;  // byte d: position of the head / next entry of direction d
     unsigned chg = 0;         // bit d: incoming history d changed in the previous iteration
     unsigned qd[4];           // ... its first changed entry
+    // the four neighbours' edge selector pairs, all in flight before any is
+    // used (a direction without one re-reads the region's own pair)
+    ulonglong2 wpn[4];
+    bool use[4];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const bool axis_off = (d < 2) ? wrapY : wrapX;
+      const bool ghost = a.world > 1 && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
+      use[d] = !a.first && !axis_off && !ghost;
+      const int nr = d == EDGE_N ? wdec(r, a.RYl) : d == EDGE_S ? winc(r, a.RYl) : r;
+      const int nc = d == EDGE_W ? wdec(c, a.RX) : d == EDGE_E ? winc(c, a.RX) : c;
+      wpn[d] = __ldcg(reinterpret_cast<const ulonglong2*>(a.sel) +
+                      (use[d] ? ((long long)nr * a.RX + nc) * 4 + (d ^ 1) : (long long)idx * 4));
+    }
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
       hcnt[d] = 0; hidx[d] = 0; hsrc[d] = 0; hoff[d] = 0; ht[d] = dinf(); hn[d] = dinf(); qd[d] = 0;
       const bool axis_off = (d < 2) ? wrapY : wrapX;
       if (a.first || axis_off) continue;
-      const bool ghost = a.world > 1 && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
+      const bool ghost = !use[d];
       if (ghost) {
         const GhostView& gv = d == EDGE_N ? a.gh_up : a.gh_down;
         hcnt[d] = gv.cnt[c];
@@ -275,7 +289,7 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
       } else {
         const int nr = d == EDGE_N ? wdec(r, a.RYl) : d == EDGE_S ? winc(r, a.RYl) : r;
         const int nc = d == EDGE_W ? wdec(c, a.RX) : d == EDGE_E ? winc(c, a.RX) : c;
-        const unsigned long long v = latest_edge_word(a.sel, ((long long)nr * a.RX + nc) * 4 + (d ^ 1), K);
+        const unsigned long long v = latest_word(wpn[d], K);
         if (word_valid(v, K0)) {
           hcnt[d] = ew_count(v);
           hsrc[d] = ew_slot(v);
