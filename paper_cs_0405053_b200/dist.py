@@ -59,9 +59,11 @@ def halo_exchange(send_up: Sequence[torch.Tensor], send_down: Sequence[torch.Ten
     dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
 
 
-def make_exchange(rank: int, world: int, device: int, group=None):
+def make_exchange(rank: int, world: int, device: int, group=None, host_staging: bool = False):
     """Exchange callback for IsingSR(world > 1): wraps the library's device
-    pointers (ising_sr_halo) as tensors and runs `halo_exchange` over NCCL."""
+    pointers (ising_sr_halo) as tensors and runs `halo_exchange` over NCCL.
+    host_staging: copy through host memory (for a CPU backend such as gloo,
+    e.g. several ranks on one device in tests)."""
 
     def _exchange(h) -> int:
         n = h.nchunks
@@ -70,7 +72,17 @@ def make_exchange(rank: int, world: int, device: int, group=None):
         ru = [device_view(h.recv_from_up[k], h.chunk_bytes[k], device) for k in range(n)]
         rd = [device_view(h.recv_from_down[k], h.chunk_bytes[k], device) for k in range(n)]
         fl = device_view(h.flags, 8, device, "<i4", 4)
-        halo_exchange(su, sd, ru, rd, fl, rank, world, group)
+        if not host_staging:
+            halo_exchange(su, sd, ru, rd, fl, rank, world, group)
+            return 0
+        torch.cuda.synchronize(device)
+        hs = [[t.cpu() for t in ts] for ts in (su, sd)]
+        hr = [[torch.empty_like(t, device="cpu") for t in ts] for ts in (ru, rd)]
+        hf = fl.cpu()
+        halo_exchange(hs[0], hs[1], hr[0], hr[1], hf, rank, world, group)
+        for dst, src in zip(ru + rd + [fl], hr[0] + hr[1] + [hf]):
+            dst.copy_(src)
+        torch.cuda.synchronize(device)
         return 0
 
     return _exchange
