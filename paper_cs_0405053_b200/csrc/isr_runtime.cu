@@ -506,9 +506,14 @@ ising_sr_status check(const ising_sr_ctx* c) {
   return c->sticky;
 }
 
-// work items per block: enough blocks for >= 4 per SM, at most 16 items per lane
+// work items per block: enough blocks for >= 4 per SM, at most 16 items per
+// lane (env ISING_SR_TILE_PER overrides the cap)
 int tile_for(int n) {
-  const int per = std::max(1, std::min(16, n / (kThreads * 148 * 4)));
+  static const int cap = [] {
+    const char* e = std::getenv("ISING_SR_TILE_PER");
+    return e ? std::max(1, std::atoi(e)) : 16;
+  }();
+  const int per = std::max(1, std::min(cap, n / (kThreads * 148 * 4)));
   return kThreads * per;
 }
 

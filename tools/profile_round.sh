@@ -1,3 +1,6 @@
+# Round profile: GPU tests, the c4 bench line, the reference arm, the K1 launch list,
+# one ncu --set full capture of a whole c4 window, c1-c3 parity reports, the c5 sweep.
+# Run on the GPU box: gpurun -- bash tools/profile_round.sh (outputs in gpurun_out/).
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/gputests.log 2>&1
 timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
