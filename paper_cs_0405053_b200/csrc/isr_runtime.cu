@@ -506,12 +506,12 @@ ising_sr_status check(const ising_sr_ctx* c) {
   return c->sticky;
 }
 
-// work items per block: enough blocks for >= 4 per SM, at most 16 items per
+// work items per block: enough blocks for >= 4 per SM, at most 8 items per
 // lane (env ISING_SR_TILE_PER overrides the cap)
 int tile_for(int n) {
   static const int cap = [] {
     const char* e = std::getenv("ISING_SR_TILE_PER");
-    return e ? std::max(1, std::atoi(e)) : 16;
+    return e ? std::max(1, std::atoi(e)) : 8;  // c4: 8 > 16 (+1 %) > 4, 32, 64
   }();
   const int per = std::max(1, std::min(cap, n / (kThreads * 148 * 4)));
   return kThreads * per;
