@@ -16,7 +16,8 @@
  * compared with the previous iteration's and the iteration repeats until no
  * history changes.  The fixed point is the unique
  * trajectory of the per-region-stream dynamics; it is
- * independent of W and of the number of shards.
+ * independent of W (except with ISING_SR_FLAG_FRESH_WINDOW) and of the number
+ * of shards.
  *
  * Bit-level semantics (Philox layout, E(U), Lambda fold order, selection,
  * candidate bump, tie order) are frozen in DESIGN.md §3; results are

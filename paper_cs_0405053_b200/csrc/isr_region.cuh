@@ -459,10 +459,14 @@ __device__ __forceinline__ int div_rx(const KArgs& a, int idx) {
 // change the iteration count g or any result.
 //
 // Lane-persistent scheduling: each block owns a tile of `tile` consecutive
-// work items; every lane pulls its next region from the block's shared
-// queue the moment its current region reaches the window end, so a warp no
-// longer idles while its slowest region finishes (region histories have
-// Poisson-distributed lengths).
+// work items; a lane whose region reached the window end waits until
+// `refill` lanes of its warp are idle, then they publish their regions and
+// pull the next ones from the block's shared queue together, so a warp does
+// not idle while its slowest region finishes (region histories have
+// Poisson-distributed lengths) and the memory-heavy load/publish code runs
+// with many lanes at once.  Each round, every active lane performs exactly one
+// step -- its next break point or its own event -- and both kinds then share
+// the draw of the next pair and the refold/selection/candidate code.
 // ---------------------------------------------------------------------------
 // Per-lane shared-memory stage of the histories a region reads: up to CI
 // entries of each incoming direction and of each of its own latest edge
