@@ -163,6 +163,20 @@ def test_determinism_and_idempotence():
     sim.close()
 
 
+def test_c4_full_lattice_across_a_window_boundary():
+    """BASELINE config 4 at full size over t < 0.52: the first window [0, 0.5)
+    with its full relaxation, its commit, and the start of the second window
+    -- the bench's launch configuration -- against the oracle, region by
+    region (about 3 minutes, mostly the serial oracle)."""
+    w = workloads.get("c4", t_end=0.52)
+    ref = oracle.des_workload(w)
+    gpu = run_gpu(w, flags=FLAG_DIGEST)
+    assert len(gpu["g"]) == 2 and gpu["events"] == ref["n_events"] > 5 * 10**7
+    assert np.array_equal(gpu["count"], ref["count"])
+    assert np.array_equal(gpu["digest"], ref["digest"])
+    assert np.array_equal(gpu["spins"], ref["spins"])
+
+
 def test_c4_full_lattice_prefix():
     """BASELINE config 4 at its full size (16384^2, 4x4 regions, T=2, W=0.5) on
     the prefix t < 0.02: every region's digest and count, and all spins."""
