@@ -585,7 +585,11 @@ __device__ __forceinline__ void obs_advance(Lane<G>& L, double t) {
 
 // FULL = false: stop after the state and histories are in; the caller draws
 // the pair and refolds (sharing that code with the step)
-template <class G, bool LOG, class SG, bool FULL = true, bool OBS = false>
+// FIRST: the window's first iteration (canonical assumption): no
+// incoming histories to read or stage.  The own selector pair is still read:
+// the new word must flip the slot bit of every changed edge relative to the
+// other word (pack_kernel's change test for the strip exchange).
+template <class G, bool LOG, class SG, bool FULL = true, bool OBS = false, bool FIRST = false>
 __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, SG& S, const ProdTable<G>& PT,
                                           int si) {
   using M = typename G::M;
@@ -607,7 +611,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
     cnt[d] = 0;
     src[d] = 0;
     const bool axis_off = (d < 2) ? wrapY : wrapX;
-    if (a.first || axis_off) continue;
+    if (FIRST || a.first || axis_off) continue;
     const bool ghost = a.world > 1 && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
     if (ghost) {
       cnt[d] = (d == EDGE_N ? a.gh_up : a.gh_down).cnt[c];
@@ -997,7 +1001,7 @@ __device__ __forceinline__ void refold(const KArgs& a, Lane<G>& L, const ProdTab
 
 // GQ (persistent launch): the worklist is one global queue (a.work_ctr) and
 // its length is read on the device; otherwise each block owns a static tile.
-template <int BX, int BY, bool LOG, bool GQ, bool OBS>
+template <int BX, int BY, bool LOG, bool GQ, bool OBS, bool FIRST>
 __device__ __forceinline__ void region_body(const KArgs& a) {
   using G = Geo<BX, BY>;
   __shared__ unsigned q_next;
@@ -1065,7 +1069,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
           if (item < 0 && !global_q) item = (int)atomicAdd(&q_next, 1u);
           if (item >= 0 && item < tile_n) {
             const int idx = a.wl_in ? (int)a.wl_in[tile_begin + item] : tile_begin + item;
-            lane_load<G, LOG, Stage, !ISR_FRESH, OBS>(a, L, idx, S, PT, threadIdx.x);
+            lane_load<G, LOG, Stage, !ISR_FRESH, OBS, FIRST>(a, L, idx, S, PT, threadIdx.x);
             fresh = true;
             n_in += (L.hm[0] & 0xFFu) + (L.hm[1] & 0xFFu) + (L.hm[2] & 0xFFu) + (L.hm[3] & 0xFFu);
             n_cmp += ((L.om[0] >> 8) & 0xFFu) + ((L.om[1] >> 8) & 0xFFu) + ((L.om[2] >> 8) & 0xFFu) +
@@ -1086,8 +1090,8 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
       constexpr bool SHARE = ISR_FRESH;
       bool go = true, ev = false;
       if (!SHARE || !fresh) {
-        double tb;
-        const int d = next_bp2<G>(a, L, tb);
+        double tb = 0.0;
+        const int d = FIRST ? -1 : next_bp2<G>(a, L, tb);  // no break points in the first iteration
         if (d < 0 && !(L.tc < a.t_w)) {
           active = false;
           go = false;
@@ -1150,13 +1154,13 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
 #else
 #define ISR_K1_BOUNDS __launch_bounds__(NT)
 #endif
-template <int BX, int BY, bool LOG, bool GQ = false, bool OBS = false>
+template <int BX, int BY, bool LOG, bool GQ = false, bool OBS = false, bool FIRST = false>
 __global__ void ISR_K1_BOUNDS region_kernel(const KArgs a) {
-  region_body<BX, BY, LOG, GQ, OBS>(a);
+  region_body<BX, BY, LOG, GQ, OBS, FIRST>(a);
 }
-template <int BX, int BY, bool LOG, bool GQ = false, bool OBS = false>
+template <int BX, int BY, bool LOG, bool GQ = false, bool OBS = false, bool FIRST = false>
 __global__ void __launch_bounds__(NT, 5) region_kernel_mb(const KArgs a) {
-  region_body<BX, BY, LOG, GQ, OBS>(a);
+  region_body<BX, BY, LOG, GQ, OBS, FIRST>(a);
 }
 
 // ---------------------------------------------------------------------------

@@ -74,9 +74,19 @@ ShapeOps make_ops() {
   o.sel_read_bytes = 5 * 16.0;
   o.region = [](const KArgs& a, int n, cudaStream_t s) {
     const int grid = (n + a.tile - 1) / a.tile;
-    if (a.obs) {  // FLAG_OBSERVABLES: the instantiation that integrates M and B
-      if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, true><<<grid, kThreads, 0, s>>>(a);
-      else isr::region_kernel<BX, BY, false, false, true><<<grid, kThreads, 0, s>>>(a);
+    // instantiations: FLAG_OBSERVABLES (integrate M and B) x the window's first
+    // iteration (no incoming histories: break-point and staging code compiled out)
+    if (a.obs) {
+      if (a.first) {
+        if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, true, true><<<grid, kThreads, 0, s>>>(a);
+        else isr::region_kernel<BX, BY, false, false, true, true><<<grid, kThreads, 0, s>>>(a);
+      } else {
+        if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, true><<<grid, kThreads, 0, s>>>(a);
+        else isr::region_kernel<BX, BY, false, false, true><<<grid, kThreads, 0, s>>>(a);
+      }
+    } else if (a.first) {
+      if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, false, true><<<grid, kThreads, 0, s>>>(a);
+      else isr::region_kernel<BX, BY, false, false, false, true><<<grid, kThreads, 0, s>>>(a);
     } else {
       if constexpr (kMB) isr::region_kernel_mb<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
       else isr::region_kernel<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
