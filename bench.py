@@ -219,6 +219,7 @@ def run_ising(args):
     e2e = None
     if not args.no_e2e:
         pinned = torch.from_numpy(spins).pin_memory()
+        pinned_out = torch.empty((w.Ly // world) * w.Lx, dtype=torch.uint8).pin_memory()
         barrier()
         t0 = time.perf_counter()
         sim2 = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), pinned.numpy(), w.W, t_end, w.seed, flags=flags,
@@ -227,7 +228,7 @@ def run_ising(args):
         for _ in range(args.steps):
             sim2.run_window()
             ev2 += sim2.commit()
-        out = sim2.spins()
+        out = sim2.spins(out=pinned_out.numpy())
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         sim2.close()

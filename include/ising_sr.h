@@ -148,8 +148,10 @@ typedef struct {
 } ising_sr_stats;
 
 /* Validate cfg, allocate device state, copy the full Ly*Lx row-major spin
- * configuration (1 = up, 0 = down; caller-owned, copied) and set committed
- * time 0.  Each rank passes the whole lattice and keeps its strip. */
+ * configuration (nonzero = up, 0 = down; caller-owned, copied) and set
+ * committed time 0.  Each rank passes the whole lattice and keeps
+ * its strip; only its rows (+1 halo row each side) are read, by host-to-device
+ * copies straight from `spins` (full DMA speed when it is page-locked). */
 ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, ising_sr_ctx** out);
 
 /* Relax the window [t_c, min(t_c + W, t_end)) to the fixed point.
@@ -168,7 +170,8 @@ ising_sr_status ising_sr_run(ising_sr_ctx* ctx, int64_t* events_out);
 
 ising_sr_status ising_sr_stats_get(const ising_sr_ctx* ctx, ising_sr_stats* out);
 
-/* Own strip's committed spins, (Ly/world) x Lx row-major, 1 = up. */
+/* Own strip's committed spins, (Ly/world) x Lx row-major, 1 = up, into the
+ * caller's buffer (page-locked memory gives a full-speed copy). */
 ising_sr_status ising_sr_get_spins(ising_sr_ctx* ctx, uint8_t* out);
 
 /* Last committed window's event log (requires FLAG_LOG_EVENTS), ordered by

@@ -223,10 +223,17 @@ class IsingSR:
         d["g_hist"] = list(s.g_hist)
         return d
 
-    def spins(self) -> np.ndarray:
-        out = np.zeros((self.Ly // self.world) * self.Lx, dtype=np.uint8)
+    def spins(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """This rank's strip of committed spins, row-major uint8 (1 = up).
+        `out`: optional caller buffer of that size (e.g. a pinned tensor's
+        .numpy(), for a full-speed D2H copy)."""
+        n = (self.Ly // self.world) * self.Lx
+        if out is None:
+            out = np.empty(n, dtype=np.uint8)
+        elif out.dtype != np.uint8 or out.size != n or not out.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"out must be a contiguous uint8 array of {n} elements")
         _check(self._L.ising_sr_get_spins(self._h, out.ctypes.data), "ising_sr_get_spins")
-        return out
+        return out.reshape(-1)
 
     def events(self, cap: Optional[int] = None):
         n = ctypes.c_int64()

@@ -977,22 +977,23 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   }
   c->stats.hist_capacity = c->K;
 
-  // strip + one halo row above and below (periodic), packed by K0
+  // strip + one halo row above and below (periodic), packed by K0 (any
+  // nonzero byte is an up spin).  Copied straight from the caller's buffer in
+  // at most three row runs (DMA at full speed when it is pinned).
   const int Lx = cfg->Lx, Ly = cfg->Ly, by = cfg->by;
   const int rows = c->RYl * by + 2;
-  std::vector<uint8_t> buf((size_t)rows * Lx);
   const int y_first = c->row0 * by - 1;
-  for (int q = 0; q < rows; ++q) {
-    const int y = ((y_first + q) % Ly + Ly) % Ly;
-    const uint8_t* src = spins + (size_t)y * Lx;
-    uint8_t* dst = buf.data() + (size_t)q * Lx;
-    for (int x = 0; x < Lx; ++x) dst[x] = src[x] ? 1 : 0;
-  }
   uint8_t* dbuf = nullptr;
-  if (cudaMalloc(&dbuf, buf.size()) != cudaSuccess) return bail(ISING_SR_E_OOM);
-  if (cudaMemcpyAsync(dbuf, buf.data(), buf.size(), cudaMemcpyHostToDevice, c->stream) != cudaSuccess) {
-    cudaFree(dbuf);
-    return bail(ISING_SR_E_CUDA);
+  if (cudaMalloc(&dbuf, (size_t)rows * Lx) != cudaSuccess) return bail(ISING_SR_E_OOM);
+  for (int q = 0; q < rows;) {
+    const int y = ((y_first + q) % Ly + Ly) % Ly;
+    const int run = std::min(rows - q, Ly - y);  // contiguous up to the lattice's last row
+    if (cudaMemcpyAsync(dbuf + (size_t)q * Lx, spins + (size_t)y * Lx, (size_t)run * Lx, cudaMemcpyHostToDevice,
+                        c->stream) != cudaSuccess) {
+      cudaFree(dbuf);
+      return bail(ISING_SR_E_CUDA);
+    }
+    q += run;
   }
   ops->init(dbuf, Lx, RX, c->RYl, c->row0, cfg->seed, c->st[0], c->stream);
   c->launches++;

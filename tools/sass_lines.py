@@ -80,7 +80,12 @@ def main():
     for r in rows:
         off = int(r[ia], 16) - base
         locs = lm.get(off, [("?", 0)])
-        key = locs[-1] if args.depth == "outer" else locs[0]
+        if args.depth == "outer":
+            key = locs[-1]
+        elif args.depth == "inner":
+            key = locs[0]
+        else:  # integer: that many inlining levels below the outermost call site
+            key = locs[max(-len(locs), -1 - int(args.depth))]
         v = [int(r[iss] or 0), int(r[iie] or 0), int(r[ite] or 0)]
         for i in range(3):
             agg[key][i] += v[i]
