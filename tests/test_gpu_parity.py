@@ -229,8 +229,10 @@ def test_c5_geometry_sample_bit_exact():
 
 
 # ---------------------------------------------------------------------------
-# both schedules of the lane-form K1 (slot pool: default; lane-persistent:
-# ISING_SR_POOL=0) and extreme refill thresholds give the oracle's bits
+# every schedule of the lane-form K1 (lane-persistent: default; slot pool:
+# ISING_SR_POOL=1; persistent global queue: ISING_SR_BATCH and the tail
+# batching ISING_SR_TAIL_N/ISING_SR_TAIL_BATCH) and extreme refill
+# thresholds give the oracle's bits
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("env", [
     {"ISING_SR_POOL": "0"},

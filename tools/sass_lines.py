@@ -56,6 +56,8 @@ def ncu_sections(rep):
     for chunk in out.split('"Kernel Name"')[1:]:
         rows = list(csv.reader(io.StringIO('"Kernel Name"' + chunk)))
         hdr = rows[1]
+        if secs and secs[-1][0] == rows[0][1] and secs[-1][2] == rows[2:]:
+            continue  # ncu prints each launch's source table twice
         secs.append((rows[0][1], hdr, rows[2:]))
     return secs
 
