@@ -1005,7 +1005,11 @@ template <int BX, int BY, bool LOG, bool GQ, bool OBS, bool FIRST>
 __device__ __forceinline__ void region_body(const KArgs& a) {
   using G = Geo<BX, BY>;
   __shared__ unsigned q_next;
-  __shared__ Stage S;
+  // the first iteration stages nothing (no incoming histories, no latest own
+  // history in this window): a minimal stage frees shared memory for a sixth
+  // resident block
+  using SG = typename std::conditional<FIRST, StageT<NT, false, 1>, Stage>::type;
+  __shared__ SG S;
   __shared__ ProdTable<G> PT;
   // work: a static tile per block (lanes take items from a block queue), or
   // (work_ctr set) the whole worklist as a global queue served to a
@@ -1069,7 +1073,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
           if (item < 0 && !global_q) item = (int)atomicAdd(&q_next, 1u);
           if (item >= 0 && item < tile_n) {
             const int idx = a.wl_in ? (int)a.wl_in[tile_begin + item] : tile_begin + item;
-            lane_load<G, LOG, Stage, !ISR_FRESH, OBS, FIRST>(a, L, idx, S, PT, threadIdx.x);
+            lane_load<G, LOG, SG, !ISR_FRESH, OBS, FIRST>(a, L, idx, S, PT, threadIdx.x);
             fresh = true;
             n_in += (L.hm[0] & 0xFFu) + (L.hm[1] & 0xFFu) + (L.hm[2] & 0xFFu) + (L.hm[3] & 0xFFu);
             n_cmp += ((L.om[0] >> 8) & 0xFFu) + ((L.om[1] >> 8) & 0xFFu) + ((L.om[2] >> 8) & 0xFFu) +
@@ -1100,7 +1104,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
           bp_pre2<G>(a, L, S, threadIdx.x, d, tb);
         } else {
           if (OBS && !LOG) obs_advance<G>(L, L.tc);
-          ev_pre2<G, LOG, false, Stage, !SHARE>(a, L, S, PT, threadIdx.x, n_out, overflow);
+          ev_pre2<G, LOG, false, SG, !SHARE>(a, L, S, PT, threadIdx.x, n_out, overflow);
           ev = true;
         }
       }
@@ -1161,6 +1165,21 @@ __global__ void ISR_K1_BOUNDS region_kernel(const KArgs a) {
 template <int BX, int BY, bool LOG, bool GQ = false, bool OBS = false, bool FIRST = false>
 __global__ void __launch_bounds__(NT, 5) region_kernel_mb(const KArgs a) {
   region_body<BX, BY, LOG, GQ, OBS, FIRST>(a);
+}
+// the window's first iteration (≤ 32-site regions): no staging, so shared
+// memory no longer caps the resident blocks; ISR_FIRST_MINB asks ptxas for
+// that many (0: its own choice; 8 = 64 registers spills)
+#ifndef ISR_FIRST_MINB
+#define ISR_FIRST_MINB 7  // 72 registers, 7 blocks: +0.7 % on c4 over 6 blocks (80 registers)
+#endif
+#if ISR_FIRST_MINB > 0
+#define ISR_FIRST_BOUNDS __launch_bounds__(NT, ISR_FIRST_MINB)
+#else
+#define ISR_FIRST_BOUNDS __launch_bounds__(NT)
+#endif
+template <int BX, int BY, bool OBS = false>
+__global__ void ISR_FIRST_BOUNDS region_kernel_first(const KArgs a) {
+  region_body<BX, BY, false, false, OBS, true>(a);
 }
 
 // ---------------------------------------------------------------------------

@@ -79,14 +79,14 @@ ShapeOps make_ops() {
     if (a.obs) {
       if (a.first) {
         if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, true, true><<<grid, kThreads, 0, s>>>(a);
-        else isr::region_kernel<BX, BY, false, false, true, true><<<grid, kThreads, 0, s>>>(a);
+        else isr::region_kernel_first<BX, BY, true><<<grid, kThreads, 0, s>>>(a);
       } else {
         if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, true><<<grid, kThreads, 0, s>>>(a);
         else isr::region_kernel<BX, BY, false, false, true><<<grid, kThreads, 0, s>>>(a);
       }
     } else if (a.first) {
       if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, false, true><<<grid, kThreads, 0, s>>>(a);
-      else isr::region_kernel<BX, BY, false, false, false, true><<<grid, kThreads, 0, s>>>(a);
+      else isr::region_kernel_first<BX, BY><<<grid, kThreads, 0, s>>>(a);
     } else {
       if constexpr (kMB) isr::region_kernel_mb<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
       else isr::region_kernel<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
