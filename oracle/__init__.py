@@ -250,3 +250,20 @@ def des_workload(w, t_end: Optional[float] = None, **kw):
     """Run O1 on a workloads.Workload."""
     return des_run(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.seed, w.spins(),
                    w.t_end if t_end is None else t_end, **kw)
+
+
+def cb_run(spins, Lx: int, Ly: int, p: Sequence[float], seed: int, sweep0: int, nsweeps: int):
+    """Checkerboard Metropolis sweeps (orc_cb_run): returns (spins 0/1, flips)."""
+    L = lib()
+    L.orc_cb_run.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int64,
+                             ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
+    L.orc_cb_run.restype = ctypes.c_int
+    s = np.ascontiguousarray(spins, dtype=np.uint8).reshape(-1).copy()
+    if s.size != Lx * Ly:
+        raise ValueError("spins must have Lx*Ly entries")
+    pr = np.ascontiguousarray(p, dtype=np.float64)
+    fl = ctypes.c_int64(0)
+    rc = L.orc_cb_run(Lx, Ly, pr.ctypes.data, seed, sweep0, nsweeps, s.ctypes.data, ctypes.byref(fl))
+    if rc != 0:
+        raise ValueError("orc_cb_run: invalid arguments")
+    return s, int(fl.value)

@@ -105,6 +105,22 @@ void orc_select(const int32_t* N, const double* rate, double V, double lam, int3
 int orc_class_counts(int32_t Lx, int32_t Ly, int32_t bx, int32_t by, const uint8_t* spins,
                      int32_t* N);
 
+/* Second workload: the discrete-time Metropolis dynamics
+ * of §2: a visited atom v flips with probability p(v) = p_k of
+ * its class k = 5(s+1)/2 + u (eq. p and the table of; p_k is the
+ * rate table with lambda = 1), else stays.  Visiting order: the conventional
+ * two-colour (checkerboard) sweep -- first every site with (x + y) even,
+ * then every site with (x + y) odd, each colour in row-major order.  (Sites
+ * of one colour share no bond, so any order within a colour gives the same
+ * result.)  The decision for site i = y*Lx + x in global sweep s uses
+ * Philox4x32-10 with key = (0xFFFFFFFE, seed_lo), counter = (i, s_lo, s_hi,
+ * seed_hi), U from (x0, x1) as in orc_pair: flip iff U < p_k.
+ * Lx, Ly even and >= 4 (a bipartite periodic lattice); spins in/out,
+ * row-major, nonzero = up on input, 0/1 on output; *flips = accepted flips.
+ * Returns 0, or -1 on invalid arguments. */
+int orc_cb_run(int32_t Lx, int32_t Ly, const double* p, uint64_t seed, int64_t sweep0, int32_t nsweeps,
+               uint8_t* spins, int64_t* flips);
+
 /* batch forms of the scalar functions above (for tests) */
 void orc_expvar_n(const double* U, double* E, int64_t n);
 void orc_pair_n(uint64_t seed, const uint32_t* stream, const uint64_t* idx, double* U, double* V,
