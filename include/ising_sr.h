@@ -225,6 +225,42 @@ int64_t ising_sr_launch_count(const ising_sr_ctx* ctx);
 void ising_sr_destroy(ising_sr_ctx* ctx); /* NULL-safe */
 const char* ising_sr_strerror(ising_sr_status s);
 
+/* ------------------------------------------------------------------------
+ * Second workload: checkerboard Metropolis sweeps, the
+ * discrete-time dynamics of §2 -- a visited atom flips with
+ * probability p_k of its class k = 5(s+1)/2 + u (eq. p; the rate
+ * table with lambda = 1), else keeps its spin -- with the two-colour
+ * visiting order: a sweep visits every site with (x + y) even, then every
+ * site with (x + y) odd.  The decision of site i = y*Lx + x in global sweep
+ * s: Philox4x32-10, key = (0xFFFFFFFE, seed_lo), counter = (i, s_lo, s_hi,
+ * seed_hi), U = the 52-bit unit of words (x0, x1) as for the event pairs;
+ * flip iff U < p[k].  A statistical cross-check and conventional baseline for
+ * the n-fold way (same equilibrium, a different dynamics).
+ *
+ * spins: Ly*Lx row-major bytes, 0 = down, 1 = up (any nonzero byte reads as
+ * up; every byte of a visited word is rewritten as 0/1).  Lx, Ly even and
+ * >= 4 (a bipartite periodic lattice; else E_DIMENSION), Lx*Ly < 2^32;
+ * p[k] in [0, 1], nsweeps >= 0, sweep0 >= 0 (else E_INVALID_ARG).
+ * Sweeps sweep0 .. sweep0+nsweeps-1 are run, so a run split at any sweep is
+ * bit-identical to the run in one piece.
+ * ------------------------------------------------------------------------ */
+
+/* Device-resident lattice: d_spins is a device pointer (caller-owned,
+ * updated in place); *d_flips (device, may be NULL) is incremented by the
+ * number of accepted flips; the work is enqueued on `stream` (cudaStream_t,
+ * NULL = legacy default stream) and not synchronised.  E_CUDA if a launch
+ * fails. */
+ising_sr_status ising_cb_sweeps(uint8_t* d_spins, int32_t Lx, int32_t Ly, const double p[10], uint64_t seed,
+                                int64_t sweep0, int32_t nsweeps, uint64_t* d_flips, void* stream);
+
+/* Host buffers: copies spins_in (host, caller-owned) to `device`, runs the
+ * sweeps, copies the lattice back to spins_out (host, caller-owned; may
+ * equal spins_in) and stores the accepted flips in *flips_out (may be NULL).
+ * Synchronous.  E_OOM / E_CUDA on device failures. */
+ising_sr_status ising_cb_run(const uint8_t* spins_in, uint8_t* spins_out, int32_t Lx, int32_t Ly,
+                             const double p[10], uint64_t seed, int64_t sweep0, int32_t nsweeps,
+                             int64_t* flips_out, int32_t device);
+
 #ifdef __cplusplus
 }
 #endif

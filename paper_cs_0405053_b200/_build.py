@@ -8,7 +8,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libising_sr.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("isr_runtime.cu",)]
+SOURCES = [os.path.join(CSRC, f) for f in ("isr_runtime.cu", "isr_checkerboard.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("isr_region.cuh", "isr_warp.cuh", "isr_pool.cuh", "isr_big.cuh", "isr_device.cuh")] + [
     os.path.join(os.path.dirname(PKG), "include", "ising_sr.h")]
 

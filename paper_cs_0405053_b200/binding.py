@@ -78,7 +78,8 @@ EXPORTS = ["ising_sr_init", "ising_sr_run_window", "ising_sr_commit", "ising_sr_
            "ising_sr_begin_window", "ising_sr_iterate", "ising_sr_halo_get", "ising_sr_exchange_done",
            "ising_sr_end_iterations",
            "ising_sr_checkpoint_size", "ising_sr_checkpoint_save", "ising_sr_checkpoint_load",
-           "ising_sr_launch_count", "ising_sr_destroy", "ising_sr_strerror"]
+           "ising_sr_launch_count", "ising_sr_destroy", "ising_sr_strerror",
+           "ising_cb_sweeps", "ising_cb_run"]
 
 
 def load_library(path: str = LIB_PATH):
@@ -113,6 +114,8 @@ def load_library(path: str = LIB_PATH):
     L.ising_sr_destroy.restype = None
     L.ising_sr_strerror.argtypes = [i32]
     L.ising_sr_strerror.restype = ctypes.c_char_p
+    L.ising_cb_sweeps.argtypes = [vp, i32, i32, vp, ctypes.c_uint64, i64, i32, vp, vp]
+    L.ising_cb_run.argtypes = [vp, vp, i32, i32, vp, ctypes.c_uint64, i64, i32, ctypes.POINTER(i64), i32]
     for name in EXPORTS:
         if name not in ("ising_sr_launch_count", "ising_sr_destroy", "ising_sr_strerror"):
             getattr(L, name).restype = i32
@@ -294,3 +297,45 @@ def from_workload(w, *, spins: Optional[np.ndarray] = None, **kw) -> IsingSR:
     s = w.spins() if spins is None else spins
     return IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), s, w.W, w.t_end, w.seed,
                    J=w.J, H=w.H, T=w.T, **kw)
+
+
+# ---------------------------------------------------------------------------
+# second workload: checkerboard Metropolis sweeps (include/ising_sr.h, ising_cb_*)
+# ---------------------------------------------------------------------------
+def _probs(p: Sequence[float]) -> np.ndarray:
+    a = np.ascontiguousarray(p, dtype=np.float64)
+    if a.shape != (10,):
+        raise ValueError("p must hold the 10 class probabilities")
+    return a
+
+
+def checkerboard_run(spins: np.ndarray, Lx: int, Ly: int, p: Sequence[float], seed: int, sweep0: int,
+                     nsweeps: int, device: int = 0, out: Optional[np.ndarray] = None):
+    """ising_cb_run: `nsweeps` checkerboard Metropolis sweeps of a host
+    lattice (Ly*Lx uint8, 1 = up), starting at global sweep `sweep0`.
+    Returns (spins, accepted flips)."""
+    L = load_library()
+    s = np.ascontiguousarray(spins, dtype=np.uint8).reshape(-1)
+    if s.size != Lx * Ly:
+        raise ValueError("spins must have Lx*Ly entries")
+    if out is None:
+        out = np.empty_like(s)
+    elif out.dtype != np.uint8 or out.size != s.size or not out.flags["C_CONTIGUOUS"]:
+        raise ValueError("out must be a contiguous uint8 array of Lx*Ly elements")
+    pr = _probs(p)
+    fl = ctypes.c_int64()
+    _check(L.ising_cb_run(s.ctypes.data, out.ctypes.data, Lx, Ly, pr.ctypes.data, seed, sweep0, nsweeps,
+                          ctypes.byref(fl), device), "ising_cb_run")
+    return out.reshape(-1), int(fl.value)
+
+
+def checkerboard_sweeps(d_spins: int, Lx: int, Ly: int, p: Sequence[float], seed: int, sweep0: int, nsweeps: int,
+                        d_flips: Optional[int] = None, stream: Optional[int] = None, device: int = 0):
+    """ising_cb_sweeps on a device-resident lattice (raw device pointers,
+    e.g. tensor.data_ptr()); enqueued on `stream` (default: torch's current
+    stream), not synchronised."""
+    L = load_library()
+    pr = _probs(p)
+    st = stream if stream is not None else _current_stream_ptr(device)
+    _check(L.ising_cb_sweeps(d_spins, Lx, Ly, pr.ctypes.data, seed, sweep0, nsweeps, d_flips, st),
+           "ising_cb_sweeps")
