@@ -298,7 +298,7 @@ def run_ising(args):
 # second workload (--config cb): checkerboard Metropolis sweeps of the c4
 # lattice (16384^2, T = 2, H = 0, seed 1); a step = one sweep (both colours)
 # --------------------------------------------------------------------------
-CB_OPS_PER_SITE = 80  # integer ops of one visit: Philox4x32-10 (10 rounds x 7) + U, class, compare
+CB_OPS_PER_SITE = 45  # integer ops of one visit: half a Philox4x32-10 draw (10 rounds x 7 / 2) + U, class, compare
 
 
 def run_cb(args):

@@ -231,16 +231,19 @@ const char* ising_sr_strerror(ising_sr_status s);
  * probability p_k of its class k = 5(s+1)/2 + u (eq. p; the rate
  * table with lambda = 1), else keeps its spin -- with the two-colour
  * visiting order: a sweep visits every site with (x + y) even, then every
- * site with (x + y) odd.  The decision of site i = y*Lx + x in global sweep
- * s: Philox4x32-10, key = (0xFFFFFFFE, seed_lo), counter = (i, s_lo, s_hi,
- * seed_hi), U = the 52-bit unit of words (x0, x1) as for the event pairs;
- * flip iff U < p[k].  A statistical cross-check and conventional baseline for
+ * site with (x + y) odd.  Random numbers (R29): in row y the
+ * sites of colour c are numbered j = 0, 1, ... in increasing x; sites 2m and
+ * 2m+1 share the Philox4x32-10 draw with key = (0xFFFFFFFE, seed_lo),
+ * counter = (y*ceil(Lx/4) + m, s_lo, s_hi | c << 31, seed_hi), s the global
+ * sweep; site 2m takes U = the 52-bit unit of words (x0, x1), site 2m+1 of
+ * (x2, x3), as for the event pairs; a site flips iff U < p[k].  A statistical cross-check and conventional baseline for
  * the n-fold way (same equilibrium, a different dynamics).
  *
  * spins: Ly*Lx row-major bytes, 0 = down, 1 = up (any nonzero byte reads as
  * up; every byte of a visited word is rewritten as 0/1).  Lx, Ly even and
  * >= 4 (a bipartite periodic lattice; else E_DIMENSION), Lx*Ly < 2^32;
- * p[k] in [0, 1], nsweeps >= 0, sweep0 >= 0 (else E_INVALID_ARG).
+ * p[k] in [0, 1], nsweeps >= 0, 0 <= sweep0, sweep0 + nsweeps < 2^62
+ * (else E_INVALID_ARG).
  * Sweeps sweep0 .. sweep0+nsweeps-1 are run, so a run split at any sweep is
  * bit-identical to the run in one piece.
  * ------------------------------------------------------------------------ */

@@ -646,10 +646,12 @@ int orc_class_counts(int32_t Lx, int32_t Ly, int32_t bx, int32_t by, const uint8
 int orc_cb_run(int32_t Lx, int32_t Ly, const double* p, uint64_t seed, int64_t sweep0, int32_t nsweeps,
                uint8_t* spins, int64_t* flips) {
   if (Lx < 4 || Ly < 4 || (Lx & 1) || (Ly & 1) || nsweeps < 0 || sweep0 < 0 || !spins || !p) return -1;
+  if ((int64_t)Lx * Ly > 0xFFFFFFFFLL || sweep0 + (int64_t)nsweeps > 0x7FFFFFFFFFFFFFFFLL / 2) return -1;
   for (int k = 0; k < 10; ++k)
     if (!(p[k] >= 0.0 && p[k] <= 1.0)) return -1;
   const int64_t N = (int64_t)Lx * Ly;
   for (int64_t i = 0; i < N; ++i) spins[i] = spins[i] ? 1 : 0;
+  const int32_t ppr = (Lx + 2) / 4;  /* draws per row and colour: ceil((Lx/2) / 2) */
   int64_t nflip = 0;
   for (int64_t s = sweep0; s < sweep0 + nsweeps; ++s) {
     for (int colour = 0; colour < 2; ++colour) {
@@ -661,11 +663,16 @@ int orc_cb_run(int32_t Lx, int32_t Ly, const double* p, uint64_t seed, int64_t s
           const int up = spins[(int64_t)((y + Ly - 1) % Ly) * Lx + x] + spins[(int64_t)((y + 1) % Ly) * Lx + x] +
                          spins[(int64_t)y * Lx + (x + Lx - 1) % Lx] + spins[(int64_t)y * Lx + (x + 1) % Lx];
           const int k = (spins[i] ? 5 : 0) + up;
-          uint32_t ctr[4] = {(uint32_t)i, (uint32_t)s, (uint32_t)((uint64_t)s >> 32), (uint32_t)(seed >> 32)};
+          /* this site is the j-th of its colour in row y; sites 2m and 2m+1
+             share draw q = y * ppr + m: U from words (x0,x1), resp. (x2,x3) */
+          const int32_t j = x >> 1, m = j >> 1;
+          const uint32_t q = (uint32_t)((int64_t)y * ppr + m);
+          uint32_t ctr[4] = {q, (uint32_t)s, (uint32_t)((uint64_t)s >> 32) | ((uint32_t)colour << 31),
+                             (uint32_t)(seed >> 32)};
           uint32_t key[2] = {0xFFFFFFFEu, (uint32_t)seed};
           uint32_t xw[4];
           orc_philox4x32_10(ctr, key, xw);
-          const double U = unit_from_words(xw[0], xw[1]);
+          const double U = (j & 1) ? unit_from_words(xw[2], xw[3]) : unit_from_words(xw[0], xw[1]);
           if (U < p[k]) {
             spins[i] ^= 1;
             ++nflip;

@@ -112,9 +112,12 @@ int orc_class_counts(int32_t Lx, int32_t Ly, int32_t bx, int32_t by, const uint8
  * two-colour (checkerboard) sweep -- first every site with (x + y) even,
  * then every site with (x + y) odd, each colour in row-major order.  (Sites
  * of one colour share no bond, so any order within a colour gives the same
- * result.)  The decision for site i = y*Lx + x in global sweep s uses
- * Philox4x32-10 with key = (0xFFFFFFFE, seed_lo), counter = (i, s_lo, s_hi,
- * seed_hi), U from (x0, x1) as in orc_pair: flip iff U < p_k.
+ * result.)  Random numbers (R29): in row y the sites of colour c
+ * in increasing x are numbered j = 0, 1, ...; sites 2m and 2m+1 share the
+ * Philox4x32-10 draw with key = (0xFFFFFFFE, seed_lo), counter = (q, s_lo,
+ * s_hi | c << 31, seed_hi), q = y * ceil(Lx/4) + m, s the global sweep; site
+ * 2m takes U from words (x0, x1), site 2m+1 from (x2, x3), mapped as in
+ * orc_pair; the site flips iff U < p_k.
  * Lx, Ly even and >= 4 (a bipartite periodic lattice); spins in/out,
  * row-major, nonzero = up on input, 0/1 on output; *flips = accepted flips.
  * Returns 0, or -1 on invalid arguments. */

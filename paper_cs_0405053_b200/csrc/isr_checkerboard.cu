@@ -4,14 +4,17 @@
 // P:166-181), else keeps its spin.  Visiting order: the two-colour sweep,
 // first every site with (x + y) even, then every site with (x + y) odd;
 // sites of one colour share no bond, so one colour is one data-parallel pass.
-// Site i = y Lx + x in global sweep s decides with Philox4x32-10, key =
-// (0xFFFFFFFE, seed_lo), counter = (i, s_lo, s_hi, seed_hi), U from words
-// (x0, x1) exactly as the n-fold way's pairs (isr_device.cuh): flip iff
-// U < p_k.  include/ising_sr.h documents the C ABI.
+// Random numbers (R29): in row y the sites of colour c are
+// numbered j = 0, 1, ... in increasing x; sites 2m and 2m+1 share one
+// Philox4x32-10 draw, key = (0xFFFFFFFE, seed_lo), counter = (q, s_lo,
+// s_hi | c << 31, seed_hi), q = y ceil(Lx/4) + m; site 2m takes U from words
+// (x0, x1), site 2m+1 from (x2, x3), mapped exactly as the n-fold way's pairs
+// (isr_device.cuh); a site flips iff U < p_k.  include/ising_sr.h documents
+// the C ABI.
 //
-// The pass is bound by integer issue (one Philox-10 per visited site), not
-// by HBM: a thread owns one aligned 4-byte word of a row (2 sites of the
-// colour), reads it and the words above and below (coalesced), the two
+// The pass is bound by integer issue (one Philox-10 per two visited sites),
+// not by HBM: a thread owns one aligned 4-byte word of a row (the 2 sites of
+// the colour that share a draw), reads it and the words above and below (coalesced), the two
 // bytes left and right of it (L1 hits: the neighbouring lanes' words), and
 // writes the word back only when a site flipped.  Grid-stride over the
 // lattice's words, one flip-count atomic per block.
@@ -30,6 +33,23 @@ struct Probs {
 
 constexpr int kThreads = 256;
 
+// i / d == (i * M) >> k for every i < 2^31 (k = 31 + ceil(log2 d), M = ceil(2^k / d))
+struct Div {
+  unsigned M;
+  int k;
+  __device__ __forceinline__ unsigned operator()(unsigned i) const {
+    return (unsigned)(((unsigned long long)i * M) >> k);
+  }
+};
+Div make_div(unsigned d) {
+  int l = 0;
+  while ((1ull << l) < d) ++l;
+  Div v;
+  v.k = 31 + l;
+  v.M = (unsigned)(((1ull << v.k) + d - 1) / d);
+  return v;
+}
+
 // 0x01 in every nonzero byte of w
 __device__ __forceinline__ uint32_t nz_bytes(uint32_t w) {
   return (((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w) >> 7 & 0x01010101u;
@@ -45,14 +65,14 @@ __device__ __forceinline__ uint32_t nz_bytes(uint32_t w) {
   }                                                                                        \
   __syncthreads();
 
-__device__ __forceinline__ bool decide(const double* p, unsigned long long seed, uint32_t site,
-                                       unsigned long long sweep, int k) {
-  U4 c{site, (uint32_t)sweep, (uint32_t)(sweep >> 32), (uint32_t)(seed >> 32)};
-  const U4 x = philox4x32_10(c, 0xFFFFFFFEu, (uint32_t)seed);
-  return unit52(x.x, x.y) < p[k];
+// the draw shared by sites 2m and 2m+1 of colour `colour` in a row (q = y ceil(Lx/4) + m)
+__device__ __forceinline__ U4 draw_cb(unsigned long long seed, uint32_t q, unsigned long long sweep, int colour) {
+  U4 c{q, (uint32_t)sweep, (uint32_t)(sweep >> 32) | ((uint32_t)colour << 31), (uint32_t)(seed >> 32)};
+  return philox4x32_10(c, 0xFFFFFFFEu, (uint32_t)seed);
 }
 
-__device__ __forceinline__ void block_count(unsigned long long n, unsigned long long* flips) {
+__device__ __forceinline__ void block_count(unsigned n32, unsigned long long* flips) {
+  unsigned long long n = n32;
   __shared__ unsigned long long part[kThreads / 32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
@@ -68,33 +88,35 @@ __device__ __forceinline__ void block_count(unsigned long long n, unsigned long 
 // word form (Lx % 4 == 0): thread = one aligned word of 4 sites
 __global__ void __launch_bounds__(kThreads) half_sweep_w(uint8_t* spins, int Lx, int Ly, Probs P,
                                                           unsigned long long seed, unsigned long long sweep, int colour,
-                                                          unsigned long long* flips) {
+                                                          unsigned long long* flips, Div dw) {
   const int wpr = Lx >> 2;  // words per row
-  const long long nw = (long long)wpr * Ly;
+  const unsigned nw = (unsigned)wpr * (unsigned)Ly;  // < 2^30
   uint32_t* W = reinterpret_cast<uint32_t*>(spins);
   ISR_CB_STAGE_PROBS(P, p)
-  unsigned long long n = 0;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < nw; t += (long long)gridDim.x * blockDim.x) {
-    const int y = (int)(t / wpr), j = (int)(t - (long long)y * wpr);
+  unsigned n = 0;
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < nw; t += gridDim.x * blockDim.x) {
+    const int y = (int)dw(t), j = (int)(t - (unsigned)y * wpr);
     const int yu = y == 0 ? Ly - 1 : y - 1, yd = y == Ly - 1 ? 0 : y + 1;
     const uint32_t w = nz_bytes(__ldcg(W + t));
-    const uint32_t wu = nz_bytes(__ldcg(W + (long long)yu * wpr + j));
-    const uint32_t wd = nz_bytes(__ldcg(W + (long long)yd * wpr + j));
+    const uint32_t wu = nz_bytes(__ldcg(W + ((unsigned)yu * wpr + j)));
+    const uint32_t wd = nz_bytes(__ldcg(W + ((unsigned)yd * wpr + j)));
     const int x0 = j << 2;
-    const uint8_t* row = spins + (long long)y * Lx;
+    const uint8_t* row = spins + (unsigned)y * Lx;
     const uint32_t bl = row[x0 == 0 ? Lx - 1 : x0 - 1] != 0;
     const uint32_t br = row[x0 + 4 == Lx ? 0 : x0 + 4] != 0;
     // horizontal neighbours of each byte: (w << 8 | bl) and (w >> 8 | br << 24)
     const uint32_t left = (w << 8) | bl, right = (w >> 8) | (br << 24);
     const uint32_t ups = wu + wd + left + right;  // per byte: up neighbours, 0..4 (no carries)
     const int o = (y + colour) & 1;               // first byte of the colour in this word
+    const U4 r = draw_cb(seed, (uint32_t)t, sweep, colour);  // q = y (Lx/4) + j = t: sites 2t', 2t'+1 of the row
     uint32_t out = w;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int b = o + 2 * h;
       const int s = (int)((w >> (8 * b)) & 1u);
       const int k = 5 * s + (int)((ups >> (8 * b)) & 0xFFu);
-      if (decide(p, seed, (uint32_t)((long long)y * Lx + x0 + b), sweep, k)) {
+      const double U = h ? unit52(r.z, r.w) : unit52(r.x, r.y);
+      if (U < p[k]) {
         out ^= 1u << (8 * b);
         ++n;
       }
@@ -104,28 +126,36 @@ __global__ void __launch_bounds__(kThreads) half_sweep_w(uint8_t* spins, int Lx,
   block_count(n, flips);
 }
 
-// site form (any even Lx): thread = one site of the colour
+// site form (any even Lx): thread = the (one or two) sites of the colour
+// that share a draw
 __global__ void __launch_bounds__(kThreads) half_sweep_s(uint8_t* spins, int Lx, int Ly, Probs P,
                                                           unsigned long long seed, unsigned long long sweep, int colour,
-                                                          unsigned long long* flips) {
-  const int hx = Lx >> 1;
-  const long long ns = (long long)hx * Ly;
+                                                          unsigned long long* flips, Div dq) {
+  const int hx = Lx >> 1, ppr = (Lx + 2) >> 2;  // sites of the colour per row, draws per row
+  const unsigned nq = (unsigned)ppr * (unsigned)Ly;  // < 2^31
   ISR_CB_STAGE_PROBS(P, p)
-  unsigned long long n = 0;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < ns; t += (long long)gridDim.x * blockDim.x) {
-    const int y = (int)(t / hx);
-    const int x = 2 * (int)(t - (long long)y * hx) + ((y + colour) & 1);
+  unsigned n = 0;
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < nq; t += gridDim.x * blockDim.x) {
+    const int y = (int)dq(t), m = (int)(t - (unsigned)y * ppr);
     const int yu = y == 0 ? Ly - 1 : y - 1, yd = y == Ly - 1 ? 0 : y + 1;
-    const int xl = x == 0 ? Lx - 1 : x - 1, xr = x == Lx - 1 ? 0 : x + 1;
-    const long long i = (long long)y * Lx + x;
-    const uint8_t v = spins[i];
-    const int up = (spins[(long long)yu * Lx + x] != 0) + (spins[(long long)yd * Lx + x] != 0) +
-                   (spins[(long long)y * Lx + xl] != 0) + (spins[(long long)y * Lx + xr] != 0);
-    const int s = v != 0;
-    const bool f = decide(p, seed, (uint32_t)i, sweep, 5 * s + up);
-    n += f;
-    const uint8_t nv = (uint8_t)(f ? 1 - s : s);
-    if (nv != v) spins[i] = nv;
+    const U4 r = draw_cb(seed, (uint32_t)t, sweep, colour);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = 2 * m + h;
+      if (j >= hx) break;
+      const int x = 2 * j + ((y + colour) & 1);
+      const int xl = x == 0 ? Lx - 1 : x - 1, xr = x == Lx - 1 ? 0 : x + 1;
+      const unsigned i = (unsigned)y * Lx + x;  // < 2^32
+      const uint8_t v = spins[i];
+      const int up = (spins[(unsigned)yu * Lx + x] != 0) + (spins[(unsigned)yd * Lx + x] != 0) +
+                     (spins[(unsigned)y * Lx + xl] != 0) + (spins[(unsigned)y * Lx + xr] != 0);
+      const int s = v != 0;
+      const double U = h ? unit52(r.z, r.w) : unit52(r.x, r.y);
+      const bool f = U < p[5 * s + up];
+      n += f;
+      const uint8_t nv = (uint8_t)(f ? 1 - s : s);
+      if (nv != v) spins[i] = nv;
+    }
   }
   block_count(n, flips);
 }
@@ -139,7 +169,8 @@ ising_sr_status check_args(const uint8_t* spins, int32_t Lx, int32_t Ly, const d
                            int32_t nsweeps) {
   if (!spins || !p || nsweeps < 0 || sweep0 < 0) return ISING_SR_E_INVALID_ARG;
   if (Lx < 4 || Ly < 4 || (Lx & 1) || (Ly & 1)) return ISING_SR_E_DIMENSION;
-  if ((long long)Lx * Ly > 0xffffffffLL) return ISING_SR_E_INVALID_ARG;  // site ids are 32-bit counters
+  if ((long long)Lx * Ly > 0xffffffffLL) return ISING_SR_E_INVALID_ARG;  // draw ids are 32-bit counters
+  if (sweep0 + (long long)nsweeps > 0x3fffffffffffffffLL) return ISING_SR_E_INVALID_ARG;  // the colour bit of s_hi
   for (int k = 0; k < 10; ++k)
     if (!(p[k] >= 0.0 && p[k] <= 1.0)) return ISING_SR_E_INVALID_ARG;
   return ISING_SR_OK;
@@ -159,15 +190,18 @@ ising_sr_status ising_cb_sweeps(uint8_t* d_spins, int32_t Lx, int32_t Ly, const 
   for (int k = 0; k < 10; ++k) P.p[k] = p[k];
   cudaStream_t s = (cudaStream_t)stream;
   const bool word = (Lx & 3) == 0 && ((uintptr_t)d_spins & 3) == 0;
-  const long long items = word ? (long long)(Lx >> 2) * Ly : (long long)(Lx >> 1) * Ly;
+  const long long items = word ? (long long)(Lx >> 2) * Ly : (long long)((Lx + 2) >> 2) * Ly;
   const int grid = grid_for(items);
+  const Div dv = make_div(word ? (unsigned)(Lx >> 2) : (unsigned)((Lx + 2) >> 2));
   for (int64_t q = 0; q < nsweeps; ++q) {
     const unsigned long long sw = (unsigned long long)(sweep0 + q);
     for (int colour = 0; colour < 2; ++colour) {
       if (word)
-        half_sweep_w<<<grid, kThreads, 0, s>>>(d_spins, Lx, Ly, P, seed, sw, colour, (unsigned long long*)d_flips);
+        half_sweep_w<<<grid, kThreads, 0, s>>>(d_spins, Lx, Ly, P, seed, sw, colour, (unsigned long long*)d_flips,
+                                                dv);
       else
-        half_sweep_s<<<grid, kThreads, 0, s>>>(d_spins, Lx, Ly, P, seed, sw, colour, (unsigned long long*)d_flips);
+        half_sweep_s<<<grid, kThreads, 0, s>>>(d_spins, Lx, Ly, P, seed, sw, colour, (unsigned long long*)d_flips,
+                                                dv);
     }
   }
   return cudaGetLastError() == cudaSuccess ? ISING_SR_OK : ISING_SR_E_CUDA;

@@ -52,6 +52,8 @@ def test_cb_invalid_arguments():
         checkerboard_run(np.zeros(16, np.uint8), 4, 4, [2.0] + [0.5] * 9, 1, 0, 1)
     with pytest.raises(IsingSRError):
         checkerboard_run(np.zeros(16, np.uint8), 4, 4, [0.5] * 10, 1, -1, 1)
+    with pytest.raises(IsingSRError):
+        checkerboard_run(np.zeros(16, np.uint8), 4, 4, [0.5] * 10, 1, 2**62, 1)  # the colour bit of the counter
 
 
 def test_cb_device_api_split_run():

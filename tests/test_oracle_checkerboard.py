@@ -61,16 +61,20 @@ def test_split_run_equals_one_run():
     assert np.array_equal(a, b2) and fa == f1 + f2
 
 
-def _philox_u(i, s, seed):
-    x = oracle.philox([i, s & 0xFFFFFFFF, s >> 32, seed >> 32], [0xFFFFFFFE, seed & 0xFFFFFFFF])
-    a = ((int(x[0]) << 32) | int(x[1])) >> 12
+def _philox_u(Lx, y, x, colour, s, seed):
+    j = x // 2
+    q = y * ((Lx + 2) // 4) + j // 2
+    w = oracle.philox([q, s & 0xFFFFFFFF, (s >> 32) | (colour << 31), seed >> 32], [0xFFFFFFFE, seed & 0xFFFFFFFF])
+    hi, lo = (w[2], w[3]) if j % 2 else (w[0], w[1])
+    a = ((int(hi) << 32) | int(lo)) >> 12
     return (a + 0.5) * 2.0 ** -52
 
 
-def test_any_order_within_a_colour():
+@pytest.mark.parametrize("Lx,Ly", [(6, 4), (8, 6)])  # Lx % 4 == 2: the last site of a row and colour draws alone
+def test_any_order_within_a_colour(Lx, Ly):
     """Brute force: visit each colour's sites in reverse (column-major,
     bottom-up) order, deciding every site with its pinned Philox draw."""
-    Lx, Ly, seed = 6, 4, 11
+    seed = 11
     p = [0.05 * (k + 1) for k in range(10)]  # distinct per class: a wrong class index shows
     s0 = workloads.initial_spins(Lx, Ly, "random", 4).reshape(Ly, Lx).astype(np.int64)
     s = s0.copy()
@@ -82,7 +86,7 @@ def test_any_order_within_a_colour():
                         continue
                     u = s[(y - 1) % Ly, x] + s[(y + 1) % Ly, x] + s[y, (x - 1) % Lx] + s[y, (x + 1) % Lx]
                     k = 5 * s[y, x] + u
-                    if _philox_u(y * Lx + x, sw, seed) < p[k]:
+                    if _philox_u(Lx, y, x, colour, sw, seed) < p[k]:
                         s[y, x] ^= 1
     got, _ = oracle.cb_run(s0.astype(np.uint8), Lx, Ly, p, seed, 0, 3)
     assert np.array_equal(got, s.reshape(-1).astype(np.uint8))
