@@ -106,7 +106,9 @@ typedef int (*ising_sr_exchange_fn)(void* user, const ising_sr_halo* halo);
 
 typedef struct {
   int32_t Lx, Ly;           /* lattice, periodic both ways; >= 3                 */
-  int32_t bx, by;           /* region size; divides Lx, Ly; supported: 1,2,4,8 (square)      */
+  int32_t bx, by;           /* region size; divides Lx, Ly; supported: 1x1, 2x2, 4x4, 8x8,   *
+                             * 4x2, 2x4, 8x4, 4x8 (lane form), 16x16, 32x32, 16x32, 32x16,   *
+                             * 16x8, 8x16 (big-region form); else E_INVALID_ARG             */
   double J, H, T;           /* recorded for observables; the dynamics use `rate` only        */
   double rate[10];          /* r_k = lambda p_k, class k = 5(s+1)/2 + u          */
   double W;                 /* window length = the paper's T_max, > 0            */
@@ -145,6 +147,12 @@ typedef struct {
   /* FLAG_OBSERVABLES: integrals over the last committed window and over all
    * committed windows (this rank's regions): int M dt, int B dt, and the time */
   double obs_M_last, obs_B_last, obs_M_total, obs_B_total, obs_time_total;
+  /* regions recomputed in relaxation iteration k+1 of the last committed
+   * window (the worklist length; bin 63 collects iterations >= 64) */
+  int64_t active_last[64];
+  /* host wall time (ms, all windows) inside the world > 1 exchange callback
+   * (halo exchange + flag all-reduce) and inside ising_sr_commit */
+  double ms_exchange_total, ms_commit_total;
 } ising_sr_stats;
 
 /* Validate cfg, allocate device state, copy the full Ly*Lx row-major spin

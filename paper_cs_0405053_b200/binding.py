@@ -68,7 +68,9 @@ class Stats(ctypes.Structure):
                 ("region_bytes", ctypes.c_double),
                 ("obs_M_last", ctypes.c_double), ("obs_B_last", ctypes.c_double),
                 ("obs_M_total", ctypes.c_double), ("obs_B_total", ctypes.c_double),
-                ("obs_time_total", ctypes.c_double)]
+                ("obs_time_total", ctypes.c_double),
+                ("active_last", ctypes.c_int64 * 64),
+                ("ms_exchange_total", ctypes.c_double), ("ms_commit_total", ctypes.c_double)]
 
 
 _lib = None
@@ -224,6 +226,7 @@ class IsingSR:
         _check(self._L.ising_sr_stats_get(self._h, ctypes.byref(s)), "ising_sr_stats_get")
         d = {name: getattr(s, name) for name, _ in Stats._fields_}
         d["g_hist"] = list(s.g_hist)
+        d["active_last"] = list(s.active_last)
         return d
 
     def spins(self, out: Optional[np.ndarray] = None) -> np.ndarray:

@@ -10,6 +10,7 @@
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys / ncu --nvtx
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -413,6 +414,7 @@ struct ising_sr_ctx {
   int g = 0;
   // per-window accumulators
   unsigned long long win_events = 0;
+  long long win_active[64] = {};  // regions recomputed per iteration of the window in progress
   double win_bytes = 0.0;
   int win_f = 0;
   long long launches = 0;
@@ -652,8 +654,10 @@ ising_sr_status mark_ghosts(ising_sr_ctx* c) {
   return compact_worklist(c);
 }
 
-void account_iteration(ising_sr_ctx* c, float kms, const unsigned long long* s) {
+// iteration `it` (1-based) of the window in progress
+void account_iteration(ising_sr_ctx* c, float kms, const unsigned long long* s, int it) {
   const double ib = iteration_bytes(c, s);
+  c->win_active[std::min(std::max(it, 1), 64) - 1] += (long long)s[5];
   c->stats.region_launches++;
   c->stats.region_ms += kms;
   c->stats.region_bytes += ib;
@@ -673,7 +677,7 @@ ising_sr_status read_flags(ising_sr_ctx* c) {
   CK(c, cudaStreamSynchronize(c->stream));
   float kms = 0.f;
   CK(c, cudaEventElapsedTime(&kms, c->kev0, c->kev1));
-  account_iteration(c, kms, c->h_stats);
+  account_iteration(c, kms, c->h_stats, c->it);
   c->n_work = (int)c->h_wlc[0];
   return ISING_SR_OK;
 }
@@ -718,6 +722,7 @@ void start_window(ising_sr_ctx* c) {
   c->win_events = 0;
   c->win_bytes = 0.0;
   c->win_f = 0;
+  std::memset(c->win_active, 0, sizeof c->win_active);
 }
 
 // ---------------------------------------------------------------------------
@@ -773,7 +778,7 @@ ising_sr_status run_window_batched(ising_sr_ctx* c, int bmax) {
     for (int j = 0; j < B; ++j) {
       float kms = 0.f;
       CK(c, cudaEventElapsedTime(&kms, c->bev[2 * j], c->bev[2 * j + 1]));
-      account_iteration(c, kms, c->h_stats + 8 * j);
+      account_iteration(c, kms, c->h_stats + 8 * j, it0 + j + 1);
       if (c->h_flags[4 * j + 1]) {  // history capacity overflow: grow and restart the window
         if ((s = grow_capacity(c))) return s;
         start_window(c);
@@ -1081,7 +1086,11 @@ ising_sr_status ising_sr_run_window(ising_sr_ctx* c, int32_t* g_out) {
       if (!c->cfg.exchange) return ISING_SR_E_INVALID_ARG;
       ising_sr_halo h;
       fill_halo(c, &h);
-      if (c->cfg.exchange(c->cfg.exchange_user, &h) != 0) return ISING_SR_E_NCCL;
+      const auto x0 = std::chrono::steady_clock::now();
+      const int xr = c->cfg.exchange(c->cfg.exchange_user, &h);
+      c->stats.ms_exchange_total +=
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - x0).count();
+      if (xr != 0) return ISING_SR_E_NCCL;
       if ((s = mark_ghosts(c))) return s;
     }
     if ((s = read_flags(c))) return s;
@@ -1110,7 +1119,7 @@ ising_sr_status ising_sr_run_window(ising_sr_ctx* c, int32_t* g_out) {
   return ISING_SR_OK;
 }
 
-ising_sr_status ising_sr_commit(ising_sr_ctx* c, int64_t* events_out) {
+static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
   NvtxRange nv("isr commit");
   ising_sr_status s = check(c);
   if (s) return s;
@@ -1197,6 +1206,7 @@ ising_sr_status ising_sr_commit(ising_sr_ctx* c, int64_t* events_out) {
   c->stats.f_last = c->win_f;
   c->stats.f_max = std::max(c->stats.f_max, c->win_f);
   c->stats.bytes_alg_last_window = c->win_bytes;
+  std::memcpy(c->stats.active_last, c->win_active, sizeof c->win_active);
   c->stats.ms_last_window = ms;
   if (obs) {
     c->stats.obs_M_last = c->h_obs[0];
@@ -1207,6 +1217,13 @@ ising_sr_status ising_sr_commit(ising_sr_ctx* c, int64_t* events_out) {
   }
   if (events_out) *events_out = (long long)c->win_events;
   return ISING_SR_OK;
+}
+
+ising_sr_status ising_sr_commit(ising_sr_ctx* c, int64_t* events_out) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const ising_sr_status s = commit_impl(c, events_out);
+  if (c) c->stats.ms_commit_total += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return s;
 }
 
 ising_sr_status ising_sr_run(ising_sr_ctx* c, int64_t* events_out) {

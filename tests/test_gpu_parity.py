@@ -406,3 +406,27 @@ def test_observables_onsager():
     assert tt == pytest.approx(40.0)
     assert abs(e - u) < 0.004, (e, u)
     assert abs(m - m0) < 0.01, (m, m0)
+
+
+@pytest.mark.parametrize("env", [{}, {"ISING_SR_BATCH": "4"}])
+def test_stats_active_regions_per_iteration(env, monkeypatch):
+    """stats.active_last: the worklist length of every iteration of the last
+    window -- all regions in iteration 1, the window's recomputations in
+    total, nothing after iteration g; commit time is accounted."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    w = workloads.Workload("act", 64, 64, 4, 4, T=2.0, W=0.5, t_end=3.0, seed=5)
+    sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed)
+    nreg = (w.Lx // w.bx) * (w.Ly // w.by)
+    prev = sim.stats()["recomputations_total"]
+    for _ in range(4):
+        sim.run_window()
+        sim.commit()
+        st = sim.stats()
+        a = st["active_last"]
+        assert a[0] == nreg
+        assert sum(a) == st["recomputations_total"] - prev
+        assert all(x == 0 for x in a[st["g_last"]:]) and all(x > 0 for x in a[:st["g_last"] - 1])
+        prev = st["recomputations_total"]
+    assert sim.stats()["ms_commit_total"] > 0.0
+    sim.close()
