@@ -168,6 +168,9 @@ def run_ising(args):
     t_end = max(w.t_end, nwin * w.W)
     spins = w.spins()
     flags = FLAG_DIGEST
+    if args.jacobi_all:
+        from paper_cs_0405053_b200 import FLAG_JACOBI_ALL
+        flags |= FLAG_JACOBI_ALL
     stream = torch.cuda.current_stream(local)
 
     def barrier():
@@ -276,6 +279,7 @@ def run_ising(args):
                                f"iid +-1 seed {w.seed}, W={w.W}, windows {args.warmup}..{nwin - 1} "
                                f"(t {args.warmup * w.W}..{nwin * w.W})",
                    "regions": w.n_regions, "l2": "inputs larger than L2 (state+histories >> 126 MB)",
+                   "schedule": "jacobi_all" if args.jacobi_all else "worklist",
                    "parallelism": f"strips{world}"},
         "events": tot_ev,
         "iterations_per_window": {"mean": float(np.mean(gs)), "max": int(max(gs)), "min": int(min(gs)),
@@ -385,6 +389,8 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--jacobi-all", action="store_true",
+                    help="paper-faithful schedule: every region in every iteration (same bits and g)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

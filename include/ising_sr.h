@@ -74,6 +74,11 @@ typedef enum {
  * in a fixed order at commit (ising_sr_stats.obs_*).  Lane-per-region K1 forms
  * only (E_INVALID_ARG with ISING_SR_POOL=1 or ISING_SR_BIG=0). */
 #define ISING_SR_FLAG_OBSERVABLES 0x8u
+/* Paper-faithful Jacobi schedule: every relaxation iteration
+ * recomputes every region, not only those whose incoming histories changed.
+ * Same fixed point, same g, same bits; only slower (the default worklist skips
+ * regions that would regenerate their previous trajectory). */
+#define ISING_SR_FLAG_JACOBI_ALL 0x10u
 
 /* Halo exchange between strips (world > 1).  Rank q owns a band of region
  * rows; "up" is toward region row 0 (rank q-1, periodic), "down" toward rank

@@ -20,6 +20,7 @@ FLAG_LOG_EVENTS = 0x1
 FLAG_DIGEST = 0x2
 FLAG_FRESH_WINDOW = 0x4  # alternate approach to subsequent steps
 FLAG_OBSERVABLES = 0x8   # time integrals of M and of the bond sum per window
+FLAG_JACOBI_ALL = 0x10   # recompute every region in every iteration (paper-faithful schedule)
 
 STATUS = {
     0: "OK", -1: "E_INVALID_ARG", -2: "E_DIMENSION", -3: "E_PARTITION", -4: "E_DIVERGED",

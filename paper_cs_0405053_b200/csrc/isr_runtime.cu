@@ -612,12 +612,13 @@ ising_sr_status launch_iteration(ising_sr_ctx* c) {
   ++c->it;
   const unsigned K = ++c->Kglob;
   const bool first = c->it == 1;
-  const int nw = first ? c->nreg : c->n_work;
+  const bool all = first || (c->cfg.flags & ISING_SR_FLAG_JACOBI_ALL);  // Jacobi: every region, every iteration
+  const int nw = all ? c->nreg : c->n_work;
   CK(c, cudaMemsetAsync(c->d_flags, 0, 4 * sizeof(int), c->stream));
   CK(c, cudaMemsetAsync(c->d_stats, 0, 8 * sizeof(unsigned long long), c->stream));
   CK(c, cudaMemsetAsync(c->d_wlc + ((K + 1) & 1), 0, sizeof(unsigned), c->stream));
   KArgs a = base_args(c, K, first);
-  a.wl_in = first ? nullptr : c->wl[K & 1];
+  a.wl_in = all ? nullptr : c->wl[K & 1];
   a.n_work = nw;
   const bool pool = c->pool && c->ops->region_pool;
   a.tile = pool ? tile_for_pool(nw) : tile_for(nw);
@@ -1073,6 +1074,7 @@ ising_sr_status ising_sr_run_window(ising_sr_ctx* c, int32_t* g_out) {
   if (s) return s;
   if ((s = ising_sr_begin_window(c))) return s;
   const bool can_batch = c->cfg.world <= 1 && c->ops->region_persistent &&
+                         !(c->cfg.flags & ISING_SR_FLAG_JACOBI_ALL) &&
                          (!c->pool || c->ops->region_pool_persistent) &&
                          !(c->cfg.flags & ISING_SR_FLAG_OBSERVABLES);  // persistent forms do not integrate
   if (can_batch && c->batch > 1) {

@@ -430,3 +430,35 @@ def test_stats_active_regions_per_iteration(env, monkeypatch):
         prev = st["recomputations_total"]
     assert sim.stats()["ms_commit_total"] > 0.0
     sim.close()
+
+
+@pytest.mark.parametrize("geom", [(64, 64, 4, 4, 2.0, 0.5), (64, 64, 16, 16, 2.269, 1.0), (32, 32, 2, 2, 1.5, 0.7)])
+def test_jacobi_all_same_fixed_point_and_g(geom):
+    """FLAG_JACOBI_ALL (every region in every iteration, the paper's schedule):
+    the oracle's bits, and per window the same g as the worklist schedule,
+    with g x N recomputations."""
+    from paper_cs_0405053_b200 import FLAG_JACOBI_ALL
+    Lx, Ly, bx, by, T, W = geom
+    w = workloads.Workload("jac", Lx, Ly, bx, by, T=T, W=W, t_end=4.0, seed=8)
+    nreg = (Lx // bx) * (Ly // by)
+    a = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed, flags=FLAG_DIGEST)
+    b = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed,
+                flags=FLAG_DIGEST | FLAG_JACOBI_ALL)
+    r0 = 0
+    for _ in range(w.n_windows()):
+        ga, gb = a.run_window(), b.run_window()
+        assert ga == gb
+        a.commit()
+        b.commit()
+        r1 = b.stats()["recomputations_total"]
+        assert r1 - r0 == gb * nreg
+        r0 = r1
+    ref = oracle.des_workload(w)
+    da, ca = a.digests()
+    db, cb = b.digests()
+    assert np.array_equal(db, da) and np.array_equal(cb, ca)
+    assert np.array_equal(cb, ref["count"])
+    assert np.array_equal(db, ref["digest"])
+    assert np.array_equal(b.spins(), ref["spins"])
+    a.close()
+    b.close()
