@@ -262,6 +262,7 @@ def run_ising(args):
                        f"{t['window']}, DRAM/alg = {t['dram_over_alg']:.2f}")
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src, "peak_kind": peak_kind,
+            "frac_vs_nominal_8000": achieved / 8000.0,  # north_star's ~8 TB/s nominal HBM3e
             "kernel": "region_kernel<4,4> (K1 trajectory + fused diff)",
             "bytes_per_launch": region_bytes / max(nlaunch, 1),
             "ms_per_launch": region_ms / max(nlaunch, 1),
