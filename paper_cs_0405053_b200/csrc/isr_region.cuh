@@ -1015,10 +1015,23 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
   // (work_ctr set) the whole worklist as a global queue served to a
   // persistent grid in per-warp chunks, its length read on the device
   constexpr bool global_q = GQ;
+  // n_work_dev (pipelined launch): the worklist length is read here; the grid
+  // was sized for an upper bound, and the tile grows if the bound was short
   const int n_all = GQ && a.n_work_dev ? (int)__ldcg(a.n_work_dev) : a.n_work;
-  const int tile_begin = global_q ? 0 : blockIdx.x * a.tile;
-  const int tile_n = global_q ? n_all : min(a.tile, n_all - tile_begin);
-  if (threadIdx.x == 0) q_next = blockDim.x;  // the first blockDim items are taken statically
+  // the block's tile (block-uniform, kept in shared memory)
+  __shared__ int s_tile_begin, s_tile_n;
+  if (threadIdx.x == 0) {
+    int tile = a.tile, n = n_all;
+    if (!GQ && a.n_work_dev) {  // the host's tile rule (tile_for) on the actual length, >= n / grid
+      n = (int)__ldcg(a.n_work_dev);
+      const int per = max(1, min(8, n / (NT * 148 * 4)));
+      const int need = (n + (int)gridDim.x - 1) / (int)gridDim.x;
+      tile = max(NT * per, (need + NT - 1) / NT * NT);
+    }
+    s_tile_begin = global_q ? 0 : blockIdx.x * tile;
+    s_tile_n = global_q ? n : min(tile, n - (int)(blockIdx.x * tile));
+    q_next = blockDim.x;  // the first blockDim items are taken statically
+  }
   fill_prod<G>(PT, a.rate);
   __syncthreads();
 
@@ -1071,8 +1084,8 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
         }
         if (!exhausted) {
           if (item < 0 && !global_q) item = (int)atomicAdd(&q_next, 1u);
-          if (item >= 0 && item < tile_n) {
-            const int idx = a.wl_in ? (int)a.wl_in[tile_begin + item] : tile_begin + item;
+          if (item >= 0 && item < s_tile_n) {
+            const int idx = a.wl_in ? (int)a.wl_in[s_tile_begin + item] : s_tile_begin + item;
             lane_load<G, LOG, SG, !ISR_FRESH, OBS, FIRST>(a, L, idx, S, PT, threadIdx.x);
             fresh = true;
             n_in += (L.hm[0] & 0xFFu) + (L.hm[1] & 0xFFu) + (L.hm[2] & 0xFFu) + (L.hm[3] & 0xFFu);

@@ -418,6 +418,8 @@ struct ising_sr_ctx {
   double win_bytes = 0.0;
   int win_f = 0;
   long long launches = 0;
+  int pipeline = 1;  // world == 1: one iteration enqueued ahead of the flag check (env ISING_SR_PIPELINE)
+  cudaEvent_t pev[2] = {};  // pipelined: results of the iteration with stamp parity j copied to the host
   int refill = 28;  // K1 batched-refill threshold (env ISING_SR_REFILL; 28 measured best after the shared fresh-load step)
   bool pool = false;    // slot-pool K1 for lane shapes (env ISING_SR_POOL=1; measured slower so far)
   int pool_refill = ISR_POOL_S / 2;  // free slots that trigger a pool refill (env ISING_SR_POOL_REFILL)
@@ -727,6 +729,95 @@ void start_window(ising_sr_ctx* c) {
 }
 
 // ---------------------------------------------------------------------------
+// Pipelined relaxation (world == 1, Jacobi worklist schedule): iteration k+1
+// is enqueued before the host reads iteration k's flags, so the host round
+// trip overlaps the GPU's work.  K1 reads the length of its worklist on the
+// device (n_work_dev); its grid is sized from an upper bound -- the length of
+// iteration k+1's worklist is known once iteration k's results are back, and
+// worklists shrink as the relaxation converges (a longer one only enlarges
+// each block's tile).  When iteration k changed nothing, the iteration
+// enqueued after it finds an empty worklist and does nothing, so g and every
+// result are those of the one-iteration-per-sync loop.  Per-iteration flags,
+// counters and kernel events use slot K & 1.
+// ---------------------------------------------------------------------------
+ising_sr_status enqueue_pipelined(ising_sr_ctx* c, int bound) {
+  NvtxRange nv("isr iteration (pipelined)");
+  ++c->it;
+  const unsigned K = ++c->Kglob;
+  const int j = (int)(K & 1u);
+  const bool first = c->it == 1;
+  const int nb = first ? c->nreg : bound;
+  CK(c, cudaMemsetAsync(c->d_flags + 4 * j, 0, 4 * sizeof(int), c->stream));
+  CK(c, cudaMemsetAsync(c->d_stats + 8 * j, 0, 8 * sizeof(unsigned long long), c->stream));
+  CK(c, cudaMemsetAsync(c->d_wlc + ((K + 1) & 1), 0, sizeof(unsigned), c->stream));
+  KArgs a = base_args(c, K, first);
+  a.flags = c->d_flags + 4 * j;
+  a.stats = c->d_stats + 8 * j;
+  a.wl_in = first ? nullptr : c->wl[K & 1];
+  a.n_work = nb;
+  a.n_work_dev = first ? nullptr : c->d_wlc + (K & 1);
+  a.tile = tile_for(std::max(nb, 1));
+  a.wl_out = c->wl[(K + 1) & 1];
+  a.wl_out_count = c->d_wlc + ((K + 1) & 1);
+  CK(c, cudaEventRecord(c->bev[2 * j], c->stream));
+  if (nb > 0) {
+    c->ops->region(a, nb, c->stream);
+    ++c->launches;
+    CK(c, cudaGetLastError());
+  }
+  CK(c, cudaEventRecord(c->bev[2 * j + 1], c->stream));
+  ising_sr_status s = compact_worklist(c);
+  if (s) return s;
+  CK(c, cudaMemcpyAsync(c->h_flags + 4 * j, c->d_flags + 4 * j, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaMemcpyAsync(c->h_stats + 8 * j, c->d_stats + 8 * j, 8 * sizeof(unsigned long long),
+                        cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaMemcpyAsync(c->h_wlc + j, c->d_wlc + ((K + 1) & 1), sizeof(unsigned), cudaMemcpyDeviceToHost,
+                        c->stream));
+  CK(c, cudaEventRecord(c->pev[j], c->stream));
+  return ISING_SR_OK;
+}
+
+ising_sr_status run_window_pipelined(ising_sr_ctx* c) {
+  ising_sr_status s;
+  int bound = c->nreg;
+  if ((s = enqueue_pipelined(c, bound))) return s;  // iteration 1: every region
+  for (;;) {
+    const int k = c->it;                 // the iteration whose results are read next
+    const unsigned Kk = c->Kglob;
+    const int j = (int)(Kk & 1u);
+    const bool ahead = k < c->cfg.max_iterations;
+    if (ahead && (s = enqueue_pipelined(c, bound))) return s;  // iteration k+1, speculative
+    CK(c, cudaEventSynchronize(c->pev[j]));
+    float kms = 0.f;
+    CK(c, cudaEventElapsedTime(&kms, c->bev[2 * j], c->bev[2 * j + 1]));
+    account_iteration(c, kms, c->h_stats + 8 * j, k);
+    const int* f = c->h_flags + 4 * j;
+    if (f[1]) {  // history capacity overflow: drain, forget the speculative iteration, grow, restart
+      CK(c, cudaStreamSynchronize(c->stream));
+      CK(c, cudaMemsetAsync(c->dirty, 0, 2 * (size_t)c->dwords * sizeof(uint32_t), c->stream));
+      if ((s = grow_capacity(c))) return s;
+      start_window(c);
+      bound = c->nreg;
+      if ((s = enqueue_pipelined(c, bound))) return s;
+      continue;
+    }
+    if (!f[0]) {  // converged at k; the iteration enqueued after it is a no-op
+      c->converged = true;
+      c->g = k;
+      c->it = k;
+      return ISING_SR_OK;
+    }
+    if (!ahead) {
+      CK(c, cudaStreamSynchronize(c->stream));
+      c->in_window = false;
+      return ISING_SR_E_DIVERGED;
+    }
+    bound = (int)c->h_wlc[j];  // length of iteration k+1's worklist: the bound for k+2
+    c->n_work = bound;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Batched relaxation (world == 1, slot-pool K1): `batch` iterations are
 // enqueued back to back -- K1 reads its worklist length on the device and
 // takes work from a global queue, so no host round trip is needed between
@@ -855,6 +946,8 @@ void ising_sr_destroy(ising_sr_ctx* c) {
   cudaFree(c->d_wctr);
   for (auto& e : c->bev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->pev)
+    if (e) cudaEventDestroy(e);
   cudaFreeHost(c->h_flags);
   cudaFreeHost(c->h_stats);
   cudaFreeHost(c->h_wlc);
@@ -902,6 +995,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   c->nreg = c->RX * c->RYl;
   c->dwords = (c->nreg + 31) / 32;
   std::memset(&c->stats, 0, sizeof c->stats);
+  if (const char* e = std::getenv("ISING_SR_PIPELINE")) c->pipeline = std::atoi(e) != 0;
   if (const char* e = std::getenv("ISING_SR_REFILL")) c->refill = std::max(1, std::min(32, std::atoi(e)));
   if (const char* e = std::getenv("ISING_SR_POOL")) c->pool = std::atoi(e) != 0;
   if ((cfg->flags & ISING_SR_FLAG_OBSERVABLES) && ((!ops->warp && c->pool) || (ops->warp && !big_enabled()))) {
@@ -950,6 +1044,8 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
     return bail(ISING_SR_E_CUDA);
   for (auto& e : c->bev)
     if (cudaEventCreate(&e) != cudaSuccess) return bail(ISING_SR_E_CUDA);
+  for (auto& e : c->pev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return bail(ISING_SR_E_CUDA);
   if (const char* e = std::getenv("ISING_SR_BATCH")) c->batch = std::max(1, std::min(kBatch, std::atoi(e)));
   if (const char* e = std::getenv("ISING_SR_TAIL_BATCH")) c->tail_batch = std::max(1, std::min(kBatch, std::atoi(e)));
   if (const char* e = std::getenv("ISING_SR_TAIL_N")) c->tail_n = std::max(0, std::atoi(e));
@@ -1077,6 +1173,13 @@ ising_sr_status ising_sr_run_window(ising_sr_ctx* c, int32_t* g_out) {
                          !(c->cfg.flags & ISING_SR_FLAG_JACOBI_ALL) &&
                          (!c->pool || c->ops->region_pool_persistent) &&
                          !(c->cfg.flags & ISING_SR_FLAG_OBSERVABLES);  // persistent forms do not integrate
+  const bool can_pipe = c->cfg.world <= 1 && c->pipeline && !c->pool &&
+                        !(c->cfg.flags & ISING_SR_FLAG_JACOBI_ALL) && c->batch <= 1 && c->tail_batch <= 1;
+  if (can_pipe) {
+    if ((s = run_window_pipelined(c))) return s;
+    if (g_out) *g_out = c->g;
+    return ISING_SR_OK;
+  }
   if (can_batch && c->batch > 1) {
     if ((s = run_window_batched(c, c->batch))) return s;
     if (g_out) *g_out = c->g;

@@ -229,13 +229,16 @@ def test_c5_geometry_sample_bit_exact():
 
 
 # ---------------------------------------------------------------------------
-# every schedule of the lane-form K1 (lane-persistent: default; slot pool:
+# every schedule of K1 (lane-persistent with the pipelined host loop:
+# default; one iteration per host sync: ISING_SR_PIPELINE=0; slot pool:
 # ISING_SR_POOL=1; persistent global queue: ISING_SR_BATCH and the tail
 # batching ISING_SR_TAIL_N/ISING_SR_TAIL_BATCH) and extreme refill
 # thresholds give the oracle's bits
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("env", [
     {"ISING_SR_POOL": "0"},
+    {"ISING_SR_PIPELINE": "0"},
+    {"ISING_SR_PIPELINE": "0", "ISING_SR_BIG": "0"},
     {"ISING_SR_POOL": "0", "ISING_SR_BATCH": "1"},
     {"ISING_SR_POOL": "0", "ISING_SR_REFILL": "1"},
     {"ISING_SR_POOL": "1", "ISING_SR_POOL_REFILL": "1"},
