@@ -127,6 +127,14 @@ typedef struct {
   void* stream;             /* cudaStream_t; NULL = library-owned stream                     */
   ising_sr_exchange_fn exchange; /* world > 1: used by run_window (step API: unused)       */
   void* exchange_user;
+  /* Optional device allocator for every device buffer of the ctx (e.g. torch's
+   * caching allocator).  dev_alloc(bytes, user) returns a device pointer or
+   * NULL (-> E_OOM); dev_free(ptr, user) releases it.  Allocations are used on
+   * `stream` only, so a stream-ordered allocator needs no extra
+   * synchronisation.  Both NULL = cudaMalloc / cudaFree. */
+  void* (*dev_alloc)(size_t bytes, void* user);
+  void (*dev_free)(void* ptr, void* user);
+  void* alloc_user;
 } ising_sr_config;
 
 typedef struct {

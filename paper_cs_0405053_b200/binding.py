@@ -43,6 +43,8 @@ class Halo(ctypes.Structure):
 
 
 EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(Halo))
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
 
 
 class Config(ctypes.Structure):
@@ -54,7 +56,8 @@ class Config(ctypes.Structure):
                 ("hist_capacity", ctypes.c_int32), ("flags", ctypes.c_uint32),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("exchange", EXCHANGE_FN),
-                ("exchange_user", ctypes.c_void_p)]
+                ("exchange_user", ctypes.c_void_p),
+                ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_user", ctypes.c_void_p)]
 
 
 class Stats(ctypes.Structure):
@@ -152,7 +155,7 @@ class IsingSR:
                  T: float = float("nan"), flags: int = FLAG_DIGEST, hist_capacity: int = 0,
                  max_iterations: int = 0, rank: int = 0, world: int = 1, device: int = 0,
                  stream: Optional[int] = None,
-                 exchange: Optional[Callable[[Halo], int]] = None):
+                 exchange: Optional[Callable[[Halo], int]] = None, torch_alloc: bool = False):
         L = load_library()
         c = Config()
         c.Lx, c.Ly, c.bx, c.by = Lx, Ly, bx, by
@@ -174,6 +177,22 @@ class IsingSR:
                     return 1
             self._cb = EXCHANGE_FN(_tramp)
             c.exchange = self._cb
+        self._alloc_cbs = None
+        if torch_alloc:  # device buffers from torch's caching allocator, on the ctx stream
+            import torch
+            st = c.stream
+
+            def _alloc(nbytes, user):
+                try:
+                    return int(torch.cuda.caching_allocator_alloc(int(nbytes), device, st))
+                except Exception:  # pragma: no cover - surfaced as E_OOM
+                    return None
+
+            def _free(ptr, user):
+                torch.cuda.caching_allocator_delete(int(ptr))
+
+            self._alloc_cbs = (ALLOC_FN(_alloc), FREE_FN(_free))
+            c.dev_alloc, c.dev_free = self._alloc_cbs
         self.cfg = c
         self.Lx, self.Ly, self.bx, self.by, self.world, self.rank = Lx, Ly, bx, by, world, rank
         self.n_regions = (Lx // bx) * (Ly // by) // world

@@ -441,18 +441,32 @@ ising_sr_status fail_cuda(ising_sr_ctx* c, cudaError_t e, const char* where) {
     if (_e != cudaSuccess) return fail_cuda((ctx), _e, #expr); \
   } while (0)
 
+// device memory: the caller's allocator hooks when given (e.g. torch's
+// caching allocator, stream-ordered on the ctx stream), else cudaMalloc/cudaFree
+cudaError_t dmalloc_bytes(ising_sr_ctx* c, void** p, size_t bytes) {
+  if (c->cfg.dev_alloc) {
+    *p = c->cfg.dev_alloc(std::max<size_t>(bytes, 1), c->cfg.alloc_user);
+    return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+  }
+  return cudaMalloc(p, std::max<size_t>(bytes, 1));
+}
 template <class T>
-cudaError_t dmalloc(T** p, size_t count) {
-  return cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T));
+cudaError_t dmalloc(ising_sr_ctx* c, T** p, size_t count) {
+  return dmalloc_bytes(c, (void**)p, std::max<size_t>(count, 1) * sizeof(T));
+}
+void dfree(ising_sr_ctx* c, void* p) {
+  if (!p) return;
+  if (c->cfg.dev_free) c->cfg.dev_free(p, c->cfg.alloc_user);
+  else cudaFree(p);
 }
 
 void free_edges(ising_sr_ctx* c) {
   for (auto& e : c->ed) {
-    cudaFree(e.t);
-    cudaFree(e.pos);
+    dfree(c, e.t);
+    dfree(c, e.pos);
     e = EdgeView{};
   }
-  cudaFree(c->gbuf);
+  dfree(c, c->gbuf);
   c->gbuf = nullptr;
   for (int i = 0; i < 2; ++i) {
     c->gsend[i] = GhostView{};
@@ -470,7 +484,7 @@ ising_sr_status alloc_edges(ising_sr_ctx* c, int K) {
   const size_t tn = cn * (size_t)K;
   if (tn / 4 >= (1ull << 32)) return ISING_SR_E_CAPACITY;  // offsets within one edge array are 32-bit
   for (auto& e : c->ed) {
-    if (dmalloc(&e.t, tn) != cudaSuccess || dmalloc(&e.pos, tn) != cudaSuccess) {
+    if (dmalloc(c, &e.t, tn) != cudaSuccess || dmalloc(c, &e.pos, tn) != cudaSuccess) {
       cudaGetLastError();
       free_edges(c);
       return ISING_SR_E_OOM;
@@ -484,7 +498,7 @@ ising_sr_status alloc_edges(ising_sr_ctx* c, int K) {
     c->gchunk[2] = RX * (size_t)K * 8;
     c->gchunk[3] = RX * (size_t)K;
     const size_t one = al(c->gchunk[0]) + al(c->gchunk[1]) + al(c->gchunk[2]) + al(c->gchunk[3]);
-    if (cudaMalloc(&c->gbuf, 4 * one) != cudaSuccess) {
+    if (dmalloc_bytes(c, (void**)&c->gbuf, 4 * one) != cudaSuccess) {
       cudaGetLastError();
       free_edges(c);
       return ISING_SR_E_OOM;
@@ -923,27 +937,27 @@ void ising_sr_destroy(ising_sr_ctx* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto& s : c->st) {
-    cudaFree(s.spins);
-    cudaFree(s.halo);
-    cudaFree(s.ts);
-    cudaFree(s.R);
-    cudaFree(s.n);
-    cudaFree(s.dig);
-    cudaFree(s.oM);
-    cudaFree(s.oB);
+    dfree(c, s.spins);
+    dfree(c, s.halo);
+    dfree(c, s.ts);
+    dfree(c, s.R);
+    dfree(c, s.n);
+    dfree(c, s.dig);
+    dfree(c, s.oM);
+    dfree(c, s.oB);
   }
   free_edges(c);
-  cudaFree(c->sel);
-  cudaFree(c->dirty);
-  cudaFree(c->lg_tR);
-  cudaFree(c->lg_c);
-  cudaFree(c->lg_meta);
-  cudaFree(c->wl[0]);
-  cudaFree(c->wl[1]);
-  cudaFree(c->d_wlc);
-  cudaFree(c->d_flags);
-  cudaFree(c->d_stats);
-  cudaFree(c->d_wctr);
+  dfree(c, c->sel);
+  dfree(c, c->dirty);
+  dfree(c, c->lg_tR);
+  dfree(c, c->lg_c);
+  dfree(c, c->lg_meta);
+  dfree(c, c->wl[0]);
+  dfree(c, c->wl[1]);
+  dfree(c, c->d_wlc);
+  dfree(c, c->d_flags);
+  dfree(c, c->d_stats);
+  dfree(c, c->d_wctr);
   for (auto& e : c->bev)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->pev)
@@ -951,13 +965,13 @@ void ising_sr_destroy(ising_sr_ctx* c) {
   cudaFreeHost(c->h_flags);
   cudaFreeHost(c->h_stats);
   cudaFreeHost(c->h_wlc);
-  cudaFree(c->log_t);
-  cudaFree(c->log_region);
-  cudaFree(c->log_site);
-  cudaFree(c->d_off);
-  cudaFree(c->d_bsum);
-  cudaFree(c->d_total);
-  cudaFree(c->d_obs);
+  dfree(c, c->log_t);
+  dfree(c, c->log_region);
+  dfree(c, c->log_site);
+  dfree(c, c->d_off);
+  dfree(c, c->d_bsum);
+  dfree(c, c->d_total);
+  dfree(c, c->d_obs);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->kev0) cudaEventDestroy(c->kev0);
@@ -1018,23 +1032,23 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   }
   const size_t n = (size_t)c->nreg;
   for (auto& s : c->st) {
-    if (cudaMalloc(&s.spins, n * ops->spin_bytes) != cudaSuccess ||
-        cudaMalloc(&s.halo, n * ops->halo_bytes) != cudaSuccess || dmalloc(&s.ts, n) != cudaSuccess ||
-        dmalloc(&s.R, n) != cudaSuccess || dmalloc(&s.n, n) != cudaSuccess || dmalloc(&s.dig, n) != cudaSuccess)
+    if (dmalloc_bytes(c, (void**)&s.spins, n * ops->spin_bytes) != cudaSuccess ||
+        dmalloc_bytes(c, (void**)&s.halo, n * ops->halo_bytes) != cudaSuccess || dmalloc(c, &s.ts, n) != cudaSuccess ||
+        dmalloc(c, &s.R, n) != cudaSuccess || dmalloc(c, &s.n, n) != cudaSuccess || dmalloc(c, &s.dig, n) != cudaSuccess)
       return bail(ISING_SR_E_OOM);
     if ((cfg->flags & ISING_SR_FLAG_OBSERVABLES) &&
-        (dmalloc(&s.oM, n) != cudaSuccess || dmalloc(&s.oB, n) != cudaSuccess))
+        (dmalloc(c, &s.oM, n) != cudaSuccess || dmalloc(c, &s.oB, n) != cudaSuccess))
       return bail(ISING_SR_E_OOM);
   }
-  if (dmalloc(&c->sel, (size_t)ops->sel_words * n) != cudaSuccess || dmalloc(&c->dirty, 2 * ((n + 31) / 32)) != cudaSuccess ||
-      dmalloc(&c->wl[0], n) != cudaSuccess || dmalloc(&c->wl[1], n) != cudaSuccess ||
-      dmalloc(&c->d_wlc, 2) != cudaSuccess || dmalloc(&c->d_flags, 4 * kBatch) != cudaSuccess ||
-      dmalloc(&c->d_stats, 8 * kBatch) != cudaSuccess || dmalloc(&c->d_wctr, kBatch) != cudaSuccess ||
+  if (dmalloc(c, &c->sel, (size_t)ops->sel_words * n) != cudaSuccess || dmalloc(c, &c->dirty, 2 * ((n + 31) / 32)) != cudaSuccess ||
+      dmalloc(c, &c->wl[0], n) != cudaSuccess || dmalloc(c, &c->wl[1], n) != cudaSuccess ||
+      dmalloc(c, &c->d_wlc, 2) != cudaSuccess || dmalloc(c, &c->d_flags, 4 * kBatch) != cudaSuccess ||
+      dmalloc(c, &c->d_stats, 8 * kBatch) != cudaSuccess || dmalloc(c, &c->d_wctr, kBatch) != cudaSuccess ||
       cudaMallocHost((void**)&c->h_flags, 4 * kBatch * sizeof(int)) != cudaSuccess ||
       cudaMallocHost((void**)&c->h_stats, 8 * kBatch * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMallocHost((void**)&c->h_wlc, 2 * sizeof(unsigned)) != cudaSuccess ||
-      dmalloc(&c->d_off, n) != cudaSuccess || dmalloc(&c->d_bsum, (n + kThreads - 1) / kThreads) != cudaSuccess ||
-      dmalloc(&c->d_total, 1) != cudaSuccess || dmalloc(&c->d_obs, 2 * kObsBlocks + 2) != cudaSuccess)
+      dmalloc(c, &c->d_off, n) != cudaSuccess || dmalloc(c, &c->d_bsum, (n + kThreads - 1) / kThreads) != cudaSuccess ||
+      dmalloc(c, &c->d_total, 1) != cudaSuccess || dmalloc(c, &c->d_obs, 2 * kObsBlocks + 2) != cudaSuccess)
     return bail(ISING_SR_E_OOM);
   if (cudaMemsetAsync(c->sel, 0, n * 8 * (size_t)ops->sel_words, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->dirty, 0, 2 * ((n + 31) / 32) * 4, c->stream) != cudaSuccess)
@@ -1066,10 +1080,10 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
     if (LC >= 16) {
       c->LC = (int)LC;
       const size_t nl = (size_t)c->nreg * (size_t)LC;
-      if (dmalloc(&c->lg_tR, nl) != cudaSuccess || dmalloc(&c->lg_c, nl) != cudaSuccess ||
-          dmalloc(&c->lg_meta, n) != cudaSuccess) {
+      if (dmalloc(c, &c->lg_tR, nl) != cudaSuccess || dmalloc(c, &c->lg_c, nl) != cudaSuccess ||
+          dmalloc(c, &c->lg_meta, n) != cudaSuccess) {
         cudaGetLastError();
-        cudaFree(c->lg_tR); cudaFree(c->lg_c); cudaFree(c->lg_meta);
+        dfree(c, c->lg_tR); dfree(c, c->lg_c); dfree(c, c->lg_meta);
         c->lg_tR = nullptr; c->lg_c = nullptr; c->lg_meta = nullptr;
         c->LC = 0;
       } else if (cudaMemsetAsync(c->lg_meta, 0, n * sizeof(uint2), c->stream) != cudaSuccess) {
@@ -1086,13 +1100,13 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   const int rows = c->RYl * by + 2;
   const int y_first = c->row0 * by - 1;
   uint8_t* dbuf = nullptr;
-  if (cudaMalloc(&dbuf, (size_t)rows * Lx) != cudaSuccess) return bail(ISING_SR_E_OOM);
+  if (dmalloc_bytes(c, (void**)&dbuf, (size_t)rows * Lx) != cudaSuccess) return bail(ISING_SR_E_OOM);
   for (int q = 0; q < rows;) {
     const int y = ((y_first + q) % Ly + Ly) % Ly;
     const int run = std::min(rows - q, Ly - y);  // contiguous up to the lattice's last row
     if (cudaMemcpyAsync(dbuf + (size_t)q * Lx, spins + (size_t)y * Lx, (size_t)run * Lx, cudaMemcpyHostToDevice,
                         c->stream) != cudaSuccess) {
-      cudaFree(dbuf);
+      dfree(c, dbuf);
       return bail(ISING_SR_E_CUDA);
     }
     q += run;
@@ -1100,7 +1114,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   ops->init(dbuf, Lx, RX, c->RYl, c->row0, cfg->seed, c->st[0], c->stream);
   c->launches++;
   cudaError_t e = cudaStreamSynchronize(c->stream);
-  cudaFree(dbuf);
+  dfree(c, dbuf);
   if (e != cudaSuccess || cudaGetLastError() != cudaSuccess) return bail(ISING_SR_E_CUDA);
   c->comm = 0;
   *out = c;
@@ -1264,15 +1278,15 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
   c->win_events = total;
   if (log) {
     if ((long long)total > c->log_cap) {
-      cudaFree(c->log_t);
-      cudaFree(c->log_region);
-      cudaFree(c->log_site);
+      dfree(c, c->log_t);
+      dfree(c, c->log_region);
+      dfree(c, c->log_site);
       c->log_t = nullptr;
       c->log_region = nullptr;
       c->log_site = nullptr;
       const long long cap = std::max<long long>((long long)total * 5 / 4 + 1024, c->log_cap * 2);
-      if (dmalloc(&c->log_t, cap) != cudaSuccess || dmalloc(&c->log_region, cap) != cudaSuccess ||
-          dmalloc(&c->log_site, cap) != cudaSuccess) {
+      if (dmalloc(c, &c->log_t, cap) != cudaSuccess || dmalloc(c, &c->log_region, cap) != cudaSuccess ||
+          dmalloc(c, &c->log_site, cap) != cudaSuccess) {
         cudaGetLastError();
         c->log_cap = 0;
         return ISING_SR_E_OOM;
@@ -1358,12 +1372,12 @@ ising_sr_status ising_sr_get_spins(ising_sr_ctx* c, uint8_t* out) {
   if (!out) return ISING_SR_E_INVALID_ARG;
   const size_t n = (size_t)c->RYl * c->cfg.by * c->cfg.Lx;
   uint8_t* d = nullptr;
-  CK(c, cudaMalloc(&d, n));
+  CK(c, dmalloc_bytes(c, (void**)&d, n));
   c->ops->unpack(c->st[c->comm], c->cfg.Lx, c->RX, c->RYl, d, c->stream);
   c->launches++;
   cudaError_t e = cudaMemcpyAsync(out, d, n, cudaMemcpyDeviceToHost, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-  cudaFree(d);
+  dfree(c, d);
   CK(c, e);
   return ISING_SR_OK;
 }

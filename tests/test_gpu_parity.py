@@ -465,3 +465,27 @@ def test_jacobi_all_same_fixed_point_and_g(geom):
     assert np.array_equal(b.spins(), ref["spins"])
     a.close()
     b.close()
+
+
+def test_torch_caching_allocator_hooks():
+    """dev_alloc/dev_free hooks (torch's caching allocator): every device
+    buffer is torch's, results are the oracle's, including a capacity-overflow
+    retry that reallocates the histories; all returned on close."""
+    import torch
+    torch.cuda.synchronize()
+    m0 = torch.cuda.memory_allocated()
+    w = workloads.Workload("cap", 32, 32, 4, 4, T=4.0, W=2.0, t_end=6.0, seed=2)
+    sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed, hist_capacity=1,
+                  torch_alloc=True)
+    assert torch.cuda.memory_allocated() > m0
+    sim.run()
+    st = sim.stats()
+    assert st["overflow_retries"] >= 1
+    dig, cnt = sim.digests()
+    spins = sim.spins()
+    sim.close()
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated() == m0
+    ref = oracle.des_workload(w)
+    assert np.array_equal(cnt, ref["count"]) and np.array_equal(dig, ref["digest"])
+    assert np.array_equal(spins, ref["spins"])
