@@ -352,6 +352,16 @@ __global__ void scan_apply(const uint32_t* n1, const uint32_t* n0, int N, const 
 // ---------------------------------------------------------------------------
 // context
 // ---------------------------------------------------------------------------
+// pipelined loop: everything one iteration reports, in one block (zeroed by
+// one memset, read back by one copy).  Slot K & 1 holds iteration K's flags
+// and counters and the length of iteration K+1's worklist.
+struct IterSlot {
+  int flags[4];
+  unsigned long long stats[8];
+  unsigned wl_next;
+  unsigned pad[3];
+};
+
 struct ising_sr_ctx {
   ising_sr_config cfg;
   const ShapeOps* ops = nullptr;
@@ -420,6 +430,8 @@ struct ising_sr_ctx {
   long long launches = 0;
   int pipeline = 1;  // world == 1: one iteration enqueued ahead of the flag check (env ISING_SR_PIPELINE)
   cudaEvent_t pev[2] = {};  // pipelined: results of the iteration with stamp parity j copied to the host
+  IterSlot* d_slot = nullptr;  // [2]
+  IterSlot* h_slot = nullptr;  // pinned mirror [2]
   int refill = 28;  // K1 batched-refill threshold (env ISING_SR_REFILL; 28 measured best after the shared fresh-load step)
   bool pool = false;    // slot-pool K1 for lane shapes (env ISING_SR_POOL=1; measured slower so far)
   int pool_refill = ISR_POOL_S / 2;  // free slots that trigger a pool refill (env ISING_SR_POOL_REFILL)
@@ -761,18 +773,18 @@ ising_sr_status enqueue_pipelined(ising_sr_ctx* c, int bound) {
   const int j = (int)(K & 1u);
   const bool first = c->it == 1;
   const int nb = first ? c->nreg : bound;
-  CK(c, cudaMemsetAsync(c->d_flags + 4 * j, 0, 4 * sizeof(int), c->stream));
-  CK(c, cudaMemsetAsync(c->d_stats + 8 * j, 0, 8 * sizeof(unsigned long long), c->stream));
-  CK(c, cudaMemsetAsync(c->d_wlc + ((K + 1) & 1), 0, sizeof(unsigned), c->stream));
+  IterSlot* sl = c->d_slot + j;             // this iteration's flags, counters, next worklist length
+  const IterSlot* prev = c->d_slot + (j ^ 1);  // ... the previous one's: this worklist's length
+  CK(c, cudaMemsetAsync(sl, 0, sizeof(IterSlot), c->stream));
   KArgs a = base_args(c, K, first);
-  a.flags = c->d_flags + 4 * j;
-  a.stats = c->d_stats + 8 * j;
+  a.flags = sl->flags;
+  a.stats = sl->stats;
   a.wl_in = first ? nullptr : c->wl[K & 1];
   a.n_work = nb;
-  a.n_work_dev = first ? nullptr : c->d_wlc + (K & 1);
+  a.n_work_dev = first ? nullptr : &prev->wl_next;
   a.tile = tile_for(std::max(nb, 1));
   a.wl_out = c->wl[(K + 1) & 1];
-  a.wl_out_count = c->d_wlc + ((K + 1) & 1);
+  a.wl_out_count = &sl->wl_next;
   CK(c, cudaEventRecord(c->bev[2 * j], c->stream));
   if (nb > 0) {
     c->ops->region(a, nb, c->stream);
@@ -780,13 +792,12 @@ ising_sr_status enqueue_pipelined(ising_sr_ctx* c, int bound) {
     CK(c, cudaGetLastError());
   }
   CK(c, cudaEventRecord(c->bev[2 * j + 1], c->stream));
-  ising_sr_status s = compact_worklist(c);
-  if (s) return s;
-  CK(c, cudaMemcpyAsync(c->h_flags + 4 * j, c->d_flags + 4 * j, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CK(c, cudaMemcpyAsync(c->h_stats + 8 * j, c->d_stats + 8 * j, 8 * sizeof(unsigned long long),
-                        cudaMemcpyDeviceToHost, c->stream));
-  CK(c, cudaMemcpyAsync(c->h_wlc + j, c->d_wlc + ((K + 1) & 1), sizeof(unsigned), cudaMemcpyDeviceToHost,
-                        c->stream));
+  isr::compact_kernel<<<(c->dwords + 255) / 256, 256, 0, c->stream>>>(c->dirty + (size_t)((K + 1) & 1) * c->dwords,
+                                                                       c->dwords, c->nreg, c->wl[(K + 1) & 1],
+                                                                       &sl->wl_next);
+  ++c->launches;
+  CK(c, cudaGetLastError());
+  CK(c, cudaMemcpyAsync(c->h_slot + j, sl, sizeof(IterSlot), cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaEventRecord(c->pev[j], c->stream));
   return ISING_SR_OK;
 }
@@ -804,8 +815,8 @@ ising_sr_status run_window_pipelined(ising_sr_ctx* c) {
     CK(c, cudaEventSynchronize(c->pev[j]));
     float kms = 0.f;
     CK(c, cudaEventElapsedTime(&kms, c->bev[2 * j], c->bev[2 * j + 1]));
-    account_iteration(c, kms, c->h_stats + 8 * j, k);
-    const int* f = c->h_flags + 4 * j;
+    account_iteration(c, kms, c->h_slot[j].stats, k);
+    const int* f = c->h_slot[j].flags;
     if (f[1]) {  // history capacity overflow: drain, forget the speculative iteration, grow, restart
       CK(c, cudaStreamSynchronize(c->stream));
       CK(c, cudaMemsetAsync(c->dirty, 0, 2 * (size_t)c->dwords * sizeof(uint32_t), c->stream));
@@ -826,7 +837,7 @@ ising_sr_status run_window_pipelined(ising_sr_ctx* c) {
       c->in_window = false;
       return ISING_SR_E_DIVERGED;
     }
-    bound = (int)c->h_wlc[j];  // length of iteration k+1's worklist: the bound for k+2
+    bound = (int)c->h_slot[j].wl_next;  // length of iteration k+1's worklist: the bound for k+2
     c->n_work = bound;
   }
 }
@@ -965,6 +976,8 @@ void ising_sr_destroy(ising_sr_ctx* c) {
   cudaFreeHost(c->h_flags);
   cudaFreeHost(c->h_stats);
   cudaFreeHost(c->h_wlc);
+  dfree(c, c->d_slot);
+  cudaFreeHost(c->h_slot);
   dfree(c, c->log_t);
   dfree(c, c->log_region);
   dfree(c, c->log_site);
@@ -1048,7 +1061,9 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
       cudaMallocHost((void**)&c->h_stats, 8 * kBatch * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMallocHost((void**)&c->h_wlc, 2 * sizeof(unsigned)) != cudaSuccess ||
       dmalloc(c, &c->d_off, n) != cudaSuccess || dmalloc(c, &c->d_bsum, (n + kThreads - 1) / kThreads) != cudaSuccess ||
-      dmalloc(c, &c->d_total, 1) != cudaSuccess || dmalloc(c, &c->d_obs, 2 * kObsBlocks + 2) != cudaSuccess)
+      dmalloc(c, &c->d_total, 1) != cudaSuccess || dmalloc(c, &c->d_obs, 2 * kObsBlocks + 2) != cudaSuccess ||
+      dmalloc(c, &c->d_slot, 2) != cudaSuccess ||
+      cudaMallocHost((void**)&c->h_slot, 2 * sizeof(IterSlot)) != cudaSuccess)
     return bail(ISING_SR_E_OOM);
   if (cudaMemsetAsync(c->sel, 0, n * 8 * (size_t)ops->sel_words, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->dirty, 0, 2 * ((n + 31) / 32) * 4, c->stream) != cudaSuccess)
