@@ -511,6 +511,9 @@ struct StageT {
   uint32_t own_p[4][OWN ? NCI : 1][OWN ? NC : 1];
 };
 using Stage = StageT<NT, true>;
+#ifndef ISR_DEFER
+#define ISR_DEFER 0  // 1: diff the own histories at publish time in global memory (no own-history stage)
+#endif
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -1008,7 +1011,9 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
   // the first iteration stages nothing (no incoming histories, no latest own
   // history in this window): a minimal stage frees shared memory for a sixth
   // resident block
-  using SG = typename std::conditional<FIRST, StageT<NT, false, 1>, Stage>::type;
+  constexpr bool DEFER = ISR_DEFER && !FIRST;
+  using SG = typename std::conditional<FIRST, StageT<NT, false, 1>,
+                                       typename std::conditional<DEFER, StageT<NT, false>, Stage>::type>::type;
   __shared__ SG S;
   __shared__ ProdTable<G> PT;
   // work: a static tile per block (lanes take items from a block queue), or
@@ -1077,7 +1082,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
       }
       if (!active) {
         if (pending) {
-          if (!LOG) lane_finish<G, false, OBS>(a, L, changed, overflow);
+          if (!LOG) lane_finish<G, DEFER, OBS>(a, L, changed, overflow);
           n_ev += L.n_ev;
           n_bev = max(n_bev, L.bev);
           pending = false;
@@ -1117,7 +1122,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
           bp_pre2<G>(a, L, S, threadIdx.x, d, tb);
         } else {
           if (OBS && !LOG) obs_advance<G>(L, L.tc);
-          ev_pre2<G, LOG, false, SG, !SHARE>(a, L, S, PT, threadIdx.x, n_out, overflow);
+          ev_pre2<G, LOG, DEFER, SG, !SHARE>(a, L, S, PT, threadIdx.x, n_out, overflow);
           ev = true;
         }
       }
