@@ -501,16 +501,20 @@ constexpr int CI = ISR_CI;   // staged entries per history
 
 // Staged history entries, column si per region in flight: incoming
 // histories (and, with OWN, the region's own latest ones for the diff).
-template <int NC, bool OWN, int NCI = CI>
+template <int NC, bool OWN, int NCI = CI, int NCO = NCI>
 struct StageT {
   static constexpr bool HAS_OWN = OWN;
-  static constexpr int CIN = NCI;  // staged entries per history
+  static constexpr int CIN = NCI;  // staged entries per incoming history
+  static constexpr int CIO = NCO;  // ... per own latest history
   double in_t[4][NCI][NC];
   uint32_t in_p[4][NCI][NC];   // 4-byte word holding the position byte, then the byte itself
-  double own_t[4][OWN ? NCI : 1][OWN ? NC : 1];
-  uint32_t own_p[4][OWN ? NCI : 1][OWN ? NC : 1];
+  double own_t[4][OWN ? NCO : 1][OWN ? NC : 1];
+  uint32_t own_p[4][OWN ? NCO : 1][OWN ? NC : 1];
 };
-using Stage = StageT<NT, true>;
+#ifndef ISR_CO
+#define ISR_CO ISR_CI  // staged own latest entries per edge
+#endif
+using Stage = StageT<NT, true, CI, ISR_CO>;
 #ifndef ISR_DEFER
 #define ISR_DEFER 0  // 1: diff the own histories at publish time in global memory (no own-history stage)
 #endif
@@ -687,13 +691,13 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   for (int e = 0; e < 4; ++e) {
     const unsigned pc = word_count(vown, e), ps = (unsigned)word_slot(vown, e);
     unsigned st = 0;
-    if (SG::HAS_OWN && !LOG && pc > 0 && pc <= (unsigned)SG::CIN) {
+    if (SG::HAS_OWN && !LOG && pc > 0 && pc <= (unsigned)SG::CIO) {
       st = 1;
       staged_any = true;
       const double* Et = src_t(a, ps, e);
       const uint8_t* Ep = src_p(a, ps, e);
 #pragma unroll
-      for (int q = 0; q < SG::CIN; ++q) {
+      for (int q = 0; q < SG::CIO; ++q) {
         if (q < (int)pc) {
           const unsigned o = L.obase + (unsigned)q * (unsigned)a.RX;
           cp_async8(&S.own_t[e][q][lane], Et + o);
@@ -724,7 +728,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
       if (!((L.om[e] >> 18) & 1u)) continue;
       const uint8_t* Ep = src_p(a, (L.om[e] >> 16) & 1u, e);
 #pragma unroll
-      for (int q = 0; q < SG::CIN; ++q)
+      for (int q = 0; q < SG::CIO; ++q)
         if (q < (int)((L.om[e] >> 8) & 0xFFu)) {
           const unsigned o = L.obase + (unsigned)q * (unsigned)a.RX;
           S.own_p[e][q][lane] = (S.own_p[e][q][lane] >> byte_shift(Ep + o)) & 0xFFu;
