@@ -511,6 +511,9 @@ struct StageT {
   double own_t[4][OWN ? NCO : 1][OWN ? NC : 1];
   uint32_t own_p[4][OWN ? NCO : 1][OWN ? NC : 1];
 };
+#ifndef ISR_LAZYPOS
+#define ISR_LAZYPOS 0  // 1: keep staged position words whole, extract the byte at its use
+#endif
 #ifndef ISR_CO
 #define ISR_CO ISR_CI  // staged own latest entries per edge
 #endif
@@ -714,17 +717,23 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
       if (!(L.hm[d] & (1u << 28))) continue;
       const unsigned off = L.hoff[d];
       const uint8_t* P = src_p(a, (L.hm[d] >> 24) & 3u, d ^ 1);
+#if ISR_LAZYPOS
+      // staged position words stay whole: the byte is taken where it is used
+      L.hm[d] |= ((S.in_p[d][0][lane] >> byte_shift(P + off)) & 0xFFu) << 16;
+#else
 #pragma unroll
       for (int q = 0; q < SG::CIN; ++q)
         if (q < (int)(L.hm[d] & 0xFFu)) {
           const unsigned o = off + (unsigned)q * (unsigned)a.RX;
           S.in_p[d][q][lane] = (S.in_p[d][q][lane] >> byte_shift(P + o)) & 0xFFu;
         }
-      L.ht[d] = S.in_t[d][0][lane];
       L.hm[d] |= S.in_p[d][0][lane] << 16;
+#endif
+      L.ht[d] = S.in_t[d][0][lane];
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
+      if (ISR_LAZYPOS) break;
       if (!((L.om[e] >> 18) & 1u)) continue;
       const uint8_t* Ep = src_p(a, (L.om[e] >> 16) & 1u, e);
 #pragma unroll
@@ -875,7 +884,13 @@ __device__ __forceinline__ void bp_pre2(const KArgs& a, Lane<G>& L, SG& S, int s
   if (nx < (hmd & 0xFFu)) {
     if (hmd & (1u << 28)) {
       tn = S.in_t[dstar][nx][lane];
+#if ISR_LAZYPOS
+      const unsigned hoffl = dstar == 0 ? L.hoff[0] : dstar == 1 ? L.hoff[1] : dstar == 2 ? L.hoff[2] : L.hoff[3];
+      pos = (S.in_p[dstar][nx][lane] >>
+             byte_shift(src_p(a, (hmd >> 24) & 3u, dstar ^ 1) + hoffl + nx * (unsigned)a.RX)) & 0xFFu;
+#else
       pos = S.in_p[dstar][nx][lane];
+#endif
     } else {
       const unsigned src = (hmd >> 24) & 3u;
       const unsigned hoff = dstar == 0 ? L.hoff[0] : dstar == 1 ? L.hoff[1] : dstar == 2 ? L.hoff[2] : L.hoff[3];
@@ -913,7 +928,10 @@ __device__ __forceinline__ unsigned hist_put(const KArgs& a, unsigned om, int e,
       if (k >= pc) {
         dv = 1;
       } else if (SG::HAS_OWN && ((om >> 18) & 1u)) {
-        dv = (__double_as_longlong(S.own_t[e][k][lane]) != __double_as_longlong(tc) || S.own_p[e][k][lane] != p)
+        const unsigned pw = ISR_LAZYPOS ? (S.own_p[e][k][lane] >> byte_shift((ps ? a.ed[1].pos : a.ed[0].pos) +
+                                                                        e * a.tstride + o)) & 0xFFu
+                                        : S.own_p[e][k][lane];
+        dv = (__double_as_longlong(S.own_t[e][k][lane]) != __double_as_longlong(tc) || pw != p)
                  ? 1u : 0u;
       } else {
         const double* To = (ps ? a.ed[1].t : a.ed[0].t) + e * a.tstride;
