@@ -166,6 +166,10 @@ typedef struct {
   /* host wall time (ms, all windows) inside the world > 1 exchange callback
    * (halo exchange + flag all-reduce) and inside ising_sr_commit */
   double ms_exchange_total, ms_commit_total;
+  /* FLAG_OBSERVABLES: M = sum s and the bond sum B (E = -J B - H M) of the
+   * configuration at the committed time t_c (this rank's regions, each owning
+   * its internal bonds and those to its north and west neighbours), exact */
+  int64_t obs_M_now, obs_B_now;
 } ising_sr_stats;
 
 /* Validate cfg, allocate device state, copy the full Ly*Lx row-major spin

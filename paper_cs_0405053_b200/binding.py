@@ -74,7 +74,8 @@ class Stats(ctypes.Structure):
                 ("obs_M_total", ctypes.c_double), ("obs_B_total", ctypes.c_double),
                 ("obs_time_total", ctypes.c_double),
                 ("active_last", ctypes.c_int64 * 64),
-                ("ms_exchange_total", ctypes.c_double), ("ms_commit_total", ctypes.c_double)]
+                ("ms_exchange_total", ctypes.c_double), ("ms_commit_total", ctypes.c_double),
+                ("obs_M_now", ctypes.c_int64), ("obs_B_now", ctypes.c_int64)]
 
 
 _lib = None

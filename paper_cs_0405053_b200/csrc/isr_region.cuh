@@ -1351,6 +1351,35 @@ __global__ void init_kernel(const uint8_t* buf, int Lx, int RX, int RYl, int row
   st.dig[idx] = 0ull;
 }
 
+// FLAG_OBSERVABLES snapshot: M = sum s and the bond sum B of a committed
+// configuration, each region contributing its own sites and the bonds it owns
+// (internal, to its north and west neighbours: every bond exactly once; the
+// ghost bits are the neighbours' committed spins).  Integers: exact in any order.
+template <int BX, int BY>
+__global__ void __launch_bounds__(256) snap_kernel(StateView st, int n, int RX, int RYg, unsigned long long* out) {
+  using G = Geo<BX, BY>;
+  using M = typename G::M;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  long long m = 0, b = 0;
+  if (idx < n) {
+    M gN, gS, gW, gE;
+    expand_halo<G>((unsigned long long)((const typename G::HT*)st.halo)[idx], gN, gS, gW, gE);
+    int Mi, Bi;
+    obs_counts<G>((M)((const typename G::ST*)st.spins)[idx], gN, gW, RX == 1, RYg == 1, Mi, Bi);
+    m = Mi;
+    b = Bi;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    m += __shfl_xor_sync(0xffffffffu, m, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out, (unsigned long long)m);
+    atomicAdd(out + 1, (unsigned long long)b);
+  }
+}
+
 // unpack committed region spins to a row-major uint8 strip
 template <int BX, int BY>
 __global__ void unpack_kernel(StateView st, int Lx, int RX, int RYl, uint8_t* out) {

@@ -58,6 +58,7 @@ struct ShapeOps {
   void (*init)(const uint8_t*, int, int, int, int, unsigned long long, StateView, cudaStream_t);
   void (*unpack)(StateView, int, int, int, uint8_t*, cudaStream_t);
   void (*pack)(const KArgs&, GhostView, GhostView, int RX, cudaStream_t);
+  void (*snap)(StateView, int n, int RX, int RYg, unsigned long long* out, cudaStream_t);  // M, B of a state
 };
 
 template <int BX, int BY>
@@ -146,6 +147,9 @@ ShapeOps make_ops() {
   o.pack = [](const KArgs& a, GhostView up, GhostView down, int RX, cudaStream_t s) {
     isr::pack_kernel<<<(2 * RX + 127) / 128, 128, 0, s>>>(a, up, down);
   };
+  o.snap = [](StateView st, int n, int RX, int RYg, unsigned long long* out, cudaStream_t s) {
+    isr::snap_kernel<BX, BY><<<(n + 255) / 256, 256, 0, s>>>(st, n, RX, RYg, out);
+  };
   return o;
 }
 
@@ -213,6 +217,9 @@ ShapeOps make_ops_w() {
   };
   o.pack = [](const KArgs& a, GhostView up, GhostView down, int RX, cudaStream_t s) {
     isr::pack_kernel_w<<<(2 * RX + 127) / 128, 128, 0, s>>>(a, up, down);
+  };
+  o.snap = [](StateView st, int n, int RX, int RYg, unsigned long long* out, cudaStream_t s) {
+    isr::snap_kernel_w<BX, BY><<<(n + 255) / 256, 256, 0, s>>>(st, n, RX, RYg, out);
   };
   return o;
 }
@@ -405,6 +412,8 @@ struct ising_sr_ctx {
   unsigned long long* d_total = nullptr;
   double* d_obs = nullptr;   // [2 * kObsBlocks] partial sums, then [2] window totals
   double h_obs[2] = {0.0, 0.0};
+  unsigned long long* d_snap = nullptr;  // FLAG_OBSERVABLES: {M, B} of the committed configuration
+  unsigned long long h_snap[2] = {0ull, 0ull};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t kev0 = nullptr, kev1 = nullptr;  // around each region-kernel launch
   cudaEvent_t bev[2 * 8] = {};                 // batched iterations: around launch j (2j, 2j+1)
@@ -728,6 +737,16 @@ void fill_halo(ising_sr_ctx* c, ising_sr_halo* h) {
   h->stream = (void*)c->stream;
 }
 
+// {M, B} of committed state st into c->h_snap (enqueued; read after the next sync)
+ising_sr_status enqueue_snapshot(ising_sr_ctx* c, const StateView& st) {
+  CK(c, cudaMemsetAsync(c->d_snap, 0, 2 * sizeof(unsigned long long), c->stream));
+  c->ops->snap(st, c->nreg, c->RX, c->RYg, c->d_snap, c->stream);
+  ++c->launches;
+  CK(c, cudaGetLastError());
+  CK(c, cudaMemcpyAsync(c->h_snap, c->d_snap, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+  return ISING_SR_OK;
+}
+
 ising_sr_status grow_capacity(ising_sr_ctx* c) {
   if (c->K >= c->ops->cnt_max) return ISING_SR_E_CAPACITY;
   const int K = std::min(c->ops->cnt_max, c->K * 2);
@@ -977,6 +996,7 @@ void ising_sr_destroy(ising_sr_ctx* c) {
   cudaFreeHost(c->h_stats);
   cudaFreeHost(c->h_wlc);
   dfree(c, c->d_slot);
+  dfree(c, c->d_snap);
   cudaFreeHost(c->h_slot);
   dfree(c, c->log_t);
   dfree(c, c->log_region);
@@ -1062,7 +1082,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
       cudaMallocHost((void**)&c->h_wlc, 2 * sizeof(unsigned)) != cudaSuccess ||
       dmalloc(c, &c->d_off, n) != cudaSuccess || dmalloc(c, &c->d_bsum, (n + kThreads - 1) / kThreads) != cudaSuccess ||
       dmalloc(c, &c->d_total, 1) != cudaSuccess || dmalloc(c, &c->d_obs, 2 * kObsBlocks + 2) != cudaSuccess ||
-      dmalloc(c, &c->d_slot, 2) != cudaSuccess ||
+      dmalloc(c, &c->d_slot, 2) != cudaSuccess || dmalloc(c, &c->d_snap, 2) != cudaSuccess ||
       cudaMallocHost((void**)&c->h_slot, 2 * sizeof(IterSlot)) != cudaSuccess)
     return bail(ISING_SR_E_OOM);
   if (cudaMemsetAsync(c->sel, 0, n * 8 * (size_t)ops->sel_words, c->stream) != cudaSuccess ||
@@ -1128,9 +1148,13 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   }
   ops->init(dbuf, Lx, RX, c->RYl, c->row0, cfg->seed, c->st[0], c->stream);
   c->launches++;
+  if ((cfg->flags & ISING_SR_FLAG_OBSERVABLES) && enqueue_snapshot(c, c->st[0]) != ISING_SR_OK)
+    return bail(ISING_SR_E_CUDA);
   cudaError_t e = cudaStreamSynchronize(c->stream);
   dfree(c, dbuf);
   if (e != cudaSuccess || cudaGetLastError() != cudaSuccess) return bail(ISING_SR_E_CUDA);
+  c->stats.obs_M_now = (int64_t)c->h_snap[0];
+  c->stats.obs_B_now = (int64_t)c->h_snap[1];
   c->comm = 0;
   *out = c;
   return ISING_SR_OK;
@@ -1286,6 +1310,8 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
     CK(c, cudaGetLastError());
     CK(c, cudaMemcpyAsync(c->h_obs, c->d_obs + 2 * kObsBlocks, 2 * sizeof(double), cudaMemcpyDeviceToHost,
                           c->stream));
+    ising_sr_status ss = enqueue_snapshot(c, s1);  // the configuration at the new committed time
+    if (ss) return ss;
   }
   unsigned long long total = 0;
   CK(c, cudaMemcpyAsync(&total, c->d_total, sizeof total, cudaMemcpyDeviceToHost, c->stream));
@@ -1348,6 +1374,8 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
     c->stats.obs_M_total += c->h_obs[0];
     c->stats.obs_B_total += c->h_obs[1];
     c->stats.obs_time_total += c->t_w - (double)(c->w - 1) * c->cfg.W;  // t_w - t_c of this window
+    c->stats.obs_M_now = (int64_t)c->h_snap[0];
+    c->stats.obs_B_now = (int64_t)c->h_snap[1];
   }
   if (events_out) *events_out = (long long)c->win_events;
   return ISING_SR_OK;
@@ -1548,6 +1576,13 @@ ising_sr_status ising_sr_checkpoint_load(ising_sr_ctx* c, const void* buf, int64
   c->stats.obs_M_total = h.obs_M_total;
   c->stats.obs_B_total = h.obs_B_total;
   c->stats.obs_time_total = h.obs_time_total;
+  if (c->cfg.flags & ISING_SR_FLAG_OBSERVABLES) {
+    ising_sr_status ss = enqueue_snapshot(c, st);
+    if (ss) return ss;
+    CK(c, cudaStreamSynchronize(c->stream));
+    c->stats.obs_M_now = (int64_t)c->h_snap[0];
+    c->stats.obs_B_now = (int64_t)c->h_snap[1];
+  }
   c->stats.t_c = c->t_c < c->cfg.t_end ? c->t_c : c->cfg.t_end;
   return ISING_SR_OK;
 }

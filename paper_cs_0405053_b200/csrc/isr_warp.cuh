@@ -399,6 +399,38 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
   }
 }
 
+// FLAG_OBSERVABLES snapshot for the row layout (see snap_kernel): M and the
+// owned bonds (internal, north, west) of every region, exact integers
+template <int BX, int BY>
+__global__ void __launch_bounds__(256) snap_kernel_w(StateView st, int n, int RX, int RYg, unsigned long long* out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  long long m = 0, b = 0;
+  if (idx < n) {
+    constexpr uint32_t FULL = BX == 32 ? 0xffffffffu : ((1u << BX) - 1u);
+    const uint32_t* rows = (const uint32_t*)st.spins + (long long)idx * BY;
+    const uint4 h = ((const uint4*)st.halo)[idx];
+    const bool wrapX = RX == 1, wrapY = RYg == 1;
+    for (int ly = 0; ly < BY; ++ly) {
+      const uint32_t r = rows[ly];
+      m += 2 * __popc(r) - BX;
+      if (BX > 1) b += 2 * __popc(~(r ^ (r >> 1)) & (FULL >> 1)) - (BX - 1);  // (x, x+1) in the row
+      const uint32_t up = ly > 0 ? rows[ly - 1] : (wrapY ? rows[BY - 1] : h.x);  // north neighbour row
+      b += 2 * __popc(~(r ^ up) & FULL) - BX;
+      const uint32_t wb = wrapX ? (r >> (BX - 1)) & 1u : (h.z >> ly) & 1u;        // west neighbour bit
+      b += ((r & 1u) == wb) ? 1 : -1;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    m += __shfl_xor_sync(0xffffffffu, m, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out, (unsigned long long)m);
+    atomicAdd(out + 1, (unsigned long long)b);
+  }
+}
+
 // K0 for the warp form: rows as u32 masks, halo as {N row, S row, W bits, E bits}
 template <int BX, int BY>
 __global__ void init_kernel_w(const uint8_t* buf, int Lx, int RX, int RYl, int row0, unsigned long long seed,

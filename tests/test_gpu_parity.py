@@ -399,10 +399,19 @@ def test_observables_onsager():
         sim.run_window()
         sim.commit()
     a = sim.stats()
-    sim.run()
+    absm, es = [], []
+    while sim.stats()["t_c"] < w.t_end:
+        sim.run_window()
+        sim.commit()
+        st = sim.stats()
+        absm.append(abs(st["obs_M_now"]) / 65536)
+        es.append(-st["obs_B_now"] / 65536)
     b = sim.stats()
     sim.close()
     n = 256 * 256
+    # snapshots at the 80 committed times: |M| (not a time integral) and E
+    assert abs(np.mean(absm) - m0) < 0.01, (np.mean(absm), m0)
+    assert abs(np.mean(es) - u) < 0.006, (np.mean(es), u)
     tt = b["obs_time_total"] - a["obs_time_total"]
     e = -(b["obs_B_total"] - a["obs_B_total"]) / (n * tt)   # J = 1, H = 0
     m = (b["obs_M_total"] - a["obs_M_total"]) / (n * tt)
@@ -489,3 +498,27 @@ def test_torch_caching_allocator_hooks():
     ref = oracle.des_workload(w)
     assert np.array_equal(cnt, ref["count"]) and np.array_equal(dig, ref["digest"])
     assert np.array_equal(spins, ref["spins"])
+
+
+@pytest.mark.parametrize("geom", [(64, 64, 4, 4), (8, 24, 8, 4), (64, 64, 16, 16), (32, 64, 32, 32), (24, 8, 8, 8), (64, 16, 16, 16)])
+def test_observables_snapshot_at_committed_times(geom):
+    """stats.obs_M_now / obs_B_now: M and the bond sum of the configuration at
+    every committed time, against a direct count on the returned spins
+    (lane and big regions, regions spanning the lattice width)."""
+    from paper_cs_0405053_b200 import FLAG_OBSERVABLES
+    Lx, Ly, bx, by = geom
+    w = workloads.Workload("snap", Lx, Ly, bx, by, T=2.269, W=0.5, t_end=2.0, seed=6)
+    sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed, flags=FLAG_OBSERVABLES)
+
+    def direct():
+        s = sim.spins().reshape(Ly, Lx).astype(np.int64) * 2 - 1
+        return int(s.sum()), int((s * np.roll(s, -1, 0)).sum() + (s * np.roll(s, -1, 1)).sum())
+
+    for _ in range(w.n_windows()):
+        st = sim.stats()
+        assert (st["obs_M_now"], st["obs_B_now"]) == direct()
+        sim.run_window()
+        sim.commit()
+    st = sim.stats()
+    assert (st["obs_M_now"], st["obs_B_now"]) == direct()
+    sim.close()
