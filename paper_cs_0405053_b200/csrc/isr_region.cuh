@@ -496,7 +496,10 @@ __device__ __forceinline__ int div_rx(const KArgs& a, int idx) {
 #ifndef ISR_FRESH
 #define ISR_FRESH 1  // a freshly loaded region's first pair and refold run in the shared step code
 #endif
-constexpr int NT = 128;      // threads per block of K1
+#ifndef ISR_NT
+#define ISR_NT 128
+#endif
+constexpr int NT = ISR_NT;   // threads per block of K1
 constexpr int CI = ISR_CI;   // staged entries per history
 
 // Staged history entries, column si per region in flight: incoming

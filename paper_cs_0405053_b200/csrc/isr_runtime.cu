@@ -37,7 +37,7 @@ using isr::GhostView;
 using isr::KArgs;
 using isr::StateView;
 
-constexpr int kThreads = 128;
+constexpr int kThreads = isr::NT;  // K1 block (and the small kernels')
 constexpr int kBatch = 8;  // max iterations in flight per host sync
 
 // ---------------------------------------------------------------------------
