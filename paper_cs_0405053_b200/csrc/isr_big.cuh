@@ -667,7 +667,27 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
             const uint8_t* Po = src_p(a, ps[e], e);
             double* Tn = const_cast<double*>(src_t(a, ps[e] ^ 1u, e));
             uint8_t* Pn = const_cast<uint8_t*>(src_p(a, ps[e] ^ 1u, e));
-            for (unsigned q = 0; q < k0[e]; ++q) {
+            // 8 entries per round, all loads issued before the stores (the two
+            // slots may alias as far as the compiler knows, so a plain loop
+            // serialises one memory latency per entry)
+            unsigned q = 0;
+            for (; q + 8 <= k0[e]; q += 8) {
+              double tv[8];
+              uint8_t pv[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const unsigned o = obase + (q + u) * (unsigned)a.RX;
+                tv[u] = __ldcg(To + o);
+                pv[u] = __ldcg(Po + o);
+              }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const unsigned o = obase + (q + u) * (unsigned)a.RX;
+                Tn[o] = tv[u];
+                Pn[o] = pv[u];
+              }
+            }
+            for (; q < k0[e]; ++q) {
               const unsigned o = obase + q * (unsigned)a.RX;
               Tn[o] = To[o];
               Pn[o] = Po[o];
