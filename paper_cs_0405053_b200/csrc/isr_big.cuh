@@ -475,6 +475,15 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
     double U, V;
     draw_pair(a.seed, gid, n, U, V, a.gen);
     if (a.fresh_w && lpos == 0) R = expvar(U);  // the slate is wiped at t_c; a replay restored R
+    // pair n+1 drawn one event ahead: an event takes its new budget and atom
+    // variate from here and draws the following pair off the step's critical
+    // path (the region's serial step chain bounds every iteration, §6)
+    double Rn, Vn;
+    {
+      double Un;
+      draw_pair(a.seed, gid, n + 1, Un, Vn, a.gen);
+      Rn = expvar(Un);
+    }
     double lam = big_fold(B, a.rate);
     double tc = cand_time(ts, R, lam);
 
@@ -562,6 +571,15 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
       } else {
         // own event at tc
         const int site = big_select<BX, BY>(B, a.rate, V, lam);
+        // pair n+1 (drawn ahead) becomes current; pair n+2 is drawn here, where
+        // its instructions interleave with the flip's bookkeeping below
+        R = Rn;
+        V = Vn;
+        {
+          double Un;
+          draw_pair(a.seed, gid, n + 2, Un, Vn, a.gen);
+          Rn = expvar(Un);
+        }
         const int sr = site / BX, sc = site - sr * BX;
         code = (unsigned)site;
         if (OBS && !LOG) {
@@ -634,8 +652,6 @@ __global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
         ++n_ev_r;
         ts = tc;
         ++n;
-        draw_pair(a.seed, gid, n, U, V, a.gen);
-        R = expvar(U);
       }
       if (!LOG && a.resume) {  // step log: time, budget after the step, code
         if (lpos < (unsigned)a.LC) {
