@@ -209,8 +209,16 @@ __device__ __forceinline__ int big_select(const BigRegion<BX, BY>& B, const doub
   return r * BX + nth_bit<uint32_t, 32>(B.class_mask(r, ks), jj);
 }
 
+#ifndef ISR_BIG_MINB
+#define ISR_BIG_MINB 8  // resident 64-thread blocks per SM asked of ptxas (128 registers): c3 +12 %, c5 32x32 +17-24 % over 221 unbounded
+#endif
+#if ISR_BIG_MINB > 0
+#define ISR_BIG_BOUNDS __launch_bounds__(BNT, ISR_BIG_MINB)
+#else
+#define ISR_BIG_BOUNDS __launch_bounds__(BNT)
+#endif
 template <int BX, int BY, bool LOG, bool OBS = false>
-__global__ void __launch_bounds__(BNT) region_kernel_big(const KArgs a) {
+__global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
   using BR = BigRegion<BX, BY>;
   static_assert(BX <= 32 && BY <= 32 && BX >= 3 && BY >= 3, "rows of up to 32 sites");
   __shared__ BigSmem<BX, BY> SM;
