@@ -1205,8 +1205,11 @@ template <int BX, int BY, bool LOG, bool GQ = false, bool OBS = false, bool FIRS
 __global__ void ISR_K1_BOUNDS region_kernel(const KArgs a) {
   region_body<BX, BY, LOG, GQ, OBS, FIRST>(a);
 }
+#ifndef ISR_MB_MINB
+#define ISR_MB_MINB 5
+#endif
 template <int BX, int BY, bool LOG, bool GQ = false, bool OBS = false, bool FIRST = false>
-__global__ void __launch_bounds__(NT, 5) region_kernel_mb(const KArgs a) {
+__global__ void __launch_bounds__(NT, ISR_MB_MINB) region_kernel_mb(const KArgs a) {
   region_body<BX, BY, LOG, GQ, OBS, FIRST>(a);
 }
 // the window's first iteration (≤ 32-site regions): no staging, so shared
