@@ -210,7 +210,7 @@ __device__ __forceinline__ int big_select(const BigRegion<BX, BY>& B, const doub
 }
 
 #ifndef ISR_BIG_MINB
-#define ISR_BIG_MINB 8  // resident 64-thread blocks per SM asked of ptxas (128 registers): c3 +12 %, c5 32x32 +17-24 % over 221 unbounded
+#define ISR_BIG_MINB 7  // resident 64-thread blocks per SM asked of ptxas (128 registers, 8 fit): c3 +14 %, c5 32x32 +20-27 % over 221 unbounded
 #endif
 #if ISR_BIG_MINB > 0
 #define ISR_BIG_BOUNDS __launch_bounds__(BNT, ISR_BIG_MINB)
