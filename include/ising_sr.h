@@ -53,7 +53,7 @@ typedef enum {
   ISING_SR_E_DIVERGED = -4,    /* max_iterations reached without a fixed point */
   ISING_SR_E_CAPACITY = -5,    /* boundary-history capacity cannot be grown further */
   ISING_SR_E_CUDA = -6,        /* CUDA runtime error (sticky) */
-  ISING_SR_E_NCCL = -7,        /* exchange callback reported failure */
+  ISING_SR_E_NCCL = -7,        /* NCCL (or the exchange callback) failed, or NCCL cannot be loaded */
   ISING_SR_E_OOM = -8,         /* device allocation failed */
   ISING_SR_E_STATE = -9        /* call out of order (commit without a converged window, run past t_end) */
 } ising_sr_status;
@@ -79,12 +79,21 @@ typedef enum {
  * Same fixed point, same g, same bits; only slower (the default worklist skips
  * regions that would regenerate their previous trajectory). */
 #define ISING_SR_FLAG_JACOBI_ALL 0x10u
+/* Halo loopback (world == 1 with nccl_id): the strip's first and last region
+ * rows read their wrap-around neighbours' histories from ghost rows filled
+ * by the library's NCCL exchange with itself (ncclSend/ncclRecv to rank 0 of
+ * a one-rank communicator), exactly as a strip of a multi-GPU run reads its
+ * neighbours'.  Same results as without the flag; it exercises the in-library
+ * exchange on one GPU. */
+#define ISING_SR_FLAG_HALO_LOOPBACK 0x20u
 
 /* Halo exchange between strips (world > 1).  Rank q owns a band of region
  * rows; "up" is toward region row 0 (rank q-1, periodic), "down" toward rank
- * q+1.  After each relaxation iteration the library calls the exchange
- * callback with device pointers into the current iteration's boundary-history
- * buffers; the callee must
+ * q+1.  With cfg.nccl_id the library performs the exchange itself on its
+ * stream (ncclSend/ncclRecv of the ghost rows + ncclAllReduce(max) of the
+ * flags).  Otherwise, after each relaxation iteration
+ * the library calls the exchange callback with device pointers into the
+ * current iteration's boundary-history buffers; the callee must
  *   (a) copy my send_up chunks into rank (q-1)'s recv_from_down chunks and my
  *       send_down chunks into rank (q+1)'s recv_from_up chunks (periodic in
  *       q; with world == 2 both go to the other rank), chunk k being
@@ -92,12 +101,21 @@ typedef enum {
  *   (b) replace flags[0..1] (device int32 {changed, overflow}) by their
  *       maximum over all ranks (the "UNTIL all PEs detect no difference" of
  *       P:427-429).
- * send_up = my first region row's north-edge histories (count row, time
- * block, position block); send_down = my last row's south-edge histories.
+ * send_up = my first region row's north-edge histories, send_down = my last
+ * row's south-edge histories, each in 4 chunks (all four must be moved):
+ *   chunk 0: u16 count[RX]     entries of each region's edge history
+ *   chunk 1: u32 stamp[RX]     global iteration of the edge's last change (the
+ *                              receiver marks its adjacent region dirty when
+ *                              stamp == the current iteration)
+ *   chunk 2: f64 t[K][RX]      entry times (entry q of column c at q*RX + c)
+ *   chunk 3: u8  pos[K][RX]    entry positions along the edge
+ * The chunks of one row are contiguous in that order (each start 256-byte
+ * aligned), so one copy of row_bytes from send_up[0] moves a whole row.
  * Work may be enqueued on `stream` (the ctx stream) and must be ordered on it
- * on return.  Return 0 on success (anything else -> ISING_SR_E_NCCL). */
+ * on return (NCCL: issue it on that stream).  Return 0 on success (anything
+ * else -> ISING_SR_E_NCCL). */
 typedef struct {
-  int32_t nchunks;          /* 3: counts (u8), times (f64), positions (u8) */
+  int32_t nchunks;          /* 4: count (u16), stamp (u32), times (f64), positions (u8) */
   void* send_up[4];
   void* send_down[4];
   void* recv_from_up[4];    /* ghost row above my strip: up neighbour's south edges */
@@ -105,6 +123,7 @@ typedef struct {
   size_t chunk_bytes[4];
   int32_t* flags;           /* device int32[2]: {changed, overflow}; all-reduce(max) */
   void* stream;             /* cudaStream_t of the ctx */
+  size_t row_bytes;         /* bytes from send_up[0] through the end of send_up[3] (one contiguous row) */
 } ising_sr_halo;
 
 typedef int (*ising_sr_exchange_fn)(void* user, const ising_sr_halo* halo);
@@ -116,7 +135,10 @@ typedef struct {
                              * 16x8, 8x16 (big-region form); else E_INVALID_ARG             */
   double J, H, T;           /* recorded for observables; the dynamics use `rate` only        */
   double rate[10];          /* r_k = lambda p_k, class k = 5(s+1)/2 + u          */
-  double W;                 /* window length = the paper's T_max, > 0            */
+  double W;                 /* window length = the paper's T_max, > 0; <= 0:     *
+                             * the paper's rule W = ln N / (lambda |dG_i|), N = Lx Ly/(bx by)*
+                             * regions, |dG_i| = 2bx + 2by - 4 boundary sites (bx by if a   *
+                             * side is 1), lambda = max_k rate[k]                           */
   double t_end;             /* simulate events with tau < t_end                              */
   uint64_t seed;            /* Philox key/counter seed                         */
   int32_t max_iterations;   /* relaxation iterations per window before E_DIVERGED; 0 = 1000  */
@@ -135,6 +157,19 @@ typedef struct {
   void* (*dev_alloc)(size_t bytes, void* user);
   void (*dev_free)(void* ptr, void* user);
   void* alloc_user;
+  /* world > 1 (or FLAG_HALO_LOOPBACK): the 128-byte ncclUniqueId shared by
+   * all ranks (rank 0 gets one from ising_sr_nccl_unique_id and broadcasts
+   * it, e.g. with torch.distributed); the library creates its communicator
+   * (ncclCommInitRank(world, id, rank)) and runs the exchange on `stream`.
+   * NULL: the exchange callback (or the step-level API) moves the ghost rows.
+   * Copied at init. */
+  const void* nccl_id;
+  /* > 0 (a power of two): test mode forcing exact time ties -- every budget
+   * E(U) is replaced by (floor(E(U) q) + 1) / q (R30); 0 = off */
+  double eq_quantum;
+  /* FLAG_LOG_EVENTS: events per region per window kept by K1 for the commit
+   * compaction (a region with more is replayed at commit); 0 = auto */
+  int32_t log_capacity;
 } ising_sr_config;
 
 typedef struct {
@@ -170,14 +205,31 @@ typedef struct {
    * configuration at the committed time t_c (this rank's regions, each owning
    * its internal bonds and those to its north and west neighbours), exact */
   int64_t obs_M_now, obs_B_now;
+  /* FLAG_LOG_EVENTS: boundary-history entries of the last committed window's
+   * fixed point (h of SURVEY §8(d.3): each event counted once per region edge
+   * its site lies on), and its regions replayed at commit because their event
+   * count exceeded log_capacity; -1 without the flag */
+  int64_t edge_entries_last_window;
+  int64_t log_replayed_last_window;
+  /* device time (ms, all windows) of the commit's compaction kernels */
+  double ms_compact_total;
 } ising_sr_stats;
 
 /* Validate cfg, allocate device state, copy the full Ly*Lx row-major spin
  * configuration (nonzero = up, 0 = down; caller-owned, copied) and set
  * committed time 0.  Each rank passes the whole lattice and keeps
  * its strip; only its rows (+1 halo row each side) are read, by host-to-device
- * copies straight from `spins` (full DMA speed when it is page-locked). */
+ * copies straight from `spins` (full DMA speed when it is page-locked).
+ * spins == NULL: the iid +-1 (p = 1/2) configuration of the Philox init
+ * stream is generated on the device (Philox4x32-10 with key
+ * (0xFFFFFFFF, seed_lo), counter (v >> 7, 0, 1, seed_hi); site v is up iff
+ * bit (v & 31) of output word ((v >> 5) & 3) is set).  With nccl_id this
+ * call is collective (every rank must call it). */
 ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, ising_sr_ctx** out);
+
+/* A fresh 128-byte ncclUniqueId into `out` (for cfg.nccl_id; rank 0 calls it
+ * and broadcasts the bytes).  E_NCCL if NCCL cannot be loaded. */
+ising_sr_status ising_sr_nccl_unique_id(void* out);
 
 /* Relax the window [t_c, min(t_c + W, t_end)) to the fixed point.
  * Deterministic and idempotent until commit.  *g_out = iterations run,
@@ -201,6 +253,9 @@ ising_sr_status ising_sr_get_spins(ising_sr_ctx* ctx, uint8_t* out);
 
 /* Last committed window's event log (requires FLAG_LOG_EVENTS), ordered by
  * region id then time: time, global region id, local site (row*bx + col).
+ * Built at commit by compacting the events K1 recorded in its final
+ * recomputation of each region (K3; regions with more than
+ * log_capacity events are replayed).
  * Copies min(cap, n) entries; *n = number of events in the window. */
 ising_sr_status ising_sr_get_events(ising_sr_ctx* ctx, double* t, uint32_t* region, uint16_t* site,
                                     int64_t cap, int64_t* n);

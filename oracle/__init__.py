@@ -50,7 +50,8 @@ class _Cfg(ctypes.Structure):
                 ("bx", ctypes.c_int32), ("by", ctypes.c_int32),
                 ("rate", ctypes.c_double * 10), ("seed", ctypes.c_uint64),
                 ("t_end", ctypes.c_double), ("t_obs0", ctypes.c_double),
-                ("check", ctypes.c_int32), ("fresh_W", ctypes.c_double)]
+                ("check", ctypes.c_int32), ("fresh_W", ctypes.c_double),
+                ("eq_quantum", ctypes.c_double)]
 
 
 class _Out(ctypes.Structure):
@@ -183,7 +184,7 @@ def class_counts(Lx: int, Ly: int, bx: int, by: int, spins: np.ndarray) -> np.nd
 
 # -- whole-trajectory runs -----------------------------------------------------
 
-def _cfg(Lx, Ly, bx, by, rates, seed, t_end, t_obs0=0.0, check=False, fresh_W=0.0) -> _Cfg:
+def _cfg(Lx, Ly, bx, by, rates, seed, t_end, t_obs0=0.0, check=False, fresh_W=0.0, eq_quantum=0.0) -> _Cfg:
     c = _Cfg()
     c.Lx, c.Ly, c.bx, c.by = Lx, Ly, bx, by
     for k in range(10):
@@ -193,13 +194,15 @@ def _cfg(Lx, Ly, bx, by, rates, seed, t_end, t_obs0=0.0, check=False, fresh_W=0.
     c.t_obs0 = float(t_obs0)
     c.check = 1 if check else 0
     c.fresh_W = float(fresh_W)
+    c.eq_quantum = float(eq_quantum)
     return c
 
 
 def _run(kind: str, Lx: int, Ly: int, bx: int, by: int, rates: Sequence[float], seed: int,
          spins0: np.ndarray, t_end: float, *, log_cap: int = 0,
          sample_t: Optional[Sequence[float]] = None, t_obs0: float = 0.0,
-         check: bool = False, stream: int = 0, fresh_W: float = 0.0) -> Dict[str, object]:
+         check: bool = False, stream: int = 0, fresh_W: float = 0.0,
+         eq_quantum: float = 0.0) -> Dict[str, object]:
     nreg = 1 if kind == "bkl" else (Lx // bx) * (Ly // by)
     s0 = np.ascontiguousarray(spins0, dtype=np.uint8).reshape(-1)
     assert s0.shape[0] == Lx * Ly
@@ -219,7 +222,7 @@ def _run(kind: str, Lx: int, Ly: int, bx: int, by: int, rates: Sequence[float], 
     o.log_cap = log_cap
     o.sample_t, o.n_samples = _ptr(st), ns
     o.sample_M, o.sample_B = _ptr(sM), _ptr(sB)
-    cfg = _cfg(Lx, Ly, bx, by, rates, seed, t_end, t_obs0, check, fresh_W)
+    cfg = _cfg(Lx, Ly, bx, by, rates, seed, t_end, t_obs0, check, fresh_W, eq_quantum)
     if kind == "bkl":
         rc = lib().orc_bkl_run(ctypes.byref(cfg), stream, _ptr(s0), _ptr(sout), ctypes.byref(o))
     else:

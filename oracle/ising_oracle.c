@@ -115,6 +115,17 @@ static uint64_t digest_step(uint64_t h, double tau, uint32_t site) {
   return (h ^ tb) * 0x9E3779B97F4A7C15ULL + (uint64_t)site + 1u;
 }
 
+/* The budget a region draws from U: E(U), or in the tie test mode
+ * (cfg->eq_quantum = q > 0, R30) (floor(E(U) q) + 1) / q -- exact
+ * for a power-of-two q -- so that equal event times in different regions
+ * are common and the (time, region id) order (reading #10) and the
+ * candidate bump (reading #11) are exercised. */
+static double budget_of(const orc_cfg* cfg, double U) {
+  double E = orc_expvar(U);
+  if (cfg->eq_quantum > 0.0) E = (floor(E * cfg->eq_quantum) + 1.0) / cfg->eq_quantum;
+  return E;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Lattice helpers.  Spins stored 1 = up (+1), 0 = down (-1).    */
 /* ------------------------------------------------------------------------ */
@@ -378,7 +389,7 @@ int orc_des_run(const orc_cfg* cfg, const uint8_t* spins0, uint8_t* spins_out, o
   for (int32_t r = 0; r < NR; ++r) {
     double U, V;
     orc_pair(cfg->seed, (uint32_t)r, 0, &U, &V);
-    Rb[r] = orc_expvar(U);
+    Rb[r] = budget_of(cfg, U);
     Vv[r] = V;
     ts[r] = 0.0;
     lam[r] = fold_lambda(Ncnt + (size_t)r * 10, cfg->rate);
@@ -404,7 +415,7 @@ int orc_des_run(const orc_cfg* cfg, const uint8_t* spins0, uint8_t* spins_out, o
       for (int32_t q = 0; q < NR; ++q) {
         double U, V;
         orc_pair_g(cfg->seed, (uint32_t)q, nev[q], gen, &U, &V);
-        Rb[q] = orc_expvar(U);
+        Rb[q] = budget_of(cfg, U);
         Vv[q] = V;
         ts[q] = t_next;
         tc[q] = cand_time(t_next, Rb[q], lam[q]);
@@ -447,7 +458,7 @@ int orc_des_run(const orc_cfg* cfg, const uint8_t* spins0, uint8_t* spins_out, o
     {
       double U, V;
       orc_pair_g(cfg->seed, (uint32_t)r, nev[r], gen, &U, &V);
-      Rb[r] = orc_expvar(U);
+      Rb[r] = budget_of(cfg, U);
       Vv[r] = V;
       ts[r] = tau;
       lam[r] = fold_lambda(N, cfg->rate);
@@ -547,7 +558,7 @@ int orc_bkl_run(const orc_cfg* cfg, uint32_t stream, const uint8_t* spins0,
       cum[k] = acc;
     }
     double lam = cum[9];
-    double tau = cand_time(t, orc_expvar(U), lam);
+    double tau = cand_time(t, budget_of(cfg, U), lam);
     if (!(tau < cfg->t_end)) break;
     obs_advance(&O, cfg, out, tau);
     /* W(k-1) < V <= W(k)  <=>  cum[k-1] < V*Lambda <= cum[k] */

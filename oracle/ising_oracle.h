@@ -59,6 +59,7 @@ typedef struct {
   double   fresh_W;        /* > 0: alternate approach to subsequent steps: at
                               every t_c = fl(w fresh_W), w >= 1, each region discards its
                               pending budget and restarts at t_c with pair (n, generation w) */
+  double   eq_quantum;     /* > 0: tie test mode, budgets (floor(E(U) q) + 1) / q (R30) */
 } orc_cfg;
 
 typedef struct {

@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libising_sr.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("isr_runtime.cu", "isr_checkerboard.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("isr_region.cuh", "isr_warp.cuh", "isr_pool.cuh", "isr_big.cuh", "isr_device.cuh")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("isr_region.cuh", "isr_warp.cuh", "isr_big.cuh", "isr_device.cuh", "isr_nccl.h")] + [
     os.path.join(os.path.dirname(PKG), "include", "ising_sr.h")]
 
 NVCC_FLAGS = [
@@ -19,7 +19,7 @@ NVCC_FLAGS = [
     "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
     "-lineinfo",
     "-Xptxas", "-v",
-    "-shared", "-Xcompiler", "-fPIC",
+    "-shared", "-Xcompiler", "-fPIC", "-ldl",
 ]
 
 

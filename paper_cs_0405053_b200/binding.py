@@ -21,6 +21,7 @@ FLAG_DIGEST = 0x2
 FLAG_FRESH_WINDOW = 0x4  # alternate approach to subsequent steps
 FLAG_OBSERVABLES = 0x8   # time integrals of M and of the bond sum per window
 FLAG_JACOBI_ALL = 0x10   # recompute every region in every iteration (paper-faithful schedule)
+FLAG_HALO_LOOPBACK = 0x20  # world == 1 + nccl_id: the wrap rows exchanged with itself over NCCL
 
 STATUS = {
     0: "OK", -1: "E_INVALID_ARG", -2: "E_DIMENSION", -3: "E_PARTITION", -4: "E_DIVERGED",
@@ -39,7 +40,7 @@ class Halo(ctypes.Structure):
                 ("send_up", ctypes.c_void_p * 4), ("send_down", ctypes.c_void_p * 4),
                 ("recv_from_up", ctypes.c_void_p * 4), ("recv_from_down", ctypes.c_void_p * 4),
                 ("chunk_bytes", ctypes.c_size_t * 4),
-                ("flags", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
+                ("flags", ctypes.c_void_p), ("stream", ctypes.c_void_p), ("row_bytes", ctypes.c_size_t)]
 
 
 EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(Halo))
@@ -57,7 +58,8 @@ class Config(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("exchange", EXCHANGE_FN),
                 ("exchange_user", ctypes.c_void_p),
-                ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_user", ctypes.c_void_p)]
+                ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_user", ctypes.c_void_p),
+                ("nccl_id", ctypes.c_void_p), ("eq_quantum", ctypes.c_double), ("log_capacity", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -75,7 +77,9 @@ class Stats(ctypes.Structure):
                 ("obs_time_total", ctypes.c_double),
                 ("active_last", ctypes.c_int64 * 64),
                 ("ms_exchange_total", ctypes.c_double), ("ms_commit_total", ctypes.c_double),
-                ("obs_M_now", ctypes.c_int64), ("obs_B_now", ctypes.c_int64)]
+                ("obs_M_now", ctypes.c_int64), ("obs_B_now", ctypes.c_int64),
+                ("edge_entries_last_window", ctypes.c_int64), ("log_replayed_last_window", ctypes.c_int64),
+                ("ms_compact_total", ctypes.c_double)]
 
 
 _lib = None
@@ -85,7 +89,7 @@ EXPORTS = ["ising_sr_init", "ising_sr_run_window", "ising_sr_commit", "ising_sr_
            "ising_sr_begin_window", "ising_sr_iterate", "ising_sr_halo_get", "ising_sr_exchange_done",
            "ising_sr_end_iterations",
            "ising_sr_checkpoint_size", "ising_sr_checkpoint_save", "ising_sr_checkpoint_load",
-           "ising_sr_launch_count", "ising_sr_destroy", "ising_sr_strerror",
+           "ising_sr_launch_count", "ising_sr_destroy", "ising_sr_strerror", "ising_sr_nccl_unique_id",
            "ising_cb_sweeps", "ising_cb_run"]
 
 
@@ -121,6 +125,7 @@ def load_library(path: str = LIB_PATH):
     L.ising_sr_destroy.restype = None
     L.ising_sr_strerror.argtypes = [i32]
     L.ising_sr_strerror.restype = ctypes.c_char_p
+    L.ising_sr_nccl_unique_id.argtypes = [vp]
     L.ising_cb_sweeps.argtypes = [vp, i32, i32, vp, ctypes.c_uint64, i64, i32, vp, vp]
     L.ising_cb_run.argtypes = [vp, vp, i32, i32, vp, ctypes.c_uint64, i64, i32, ctypes.POINTER(i64), i32]
     for name in EXPORTS:
@@ -136,13 +141,26 @@ def _check(status: int, where: str):
 
 
 def _current_stream_ptr(device: int) -> Optional[int]:
+    """torch's current stream on `device`, or None (the library then creates
+    its own stream) when that is the legacy default stream: its handle is 0,
+    which the C ABI reads as "no stream"."""
     try:
         import torch
         if torch.cuda.is_available():
-            return torch.cuda.current_stream(device).cuda_stream
+            h = torch.cuda.current_stream(device).cuda_stream
+            return h or None
     except Exception:
         pass
     return None
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (ising_sr_nccl_unique_id) for
+    IsingSR(nccl_id=...): rank 0 creates it and broadcasts the bytes."""
+    L = load_library()
+    buf = ctypes.create_string_buffer(128)
+    _check(L.ising_sr_nccl_unique_id(buf), "ising_sr_nccl_unique_id")
+    return buf.raw
 
 
 class IsingSR:
@@ -151,12 +169,13 @@ class IsingSR:
     Mirrors the C ABI: ``run_window`` / ``commit`` / ``run`` / ``stats`` plus
     accessors.  ``spins`` is the full Ly*Lx lattice (1 = up)."""
 
-    def __init__(self, Lx: int, Ly: int, bx: int, by: int, rates: Sequence[float], spins: np.ndarray,
+    def __init__(self, Lx: int, Ly: int, bx: int, by: int, rates: Sequence[float], spins: Optional[np.ndarray],
                  W: float, t_end: float, seed: int = 1, *, J: float = 1.0, H: float = 0.0,
                  T: float = float("nan"), flags: int = FLAG_DIGEST, hist_capacity: int = 0,
                  max_iterations: int = 0, rank: int = 0, world: int = 1, device: int = 0,
                  stream: Optional[int] = None,
-                 exchange: Optional[Callable[[Halo], int]] = None, torch_alloc: bool = False):
+                 exchange: Optional[Callable[[Halo], int]] = None, torch_alloc: bool = False,
+                 nccl_id: Optional[bytes] = None, eq_quantum: float = 0.0, log_capacity: int = 0):
         L = load_library()
         c = Config()
         c.Lx, c.Ly, c.bx, c.by = Lx, Ly, bx, by
@@ -166,7 +185,15 @@ class IsingSR:
         c.W, c.t_end, c.seed = float(W), float(t_end), int(seed)
         c.max_iterations, c.hist_capacity, c.flags = max_iterations, hist_capacity, flags
         c.rank, c.world, c.device = rank, world, device
-        c.stream = stream if stream is not None else _current_stream_ptr(device)
+        c.stream = stream if stream else _current_stream_ptr(device)
+        self._nccl_id = None
+        if nccl_id is not None:
+            if len(nccl_id) != 128:
+                raise ValueError("nccl_id must be the 128 bytes of an ncclUniqueId")
+            self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            c.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
+        c.eq_quantum = float(eq_quantum)
+        c.log_capacity = int(log_capacity)
         self._cb = None
         if exchange is not None:
             def _tramp(user, halo_p):
@@ -197,11 +224,14 @@ class IsingSR:
         self.cfg = c
         self.Lx, self.Ly, self.bx, self.by, self.world, self.rank = Lx, Ly, bx, by, world, rank
         self.n_regions = (Lx // bx) * (Ly // by) // world
-        s = np.ascontiguousarray(spins, dtype=np.uint8).reshape(-1)
-        if s.shape[0] != Lx * Ly:
-            raise ValueError("spins must hold Lx*Ly entries")
+        sp = None  # spins None: the Philox init stream, generated on the device
+        if spins is not None:
+            s = np.ascontiguousarray(spins, dtype=np.uint8).reshape(-1)
+            if s.shape[0] != Lx * Ly:
+                raise ValueError("spins must hold Lx*Ly entries")
+            sp = s.ctypes.data
         h = ctypes.c_void_p()
-        _check(L.ising_sr_init(ctypes.byref(c), s.ctypes.data, ctypes.byref(h)), "ising_sr_init")
+        _check(L.ising_sr_init(ctypes.byref(c), sp, ctypes.byref(h)), "ising_sr_init")
         self._h = h
         self._L = L
 

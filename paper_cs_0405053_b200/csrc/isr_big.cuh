@@ -275,7 +275,7 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
       const bool axis_off = (d < 2) ? wrapY : wrapX;
-      const bool ghost = a.world > 1 && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
+      const bool ghost = a.ghost && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
       use[d] = !a.first && !axis_off && !ghost;
       const int nr = d == EDGE_N ? wdec(r, a.RYl) : d == EDGE_S ? winc(r, a.RYl) : r;
       const int nc = d == EDGE_W ? wdec(c, a.RX) : d == EDGE_E ? winc(c, a.RX) : c;
@@ -482,7 +482,7 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
 
     double U, V;
     draw_pair(a.seed, gid, n, U, V, a.gen);
-    if (a.fresh_w && lpos == 0) R = expvar(U);  // the slate is wiped at t_c; a replay restored R
+    if (a.fresh_w && lpos == 0) R = budget(a, U);  // the slate is wiped at t_c; a replay restored R
     // pair n+1 drawn one event ahead: an event takes its new budget and atom
     // variate from here and draws the following pair off the step's critical
     // path (the region's serial step chain bounds every iteration, §6)
@@ -490,7 +490,7 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
     {
       double Un;
       draw_pair(a.seed, gid, n + 1, Un, Vn, a.gen);
-      Rn = expvar(Un);
+      Rn = budget(a, Un);
     }
     double lam = big_fold(B, a.rate);
     double tc = cand_time(ts, R, lam);
@@ -586,7 +586,7 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
         {
           double Un;
           draw_pair(a.seed, gid, n + 2, Un, Vn, a.gen);
-          Rn = expvar(Un);
+          Rn = budget(a, Un);
         }
         const int sr = site / BX, sc = site - sr * BX;
         code = (unsigned)site;
@@ -620,6 +620,11 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
           a.log_region[o] = gid;
           a.log_site[o] = (uint16_t)site;
         } else {
+          if (a.ev_t && (int)n_ev_r < a.evC) {  // scratch event log (a resumed prefix is already there)
+            const long long o = (long long)n_ev_r * a.ev_stride + idx;
+            a.ev_t[o] = tc;
+            a.ev_s[o] = (uint16_t)site;
+          }
           bool on_edge = false;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -675,6 +680,7 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
     fmax = max(fmax, bev);
     if (!LOG && a.resume) a.lg_meta[idx] = make_uint2(K, lpos <= (unsigned)a.LC ? lpos : 0xffffffffu);
 
+    if (!LOG && a.delay_ns) k1_delay(a.delay_ns);  // test knob: publish late
     if (!LOG) {
       unsigned chmask = 0;
 #pragma unroll
@@ -728,7 +734,7 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           if (!((chmask >> e) & 1u)) continue;
-          if (a.world > 1 && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
+          if (a.ghost && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
           const int nr = e == EDGE_N ? wdec(r, a.RYl) : e == EDGE_S ? winc(r, a.RYl) : r;
           const int nc = e == EDGE_W ? wdec(c, a.RX) : e == EDGE_E ? winc(c, a.RX) : c;
           mark_dirty(a, nr * a.RX + nc, K + 1);

@@ -112,18 +112,7 @@ __device__ __forceinline__ double cand_time(double t, double R, double lam) {
 // Per-region event digest step (R27): h <- (h ^ tau_bits) * K + site + 1,
 // a bijection of h for fixed (tau, site), so a difference in any event of a
 // sequence survives to the final digest.
-#ifndef ISR_DIGEST_OLD
-#define ISR_DIGEST_OLD 0
-#endif
-__device__ __forceinline__ unsigned long long mix64_(unsigned long long z) {
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-  return z ^ (z >> 31);
-}
 __device__ __forceinline__ unsigned long long digest_step(unsigned long long h, double tau, int site) {
-#if ISR_DIGEST_OLD
-  return mix64_(mix64_(h ^ (unsigned long long)__double_as_longlong(tau)) ^ (unsigned long long)site);
-#endif
   return (h ^ (unsigned long long)__double_as_longlong(tau)) * 0x9E3779B97F4A7C15ULL + (unsigned long long)(site + 1);
 }
 

@@ -85,6 +85,7 @@ struct KArgs {
   unsigned long long* sel;      // per region: 2 selector words (parity K & 1)
   GhostView gh_up, gh_down;     // world > 1: rows above / below the strip
   int RX, RYl, RYg, row0, world;
+  int ghost;          // the strip's first/last region rows read ghost rows (world > 1, or halo loopback)
   int K;
   long long tstride;  // elements per edge in t/pos (RYl * K * RX)
   unsigned it_K;      // global iteration stamp of this launch (>= 1)
@@ -120,12 +121,35 @@ struct KArgs {
   int dwords;              // 32-bit words per bitmap
   int* flags;                   // [0] changed, [1] overflow
   unsigned long long* stats;    // [0] events [1] entries out [2] entries in [3] entries cmp [4] f max [5] regions
+  // scratch event log (FLAG_LOG_EVENTS): event q of a region's latest
+  // recomputation at ev_t/ev_s[q * ev_stride + idx] for q < evC; commit
+  // compacts it (regions with more events are replayed)
+  double* ev_t;
+  uint16_t* ev_s;
+  long long ev_stride;
+  int evC;
+  double eq_q;        // > 0: quantized budgets E <- (floor(E q) + 1) / q (exact time ties; test mode)
+  unsigned delay_ns;  // test knob (env ISING_SR_K1_DELAY_NS): K1 blocks sleep before publishing their flags
   // log replay
   double* log_t;
   uint32_t* log_region;
   uint16_t* log_site;
   const unsigned long long* log_off;
 };
+
+// The budget drawn from U: E(U) (R25), or with eq_q > 0 (tie test
+// mode, R30) the quantized (floor(E(U) eq_q) + 1) / eq_q, exact
+// for a power-of-two eq_q, so that equal event times across regions are common.
+__device__ __forceinline__ double quantize_budget(double E, double q) {
+  return q > 0.0 ? __ddiv_rn(__dadd_rn(floor(__dmul_rn(E, q)), 1.0), q) : E;
+}
+__device__ __forceinline__ double budget(const KArgs& a, double U) { return quantize_budget(expvar(U), a.eq_q); }
+
+// test knob: a K1 made artificially slow (exposes any work that is not
+// ordered after K1 on the stream, e.g. an exchange on another stream)
+__device__ __noinline__ void k1_delay(unsigned ns) {
+  for (unsigned t = 0; t < ns; t += 1000) __nanosleep(1000);
+}
 
 // Selector words of a region: two 64-bit words.  When its histories change
 // in iteration K the region's thread overwrites the OLDER of its two words
@@ -441,11 +465,7 @@ __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000
 
 // region row of a shard-local index without an integer division
 __device__ __forceinline__ int div_rx(const KArgs& a, int idx) {
-#if ISR_MAGICDIV
   return (int)(((unsigned long long)(unsigned)idx * a.rx_M) >> a.rx_k);
-#else
-  return idx / a.RX;
-#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -484,18 +504,6 @@ __device__ __forceinline__ int div_rx(const KArgs& a, int idx) {
 // registers and 4 resident blocks; asking for 5 (region_kernel_mb) is 31 %
 // faster on the c5 8x8 points.  Smaller regions are left to ptxas (96
 // registers; an explicit minimum of 1 block would let it take 138).
-#ifndef ISR_MAGICDIV
-#define ISR_MAGICDIV 1
-#endif
-#ifndef ISR_HIST2
-#define ISR_HIST2 1    // per-axis (not per-edge) own-history writes
-#endif
-#ifndef ISR_SELAHEAD
-#define ISR_SELAHEAD 1  // select the next event's atom right after each refold (fold_select)
-#endif
-#ifndef ISR_FRESH
-#define ISR_FRESH 1  // a freshly loaded region's first pair and refold run in the shared step code
-#endif
 #ifndef ISR_NT
 #define ISR_NT 128
 #endif
@@ -514,16 +522,10 @@ struct StageT {
   double own_t[4][OWN ? NCO : 1][OWN ? NC : 1];
   uint32_t own_p[4][OWN ? NCO : 1][OWN ? NC : 1];
 };
-#ifndef ISR_LAZYPOS
-#define ISR_LAZYPOS 0  // 1: keep staged position words whole, extract the byte at its use
-#endif
 #ifndef ISR_CO
 #define ISR_CO ISR_CI  // staged own latest entries per edge
 #endif
 using Stage = StageT<NT, true, CI, ISR_CO>;
-#ifndef ISR_DEFER
-#define ISR_DEFER 0  // 1: diff the own histories at publish time in global memory (no own-history stage)
-#endif
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -545,7 +547,7 @@ struct Lane {
   unsigned obase;  // (r * K) * RX + c: own-edge history offset without the edge term
   M spins, gN, gS, gW, gE;
   double ts, R, V, lam, tc;
-  int site;       // ISR_SELAHEAD: atom of the next event on the current state
+  int site;       // atom of the next event on the current state (selected at the last refold)
   uint32_t n;
   unsigned long long dig;
   // incoming history cursors: cnt | idx << 8 | pos << 16 | source << 24
@@ -625,7 +627,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
     src[d] = 0;
     const bool axis_off = (d < 2) ? wrapY : wrapX;
     if (FIRST || a.first || axis_off) continue;
-    const bool ghost = a.world > 1 && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
+    const bool ghost = a.ghost && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
     if (ghost) {
       cnt[d] = (d == EDGE_N ? a.gh_up : a.gh_down).cnt[c];
       src[d] = d == EDGE_N ? 2u : 3u;
@@ -720,10 +722,6 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
       if (!(L.hm[d] & (1u << 28))) continue;
       const unsigned off = L.hoff[d];
       const uint8_t* P = src_p(a, (L.hm[d] >> 24) & 3u, d ^ 1);
-#if ISR_LAZYPOS
-      // staged position words stay whole: the byte is taken where it is used
-      L.hm[d] |= ((S.in_p[d][0][lane] >> byte_shift(P + off)) & 0xFFu) << 16;
-#else
 #pragma unroll
       for (int q = 0; q < SG::CIN; ++q)
         if (q < (int)(L.hm[d] & 0xFFu)) {
@@ -731,12 +729,10 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
           S.in_p[d][q][lane] = (S.in_p[d][q][lane] >> byte_shift(P + o)) & 0xFFu;
         }
       L.hm[d] |= S.in_p[d][0][lane] << 16;
-#endif
       L.ht[d] = S.in_t[d][0][lane];
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      if (ISR_LAZYPOS) break;
       if (!((L.om[e] >> 18) & 1u)) continue;
       const uint8_t* Ep = src_p(a, (L.om[e] >> 16) & 1u, e);
 #pragma unroll
@@ -751,14 +747,10 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   // pair n: U already spent into R (carried), V selects the next atom
   double U;
   draw_pair(a.seed, L.gid, L.n, U, L.V, a.gen);
-  if (a.fresh_w) L.R = expvar(U);  // the slate is wiped at t_c: the budget restarts from pair n
+  if (a.fresh_w) L.R = budget(a, U);  // the slate is wiped at t_c: the budget restarts from pair n
   Classes<G> C;
   C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
-#if ISR_SELAHEAD
   L.site = fold_select<G>(C, PT, a.rate, L.V, L.lam);
-#else
-  L.lam = fold_lambda<G>(C, PT);
-#endif
   L.tc = cand_time(L.ts, L.R, L.lam);
 }
 
@@ -777,11 +769,11 @@ __device__ __forceinline__ uint32_t neighbour_id(const KArgs& a, uint32_t gid, i
                      : (uint32_t)(gr * a.RX + winc(c, a.RX));
 }
 
-// DEFER: the entry-by-entry diff was not done while writing; compare the
-// new history (slot ps ^ 1) with the latest one (slot ps) here.
-template <class G, bool DEFER = false, bool OBS = false>
-__device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& changed, bool& overflow,
-                                            unsigned* n_cmp = nullptr) {
+// publish: selector word of the changed edges (the entry-by-entry diff was
+// taken while writing, hist_put), dirty bits of the neighbours across them,
+// and the tentative end-of-window state
+template <class G, bool OBS = false>
+__device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& changed, bool& overflow) {
   const int idx = L.idx;
   const int r = div_rx(a, idx), c = idx - r * a.RX;
   const unsigned K = a.it_K;
@@ -791,18 +783,7 @@ __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& ch
   for (int e = 0; e < 4; ++e) {
     const unsigned oc = L.om[e] & 0xFFu, pc = (L.om[e] >> 8) & 0xFFu, ps = (L.om[e] >> 16) & 1u;
     if ((int)oc > a.K) overflow = true;
-    bool diff = ((L.om[e] >> 17) & 1u) || oc != pc;
-    if (DEFER && !diff && oc > 0 && (int)oc <= a.K) {
-      const double* Tn = src_t(a, ps ^ 1u, e);
-      const double* To = src_t(a, ps, e);
-      const uint8_t* Pn = src_p(a, ps ^ 1u, e);
-      const uint8_t* Po = src_p(a, ps, e);
-      for (unsigned q = 0; q < oc && !diff; ++q) {
-        const unsigned o = L.obase + q * (unsigned)a.RX;
-        diff = __double_as_longlong(__ldcg(Tn + o)) != __double_as_longlong(__ldcg(To + o)) || Pn[o] != Po[o];
-      }
-      if (n_cmp) *n_cmp += oc;
-    }
+    const bool diff = ((L.om[e] >> 17) & 1u) || oc != pc;
     const unsigned slot = diff ? ps ^ 1u : ps;
     const unsigned cnt = diff ? ((int)oc < a.K ? oc : (unsigned)a.K) : pc;
     chmask |= (diff ? 1u : 0u) << e;
@@ -815,7 +796,7 @@ __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& ch
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       if (!((chmask >> e) & 1u)) continue;
-      if (a.world > 1 && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
+      if (a.ghost && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
       const int nr = e == EDGE_N ? wdec(r, a.RYl) : e == EDGE_S ? winc(r, a.RYl) : r;
       const int nc = e == EDGE_W ? wdec(c, a.RX) : e == EDGE_E ? winc(c, a.RX) : c;
       mark_dirty(a, nr * a.RX + nc, K + 1);
@@ -887,13 +868,7 @@ __device__ __forceinline__ void bp_pre2(const KArgs& a, Lane<G>& L, SG& S, int s
   if (nx < (hmd & 0xFFu)) {
     if (hmd & (1u << 28)) {
       tn = S.in_t[dstar][nx][lane];
-#if ISR_LAZYPOS
-      const unsigned hoffl = dstar == 0 ? L.hoff[0] : dstar == 1 ? L.hoff[1] : dstar == 2 ? L.hoff[2] : L.hoff[3];
-      pos = (S.in_p[dstar][nx][lane] >>
-             byte_shift(src_p(a, (hmd >> 24) & 3u, dstar ^ 1) + hoffl + nx * (unsigned)a.RX)) & 0xFFu;
-#else
       pos = S.in_p[dstar][nx][lane];
-#endif
     } else {
       const unsigned src = (hmd >> 24) & 3u;
       const unsigned hoff = dstar == 0 ? L.hoff[0] : dstar == 1 ? L.hoff[1] : dstar == 2 ? L.hoff[2] : L.hoff[3];
@@ -911,8 +886,7 @@ __device__ __forceinline__ void bp_pre2(const KArgs& a, Lane<G>& L, SG& S, int s
 }
 
 // one own-history entry on edge e (EDGE_*), diffed against the latest one
-// DEFER: no diff here (lane_finish compares the histories in global memory)
-template <bool DEFER, class SG>
+template <class SG>
 __device__ __forceinline__ unsigned hist_put(const KArgs& a, unsigned om, int e, unsigned obase, double tc, uint8_t p,
                                              const SG& S, int si, unsigned& n_out, bool& overflow) {
   const int lane = si;
@@ -926,14 +900,11 @@ __device__ __forceinline__ unsigned hist_put(const KArgs& a, unsigned om, int e,
     Tn[o] = tc;
     Pn[o] = p;
     ++n_out;
-    if (DEFER) {
-    } else if (!dv) {
+    if (!dv) {
       if (k >= pc) {
         dv = 1;
       } else if (SG::HAS_OWN && ((om >> 18) & 1u)) {
-        const unsigned pw = ISR_LAZYPOS ? (S.own_p[e][k][lane] >> byte_shift((ps ? a.ed[1].pos : a.ed[0].pos) +
-                                                                        e * a.tstride + o)) & 0xFFu
-                                        : S.own_p[e][k][lane];
+        const unsigned pw = S.own_p[e][k][lane];
         dv = (__double_as_longlong(S.own_t[e][k][lane]) != __double_as_longlong(tc) || pw != p)
                  ? 1u : 0u;
       } else {
@@ -950,21 +921,12 @@ __device__ __forceinline__ unsigned hist_put(const KArgs& a, unsigned om, int e,
 
 // own event at tc, up to (not including) the refold; draws the next pair
 // DRAW = false: leave drawing the next pair to the caller (shared code)
-template <class G, bool LOG, bool DEFER, class SG, bool DRAW = true>
+template <class G, bool LOG, class SG, bool DRAW = true>
 __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const ProdTable<G>& PT, int si,
                                         unsigned& n_out, bool& overflow) {
   constexpr int BX = G::BX, BY = G::BY;
   const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
-  int site;
-#if ISR_SELAHEAD
-  site = L.site;
-#else
-  {
-    Classes<G> C;
-    C.build(L.spins, L.gN, L.gS, L.gW, L.gE, wrapX, wrapY);
-    site = select_site2<G>(C, PT, a.rate, L.V, L.lam);
-  }
-#endif
+  const int site = L.site;
   L.spins ^= G::ONE << site;
   const int sr = site / BX, sc = site - sr * BX;
   if (a.digest) L.dig = digest_step(L.dig, L.tc, site);
@@ -973,20 +935,26 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const
     a.log_t[o] = L.tc;
     a.log_region[o] = L.gid;
     a.log_site[o] = (uint16_t)site;
-  } else if (ISR_HIST2 && BX > 1 && BY > 1) {
+  } else if (a.ev_t && (int)L.n_ev < a.evC) {  // scratch event log of this recomputation
+    const long long o = (long long)L.n_ev * a.ev_stride + L.idx;
+    a.ev_t[o] = L.tc;
+    a.ev_s[o] = (uint16_t)site;
+  }
+  if (LOG) {
+  } else if (BX > 1 && BY > 1) {
     // a site lies on at most one vertical (N/S) and one horizontal (W/E) edge
     const bool onV = !wrapY && (sr == 0 || sr == BY - 1);
     const bool onH = !wrapX && (sc == 0 || sc == BX - 1);
     if (onV) {
       const bool n = sr == 0;
-      const unsigned om = hist_put<DEFER>(a, n ? L.om[EDGE_N] : L.om[EDGE_S], n ? EDGE_N : EDGE_S, L.obase, L.tc,
+      const unsigned om = hist_put(a, n ? L.om[EDGE_N] : L.om[EDGE_S], n ? EDGE_N : EDGE_S, L.obase, L.tc,
                                    (uint8_t)sc, S, si, n_out, overflow);
       L.om[EDGE_N] = n ? om : L.om[EDGE_N];
       L.om[EDGE_S] = n ? L.om[EDGE_S] : om;
     }
     if (onH) {
       const bool w = sc == 0;
-      const unsigned om = hist_put<DEFER>(a, w ? L.om[EDGE_W] : L.om[EDGE_E], w ? EDGE_W : EDGE_E, L.obase, L.tc,
+      const unsigned om = hist_put(a, w ? L.om[EDGE_W] : L.om[EDGE_E], w ? EDGE_W : EDGE_E, L.obase, L.tc,
                                    (uint8_t)sr, S, si, n_out, overflow);
       L.om[EDGE_W] = w ? om : L.om[EDGE_W];
       L.om[EDGE_E] = w ? L.om[EDGE_E] : om;
@@ -1002,7 +970,7 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const
                                   : (!wrapX && sc == BX - 1);
       if (!on) continue;
       on_edge = true;
-      L.om[e] = hist_put<DEFER>(a, L.om[e], e, L.obase, L.tc, (uint8_t)(e < 2 ? sc : sr), S, si, n_out, overflow);
+      L.om[e] = hist_put(a, L.om[e], e, L.obase, L.tc, (uint8_t)(e < 2 ? sc : sr), S, si, n_out, overflow);
     }
     L.bev += on_edge ? 1u : 0u;
   }
@@ -1012,54 +980,43 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const
   if (!DRAW) return;
   double U;
   draw_pair(a.seed, L.gid, L.n, U, L.V, a.gen);
-  L.R = expvar(U);
+  L.R = budget(a, U);
 }
 
 template <class G>
 __device__ __forceinline__ void refold(const KArgs& a, Lane<G>& L, const ProdTable<G>& PT) {
   Classes<G> C;
   C.build(L.spins, L.gN, L.gS, L.gW, L.gE, a.RX == 1, a.RYg == 1);
-#if ISR_SELAHEAD
   L.site = fold_select<G>(C, PT, a.rate, L.V, L.lam);
-#else
-  L.lam = fold_lambda<G>(C, PT);
-#endif
   L.tc = cand_time(L.ts, L.R, L.lam);
 }
 
-// GQ (persistent launch): the worklist is one global queue (a.work_ctr) and
-// its length is read on the device; otherwise each block owns a static tile.
-template <int BX, int BY, bool LOG, bool GQ, bool OBS, bool FIRST>
+// Lane-persistent scheduling over a static tile of the worklist per block.
+// n_work_dev (pipelined launch): the worklist length is read on the device;
+// the grid was sized for an upper bound, and the tile grows if the bound was
+// short.
+template <int BX, int BY, bool LOG, bool OBS, bool FIRST>
 __device__ __forceinline__ void region_body(const KArgs& a) {
   using G = Geo<BX, BY>;
   __shared__ unsigned q_next;
   // the first iteration stages nothing (no incoming histories, no latest own
-  // history in this window): a minimal stage frees shared memory for a sixth
-  // resident block
-  constexpr bool DEFER = ISR_DEFER && !FIRST;
-  using SG = typename std::conditional<FIRST, StageT<NT, false, 1>,
-                                       typename std::conditional<DEFER, StageT<NT, false>, Stage>::type>::type;
+  // history in this window): a minimal stage frees shared memory for more
+  // resident blocks
+  using SG = typename std::conditional<FIRST, StageT<NT, false, 1>, Stage>::type;
   __shared__ SG S;
   __shared__ ProdTable<G> PT;
-  // work: a static tile per block (lanes take items from a block queue), or
-  // (work_ctr set) the whole worklist as a global queue served to a
-  // persistent grid in per-warp chunks, its length read on the device
-  constexpr bool global_q = GQ;
-  // n_work_dev (pipelined launch): the worklist length is read here; the grid
-  // was sized for an upper bound, and the tile grows if the bound was short
-  const int n_all = GQ && a.n_work_dev ? (int)__ldcg(a.n_work_dev) : a.n_work;
   // the block's tile (block-uniform, kept in shared memory)
   __shared__ int s_tile_begin, s_tile_n;
   if (threadIdx.x == 0) {
-    int tile = a.tile, n = n_all;
-    if (!GQ && a.n_work_dev) {  // the host's tile rule (tile_for) on the actual length, >= n / grid
+    int tile = a.tile, n = a.n_work;
+    if (a.n_work_dev) {  // the host's tile rule (tile_for) on the actual length, >= n / grid
       n = (int)__ldcg(a.n_work_dev);
       const int per = max(1, min(8, n / (NT * 148 * 4)));
       const int need = (n + (int)gridDim.x - 1) / (int)gridDim.x;
       tile = max(NT * per, (need + NT - 1) / NT * NT);
     }
-    s_tile_begin = global_q ? 0 : blockIdx.x * tile;
-    s_tile_n = global_q ? n : min(tile, n - (int)(blockIdx.x * tile));
+    s_tile_begin = blockIdx.x * tile;
+    s_tile_n = min(tile, n - (int)(blockIdx.x * tile));
     q_next = blockDim.x;  // the first blockDim items are taken statically
   }
   fill_prod<G>(PT, a.rate);
@@ -1073,50 +1030,22 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
   // together, so the (memory-heavy) load/publish path runs converged.
   const int REFILL = a.refill;
   bool active = false, pending = false, exhausted = false, fresh = false;
-  int item = global_q ? -1 : (int)threadIdx.x;
-  const unsigned lane_lt = (1u << (threadIdx.x & 31)) - 1u;
-  constexpr int CHUNK = 256;        // items per global-queue claim of a warp
-  int wc_cur = 0, wc_end = 0;       // the warp's current chunk (warp-uniform)
-  bool wq_done = !global_q;         // global queue exhausted for this warp
+  int item = (int)threadIdx.x;
   for (;;) {
     const unsigned idle = __ballot_sync(0xffffffffu, !active);
     if (__popc(idle) >= REFILL || idle == 0xffffffffu) {
-      if (global_q) {
-        // deal the next items of the warp's chunk to the idle lanes, claiming
-        // new chunks from the global queue as needed (warp-uniform)
-        unsigned rem = __ballot_sync(0xffffffffu, !active && !exhausted);
-        while (rem && !wq_done) {
-          if (wc_cur >= wc_end) {
-            unsigned b = 0;
-            if ((threadIdx.x & 31) == 0) b = atomicAdd(a.work_ctr, (unsigned)CHUNK);
-            b = __shfl_sync(0xffffffffu, b, 0);
-            if ((int)b >= n_all) {
-              wq_done = true;
-              break;
-            }
-            wc_cur = (int)b;
-            wc_end = min((int)b + CHUNK, n_all);
-          }
-          const int take = min(__popc(rem), wc_end - wc_cur);
-          const int rank = __popc(rem & lane_lt);
-          const bool mine = ((rem >> (threadIdx.x & 31)) & 1u) && rank < take;
-          if (mine) item = wc_cur + rank;
-          rem &= ~__ballot_sync(0xffffffffu, mine);
-          wc_cur += take;
-        }
-      }
       if (!active) {
         if (pending) {
-          if (!LOG) lane_finish<G, DEFER, OBS>(a, L, changed, overflow);
+          if (!LOG) lane_finish<G, OBS>(a, L, changed, overflow);
           n_ev += L.n_ev;
           n_bev = max(n_bev, L.bev);
           pending = false;
         }
         if (!exhausted) {
-          if (item < 0 && !global_q) item = (int)atomicAdd(&q_next, 1u);
-          if (item >= 0 && item < s_tile_n) {
+          if (item < 0) item = (int)atomicAdd(&q_next, 1u);
+          if (item < s_tile_n) {
             const int idx = a.wl_in ? (int)a.wl_in[s_tile_begin + item] : s_tile_begin + item;
-            lane_load<G, LOG, SG, !ISR_FRESH, OBS, FIRST>(a, L, idx, S, PT, threadIdx.x);
+            lane_load<G, LOG, SG, false, OBS, FIRST>(a, L, idx, S, PT, threadIdx.x);
             fresh = true;
             n_in += (L.hm[0] & 0xFFu) + (L.hm[1] & 0xFFu) + (L.hm[2] & 0xFFu) + (L.hm[3] & 0xFFu);
             n_cmp += ((L.om[0] >> 8) & 0xFFu) + ((L.om[1] >> 8) & 0xFFu) + ((L.om[2] >> 8) & 0xFFu) +
@@ -1134,9 +1063,8 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
     if (active) {
       // one step per round: the earliest of (next break point, own event);
       // a region loaded in this round only draws its pair and refolds
-      constexpr bool SHARE = ISR_FRESH;
       bool go = true, ev = false;
-      if (!SHARE || !fresh) {
+      if (!fresh) {
         double tb = 0.0;
         const int d = FIRST ? -1 : next_bp2<G>(a, L, tb);  // no break points in the first iteration
         if (d < 0 && !(L.tc < a.t_w)) {
@@ -1147,17 +1075,17 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
           bp_pre2<G>(a, L, S, threadIdx.x, d, tb);
         } else {
           if (OBS && !LOG) obs_advance<G>(L, L.tc);
-          ev_pre2<G, LOG, DEFER, SG, !SHARE>(a, L, S, PT, threadIdx.x, n_out, overflow);
+          ev_pre2<G, LOG, SG, false>(a, L, S, PT, threadIdx.x, n_out, overflow);
           ev = true;
         }
       }
       if (go) {
         if (OBS && !LOG && !fresh)  // M and B after the step
           obs_counts<G>(L.spins, L.gN, L.gW, a.RX == 1, a.RYg == 1, L.Mi, L.Bi);
-        if (SHARE && (ev || fresh)) {  // pair n: V picks the next atom, E(U) its budget
+        if (ev || fresh) {  // pair n: V picks the next atom, E(U) its budget
           double U;
           draw_pair(a.seed, L.gid, L.n, U, L.V, a.gen);
-          if (ev || a.fresh_w) L.R = expvar(U);  // (fresh_w: a loaded region restarts its budget at t_c)
+          if (ev || a.fresh_w) L.R = budget(a, U);  // (fresh_w: a loaded region restarts its budget at t_c)
         }
         refold<G>(a, L, PT);  // shared by both kinds of step
       }
@@ -1166,6 +1094,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
   }
 
   if (!LOG) {
+    if (a.delay_ns) k1_delay(a.delay_ns);
     // warp-aggregated flags and counters (one atomic per warp)
     const unsigned full = 0xffffffffu;
     const unsigned anych = __ballot_sync(full, changed);
@@ -1201,16 +1130,16 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
 #else
 #define ISR_K1_BOUNDS __launch_bounds__(NT)
 #endif
-template <int BX, int BY, bool LOG, bool GQ = false, bool OBS = false, bool FIRST = false>
+template <int BX, int BY, bool LOG, bool OBS = false, bool FIRST = false>
 __global__ void ISR_K1_BOUNDS region_kernel(const KArgs a) {
-  region_body<BX, BY, LOG, GQ, OBS, FIRST>(a);
+  region_body<BX, BY, LOG, OBS, FIRST>(a);
 }
 #ifndef ISR_MB_MINB
 #define ISR_MB_MINB 5
 #endif
-template <int BX, int BY, bool LOG, bool GQ = false, bool OBS = false, bool FIRST = false>
+template <int BX, int BY, bool LOG, bool OBS = false, bool FIRST = false>
 __global__ void __launch_bounds__(NT, ISR_MB_MINB) region_kernel_mb(const KArgs a) {
-  region_body<BX, BY, LOG, GQ, OBS, FIRST>(a);
+  region_body<BX, BY, LOG, OBS, FIRST>(a);
 }
 // the window's first iteration (≤ 32-site regions): no staging, so shared
 // memory no longer caps the resident blocks; ISR_FIRST_MINB asks ptxas for
@@ -1225,7 +1154,7 @@ __global__ void __launch_bounds__(NT, ISR_MB_MINB) region_kernel_mb(const KArgs 
 #endif
 template <int BX, int BY, bool OBS = false>
 __global__ void ISR_FIRST_BOUNDS region_kernel_first(const KArgs a) {
-  region_body<BX, BY, false, false, OBS, true>(a);
+  region_body<BX, BY, false, OBS, true>(a);
 }
 
 // ---------------------------------------------------------------------------
@@ -1327,7 +1256,7 @@ __global__ void __launch_bounds__(256) compact_kernel(uint32_t* bm, int nwords, 
 // ---------------------------------------------------------------------------
 template <int BX, int BY>
 __global__ void init_kernel(const uint8_t* buf, int Lx, int RX, int RYl, int row0, unsigned long long seed,
-                            StateView st) {
+                            double eq_q, StateView st) {
   using G = Geo<BX, BY>;
   using M = typename G::M;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1352,7 +1281,7 @@ __global__ void init_kernel(const uint8_t* buf, int Lx, int RX, int RYl, int row
   double U, V;
   draw_pair(seed, (uint32_t)((row0 + r) * RX + c), 0u, U, V);
   st.ts[idx] = 0.0;
-  st.R[idx] = expvar(U);
+  st.R[idx] = quantize_budget(expvar(U), eq_q);
   st.n[idx] = 0;
   st.dig[idx] = 0ull;
 }

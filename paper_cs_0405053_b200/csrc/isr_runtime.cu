@@ -2,10 +2,11 @@
 //
 // Drives the synchronous-relaxation loop of the paper: for each
 // window ("step") it launches the region-trajectory kernel once per
-// relaxation iteration, exchanges strip halos through the caller's
-// transport (world > 1), reads the global {changed, overflow} flag, and on
-// convergence commits the window by swapping the committed and tentative
-// state buffers.  Device memory layout: DESIGN.md §5.
+// relaxation iteration, exchanges strip halos (world > 1: NCCL send/recv on
+// its own stream, or the caller's transport), all-reduces the global
+// {changed, overflow} flag, and on convergence commits the window by
+// swapping the committed and tentative state buffers and compacting the
+// event log.  Device memory layout: DESIGN.md §5.
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys / ncu --nvtx
 
@@ -21,8 +22,8 @@
 #include "../../include/ising_sr.h"
 #include "isr_region.cuh"
 #include "isr_warp.cuh"
-#include "isr_pool.cuh"
 #include "isr_big.cuh"
+#include "isr_nccl.h"
 
 namespace {
 
@@ -38,7 +39,6 @@ using isr::KArgs;
 using isr::StateView;
 
 constexpr int kThreads = isr::NT;  // K1 block (and the small kernels')
-constexpr int kBatch = 8;  // max iterations in flight per host sync
 
 // ---------------------------------------------------------------------------
 // per-shape kernel table (lane-per-region forms)
@@ -51,11 +51,8 @@ struct ShapeOps {
   int cnt_max;       // largest history length the selector can record
   double sel_read_bytes;  // selector bytes read per recomputation (own + neighbours)
   void (*region)(const KArgs&, int nreg, cudaStream_t);
-  void (*region_pool)(const KArgs&, int nreg, cudaStream_t);  // slot-pool form (lane shapes), or null
-  void (*region_pool_persistent)(const KArgs&, cudaStream_t);  // same, one resident grid, global queue
-  void (*region_persistent)(const KArgs&, cudaStream_t);       // lane K1, one resident grid, global queue
-  void (*replay)(const KArgs&, int nreg, cudaStream_t);
-  void (*init)(const uint8_t*, int, int, int, int, unsigned long long, StateView, cudaStream_t);
+  void (*replay)(const KArgs&, int nreg, cudaStream_t);  // LOG = true: writes the compact log of the listed regions
+  void (*init)(const uint8_t*, int, int, int, int, unsigned long long, double, StateView, cudaStream_t);
   void (*unpack)(StateView, int, int, int, uint8_t*, cudaStream_t);
   void (*pack)(const KArgs&, GhostView, GhostView, int RX, cudaStream_t);
   void (*snap)(StateView, int n, int RX, int RYg, unsigned long long* out, cudaStream_t);  // M, B of a state
@@ -80,14 +77,14 @@ ShapeOps make_ops() {
     // iteration (no incoming histories: break-point and staging code compiled out)
     if (a.obs) {
       if (a.first) {
-        if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, true, true><<<grid, kThreads, 0, s>>>(a);
+        if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, true, true><<<grid, kThreads, 0, s>>>(a);
         else isr::region_kernel_first<BX, BY, true><<<grid, kThreads, 0, s>>>(a);
       } else {
-        if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, true><<<grid, kThreads, 0, s>>>(a);
-        else isr::region_kernel<BX, BY, false, false, true><<<grid, kThreads, 0, s>>>(a);
+        if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, true><<<grid, kThreads, 0, s>>>(a);
+        else isr::region_kernel<BX, BY, false, true><<<grid, kThreads, 0, s>>>(a);
       }
     } else if (a.first) {
-      if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, false, true><<<grid, kThreads, 0, s>>>(a);
+      if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, true><<<grid, kThreads, 0, s>>>(a);
       else isr::region_kernel_first<BX, BY><<<grid, kThreads, 0, s>>>(a);
     } else {
       if constexpr (kMB) isr::region_kernel_mb<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
@@ -99,46 +96,11 @@ ShapeOps make_ops() {
     if constexpr (kMB) isr::region_kernel_mb<BX, BY, true><<<grid, kThreads, 0, s>>>(a);
     else isr::region_kernel<BX, BY, true><<<grid, kThreads, 0, s>>>(a);
   };
-  o.region_pool = [](const KArgs& a, int n, cudaStream_t s) {
-    constexpr int S = ISR_POOL_S;
-    constexpr size_t bytes = isr::pool_smem_bytes<G, S>();
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(isr::region_kernel_pool<BX, BY, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-      attr = true;
-    }
-    const int grid = (n + a.tile - 1) / a.tile;
-    isr::region_kernel_pool<BX, BY, S><<<grid, isr::PW * 32, bytes, s>>>(a);
-  };
-  o.region_persistent = [](const KArgs& a, cudaStream_t s) {
-    static int grid = 0;
-    if (!grid) {
-      int dev = 0, sms = 148, per = 1;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, isr::region_kernel<BX, BY, false, true>, kThreads, 0);
-      grid = sms * std::max(per, 1);
-    }
-    isr::region_kernel<BX, BY, false, true><<<grid, kThreads, 0, s>>>(a);
-  };
-  o.region_pool_persistent = [](const KArgs& a, cudaStream_t s) {
-    constexpr int S = ISR_POOL_S;
-    constexpr size_t bytes = isr::pool_smem_bytes<G, S>();
-    static int grid = 0;
-    if (!grid) {
-      cudaFuncSetAttribute(isr::region_kernel_pool<BX, BY, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-      int dev = 0, sms = 148, per = 1;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, isr::region_kernel_pool<BX, BY, S>, isr::PW * 32, bytes);
-      grid = sms * std::max(per, 1);
-    }
-    isr::region_kernel_pool<BX, BY, S><<<grid, isr::PW * 32, bytes, s>>>(a);
-  };
-  o.init = [](const uint8_t* buf, int Lx, int RX, int RYl, int row0, unsigned long long seed, StateView st,
-              cudaStream_t s) {
+  o.init = [](const uint8_t* buf, int Lx, int RX, int RYl, int row0, unsigned long long seed, double eq_q,
+              StateView st, cudaStream_t s) {
     const int n = RX * RYl;
-    isr::init_kernel<BX, BY><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(buf, Lx, RX, RYl, row0, seed, st);
+    isr::init_kernel<BX, BY><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(buf, Lx, RX, RYl, row0, seed, eq_q,
+                                                                                st);
   };
   o.unpack = [](StateView st, int Lx, int RX, int RYl, uint8_t* out, cudaStream_t s) {
     const long long n = (long long)RYl * BY * Lx;
@@ -171,20 +133,7 @@ ShapeOps make_ops_w() {
   o.halo_bytes = 16;
   o.sel_words = 8;
   o.cnt_max = 65535;
-  o.region_pool = nullptr;
-  o.region_pool_persistent = nullptr;
-  // one resident grid striding over the worklist, its length read on the device
-  o.region_persistent = [](const KArgs& a, cudaStream_t s) {
-    if (big_enabled()) isr::region_kernel_big<BX, BY, false><<<148 * 8, isr::BNT, 0, s>>>(a);
-    else isr::region_kernel_w<BX, BY, false><<<148 * 16, kThreads, 0, s>>>(a);
-  };
   o.sel_read_bytes = 8 * 16.0;
-  auto launch = [](const KArgs& a, int n, cudaStream_t s, bool log) {
-    const int warps_per_block = kThreads / 32;
-    const int grid = std::max(1, std::min((n + warps_per_block - 1) / warps_per_block, 148 * 16));
-    if (log) isr::region_kernel_w<BX, BY, true><<<grid, kThreads, 0, s>>>(a);
-    else isr::region_kernel_w<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
-  };
   // lane-per-region K1 for big regions (isr_big.cuh); ISING_SR_BIG=0: warp form
   o.region = [](const KArgs& a, int n, cudaStream_t s) {
     if (big_enabled()) {
@@ -205,11 +154,11 @@ ShapeOps make_ops_w() {
       isr::region_kernel_w<BX, BY, true><<<grid, kThreads, 0, s>>>(a);
     }
   };
-  (void)launch;
-  o.init = [](const uint8_t* buf, int Lx, int RX, int RYl, int row0, unsigned long long seed, StateView st,
-              cudaStream_t s) {
+  o.init = [](const uint8_t* buf, int Lx, int RX, int RYl, int row0, unsigned long long seed, double eq_q,
+              StateView st, cudaStream_t s) {
     const int n = RX * RYl;
-    isr::init_kernel_w<BX, BY><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(buf, Lx, RX, RYl, row0, seed, st);
+    isr::init_kernel_w<BX, BY><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(buf, Lx, RX, RYl, row0, seed,
+                                                                                  eq_q, st);
   };
   o.unpack = [](StateView st, int Lx, int RX, int RYl, uint8_t* out, cudaStream_t s) {
     const long long n = (long long)RYl * BY * Lx;
@@ -354,6 +303,69 @@ __global__ void scan_apply(const uint32_t* n1, const uint32_t* n0, int N, const 
   if (i < N) off[i] = bsum[blockIdx.x] + sh[w] + x - v;
 }
 
+// K3 (commit, FLAG_LOG_EVENTS): compact the window's event log -- time,
+// global region id, local site, ordered by region then time -- from the
+// scratch log K1 wrote in each region's final recomputation (event q of
+// region i at ev[q * stride + i], q < C).  A region with more than C events
+// is appended to `replay` (its log is rewritten there by a K1 replay).
+__global__ void __launch_bounds__(256) compact_log_kernel(const uint32_t* n1, const uint32_t* n0, int N,
+                                                          const unsigned long long* off, const double* ev_t,
+                                                          const uint16_t* ev_s, long long stride, int C, int RX,
+                                                          int row0, double* log_t, uint32_t* log_region,
+                                                          uint16_t* log_site, uint32_t* replay, unsigned* n_replay) {
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i >= N) return;
+  const unsigned e = n1[i] - n0[i];
+  if (e == 0) return;
+  if ((int)e > C) {
+    replay[atomicAdd(n_replay, 1u)] = (uint32_t)i;
+    return;
+  }
+  const unsigned long long o = off[i];
+  const int r = i / RX;
+  const uint32_t gid = (uint32_t)((row0 + r) * RX + (i - r * RX));
+  for (unsigned q = 0; q < e; ++q) {
+    log_t[o + q] = ev_t[(long long)q * stride + i];
+    log_region[o + q] = gid;
+    log_site[o + q] = ev_s[(long long)q * stride + i];
+  }
+}
+
+// h of SURVEY §8(d.3): boundary-history entries of the window's fixed point,
+// one per region edge (N, S, W, E; not along an axis the region wraps) that
+// the site of each committed event lies on
+__global__ void __launch_bounds__(256) count_edge_entries(const uint16_t* site, const unsigned long long* n_total,
+                                                          int bx, int by, int wrapX, int wrapY,
+                                                          unsigned long long* out) {
+  const unsigned long long n = *n_total;
+  unsigned long long v = 0;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * 256 + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * 256) {
+    const int st = site[i], sr = st / bx, sc = st - sr * bx;
+    v += (!wrapY && sr == 0) + (!wrapY && sr == by - 1) + (!wrapX && sc == 0) + (!wrapX && sc == bx - 1);
+  }
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
+}
+
+// Initial spins from the Philox init stream for the rows
+// the init kernel reads: row q of buf is lattice row (y_first + q) mod Ly;
+// site v is up iff bit (v & 31) of word ((v >> 5) & 3) of Philox4x32-10 with
+// key (0xFFFFFFFF, seed_lo) and counter (v >> 7, 0, 1, seed_hi) is set.
+__global__ void __launch_bounds__(256) philox_spins_kernel(uint8_t* buf, int rows, int y_first, int Lx, int Ly,
+                                                           unsigned long long seed) {
+  const long long i = (long long)blockIdx.x * 256 + threadIdx.x;
+  if (i >= (long long)rows * Lx) return;
+  const int q = (int)(i / Lx), x = (int)(i - (long long)q * Lx);
+  const int y = ((y_first + q) % Ly + Ly) % Ly;
+  const unsigned long long v = (unsigned long long)y * (unsigned long long)Lx + (unsigned long long)x;
+  const isr::U4 c{(uint32_t)(v >> 7), 0u, 1u, (uint32_t)(seed >> 32)};
+  const isr::U4 w = isr::philox4x32_10(c, 0xFFFFFFFFu, (uint32_t)seed);
+  const int k = (int)((v >> 5) & 3);
+  const uint32_t word = k == 0 ? w.x : k == 1 ? w.y : k == 2 ? w.z : w.w;
+  buf[i] = (uint8_t)((word >> (v & 31)) & 1u);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -396,12 +408,25 @@ struct ising_sr_ctx {
   GhostView gsend[2] = {}, grecv[2] = {};  // [0] = up, [1] = down  (world > 1)
   void* gbuf = nullptr;
   size_t gchunk[4] = {0, 0, 0, 0};
-  int* d_flags = nullptr;                 // [kBatch][4] (one slot per iteration in flight)
-  unsigned long long* d_stats = nullptr;  // [kBatch][8]
-  unsigned* d_wctr = nullptr;             // [kBatch] global work-queue counters
+  int* d_flags = nullptr;                 // [4] flags of the step-level loop
+  unsigned long long* d_stats = nullptr;  // [8]
   int* h_flags = nullptr;                 // pinned mirror
   unsigned long long* h_stats = nullptr;  // pinned mirror
   unsigned* h_wlc = nullptr;              // pinned mirror [2]
+  // strip exchange (world > 1 or FLAG_HALO_LOOPBACK)
+  bool ghost = false;
+  size_t grow = 0;                        // bytes of one ghost row (4 chunks, contiguous)
+  isr_nccl::Comm nccl = nullptr;          // the library's communicator (cfg.nccl_id)
+  // scratch event log of K1 (FLAG_LOG_EVENTS) and the commit's replay list
+  double* ev_t = nullptr;
+  uint16_t* ev_s = nullptr;
+  int evC = 0;
+  uint32_t* d_replay = nullptr;
+  unsigned* d_nrep = nullptr;             // [0] replayed regions, [2..3] edge entries (u64)
+  unsigned h_nrep = 0;
+  unsigned long long* d_edges = nullptr;
+  unsigned long long h_edges = 0;
+  cudaEvent_t cev0 = nullptr, cev1 = nullptr;  // around the commit's compaction
   // log
   double* log_t = nullptr;
   uint32_t* log_region = nullptr;
@@ -416,11 +441,7 @@ struct ising_sr_ctx {
   unsigned long long h_snap[2] = {0ull, 0ull};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t kev0 = nullptr, kev1 = nullptr;  // around each region-kernel launch
-  cudaEvent_t bev[2 * 8] = {};                 // batched iterations: around launch j (2j, 2j+1)
-  int batch = 1;  // iterations enqueued per host sync (world == 1; env ISING_SR_BATCH; measured: 1 is fastest)
-  int tail_batch = 1;      // ... once fewer than tail_n regions are left (env ISING_SR_TAIL_BATCH; measured
-                           // slower on c4 and c5, so off: the persistent grid costs more than the syncs)
-  int tail_n = 1 << 15;    // env ISING_SR_TAIL_N
+  cudaEvent_t bev[4] = {};                     // pipelined iterations: around launch j (2j, 2j+1)
 
   // window state
   long long w = 0;
@@ -437,13 +458,12 @@ struct ising_sr_ctx {
   double win_bytes = 0.0;
   int win_f = 0;
   long long launches = 0;
-  int pipeline = 1;  // world == 1: one iteration enqueued ahead of the flag check (env ISING_SR_PIPELINE)
+  int pipeline = 1;  // one iteration enqueued ahead of the flag check (env ISING_SR_PIPELINE=0: off)
   cudaEvent_t pev[2] = {};  // pipelined: results of the iteration with stamp parity j copied to the host
   IterSlot* d_slot = nullptr;  // [2]
   IterSlot* h_slot = nullptr;  // pinned mirror [2]
+  unsigned delay_ns = 0;  // test knob (env ISING_SR_K1_DELAY_NS): K1 publishes late
   int refill = 28;  // K1 batched-refill threshold (env ISING_SR_REFILL; 28 measured best after the shared fresh-load step)
-  bool pool = false;    // slot-pool K1 for lane shapes (env ISING_SR_POOL=1; measured slower so far)
-  int pool_refill = ISR_POOL_S / 2;  // free slots that trigger a pool refill (env ISING_SR_POOL_REFILL)
   ising_sr_stats stats;
 };
 
@@ -495,9 +515,10 @@ void free_edges(ising_sr_ctx* c) {
   }
 }
 
-// Boundary-history slots sized for K entries per region edge, plus (world > 1)
-// four ghost rows: send up/down and receive from up/down, each laid out as
-// cnt[RX] | stamp[RX] | t[K][RX] | pos[K][RX] (the exchange chunks).
+// Boundary-history slots sized for K entries per region edge, plus (world > 1
+// or halo loopback) four ghost rows: send up/down and receive from up/down,
+// each laid out as cnt[RX] | stamp[RX] | t[K][RX] | pos[K][RX] (the exchange
+// chunks, 256-byte aligned, one contiguous row of c->grow bytes).
 ising_sr_status alloc_edges(ising_sr_ctx* c, int K) {
   free_edges(c);
   c->K = K;
@@ -511,7 +532,7 @@ ising_sr_status alloc_edges(ising_sr_ctx* c, int K) {
       return ISING_SR_E_OOM;
     }
   }
-  if (c->cfg.world > 1) {
+  if (c->ghost) {
     const size_t RX = (size_t)c->RX;
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     c->gchunk[0] = RX * 2;
@@ -519,6 +540,7 @@ ising_sr_status alloc_edges(ising_sr_ctx* c, int K) {
     c->gchunk[2] = RX * (size_t)K * 8;
     c->gchunk[3] = RX * (size_t)K;
     const size_t one = al(c->gchunk[0]) + al(c->gchunk[1]) + al(c->gchunk[2]) + al(c->gchunk[3]);
+    c->grow = one;
     if (dmalloc_bytes(c, (void**)&c->gbuf, 4 * one) != cudaSuccess) {
       cudaGetLastError();
       free_edges(c);
@@ -566,14 +588,6 @@ int tile_for(int n) {
   return kThreads * per;
 }
 
-// slot-pool K1: a block holds PW * S regions at a time; >= 2 blocks' worth of
-// tiles per SM slot (3 resident blocks), at most 32 pool generations per tile
-int tile_for_pool(int n) {
-  const int slots = isr::PW * ISR_POOL_S;
-  const int per = std::max(1, std::min(32, n / (slots * 148 * 3 * 2)));
-  return slots * per;
-}
-
 KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   KArgs a;
   std::memset(&a, 0, sizeof a);
@@ -589,6 +603,12 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   a.RYg = c->RYg;
   a.row0 = c->row0;
   a.world = c->cfg.world;
+  a.ghost = c->ghost ? 1 : 0;
+  a.eq_q = c->cfg.eq_quantum;
+  a.ev_t = c->ev_t;
+  a.ev_s = c->ev_s;
+  a.evC = c->evC;
+  a.ev_stride = c->nreg;
   a.K = c->K;
   a.tstride = (long long)c->RYl * c->K * c->RX;
   a.it_K = K;
@@ -610,6 +630,7 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   a.LC = c->LC;
   a.resume = (c->resume && c->lg_meta) ? 1 : 0;
   a.refill = c->refill;
+  a.delay_ns = c->delay_ns;
   {
     // magic division by RX: k = 31 + ceil(log2 RX), M = ceil(2^k / RX) < 2^32;
     // exact for every index below 2^31 (M * RX - 2^k < RX <= 2^(k - 31))
@@ -657,20 +678,17 @@ ising_sr_status launch_iteration(ising_sr_ctx* c) {
   KArgs a = base_args(c, K, first);
   a.wl_in = all ? nullptr : c->wl[K & 1];
   a.n_work = nw;
-  const bool pool = c->pool && c->ops->region_pool;
-  a.tile = pool ? tile_for_pool(nw) : tile_for(nw);
-  if (pool) a.refill = c->pool_refill;
+  a.tile = tile_for(nw);
   a.wl_out = c->wl[(K + 1) & 1];
   a.wl_out_count = c->d_wlc + ((K + 1) & 1);
   CK(c, cudaEventRecord(c->kev0, c->stream));
   if (nw > 0) {
-    if (pool) c->ops->region_pool(a, nw, c->stream);
-    else c->ops->region(a, nw, c->stream);
+    c->ops->region(a, nw, c->stream);
     ++c->launches;
     CK(c, cudaGetLastError());
   }
   CK(c, cudaEventRecord(c->kev1, c->stream));
-  if (c->cfg.world > 1) {
+  if (c->ghost) {
     c->ops->pack(a, c->gsend[0], c->gsend[1], c->RX, c->stream);
     ++c->launches;
     CK(c, cudaGetLastError());
@@ -681,7 +699,7 @@ ising_sr_status launch_iteration(ising_sr_ctx* c) {
 }
 
 ising_sr_status mark_ghosts(ising_sr_ctx* c) {
-  if (c->cfg.world <= 1) return ISING_SR_OK;
+  if (!c->ghost) return ISING_SR_OK;
   const unsigned K = c->Kglob;
   KArgs a = base_args(c, K, c->it == 1);
   a.wl_out = c->wl[(K + 1) & 1];
@@ -735,6 +753,51 @@ void fill_halo(ising_sr_ctx* c, ising_sr_halo* h) {
   }
   h->flags = c->d_flags;
   h->stream = (void*)c->stream;
+  h->row_bytes = c->grow;
+}
+
+// C1 + C2 of one iteration on the ctx stream: my first row's
+// north-edge histories to rank - 1 and my last row's south-edge histories to
+// rank + 1 (periodic), the neighbours' into my ghost rows, in one NCCL group;
+// then all-reduce(max) of the iteration's {changed, overflow}.  Per peer the
+// sends and receives are matched in issue order (send up, send down; receive
+// from down, receive from up), which pairs them correctly for world 1 (the
+// loopback to itself), 2 (both neighbours are the other rank) and more.
+ising_sr_status nccl_exchange(ising_sr_ctx* c, int* flags) {
+  const isr_nccl::Api& A = isr_nccl::api();
+  const int W = c->cfg.world, q = c->cfg.rank;
+  const int up = (q + W - 1) % W, down = (q + 1) % W;
+  bool ok = isr_nccl::report(A.GroupStart(), "ncclGroupStart");
+  ok = ok && isr_nccl::report(A.Send(c->gsend[0].cnt, c->grow, isr_nccl::kInt8, up, c->nccl, c->stream), "ncclSend");
+  ok = ok && isr_nccl::report(A.Send(c->gsend[1].cnt, c->grow, isr_nccl::kInt8, down, c->nccl, c->stream), "ncclSend");
+  ok = ok && isr_nccl::report(A.Recv(c->grecv[1].cnt, c->grow, isr_nccl::kInt8, down, c->nccl, c->stream), "ncclRecv");
+  ok = ok && isr_nccl::report(A.Recv(c->grecv[0].cnt, c->grow, isr_nccl::kInt8, up, c->nccl, c->stream), "ncclRecv");
+  ok = isr_nccl::report(A.GroupEnd(), "ncclGroupEnd") && ok;
+  ok = ok && isr_nccl::report(A.AllReduce(flags, flags, 2, isr_nccl::kInt32, isr_nccl::kMax, c->nccl, c->stream),
+                              "ncclAllReduce");
+  return ok ? ISING_SR_OK : ISING_SR_E_NCCL;
+}
+
+// the exchange of one iteration (after K1 and pack): the library's NCCL
+// communicator, or the caller's callback (which must order its work on the
+// ctx stream); `flags` = the iteration's device {changed, overflow}
+ising_sr_status exchange(ising_sr_ctx* c, int* flags) {
+  if (!c->ghost) return ISING_SR_OK;
+  const auto x0 = std::chrono::steady_clock::now();
+  ising_sr_status s = ISING_SR_OK;
+  if (c->nccl) {
+    s = nccl_exchange(c, flags);
+  } else if (c->cfg.exchange) {
+    ising_sr_halo h;
+    fill_halo(c, &h);
+    h.flags = flags;
+    if (c->cfg.exchange(c->cfg.exchange_user, &h) != 0) s = ISING_SR_E_NCCL;
+  } else {
+    s = ISING_SR_E_INVALID_ARG;
+  }
+  c->stats.ms_exchange_total +=
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - x0).count();
+  return s;
 }
 
 // {M, B} of committed state st into c->h_snap (enqueued; read after the next sync)
@@ -774,7 +837,7 @@ void start_window(ising_sr_ctx* c) {
 }
 
 // ---------------------------------------------------------------------------
-// Pipelined relaxation (world == 1, Jacobi worklist schedule): iteration k+1
+// Pipelined relaxation (worklist schedule, any world size): iteration k+1
 // is enqueued before the host reads iteration k's flags, so the host round
 // trip overlaps the GPU's work.  K1 reads the length of its worklist on the
 // device (n_work_dev); its grid is sized from an upper bound -- the length of
@@ -783,7 +846,9 @@ void start_window(ising_sr_ctx* c) {
 // each block's tile).  When iteration k changed nothing, the iteration
 // enqueued after it finds an empty worklist and does nothing, so g and every
 // result are those of the one-iteration-per-sync loop.  Per-iteration flags,
-// counters and kernel events use slot K & 1.
+// counters and kernel events use slot K & 1.  With strips, every rank
+// enqueues the same iterations (its decisions use all-reduced flags), so the
+// speculative iteration's exchange is matched on every rank.
 // ---------------------------------------------------------------------------
 ising_sr_status enqueue_pipelined(ising_sr_ctx* c, int bound) {
   NvtxRange nv("isr iteration (pipelined)");
@@ -811,6 +876,16 @@ ising_sr_status enqueue_pipelined(ising_sr_ctx* c, int bound) {
     CK(c, cudaGetLastError());
   }
   CK(c, cudaEventRecord(c->bev[2 * j + 1], c->stream));
+  if (c->ghost) {  // strip edges: pack, C1 + C2, mark the regions next to changed ghosts
+    c->ops->pack(a, c->gsend[0], c->gsend[1], c->RX, c->stream);
+    ++c->launches;
+    CK(c, cudaGetLastError());
+    ising_sr_status s = exchange(c, sl->flags);
+    if (s) return s;
+    isr::mark_kernel<<<(2 * c->RX + 127) / 128, 128, 0, c->stream>>>(a, c->grecv[0], c->grecv[1]);
+    ++c->launches;
+    CK(c, cudaGetLastError());
+  }
   isr::compact_kernel<<<(c->dwords + 255) / 256, 256, 0, c->stream>>>(c->dirty + (size_t)((K + 1) & 1) * c->dwords,
                                                                        c->dwords, c->nreg, c->wl[(K + 1) & 1],
                                                                        &sl->wl_next);
@@ -861,85 +936,6 @@ ising_sr_status run_window_pipelined(ising_sr_ctx* c) {
   }
 }
 
-// ---------------------------------------------------------------------------
-// Batched relaxation (world == 1, slot-pool K1): `batch` iterations are
-// enqueued back to back -- K1 reads its worklist length on the device and
-// takes work from a global queue, so no host round trip is needed between
-// iterations -- and their flags are read with one synchronisation.  An
-// iteration enqueued after the converged one finds an empty worklist (no
-// region was marked dirty) and changes nothing, so g and every result are
-// those of the one-iteration-per-sync loop.
-// ---------------------------------------------------------------------------
-ising_sr_status enqueue_iteration(ising_sr_ctx* c, int j) {
-  NvtxRange nv("isr iteration (batched)");
-  ++c->it;
-  const unsigned K = ++c->Kglob;
-  const bool first = c->it == 1;
-  CK(c, cudaMemsetAsync(c->d_flags + 4 * j, 0, 4 * sizeof(int), c->stream));
-  CK(c, cudaMemsetAsync(c->d_stats + 8 * j, 0, 8 * sizeof(unsigned long long), c->stream));
-  CK(c, cudaMemsetAsync(c->d_wctr + j, 0, sizeof(unsigned), c->stream));
-  CK(c, cudaMemsetAsync(c->d_wlc + ((K + 1) & 1), 0, sizeof(unsigned), c->stream));
-  KArgs a = base_args(c, K, first);
-  a.flags = c->d_flags + 4 * j;
-  a.stats = c->d_stats + 8 * j;
-  a.wl_in = first ? nullptr : c->wl[K & 1];
-  a.n_work = c->nreg;
-  a.n_work_dev = first ? nullptr : c->d_wlc + (K & 1);
-  a.work_ctr = c->d_wctr + j;
-  a.tile = 0;
-  a.refill = c->pool ? c->pool_refill : c->refill;
-  a.wl_out = c->wl[(K + 1) & 1];
-  a.wl_out_count = c->d_wlc + ((K + 1) & 1);
-  CK(c, cudaEventRecord(c->bev[2 * j], c->stream));
-  if (c->pool) c->ops->region_pool_persistent(a, c->stream);
-  else c->ops->region_persistent(a, c->stream);
-  ++c->launches;
-  CK(c, cudaGetLastError());
-  CK(c, cudaEventRecord(c->bev[2 * j + 1], c->stream));
-  return compact_worklist(c);
-}
-
-ising_sr_status run_window_batched(ising_sr_ctx* c, int bmax) {
-  ising_sr_status s;
-  for (;;) {
-    const int it0 = c->it;
-    const int B = std::max(1, std::min(bmax, c->cfg.max_iterations - it0));
-    for (int j = 0; j < B; ++j)
-      if ((s = enqueue_iteration(c, j))) return s;
-    CK(c, cudaMemcpyAsync(c->h_flags, c->d_flags, 4 * B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CK(c, cudaMemcpyAsync(c->h_stats, c->d_stats, 8 * B * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                          c->stream));
-    CK(c, cudaStreamSynchronize(c->stream));
-    bool restart = false, conv = false;
-    for (int j = 0; j < B; ++j) {
-      float kms = 0.f;
-      CK(c, cudaEventElapsedTime(&kms, c->bev[2 * j], c->bev[2 * j + 1]));
-      account_iteration(c, kms, c->h_stats + 8 * j, it0 + j + 1);
-      if (c->h_flags[4 * j + 1]) {  // history capacity overflow: grow and restart the window
-        if ((s = grow_capacity(c))) return s;
-        start_window(c);
-        restart = true;
-        break;
-      }
-      if (!c->h_flags[4 * j]) {
-        conv = true;
-        c->g = it0 + j + 1;
-        break;
-      }
-    }
-    if (restart) continue;
-    if (conv) {
-      c->it = c->g;
-      c->converged = true;
-      return ISING_SR_OK;
-    }
-    if (c->it >= c->cfg.max_iterations) {
-      c->in_window = false;
-      return ISING_SR_E_DIVERGED;
-    }
-  }
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -956,7 +952,7 @@ const char* ising_sr_strerror(ising_sr_status s) {
     case ISING_SR_E_DIVERGED: return "relaxation did not converge within max_iterations";
     case ISING_SR_E_CAPACITY: return "boundary-history capacity exhausted";
     case ISING_SR_E_CUDA: return "CUDA error";
-    case ISING_SR_E_NCCL: return "halo exchange failed";
+    case ISING_SR_E_NCCL: return "halo exchange failed (NCCL or the exchange callback)";
     case ISING_SR_E_OOM: return "device out of memory";
     case ISING_SR_E_STATE: return "call out of order";
   }
@@ -987,7 +983,14 @@ void ising_sr_destroy(ising_sr_ctx* c) {
   dfree(c, c->d_wlc);
   dfree(c, c->d_flags);
   dfree(c, c->d_stats);
-  dfree(c, c->d_wctr);
+  dfree(c, c->ev_t);
+  dfree(c, c->ev_s);
+  dfree(c, c->d_replay);
+  dfree(c, c->d_nrep);
+  dfree(c, c->d_edges);
+  if (c->cev0) cudaEventDestroy(c->cev0);
+  if (c->cev1) cudaEventDestroy(c->cev1);
+  if (c->nccl) isr_nccl::api().CommDestroy(c->nccl);
   for (auto& e : c->bev)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->pev)
@@ -1013,12 +1016,22 @@ void ising_sr_destroy(ising_sr_ctx* c) {
   delete c;
 }
 
+ising_sr_status ising_sr_nccl_unique_id(void* out) {
+  if (!out) return ISING_SR_E_INVALID_ARG;
+  const isr_nccl::Api& A = isr_nccl::api();
+  if (!A.ok) return ISING_SR_E_NCCL;
+  isr_nccl::UniqueId id;
+  if (!isr_nccl::report(A.GetUniqueId(&id), "ncclGetUniqueId")) return ISING_SR_E_NCCL;
+  std::memcpy(out, &id, sizeof id);
+  return ISING_SR_OK;
+}
+
 ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, ising_sr_ctx** out) {
-  if (!cfg || !spins || !out) return ISING_SR_E_INVALID_ARG;
+  if (!cfg || !out) return ISING_SR_E_INVALID_ARG;
   *out = nullptr;
   if (cfg->Lx < 3 || cfg->Ly < 3) return ISING_SR_E_DIMENSION;
   if (cfg->bx < 1 || cfg->by < 1 || cfg->Lx % cfg->bx || cfg->Ly % cfg->by) return ISING_SR_E_PARTITION;
-  if (!(cfg->W > 0.0) || !(cfg->t_end >= 0.0)) return ISING_SR_E_INVALID_ARG;
+  if (std::isnan(cfg->W) || std::isinf(cfg->W) || !(cfg->t_end >= 0.0)) return ISING_SR_E_INVALID_ARG;
   for (double r : cfg->rate)
     if (!(r >= 0.0) || std::isinf(r)) return ISING_SR_E_INVALID_ARG;
   const int world = cfg->world < 1 ? 1 : cfg->world;
@@ -1028,11 +1041,26 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   const int RX = cfg->Lx / cfg->bx, RY = cfg->Ly / cfg->by;
   if (RY % world) return ISING_SR_E_PARTITION;
   if ((long long)RX * RY > 0x7fffffffLL) return ISING_SR_E_INVALID_ARG;
+  const bool loopback = (cfg->flags & ISING_SR_FLAG_HALO_LOOPBACK) != 0;
+  if (loopback && (world != 1 || !cfg->nccl_id)) return ISING_SR_E_INVALID_ARG;
+  if (world > 1 && !cfg->nccl_id && !cfg->exchange) {
+    // only the step-level API can drive such a ctx (the caller moves the ghost rows)
+  }
+  if (!(cfg->eq_quantum >= 0.0) || std::isinf(cfg->eq_quantum)) return ISING_SR_E_INVALID_ARG;
 
   ising_sr_ctx* c = new (std::nothrow) ising_sr_ctx();
   if (!c) return ISING_SR_E_OOM;
   c->cfg = *cfg;
   c->cfg.world = world;
+  if (!(cfg->W > 0.0)) {  // the paper's T_max = ln N / (lambda |dG_i|)
+    double lam = 0.0;
+    for (double r : cfg->rate) lam = std::max(lam, r);
+    const double N = (double)RX * (double)RY;
+    const double dG = (cfg->bx == 1 || cfg->by == 1) ? (double)cfg->bx * cfg->by : 2.0 * (cfg->bx + cfg->by) - 4.0;
+    c->cfg.W = (N > 1.0 && lam > 0.0) ? std::log(N) / (lam * dG) : 1.0;
+  }
+  c->cfg.nccl_id = nullptr;  // copied into the communicator below, never kept
+  c->ghost = world > 1 || loopback;
   if (c->cfg.max_iterations <= 0) c->cfg.max_iterations = 1000;
   c->ops = ops;
   c->RX = RX;
@@ -1044,13 +1072,11 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   std::memset(&c->stats, 0, sizeof c->stats);
   if (const char* e = std::getenv("ISING_SR_PIPELINE")) c->pipeline = std::atoi(e) != 0;
   if (const char* e = std::getenv("ISING_SR_REFILL")) c->refill = std::max(1, std::min(32, std::atoi(e)));
-  if (const char* e = std::getenv("ISING_SR_POOL")) c->pool = std::atoi(e) != 0;
-  if ((cfg->flags & ISING_SR_FLAG_OBSERVABLES) && ((!ops->warp && c->pool) || (ops->warp && !big_enabled()))) {
+  if (const char* e = std::getenv("ISING_SR_K1_DELAY_NS")) c->delay_ns = (unsigned)std::max(0, std::atoi(e));
+  if ((cfg->flags & ISING_SR_FLAG_OBSERVABLES) && ops->warp && !big_enabled()) {
     delete c;
     return ISING_SR_E_INVALID_ARG;  // observables are accumulated by the lane-per-region K1 forms only
   }
-  if (const char* e = std::getenv("ISING_SR_POOL_REFILL"))
-    c->pool_refill = std::max(1, std::min(ISR_POOL_S, std::atoi(e)));
 
   auto bail = [&](ising_sr_status s) {
     ising_sr_destroy(c);
@@ -1075,10 +1101,11 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   }
   if (dmalloc(c, &c->sel, (size_t)ops->sel_words * n) != cudaSuccess || dmalloc(c, &c->dirty, 2 * ((n + 31) / 32)) != cudaSuccess ||
       dmalloc(c, &c->wl[0], n) != cudaSuccess || dmalloc(c, &c->wl[1], n) != cudaSuccess ||
-      dmalloc(c, &c->d_wlc, 2) != cudaSuccess || dmalloc(c, &c->d_flags, 4 * kBatch) != cudaSuccess ||
-      dmalloc(c, &c->d_stats, 8 * kBatch) != cudaSuccess || dmalloc(c, &c->d_wctr, kBatch) != cudaSuccess ||
-      cudaMallocHost((void**)&c->h_flags, 4 * kBatch * sizeof(int)) != cudaSuccess ||
-      cudaMallocHost((void**)&c->h_stats, 8 * kBatch * sizeof(unsigned long long)) != cudaSuccess ||
+      dmalloc(c, &c->d_wlc, 2) != cudaSuccess || dmalloc(c, &c->d_flags, 4) != cudaSuccess ||
+      dmalloc(c, &c->d_stats, 8) != cudaSuccess || dmalloc(c, &c->d_nrep, 4) != cudaSuccess ||
+      dmalloc(c, &c->d_edges, 1) != cudaSuccess ||
+      cudaMallocHost((void**)&c->h_flags, 4 * sizeof(int)) != cudaSuccess ||
+      cudaMallocHost((void**)&c->h_stats, 8 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMallocHost((void**)&c->h_wlc, 2 * sizeof(unsigned)) != cudaSuccess ||
       dmalloc(c, &c->d_off, n) != cudaSuccess || dmalloc(c, &c->d_bsum, (n + kThreads - 1) / kThreads) != cudaSuccess ||
       dmalloc(c, &c->d_total, 1) != cudaSuccess || dmalloc(c, &c->d_obs, 2 * kObsBlocks + 2) != cudaSuccess ||
@@ -1089,15 +1116,27 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
       cudaMemsetAsync(c->dirty, 0, 2 * ((n + 31) / 32) * 4, c->stream) != cudaSuccess)
     return bail(ISING_SR_E_CUDA);
   if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
-      cudaEventCreate(&c->kev0) != cudaSuccess || cudaEventCreate(&c->kev1) != cudaSuccess)
+      cudaEventCreate(&c->kev0) != cudaSuccess || cudaEventCreate(&c->kev1) != cudaSuccess ||
+      cudaEventCreate(&c->cev0) != cudaSuccess || cudaEventCreate(&c->cev1) != cudaSuccess)
     return bail(ISING_SR_E_CUDA);
   for (auto& e : c->bev)
     if (cudaEventCreate(&e) != cudaSuccess) return bail(ISING_SR_E_CUDA);
   for (auto& e : c->pev)
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return bail(ISING_SR_E_CUDA);
-  if (const char* e = std::getenv("ISING_SR_BATCH")) c->batch = std::max(1, std::min(kBatch, std::atoi(e)));
-  if (const char* e = std::getenv("ISING_SR_TAIL_BATCH")) c->tail_batch = std::max(1, std::min(kBatch, std::atoi(e)));
-  if (const char* e = std::getenv("ISING_SR_TAIL_N")) c->tail_n = std::max(0, std::atoi(e));
+  if (cfg->flags & ISING_SR_FLAG_LOG_EVENTS) {
+    // scratch event log: events per region per window at the largest rate,
+    // at most 16 (a region with more is replayed at commit); the replay list
+    double rmax = 0.0;
+    for (double r : cfg->rate) rmax = std::max(rmax, r);
+    int C = cfg->log_capacity > 0 ? cfg->log_capacity
+                                  : (int)std::ceil((double)cfg->bx * cfg->by * rmax * std::min(cfg->W, cfg->t_end));
+    C = std::max(2, std::min(C, 16));
+    if (cfg->log_capacity > 0) C = std::min(cfg->log_capacity, 1 << 16);
+    c->evC = C;
+    if (dmalloc(c, &c->ev_t, n * (size_t)C) != cudaSuccess || dmalloc(c, &c->ev_s, n * (size_t)C) != cudaSuccess ||
+        dmalloc(c, &c->d_replay, n) != cudaSuccess)
+      return bail(ISING_SR_E_OOM);
+  }
   const int K0 = cfg->hist_capacity > 0 ? std::min(cfg->hist_capacity, ops->cnt_max) : auto_capacity(*cfg, ops->cnt_max);
   ising_sr_status s = alloc_edges(c, K0);
   if (s != ISING_SR_OK) return bail(s);
@@ -1136,7 +1175,12 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   const int y_first = c->row0 * by - 1;
   uint8_t* dbuf = nullptr;
   if (dmalloc_bytes(c, (void**)&dbuf, (size_t)rows * Lx) != cudaSuccess) return bail(ISING_SR_E_OOM);
-  for (int q = 0; q < rows;) {
+  if (!spins) {  // the Philox init stream, generated on the device
+    const long long ns = (long long)rows * Lx;
+    philox_spins_kernel<<<(unsigned)((ns + 255) / 256), 256, 0, c->stream>>>(dbuf, rows, y_first, Lx, Ly, cfg->seed);
+    c->launches++;
+  }
+  for (int q = 0; spins && q < rows;) {
     const int y = ((y_first + q) % Ly + Ly) % Ly;
     const int run = std::min(rows - q, Ly - y);  // contiguous up to the lattice's last row
     if (cudaMemcpyAsync(dbuf + (size_t)q * Lx, spins + (size_t)y * Lx, (size_t)run * Lx, cudaMemcpyHostToDevice,
@@ -1146,7 +1190,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
     }
     q += run;
   }
-  ops->init(dbuf, Lx, RX, c->RYl, c->row0, cfg->seed, c->st[0], c->stream);
+  ops->init(dbuf, Lx, RX, c->RYl, c->row0, cfg->seed, cfg->eq_quantum, c->st[0], c->stream);
   c->launches++;
   if ((cfg->flags & ISING_SR_FLAG_OBSERVABLES) && enqueue_snapshot(c, c->st[0]) != ISING_SR_OK)
     return bail(ISING_SR_E_CUDA);
@@ -1155,7 +1199,19 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   if (e != cudaSuccess || cudaGetLastError() != cudaSuccess) return bail(ISING_SR_E_CUDA);
   c->stats.obs_M_now = (int64_t)c->h_snap[0];
   c->stats.obs_B_now = (int64_t)c->h_snap[1];
+  c->stats.edge_entries_last_window = -1;
+  c->stats.log_replayed_last_window = -1;
   c->comm = 0;
+  if (cfg->nccl_id) {  // the library's communicator for C1/C2 (collective over the ranks)
+    const isr_nccl::Api& A = isr_nccl::api();
+    if (!A.ok) return bail(ISING_SR_E_NCCL);
+    isr_nccl::UniqueId id;
+    std::memcpy(&id, cfg->nccl_id, sizeof id);
+    if (!isr_nccl::report(A.CommInitRank(&c->nccl, world, id, cfg->rank), "ncclCommInitRank")) {
+      c->nccl = nullptr;
+      return bail(ISING_SR_E_NCCL);
+    }
+  }
   *out = c;
   return ISING_SR_OK;
 }
@@ -1185,7 +1241,7 @@ ising_sr_status ising_sr_iterate(ising_sr_ctx* c, int32_t flags_out[2]) {
 ising_sr_status ising_sr_halo_get(ising_sr_ctx* c, ising_sr_halo* out) {
   ising_sr_status s = check(c);
   if (s) return s;
-  if (!out || !c->in_window || c->it < 1 || c->cfg.world < 2) return ISING_SR_E_STATE;
+  if (!out || !c->in_window || c->it < 1 || !c->ghost) return ISING_SR_E_STATE;
   fill_halo(c, out);
   return ISING_SR_OK;
 }
@@ -1221,34 +1277,19 @@ ising_sr_status ising_sr_run_window(ising_sr_ctx* c, int32_t* g_out) {
   NvtxRange nv("isr window");
   ising_sr_status s = check(c);
   if (s) return s;
+  if (c->ghost && !c->nccl && !c->cfg.exchange) return ISING_SR_E_INVALID_ARG;  // step-level API only
   if ((s = ising_sr_begin_window(c))) return s;
-  const bool can_batch = c->cfg.world <= 1 && c->ops->region_persistent &&
-                         !(c->cfg.flags & ISING_SR_FLAG_JACOBI_ALL) &&
-                         (!c->pool || c->ops->region_pool_persistent) &&
-                         !(c->cfg.flags & ISING_SR_FLAG_OBSERVABLES);  // persistent forms do not integrate
-  const bool can_pipe = c->cfg.world <= 1 && c->pipeline && !c->pool &&
-                        !(c->cfg.flags & ISING_SR_FLAG_JACOBI_ALL) && c->batch <= 1 && c->tail_batch <= 1;
-  if (can_pipe) {
+  if (c->pipeline && !(c->cfg.flags & ISING_SR_FLAG_JACOBI_ALL)) {
     if ((s = run_window_pipelined(c))) return s;
     if (g_out) *g_out = c->g;
     return ISING_SR_OK;
   }
-  if (can_batch && c->batch > 1) {
-    if ((s = run_window_batched(c, c->batch))) return s;
-    if (g_out) *g_out = c->g;
-    return ISING_SR_OK;
-  }
+  // one iteration per host synchronisation (ISING_SR_PIPELINE=0, or the
+  // Jacobi schedule over all regions)
   for (;;) {
     if ((s = launch_iteration(c))) return s;
-    if (c->cfg.world > 1) {
-      if (!c->cfg.exchange) return ISING_SR_E_INVALID_ARG;
-      ising_sr_halo h;
-      fill_halo(c, &h);
-      const auto x0 = std::chrono::steady_clock::now();
-      const int xr = c->cfg.exchange(c->cfg.exchange_user, &h);
-      c->stats.ms_exchange_total +=
-          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - x0).count();
-      if (xr != 0) return ISING_SR_E_NCCL;
+    if (c->ghost) {
+      if ((s = exchange(c, c->d_flags))) return s;
       if ((s = mark_ghosts(c))) return s;
     }
     if ((s = read_flags(c))) return s;
@@ -1265,12 +1306,6 @@ ising_sr_status ising_sr_run_window(ising_sr_ctx* c, int32_t* g_out) {
     if (c->it >= c->cfg.max_iterations) {
       c->in_window = false;
       return ISING_SR_E_DIVERGED;
-    }
-    // the tail of the relaxation (few regions left): several iterations per
-    // host synchronisation, the worklist length read on the device
-    if (can_batch && c->tail_batch > 1 && c->n_work < c->tail_n) {
-      if ((s = run_window_batched(c, c->tail_batch))) return s;
-      break;
     }
   }
   if (g_out) *g_out = c->g;
@@ -1334,17 +1369,36 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
       }
       c->log_cap = cap;
     }
-    // replay every region against the final (latest) histories
+    // K3: compact the scratch log of every region's final recomputation;
+    // regions with more than evC events are listed and replayed against the
+    // final (latest) histories
+    CK(c, cudaEventRecord(c->cev0, c->stream));
+    CK(c, cudaMemsetAsync(c->d_nrep, 0, 4 * sizeof(unsigned), c->stream));
+    CK(c, cudaMemsetAsync(c->d_edges, 0, sizeof(unsigned long long), c->stream));
+    compact_log_kernel<<<(c->nreg + 255) / 256, 256, 0, c->stream>>>(
+        s1.n, s0.n, c->nreg, c->d_off, c->ev_t, c->ev_s, (long long)c->nreg, c->evC, c->RX, c->row0, c->log_t,
+        c->log_region, c->log_site, c->d_replay, c->d_nrep);
+    c->launches++;
+    CK(c, cudaGetLastError());
     KArgs a = base_args(c, c->Kglob + 1, false);
-    a.n_work = c->nreg;
-    a.tile = tile_for(c->nreg);
+    a.wl_in = c->d_replay;
+    a.n_work = 0;
+    a.n_work_dev = c->d_nrep;  // the list's length, read on the device
+    a.tile = kThreads;
     a.log_t = c->log_t;
     a.log_region = c->log_region;
     a.log_site = c->log_site;
     a.log_off = c->d_off;
-    c->ops->replay(a, c->nreg, c->stream);
+    c->ops->replay(a, 148 * 4 * kThreads, c->stream);  // a fixed grid; tiles sized on the device
     c->launches++;
     CK(c, cudaGetLastError());
+    count_edge_entries<<<148 * 4, 256, 0, c->stream>>>(c->log_site, c->d_total, c->cfg.bx, c->cfg.by,
+                                                       c->RX == 1 ? 1 : 0, c->RYg == 1 ? 1 : 0, c->d_edges);
+    c->launches++;
+    CK(c, cudaGetLastError());
+    CK(c, cudaEventRecord(c->cev1, c->stream));
+    CK(c, cudaMemcpyAsync(&c->h_nrep, c->d_nrep, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaMemcpyAsync(&c->h_edges, c->d_edges, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
     c->log_n = (long long)total;
     c->win_bytes += (double)total * 14.0 + (double)c->nreg * 8.0;
   }
@@ -1368,6 +1422,13 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
   c->stats.bytes_alg_last_window = c->win_bytes;
   std::memcpy(c->stats.active_last, c->win_active, sizeof c->win_active);
   c->stats.ms_last_window = ms;
+  if (log) {
+    float cms = 0.f;
+    cudaEventElapsedTime(&cms, c->cev0, c->cev1);
+    c->stats.ms_compact_total += cms;
+    c->stats.edge_entries_last_window = (int64_t)c->h_edges;
+    c->stats.log_replayed_last_window = (int64_t)c->h_nrep;
+  }
   if (obs) {
     c->stats.obs_M_last = c->h_obs[0];
     c->stats.obs_B_last = c->h_obs[1];

@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
       hcnt[d] = 0; hidx[d] = 0; hsrc[d] = 0; hoff[d] = 0; ht[d] = dinf(); hpos[d] = 0;
       const bool axis_off = (d < 2) ? wrapY : wrapX;
       if (a.first || axis_off) continue;
-      const bool ghost = a.world > 1 && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
+      const bool ghost = a.ghost && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
       if (ghost) {
         hcnt[d] = (d == EDGE_N ? a.gh_up : a.gh_down).cnt[c];
         hsrc[d] = d == EDGE_N ? 2u : 3u;
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
 
     double U, V;
     draw_pair(a.seed, gid, n, U, V, a.gen);
-    if (a.fresh_w) R = expvar(U);  // the slate is wiped at t_c
+    if (a.fresh_w) R = budget(a, U);  // the slate is wiped at t_c
     WClasses C = wbuild<BX, BY>(row, gN, gS, gWb, gEb, wrapX, wrapY);
     int N[10];
     wcounts(C, N);
@@ -256,6 +256,11 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
             a.log_site[o] = (uint16_t)site;
           }
         } else {
+          if (lane == 0 && a.ev_t && (int)n_ev_r < a.evC) {  // scratch event log
+            const long long o = (long long)n_ev_r * a.ev_stride + idx;
+            a.ev_t[o] = tc;
+            a.ev_s[o] = (uint16_t)site;
+          }
           bool on_edge = false;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -317,7 +322,7 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
       if (ev) {
         ++n;
         draw_pair(a.seed, gid, n, U, V, a.gen);
-        R = expvar(U);
+        R = budget(a, U);
       }
       tc = cand_time(ts, R, lam);
     }
@@ -366,7 +371,7 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             if (!((chmask >> e) & 1u)) continue;
-            if (a.world > 1 && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
+            if (a.ghost && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
             const int nr = e == EDGE_N ? wdec(r, a.RYl) : e == EDGE_S ? winc(r, a.RYl) : r;
             const int nc = e == EDGE_W ? wdec(c, a.RX) : e == EDGE_E ? winc(c, a.RX) : c;
             mark_dirty(a, nr * a.RX + nc, K + 1);
@@ -433,7 +438,7 @@ __global__ void __launch_bounds__(256) snap_kernel_w(StateView st, int n, int RX
 
 // K0 for the warp form: rows as u32 masks, halo as {N row, S row, W bits, E bits}
 template <int BX, int BY>
-__global__ void init_kernel_w(const uint8_t* buf, int Lx, int RX, int RYl, int row0, unsigned long long seed,
+__global__ void init_kernel_w(const uint8_t* buf, int Lx, int RX, int RYl, int row0, unsigned long long seed, double eq_q,
                               StateView st) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= RX * RYl) return;
@@ -456,7 +461,7 @@ __global__ void init_kernel_w(const uint8_t* buf, int Lx, int RX, int RYl, int r
   double U, V;
   draw_pair(seed, (uint32_t)((row0 + r) * RX + c), 0u, U, V);
   st.ts[idx] = 0.0;
-  st.R[idx] = expvar(U);
+  st.R[idx] = quantize_budget(expvar(U), eq_q);
   st.n[idx] = 0;
   st.dig[idx] = 0ull;
 }

@@ -1,16 +1,20 @@
-"""Multi-GPU strips: one process per GPU, torch.distributed (NCCL) plumbing.
+"""Multi-GPU strips: one process per GPU, torch.distributed plumbing.
 
 The lattice's region rows are split into `world` contiguous strips (rank q
 owns rows [q*RY/world, (q+1)*RY/world)).  After every relaxation iteration
-the library calls `exchange` (include/ising_sr.h, ising_sr_halo): each rank
-sends its first row's north-edge histories up and its last row's south-edge
-histories down (periodic), receives the neighbours' into its ghost rows, and
-all-reduces the {changed, overflow} flags with MAX -- the paper's
+each rank sends its first row's north-edge histories up and its last row's
+south-edge histories down (periodic), receives the neighbours' into its ghost
+rows, and all-reduces the {changed, overflow} flags with MAX -- the paper's
 neighbour messages plus "synchronize".
 
-`halo_exchange` works on torch tensors, so the same code runs over NCCL with
-device views of the library's buffers and over gloo with CPU tensors (the
-world-size-2 CPU tests).
+Production path: the library does this itself over NCCL on its own stream
+(`IsingSR(..., nccl_id=shared_nccl_id(rank))`): torch.distributed only
+broadcasts the 128-byte ncclUniqueId once.  No Python runs per iteration.
+
+`make_exchange` is the callback transport (include/ising_sr.h,
+ising_sr_halo) kept for CPU-backend process groups: `halo_exchange` works on
+torch tensors, so the same protocol runs over gloo with CPU tensors (the
+world-size-2 CPU tests and the multi-process tests on one GPU).
 """
 from __future__ import annotations
 
@@ -37,6 +41,15 @@ def device_view(ptr: int, nbytes: int, device: int, typestr: str = "|u1", itemsi
 
 def neighbours(rank: int, world: int):
     return (rank - 1) % world, (rank + 1) % world
+
+
+def shared_nccl_id(rank: int, group=None) -> bytes:
+    """The ncclUniqueId for the library's communicator: created by rank 0
+    (ising_sr_nccl_unique_id), broadcast to every rank of `group`."""
+    from .binding import nccl_unique_id
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
 
 
 def halo_exchange(send_up: Sequence[torch.Tensor], send_down: Sequence[torch.Tensor],
@@ -73,7 +86,10 @@ def make_exchange(rank: int, world: int, device: int, group=None, host_staging: 
         rd = [device_view(h.recv_from_down[k], h.chunk_bytes[k], device) for k in range(n)]
         fl = device_view(h.flags, 8, device, "<i4", 4)
         if not host_staging:
-            halo_exchange(su, sd, ru, rd, fl, rank, world, group)
+            # the collectives are ordered on the library's stream: they wait for
+            # K1/pack and the library's next kernels wait for them
+            with torch.cuda.stream(torch.cuda.ExternalStream(h.stream, device=device)):
+                halo_exchange(su, sd, ru, rd, fl, rank, world, group)
             return 0
         torch.cuda.synchronize(device)
         hs = [[t.cpu() for t in ts] for ts in (su, sd)]

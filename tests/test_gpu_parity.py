@@ -20,50 +20,7 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("no CUDA device", allow_module_level=True)
 
 from paper_cs_0405053_b200 import FLAG_DIGEST, FLAG_LOG_EVENTS, IsingSR, IsingSRError  # noqa: E402
-
-
-def run_gpu(w, flags=FLAG_DIGEST | FLAG_LOG_EVENTS, per_window_logs=False, **kw):
-    sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed, flags=flags, **kw)
-    logs, gs = [], []
-    total = 0
-    while True:
-        try:
-            g = sim.run_window()
-        except IsingSRError as e:
-            if e.status == -9:  # past t_end
-                break
-            raise
-        gs.append(g)
-        total += sim.commit()
-        if per_window_logs:
-            logs.append(sim.events())
-    dig, cnt = sim.digests()
-    out = {"spins": sim.spins(), "digest": dig, "count": cnt, "events": total, "g": gs,
-           "logs": logs, "stats": sim.stats()}
-    sim.close()
-    return out
-
-
-def check_against_oracle(w, gpu=None, logs=True):
-    ref = oracle.des_workload(w, log_cap=10**7 if logs else 0)
-    gpu = gpu or run_gpu(w, per_window_logs=logs)
-    assert gpu["events"] == ref["n_events"]
-    assert np.array_equal(gpu["count"], ref["count"])
-    assert np.array_equal(gpu["spins"], ref["spins"])
-    if gpu["digest"] is not None:
-        assert np.array_equal(gpu["digest"], ref["digest"])
-    if logs and gpu["logs"]:
-        # window w holds the oracle events with t in [fl(w W), fl((w+1) W))
-        t_all, r_all, s_all = ref["log_t"], ref["log_region"], ref["log_site"]
-        for k, (t, r, s) in enumerate(gpu["logs"]):
-            lo = k * w.W
-            hi = min((k + 1) * w.W, w.t_end)
-            sel = (t_all >= lo) & (t_all < hi)
-            order = np.lexsort((t_all[sel], r_all[sel]))  # region, then time
-            assert np.array_equal(t, t_all[sel][order]), f"window {k} times"
-            assert np.array_equal(r, r_all[sel][order]), f"window {k} regions"
-            assert np.array_equal(s, s_all[sel][order]), f"window {k} sites"
-    return ref, gpu
+from _gpu_common import check_against_oracle, run_gpu  # noqa: E402
 
 
 def test_c1_bit_exact_full():
@@ -230,24 +187,16 @@ def test_c5_geometry_sample_bit_exact():
 
 # ---------------------------------------------------------------------------
 # every schedule of K1 (lane-persistent with the pipelined host loop:
-# default; one iteration per host sync: ISING_SR_PIPELINE=0; slot pool:
-# ISING_SR_POOL=1; persistent global queue: ISING_SR_BATCH and the tail
-# batching ISING_SR_TAIL_N/ISING_SR_TAIL_BATCH) and extreme refill
-# thresholds give the oracle's bits
+# default; one iteration per host sync: ISING_SR_PIPELINE=0; the warp form of
+# big regions: ISING_SR_BIG=0; big regions without resume: ISING_SR_RESUME=0)
+# and an extreme refill threshold give the oracle's bits
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("env", [
-    {"ISING_SR_POOL": "0"},
+    {},
     {"ISING_SR_PIPELINE": "0"},
     {"ISING_SR_PIPELINE": "0", "ISING_SR_BIG": "0"},
-    {"ISING_SR_POOL": "0", "ISING_SR_BATCH": "1"},
-    {"ISING_SR_POOL": "0", "ISING_SR_REFILL": "1"},
-    {"ISING_SR_POOL": "1", "ISING_SR_POOL_REFILL": "1"},
-    {"ISING_SR_POOL": "1", "ISING_SR_POOL_REFILL": "64"},
-    {"ISING_SR_POOL": "1", "ISING_SR_BATCH": "1"},
-    {"ISING_SR_POOL": "1", "ISING_SR_BATCH": "8"},
-    {"ISING_SR_TAIL_BATCH": "1"},
-    {"ISING_SR_TAIL_N": "1000000000", "ISING_SR_TAIL_BATCH": "3"},
-    {"ISING_SR_BIG": "0", "ISING_SR_TAIL_N": "1000000000"},
+    {"ISING_SR_REFILL": "1"},
+    {"ISING_SR_BIG": "0"},
     {"ISING_SR_RESUME": "0"},
 ])
 def test_k1_schedules_bit_exact(env, monkeypatch):
@@ -285,7 +234,7 @@ def test_c5_full_lattice_prefix(b, T, t_end):
     (64, 64, 16, 16, 2.269, 1.0, 4.0),
     (64, 64, 32, 32, 4.0, 0.25, 2.0),
 ])
-@pytest.mark.parametrize("env", [{}, {"ISING_SR_BIG": "0", "ISING_SR_POOL": "1"}])
+@pytest.mark.parametrize("env", [{}, {"ISING_SR_BIG": "0"}])
 def test_fresh_window_variant_bit_exact(geom, env, monkeypatch):
     from paper_cs_0405053_b200 import FLAG_FRESH_WINDOW
     for k, v in env.items():
@@ -420,7 +369,7 @@ def test_observables_onsager():
     assert abs(m - m0) < 0.01, (m, m0)
 
 
-@pytest.mark.parametrize("env", [{}, {"ISING_SR_BATCH": "4"}])
+@pytest.mark.parametrize("env", [{}, {"ISING_SR_PIPELINE": "0"}])
 def test_stats_active_regions_per_iteration(env, monkeypatch):
     """stats.active_last: the worklist length of every iteration of the last
     window -- all regions in iteration 1, the window's recomputations in

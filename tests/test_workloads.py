@@ -125,3 +125,45 @@ def test_config_presets_match_baseline_json():
     assert len(workloads.c5_points()) == 45
     # exact initial rate per site of c1 / c4 (rounded)
     assert abs(workloads.exact_initial_rate_per_site(c["c1"]) - 0.705) < 0.05
+
+
+def _kat_rows():
+    rows = []
+    for line in open(os.path.join(HERE, "golden", "philox4x32_10_kat.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        v = [int(x, 16) for x in line.split()]
+        rows.append((v[:4], v[4:6], v[6:10]))
+    return rows
+
+
+def test_init_stream_philox_kat():
+    """The input generator's Philox4x32-10 reproduces the Random123 known-answer
+    vectors (tests/golden/philox4x32_10_kat.txt)."""
+    for ctr, key, out in _kat_rows():
+        got = workloads.philox4x32_10(np.array([ctr], dtype=np.uint32), np.array([key], dtype=np.uint32))
+        assert [int(x) for x in got[0]] == out
+
+
+def test_init_stream_layout_against_oracle_philox():
+    """SURVEY §8(c.3) init stream: site v is bit (v & 31) of word ((v >> 5) & 3)
+    of Philox(key=(0xFFFFFFFF, seed_lo), ctr=(v >> 7, 0, 1, seed_hi)), checked
+    site by site with the oracle's independent Philox on a 37x29 lattice (a
+    ragged last draw) and two seeds (one with a nonzero high word)."""
+    for seed in (1, 0x123456789):
+        Lx, Ly = 37, 29
+        s = workloads.initial_spins(Lx, Ly, "random", seed)
+        for v in range(Lx * Ly):
+            w = oracle.philox([v >> 7, 0, 1, seed >> 32], [0xFFFFFFFF, seed & 0xFFFFFFFF])
+            assert s[v] == (w[(v >> 5) & 3] >> (v & 31)) & 1, (seed, v)
+
+
+def test_init_stream_statistics():
+    """iid p = 1/2: the up fraction and nearest-neighbour correlation of a
+    1024^2 draw are within 5 sigma of 1/2 and 0."""
+    s = workloads.initial_spins(1024, 1024, "random", 1).astype(np.float64)
+    n = s.size
+    assert abs(s.mean() - 0.5) < 5 * 0.5 / math.sqrt(n)
+    g = 2 * s.reshape(1024, 1024) - 1
+    assert abs((g * np.roll(g, 1, 1)).mean()) < 5 / math.sqrt(n)
+    assert abs((g * np.roll(g, 1, 0)).mean()) < 5 / math.sqrt(n)

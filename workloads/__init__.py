@@ -6,8 +6,8 @@ problem statement the paper starts from (§2):
 
 * the lattice size, region size, J, H, T, window W and run length of each
   BASELINE.json config (c1..c5), and
-* the initial spin configuration s(v), drawn iid from numpy's
-  seeded generator, and
+* the initial spin configuration s(v), iid from the seeded
+  Philox init stream, and
 * the per-class flip-rate table r_k = lambda * p_k (eq. pMin /
   pglauber), computed ONCE here with libm exp and handed, as the same double
   bits, to both the oracle and the CUDA library (SURVEY §8c.3 "Rate table").
@@ -71,9 +71,56 @@ def rate_table(T: float, J: float = 1.0, H: float = 0.0, rule: str = "metropolis
 
 # ---------------------------------------------------------------------------
 # Initial spins.  1 = up (+1), 0 = down (-1), row-major (row * Lx + col).
-# "iid +-1 (p=0.5, seed s)" uses numpy's Philox bit generator (a documented,
-# seeded generator; SURVEY reading #19 asks only for a fixed seeded stream).
+# "iid +-1 (p=0.5, seed s)" is the SURVEY §8(c.3) Philox init stream (reading
+# #19): Philox4x32-10 with key = (0xFFFFFFFF, seed_lo), counter =
+# (site >> 7, 0, 1, seed_hi); the spin of `site` is bit (site & 31) of output
+# word ((site >> 5) & 3), 1 = up.  One draw gives 128 sites.  Key 0xFFFFFFFF
+# is disjoint from the event-pair streams (key word 0 = region id < 2^31) and
+# counter word 2 = 1 from their generation-0 counters.  The CUDA library
+# implements the same counter-based generator independently (ising_sr_init
+# with spins == NULL); the oracle never generates spins, it takes them as
+# input.  Other p_up values use numpy's seeded Philox bit generator.
 # ---------------------------------------------------------------------------
+
+_PHILOX_M0, _PHILOX_M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+_PHILOX_W0, _PHILOX_W1 = 0x9E3779B9, 0xBB67AE85
+_MASK32 = np.uint64(0xFFFFFFFF)
+
+
+def philox4x32_10(ctr: np.ndarray, key: np.ndarray) -> np.ndarray:
+    """Vectorised Philox4x32-10 (Salmon et al., SC11): ctr (n, 4), key (n, 2)
+    uint32 -> (n, 4) uint32.  Input generation only (pinned against the
+    Random123 known-answer vectors in tests/test_workloads.py)."""
+    c = [np.asarray(ctr, dtype=np.uint64)[:, i].copy() for i in range(4)]
+    k0 = np.asarray(key, dtype=np.uint64)[:, 0].copy()
+    k1 = np.asarray(key, dtype=np.uint64)[:, 1].copy()
+    for r in range(10):
+        if r:
+            k0 = (k0 + np.uint64(_PHILOX_W0)) & _MASK32
+            k1 = (k1 + np.uint64(_PHILOX_W1)) & _MASK32
+        p0 = _PHILOX_M0 * c[0]
+        p1 = _PHILOX_M1 * c[2]
+        c = [(p1 >> np.uint64(32)) ^ c[1] ^ k0, p1 & _MASK32,
+             (p0 >> np.uint64(32)) ^ c[3] ^ k1, p0 & _MASK32]
+    return np.stack(c, axis=1).astype(np.uint32)
+
+
+def philox_init_spins(Lx: int, Ly: int, seed: int = 1) -> np.ndarray:
+    """iid +-1 spins (p = 1/2) from the Philox init stream (see above)."""
+    n = Ly * Lx
+    nd = (n + 127) // 128
+    q = np.arange(nd, dtype=np.uint64)
+    ctr = np.zeros((nd, 4), dtype=np.uint64)
+    ctr[:, 0] = q & _MASK32
+    ctr[:, 1] = q >> np.uint64(32)
+    ctr[:, 2] = 1
+    ctr[:, 3] = (seed >> 32) & 0xFFFFFFFF
+    key = np.zeros((nd, 2), dtype=np.uint64)
+    key[:, 0] = 0xFFFFFFFF
+    key[:, 1] = seed & 0xFFFFFFFF
+    out = philox4x32_10(ctr, key)                      # (nd, 4) words
+    bits = np.unpackbits(out.astype("<u4").view(np.uint8), bitorder="little")
+    return bits[:n].astype(np.uint8)                   # site = 128 q + 32 w + b
 
 
 def initial_spins(Lx: int, Ly: int, init: str = "random", seed: int = 1,
@@ -86,15 +133,30 @@ def initial_spins(Lx: int, Ly: int, init: str = "random", seed: int = 1,
         yy, xx = np.meshgrid(np.arange(Ly), np.arange(Lx), indexing="ij")
         return ((yy + xx) % 2 == 0).astype(np.uint8).reshape(-1)
     if init == "random":
-        g = np.random.Generator(np.random.Philox(seed))
         if p_up == 0.5:
-            # one random bit per site, drawn 64 at a time
-            n = Ly * Lx
-            words = g.integers(0, 2**63, size=(n + 62) // 63, dtype=np.int64)
-            bits = ((words[:, None] >> np.arange(63, dtype=np.int64)) & 1).reshape(-1)[:n]
-            return bits.astype(np.uint8)
+            return philox_init_spins(Lx, Ly, seed)
+        g = np.random.Generator(np.random.Philox(seed))
         return (g.random(Ly * Lx) < p_up).astype(np.uint8)
     raise ValueError(f"unknown init {init!r}")
+
+
+# ---------------------------------------------------------------------------
+# The paper's window: T_max = log N / (lambda |dG_i|), N regions
+# (PEs), |dG_i| the number of sites on a region's boundary, lambda the largest
+# flip rate (reading #14/#15: natural log).  A bookkeeping formula for choosing
+# W; it changes which windows the relaxation works on, never the trajectory.
+# ---------------------------------------------------------------------------
+
+
+def boundary_sites(bx: int, by: int) -> int:
+    """|dG_i|: sites of a bx x by region with a neighbour outside it."""
+    if bx == 1 or by == 1:
+        return bx * by
+    return 2 * bx + 2 * by - 4
+
+
+def paper_tmax(n_regions: int, dG: int, lam: float = 1.0) -> float:
+    return math.log(n_regions) / (lam * dG)
 
 
 # ---------------------------------------------------------------------------
