@@ -54,13 +54,17 @@ def _cfg(**kw):
     c.t_end = kw.get("t_end", 10.0)
     c.world = kw.get("world", 1)
     c.rank = kw.get("rank", 0)
+    c.flags = kw.get("flags", 0)
+    c.eq_quantum = kw.get("eq_quantum", 0.0)
     return c
 
 
 @pytest.mark.parametrize("kw,status", [
     (dict(Lx=2), -2), (dict(Ly=1), -2),
     (dict(bx=3), -3), (dict(Lx=18, bx=4), -3),
-    (dict(W=0.0), -1), (dict(W=-1.0), -1),
+    (dict(W=float("nan")), -1), (dict(W=float("inf")), -1),   # W <= 0 selects the paper's T_max
+    (dict(eq_quantum=-1.0), -1), (dict(eq_quantum=float("inf")), -1),
+    (dict(flags=binding.FLAG_HALO_LOOPBACK), -1),              # loopback needs nccl_id
     (dict(rates=[-1.0] + [1.0] * 9), -1),
     (dict(bx=3, by=5, Lx=15, Ly=15), -1),        # unsupported region shape
     (dict(rank=3, world=2), -1),
