@@ -3,9 +3,20 @@
 n-fold way (arXiv cs/0405053) on BASELINE config 4 (16384^2, 4x4 regions,
 T=2, H=0, iid spins, W=0.5, t=50), strips over N GPUs.
 
-A "step" is one window of committed time (one full relaxation to the fixed
-point + commit = every §8(a) row).  W warm-up windows, then K timed windows,
-continuing the same trajectory (t_end is extended past 50 only if W+K > 100).
+A "step" is one window of committed time: the full relaxation to the fixed
+point and the commit with the compacted event log (every §8(a) row).  W
+warm-up windows, then K timed windows, continuing the same trajectory (t_end
+is extended past 50 only if W+K > 100).  N > 1: one strip per GPU, the
+library's own NCCL exchange (torch.distributed only broadcasts the NCCL id
+and reduces the timings).
+
+roofline: HBM, SURVEY §8(d.3)'s algorithmic bytes.  Per region and window
+B_alg = A (S + 3H) + S + L with S the committed state (spins b^2/8 + halo
+4b/8 + t_s 8 + R 8 + n 4 bytes), H = 4 + 9 h, L = 14 e, where A =
+recomputations, h = boundary-history entries and e = committed events per
+region per window, all measured by the run (ising_sr_stats).  The dominant
+kernel K1 moves the A (S + 3H) part; `achieved` = those bytes / K1's device
+time (CUDA events on the library's stream around every K1 launch).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ising|reference]
 
@@ -39,8 +50,49 @@ def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback"
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def state_bytes(bx: int, by: int) -> float:
+    """S of SURVEY §8(d.3): spins b^2/8 + halo (2bx + 2by)/8 + t_s 8 + R 8 + n 4."""
+    return bx * by / 8.0 + (2 * bx + 2 * by) / 8.0 + 8 + 8 + 4
+
+
+class WindowLedger:
+    """Per-window A, h, e, g, f from ising_sr_stats after each commit, and the
+    §8(d.3) algorithmic bytes they imply."""
+
+    def __init__(self, w, nreg):
+        self.S = state_bytes(w.bx, w.by)
+        self.nreg = nreg
+        self.rows = []
+
+    def add(self, st):
+        A_tot = float(sum(st["active_last"]))
+        h = float(max(st["edge_entries_last_window"], 0))
+        e = float(st["events_last_window"])
+        H = 4.0 + 9.0 * h / self.nreg
+        k1 = A_tot * (self.S + 3.0 * H)
+        commit = self.nreg * self.S + 14.0 * e
+        self.rows.append({"A": A_tot / self.nreg, "h": h / self.nreg, "e": e / self.nreg, "g": st["g_last"],
+                          "f": st["f_last"], "k1_bytes": k1, "bytes": k1 + commit, "events": e})
+
+    def total(self, key):
+        return sum(r[key] for r in self.rows)
+
+    def mean(self, key):
+        return float(np.mean([r[key] for r in self.rows])) if self.rows else 0.0
 
 
 # --------------------------------------------------------------------------
@@ -148,7 +200,7 @@ def run_reference(args):
 # --------------------------------------------------------------------------
 def run_ising(args):
     import torch
-    from paper_cs_0405053_b200 import FLAG_DIGEST, IsingSR
+    from paper_cs_0405053_b200 import FLAG_DIGEST, FLAG_LOG_EVENTS, IsingSR
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -156,22 +208,26 @@ def run_ising(args):
     if args.gpus != world and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
-    exchange = None
+    nccl_id = None
     if world > 1:
         import torch.distributed as dist
-        from paper_cs_0405053_b200.dist import make_exchange
+        from paper_cs_0405053_b200.dist import shared_nccl_id
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-        exchange = make_exchange(rank, world, local)
+        nccl_id = shared_nccl_id(rank)  # the library's own communicator does C1/C2
 
     w = workloads.get(args.config)
+    if args.window == "tmax":  # the paper's T_max = ln N / (lambda |dG_i|)
+        w = w.replace(W=workloads.paper_tmax(w.n_regions, workloads.boundary_sites(w.bx, w.by), max(w.rates())))
     nwin = args.warmup + args.steps
     t_end = max(w.t_end, nwin * w.W)
     spins = w.spins()
-    flags = FLAG_DIGEST
+    flags = FLAG_DIGEST | FLAG_LOG_EVENTS  # the commit compacts the window's event log (K3) inside the timed region
     if args.jacobi_all:
         from paper_cs_0405053_b200 import FLAG_JACOBI_ALL
         flags |= FLAG_JACOBI_ALL
-    stream = torch.cuda.current_stream(local)
+    # the library's stream: every kernel of the path runs on it, and the
+    # timing events are recorded on it
+    stream = torch.cuda.Stream(device=local)
 
     def barrier():
         if world > 1:
@@ -180,13 +236,13 @@ def run_ising(args):
         torch.cuda.synchronize()
 
     sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), spins, w.W, t_end, w.seed, J=w.J, H=w.H, T=w.T,
-                  flags=flags, rank=rank, world=world, device=local, stream=stream.cuda_stream,
-                  exchange=exchange)
+                  flags=flags, rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=nccl_id)
     for _ in range(args.warmup):
         sim.run_window()
         sim.commit()
     st0 = sim.stats()
     launches0 = sim.launch_count()
+    ledger = WindowLedger(w, sim.n_regions)
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -197,23 +253,27 @@ def run_ising(args):
         for _ in range(args.steps):
             gs.append(sim.run_window())
             ev += sim.commit()
+            ledger.add(sim.stats())  # a host copy of the stats struct (no device work)
         e1.record(stream)
         barrier()
     ms = e0.elapsed_time(e1)
     st1 = sim.stats()
     launches = sim.launch_count() - launches0
-    # whole-job numbers: events summed, time max over ranks
+    # whole-job numbers: events and bytes summed, time max over ranks
     tot_ev, max_ms = ev, ms
     region_ms = st1["region_ms"] - st0["region_ms"]
-    region_bytes = st1["region_bytes"] - st0["region_bytes"]
+    impl_bytes = st1["region_bytes"] - st0["region_bytes"]
     nlaunch = st1["region_launches"] - st0["region_launches"]
+    k1_bytes, alg_bytes = ledger.total("k1_bytes"), ledger.total("bytes")
+    compact_ms = st1["ms_compact_total"] - st0["ms_compact_total"]
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([float(ev), region_bytes], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([float(ev), k1_bytes, alg_bytes, impl_bytes], dtype=torch.float64, device=f"cuda:{local}")
         dist.all_reduce(t)
         m = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
         tot_ev, max_ms = int(t[0].item()), float(m[0].item())
+        k1_bytes, alg_bytes, impl_bytes = (float(x) for x in t[1:].tolist())
     digest, count = sim.digests()
     sim.close()
 
@@ -226,7 +286,7 @@ def run_ising(args):
         barrier()
         t0 = time.perf_counter()
         sim2 = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), pinned.numpy(), w.W, t_end, w.seed, flags=flags,
-                       rank=rank, world=world, device=local, stream=stream.cuda_stream, exchange=exchange)
+                       rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=nccl_id)
         ev2 = 0
         for _ in range(args.steps):
             sim2.run_window()
@@ -249,28 +309,36 @@ def run_ising(args):
     if rank != 0:
         return 0
     peak, peak_kind = _peaks()
-    achieved = (region_bytes / (region_ms * 1e-3)) / 1e9 if region_ms > 0 else 0.0
-    # DRAM bytes per K1 launch from the committed ncu capture of one c4 window
-    # (tools/ncu_traffic.py); scaled to this run's launches by the measured
-    # DRAM/algorithmic ratio of that window
+    k1_alg_per_launch = k1_bytes / max(nlaunch, 1) / world
+    achieved = (k1_bytes / world / (region_ms * 1e-3)) / 1e9 if region_ms > 0 else 0.0
+    # DRAM bytes per K1 launch: the DRAM / §8(d.3)-algorithmic ratio of the
+    # committed ncu capture of every K1 launch of one c4 window
+    # (tools/ncu_traffic.py) times this run's algorithmic bytes per launch
     traffic, traffic_src = None, None
-    tp = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "k1_traffic_r02.json")
     if args.config == "c4" and os.path.exists(tp):
         t = json.load(open(tp))
-        traffic = t["dram_over_alg"] * region_bytes / max(nlaunch, 1)
-        traffic_src = (f"profiles/k1_traffic.json: ncu --set full of all {t['launches']} K1 launches of c4 window "
-                       f"{t['window']}, DRAM/alg = {t['dram_over_alg']:.2f}")
+        traffic = t["dram_over_alg"] * k1_alg_per_launch
+        traffic_src = (f"profiles/k1_traffic_r02.json: ncu --set full of all {t['launches']} K1 launches of c4 "
+                       f"window {t['window']}, DRAM / §8(d.3) K1 bytes = {t['dram_over_alg']:.2f}")
+    window_bw = alg_bytes / (max_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src, "peak_kind": peak_kind,
-            "frac_vs_nominal_8000": achieved / 8000.0,  # north_star's ~8 TB/s nominal HBM3e
-            "kernel": "region_kernel<4,4> (K1 trajectory + fused diff)",
-            "bytes_per_launch": region_bytes / max(nlaunch, 1),
+            "kernel": "K1 region_kernel<4,4> (+ region_kernel_first for each window's iteration 1)",
+            "byte_model": "SURVEY §8(d.3): K1 moves A (S + 3H) per region per window; S, H, A, h measured",
+            "bytes_per_launch": k1_alg_per_launch,
             "ms_per_launch": region_ms / max(nlaunch, 1),
-            "share_of_step": region_ms / ms if ms > 0 else None}
+            "share_of_step": region_ms / max_ms if max_ms > 0 else None,
+            "window": {"bytes_alg_per_event": alg_bytes / max(tot_ev, 1), "achieved_gbs": window_bw,
+                       "frac": window_bw / peak / world, "frac_vs_nominal_8000": window_bw / 8000.0 / world,
+                       "formula": "B_alg = [A (S + 3H) + S + L] / e per committed event (SURVEY §8(d.3))"},
+            "impl_bytes_per_event": impl_bytes / max(tot_ev, 1),
+            "impl_bytes_note": "the library's own count of what K1 touches (DESIGN.md §6), not the roofline numerator"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         n_ev, secs, sample = oracle_sample()
-        cpu = {"value": n_ev / secs, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
+        cpu = {"value": n_ev / secs, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+               "cpu_model": _cpu_model(), "host_cores": os.cpu_count()}
     line = {
         "metric": METRIC, "value": tot_ev / (max_ms * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
@@ -281,11 +349,18 @@ def run_ising(args):
                                f"(t {args.warmup * w.W}..{nwin * w.W})",
                    "regions": w.n_regions, "l2": "inputs larger than L2 (state+histories >> 126 MB)",
                    "schedule": "jacobi_all" if args.jacobi_all else "worklist",
+                   "event_log": "compacted at every commit (FLAG_LOG_EVENTS), in the timed region",
                    "parallelism": f"strips{world}"},
         "events": tot_ev,
-        "iterations_per_window": {"mean": float(np.mean(gs)), "max": int(max(gs)), "min": int(min(gs)),
-                                  "ln_N": math.log(w.n_regions)},
-        "bytes_alg_per_event": region_bytes / max(ev, 1),
+        "iterations_per_window": {"mean": float(np.mean(gs)), "p50": float(np.percentile(gs, 50)),
+                                  "p99": float(np.percentile(gs, 99)), "max": int(max(gs)), "min": int(min(gs)),
+                                  "ln_N": math.log(w.n_regions),
+                                  "paper_tmax": workloads.paper_tmax(w.n_regions, workloads.boundary_sites(w.bx, w.by),
+                                                                     max(w.rates()))},
+        "per_region_per_window": {"A_recomputations": ledger.mean("A"), "h_edge_entries": ledger.mean("h"),
+                                  "e_events": ledger.mean("e"), "S_state_bytes": ledger.S,
+                                  "f_max": int(max(r["f"] for r in ledger.rows))},
+        "commit_compaction_ms_per_window": compact_ms / args.steps,
         "gpu_launches": launches,
         "roofline": roof,
         "cpu_baseline": cpu,
@@ -390,6 +465,8 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--window", default="config", choices=["config", "tmax"],
+                    help="W of the config, or the paper's T_max = ln N/(lambda |dG|) (P:502-515)")
     ap.add_argument("--jacobi-all", action="store_true",
                     help="paper-faithful schedule: every region in every iteration (same bits and g)")
     args = ap.parse_args()

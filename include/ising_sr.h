@@ -86,6 +86,13 @@ typedef enum {
  * neighbours'.  Same results as without the flag; it exercises the in-library
  * exchange on one GPU. */
 #define ISING_SR_FLAG_HALO_LOOPBACK 0x20u
+/* Time integrals of |M| and M^2 over every committed window (the model's
+ * observable; stats.obs_absM_* / obs_M2_*): the commit sorts the
+ * window's events by time on the device (bucket sort + per-bucket insertion
+ * sort), prefix-sums dM = +-2 from M(t_c) and reduces |M| dt and M^2 dt in a
+ * fixed order.  Implies FLAG_LOG_EVENTS and FLAG_OBSERVABLES; world == 1
+ * only (E_INVALID_ARG otherwise: it needs the global time order). */
+#define ISING_SR_FLAG_MAG_MOMENTS 0x40u
 
 /* Halo exchange between strips (world > 1).  Rank q owns a band of region
  * rows; "up" is toward region row 0 (rank q-1, periodic), "down" toward rank
@@ -213,6 +220,9 @@ typedef struct {
   int64_t log_replayed_last_window;
   /* device time (ms, all windows) of the commit's compaction kernels */
   double ms_compact_total;
+  /* FLAG_MAG_MOMENTS: int |M| dt and int M^2 dt over the last committed
+   * window and over all committed windows */
+  double obs_absM_last, obs_M2_last, obs_absM_total, obs_M2_total;
 } ising_sr_stats;
 
 /* Validate cfg, allocate device state, copy the full Ly*Lx row-major spin

@@ -22,6 +22,7 @@ FLAG_FRESH_WINDOW = 0x4  # alternate approach to subsequent steps
 FLAG_OBSERVABLES = 0x8   # time integrals of M and of the bond sum per window
 FLAG_JACOBI_ALL = 0x10   # recompute every region in every iteration (paper-faithful schedule)
 FLAG_HALO_LOOPBACK = 0x20  # world == 1 + nccl_id: the wrap rows exchanged with itself over NCCL
+FLAG_MAG_MOMENTS = 0x40   # time integrals of |M| and M^2 per window (device time sort of the log)
 
 STATUS = {
     0: "OK", -1: "E_INVALID_ARG", -2: "E_DIMENSION", -3: "E_PARTITION", -4: "E_DIVERGED",
@@ -79,7 +80,9 @@ class Stats(ctypes.Structure):
                 ("ms_exchange_total", ctypes.c_double), ("ms_commit_total", ctypes.c_double),
                 ("obs_M_now", ctypes.c_int64), ("obs_B_now", ctypes.c_int64),
                 ("edge_entries_last_window", ctypes.c_int64), ("log_replayed_last_window", ctypes.c_int64),
-                ("ms_compact_total", ctypes.c_double)]
+                ("ms_compact_total", ctypes.c_double),
+                ("obs_absM_last", ctypes.c_double), ("obs_M2_last", ctypes.c_double),
+                ("obs_absM_total", ctypes.c_double), ("obs_M2_total", ctypes.c_double)]
 
 
 _lib = None

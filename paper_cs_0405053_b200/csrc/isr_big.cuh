@@ -614,16 +614,18 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
           else if (wrapX) B.neighbour_changed(sr, 0, du);
         }
         if (a.digest) dig = digest_step(dig, tc, site);
+        const unsigned up_new = (SM.rows[sr][t] >> sc) & 1u;  // the flipped site's new spin (for dM)
         if (LOG) {
           const unsigned long long o = a.log_off[idx] + n_ev_r;
           a.log_t[o] = tc;
           a.log_region[o] = gid;
           a.log_site[o] = (uint16_t)site;
+          if (a.log_dm) a.log_dm[o] = up_new ? 2 : -2;
         } else {
           if (a.ev_t && (int)n_ev_r < a.evC) {  // scratch event log (a resumed prefix is already there)
             const long long o = (long long)n_ev_r * a.ev_stride + idx;
             a.ev_t[o] = tc;
-            a.ev_s[o] = (uint16_t)site;
+            a.ev_s[o] = (uint16_t)(site | (up_new << 15));
           }
           bool on_edge = false;
 #pragma unroll

@@ -131,6 +131,7 @@ struct KArgs {
   double eq_q;        // > 0: quantized budgets E <- (floor(E q) + 1) / q (exact time ties; test mode)
   unsigned delay_ns;  // test knob (env ISING_SR_K1_DELAY_NS): K1 blocks sleep before publishing their flags
   // log replay
+  int8_t* log_dm;     // dM of each logged event (+2 / -2), may be null
   double* log_t;
   uint32_t* log_region;
   uint16_t* log_site;
@@ -935,10 +936,11 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const
     a.log_t[o] = L.tc;
     a.log_region[o] = L.gid;
     a.log_site[o] = (uint16_t)site;
+    if (a.log_dm) a.log_dm[o] = ((L.spins >> site) & 1) ? 2 : -2;
   } else if (a.ev_t && (int)L.n_ev < a.evC) {  // scratch event log of this recomputation
     const long long o = (long long)L.n_ev * a.ev_stride + L.idx;
     a.ev_t[o] = L.tc;
-    a.ev_s[o] = (uint16_t)site;
+    a.ev_s[o] = (uint16_t)(site | (((unsigned)(L.spins >> site) & 1u) << 15));  // bit 15: the new spin
   }
   if (LOG) {
   } else if (BX > 1 && BY > 1) {

@@ -312,7 +312,8 @@ __global__ void __launch_bounds__(256) compact_log_kernel(const uint32_t* n1, co
                                                           const unsigned long long* off, const double* ev_t,
                                                           const uint16_t* ev_s, long long stride, int C, int RX,
                                                           int row0, double* log_t, uint32_t* log_region,
-                                                          uint16_t* log_site, uint32_t* replay, unsigned* n_replay) {
+                                                          uint16_t* log_site, int8_t* log_dm, uint32_t* replay,
+                                                          unsigned* n_replay) {
   const int i = blockIdx.x * 256 + threadIdx.x;
   if (i >= N) return;
   const unsigned e = n1[i] - n0[i];
@@ -325,9 +326,197 @@ __global__ void __launch_bounds__(256) compact_log_kernel(const uint32_t* n1, co
   const int r = i / RX;
   const uint32_t gid = (uint32_t)((row0 + r) * RX + (i - r * RX));
   for (unsigned q = 0; q < e; ++q) {
+    const unsigned sv = ev_s[(long long)q * stride + i];  // bit 15: the flipped site's new spin
     log_t[o + q] = ev_t[(long long)q * stride + i];
     log_region[o + q] = gid;
-    log_site[o + q] = ev_s[(long long)q * stride + i];
+    log_site[o + q] = (uint16_t)(sv & 0x7FFFu);
+    if (log_dm) log_dm[o + q] = (sv >> 15) ? 2 : -2;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FLAG_MAG_MOMENTS: time integrals of |M| and M^2 over the window [t_c, t_w)
+// (the magnetisation is the model's observable).  M(t) is piecewise
+// constant and jumps by dM = +-2 at each committed event, so the integrals
+// need the window's events in global time order: a bucket sort by time
+// (monotone bucket index, then an insertion sort of each bucket by exact
+// time; events at equal times may come in any order, they bound intervals
+// of length 0), a prefix sum of dM from M(t_c), and fixed-order reductions
+// (the result does not depend on the schedule).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int mm_bucket(double t, double t0, double scale, int B) {
+  const int b = (int)__dmul_rn(__dsub_rn(t, t0), scale);
+  return b < 0 ? 0 : b >= B ? B - 1 : b;
+}
+
+__global__ void __launch_bounds__(256) mm_count(const double* t, const unsigned long long* n_total, double t0,
+                                                double scale, int B, unsigned* cnt) {
+  const unsigned long long n = *n_total;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * 256 + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * 256)
+    atomicAdd(&cnt[mm_bucket(t[i], t0, scale, B)], 1u);
+}
+
+// exclusive scan of cnt[0..B) into off[0..B] in one block (B <= 2^22)
+__global__ void __launch_bounds__(1024) mm_scan_buckets(const unsigned* cnt, int B, unsigned* off) {
+  __shared__ unsigned sh[1024];
+  const int per = (B + 1023) / 1024;
+  const int b0 = threadIdx.x * per, b1 = min(B, b0 + per);
+  unsigned sum = 0;
+  for (int b = b0; b < b1; ++b) sum += cnt[b];
+  sh[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const unsigned v = threadIdx.x >= (unsigned)o ? sh[threadIdx.x - o] : 0u;
+    __syncthreads();
+    sh[threadIdx.x] += v;
+    __syncthreads();
+  }
+  unsigned run = sh[threadIdx.x] - sum;
+  for (int b = b0; b < b1; ++b) {
+    off[b] = run;
+    run += cnt[b];
+  }
+  if (threadIdx.x == 1023) off[B] = sh[1023];
+}
+
+__global__ void __launch_bounds__(256) mm_scatter(const double* t, const int8_t* dm, const unsigned long long* n_total,
+                                                  double t0, double scale, int B, const unsigned* off, unsigned* fill,
+                                                  double* ts, int8_t* dms) {
+  const unsigned long long n = *n_total;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * 256 + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * 256) {
+    const int b = mm_bucket(t[i], t0, scale, B);
+    const unsigned p = off[b] + atomicAdd(&fill[b], 1u);
+    ts[p] = t[i];
+    dms[p] = dm[i];
+  }
+}
+
+// each bucket sorted by exact time (insertion sort; a bucket holds ~16 events)
+__global__ void __launch_bounds__(256) mm_sort_buckets(const unsigned* off, int B, double* ts, int8_t* dms) {
+  const int b = blockIdx.x * 256 + threadIdx.x;
+  if (b >= B) return;
+  const unsigned lo = off[b], hi = off[b + 1];
+  for (unsigned i = lo + 1; i < hi; ++i) {
+    const double x = ts[i];
+    const int8_t d = dms[i];
+    unsigned j = i;
+    while (j > lo && ts[j - 1] > x) {
+      ts[j] = ts[j - 1];
+      dms[j] = dms[j - 1];
+      --j;
+    }
+    ts[j] = x;
+    dms[j] = d;
+  }
+}
+
+constexpr int kMmBlocks = 1024;
+// pass 1: sum of dM over each block's fixed chunk of the sorted events
+__global__ void __launch_bounds__(256) mm_chunk_sums(const int8_t* dms, const unsigned long long* n_total,
+                                                     long long* csum) {
+  const long long n = (long long)*n_total;
+  const long long chunk = (n + kMmBlocks - 1) / kMmBlocks;
+  const long long beg = blockIdx.x * chunk, end = min(n, beg + chunk);
+  long long v = 0;
+  for (long long i = beg + threadIdx.x; i < end; i += 256) v += dms[i];
+  __shared__ long long sh[256];
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) csum[blockIdx.x] = sh[0];
+}
+
+// pass 2: each block walks its chunk in tiles of 256 events with a running M
+// (M(t_c) + the dM of all earlier chunks + a block scan), adding
+// |M_k| (t_{k+1} - t_k) and M_k^2 (t_{k+1} - t_k) for the interval after
+// event k (t_n = t_w); fixed per-thread order and a fixed tree per block
+__global__ void __launch_bounds__(256) mm_integrate(const double* ts, const int8_t* dms,
+                                                    const unsigned long long* n_total, const long long* csum,
+                                                    const unsigned long long* M0p, double t_w, double* part) {
+  const long long n = (long long)*n_total;
+  const long long chunk = (n + kMmBlocks - 1) / kMmBlocks;
+  const long long beg = blockIdx.x * chunk, end = min(n, beg + chunk);
+  __shared__ long long carry;
+  __shared__ int wsum[8];
+  if (threadIdx.x == 0) {
+    long long c = (long long)*M0p;
+    for (int j = 0; j < (int)blockIdx.x; ++j) c += csum[j];
+    carry = c;
+  }
+  __syncthreads();
+  double a1 = 0.0, a2 = 0.0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (long long base = beg; base < end; base += 256) {
+    const long long i = base + threadIdx.x;
+    const int d = i < end ? dms[i] : 0;
+    int x = d;  // inclusive block scan of dM
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    int wpre = 0, tile = 0;
+    for (int q = 0; q < 8; ++q) {
+      wpre += q < wid ? wsum[q] : 0;
+      tile += wsum[q];
+    }
+    if (i < end) {
+      const long long M = carry + wpre + x;  // M after event i
+      const double tn = i + 1 < n ? ts[i + 1] : t_w;
+      const double dt = __dsub_rn(tn, ts[i]);
+      const double Md = (double)M;
+      a1 = __dadd_rn(a1, __dmul_rn(fabs(Md), dt));
+      a2 = __dadd_rn(a2, __dmul_rn(__dmul_rn(Md, Md), dt));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tile;
+    __syncthreads();
+  }
+  __shared__ double s1[256], s2[256];
+  s1[threadIdx.x] = a1;
+  s2[threadIdx.x] = a2;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      s1[threadIdx.x] = __dadd_rn(s1[threadIdx.x], s1[threadIdx.x + o]);
+      s2[threadIdx.x] = __dadd_rn(s2[threadIdx.x], s2[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s1[0];
+    part[2 * blockIdx.x + 1] = s2[0];
+  }
+}
+
+// pass 3: the interval before the first event, |M(t_c)| (t_0 - t_c), plus the
+// blocks' partial sums in a fixed tree -> out[0] = int |M| dt, out[1] = int M^2 dt
+__global__ void __launch_bounds__(1024) mm_final(const double* part, const double* ts,
+                                                 const unsigned long long* n_total, const unsigned long long* M0p,
+                                                 double t_c, double t_w, double* out) {
+  __shared__ double s1[1024], s2[1024];
+  s1[threadIdx.x] = part[2 * threadIdx.x];
+  s2[threadIdx.x] = part[2 * threadIdx.x + 1];
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      s1[threadIdx.x] = __dadd_rn(s1[threadIdx.x], s1[threadIdx.x + o]);
+      s2[threadIdx.x] = __dadd_rn(s2[threadIdx.x], s2[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double M0 = (double)(long long)*M0p;
+    const double t0 = *n_total ? ts[0] : t_w;
+    const double dt = __dsub_rn(t0, t_c);
+    out[0] = __dadd_rn(__dmul_rn(fabs(M0), dt), s1[0]);
+    out[1] = __dadd_rn(__dmul_rn(__dmul_rn(M0, M0), dt), s2[0]);
   }
 }
 
@@ -427,6 +616,16 @@ struct ising_sr_ctx {
   unsigned long long* d_edges = nullptr;
   unsigned long long h_edges = 0;
   cudaEvent_t cev0 = nullptr, cev1 = nullptr;  // around the commit's compaction
+  // FLAG_MAG_MOMENTS: dM per logged event, the time-sorted copy, buckets, partial sums
+  int8_t* log_dm = nullptr;
+  double* mm_ts = nullptr;
+  int8_t* mm_dm = nullptr;
+  unsigned* mm_cnt = nullptr;  // [2 * mm_B + 1]: counts / fill, then offsets
+  unsigned* mm_off = nullptr;
+  int mm_B = 0;
+  long long* mm_csum = nullptr;
+  double* mm_part = nullptr;   // [2 * kMmBlocks + 2]
+  double h_mm[2] = {0.0, 0.0};
   // log
   double* log_t = nullptr;
   uint32_t* log_region = nullptr;
@@ -936,6 +1135,43 @@ ising_sr_status run_window_pipelined(ising_sr_ctx* c) {
   }
 }
 
+// FLAG_MAG_MOMENTS: the window's int |M| dt and int M^2 dt into c->h_mm
+// (enqueued; read after the commit's synchronisation).  n = events of the
+// window (the log is complete on the stream).
+ising_sr_status mag_moments(ising_sr_ctx* c, long long n) {
+  int B = 1024;
+  while (B < (1 << 22) && (long long)B * 16 < n) B <<= 1;
+  if (B > c->mm_B) {
+    dfree(c, c->mm_cnt);
+    c->mm_cnt = nullptr;
+    if (dmalloc(c, &c->mm_cnt, 3 * (size_t)B + 1) != cudaSuccess) return ISING_SR_E_OOM;
+    c->mm_B = B;
+  }
+  if (!c->mm_csum && (dmalloc(c, &c->mm_csum, kMmBlocks) != cudaSuccess ||
+                      dmalloc(c, &c->mm_part, 2 * kMmBlocks + 2) != cudaSuccess))
+    return ISING_SR_E_OOM;
+  unsigned* cnt = c->mm_cnt;
+  unsigned* fill = cnt + B;
+  unsigned* off = cnt + 2 * B;
+  CK(c, cudaMemsetAsync(cnt, 0, 2 * (size_t)B * sizeof(unsigned), c->stream));
+  const double scale = (double)B / (c->t_w - c->t_c);
+  mm_count<<<148 * 4, 256, 0, c->stream>>>(c->log_t, c->d_total, c->t_c, scale, B, cnt);
+  mm_scan_buckets<<<1, 1024, 0, c->stream>>>(cnt, B, off);
+  mm_scatter<<<148 * 4, 256, 0, c->stream>>>(c->log_t, c->log_dm, c->d_total, c->t_c, scale, B, off, fill, c->mm_ts,
+                                             c->mm_dm);
+  mm_sort_buckets<<<(B + 255) / 256, 256, 0, c->stream>>>(off, B, c->mm_ts, c->mm_dm);
+  mm_chunk_sums<<<kMmBlocks, 256, 0, c->stream>>>(c->mm_dm, c->d_total, c->mm_csum);
+  mm_integrate<<<kMmBlocks, 256, 0, c->stream>>>(c->mm_ts, c->mm_dm, c->d_total, c->mm_csum, c->d_snap, c->t_w,
+                                                 c->mm_part);
+  mm_final<<<1, 1024, 0, c->stream>>>(c->mm_part, c->mm_ts, c->d_total, c->d_snap, c->t_c, c->t_w,
+                                      c->mm_part + 2 * kMmBlocks);
+  c->launches += 7;
+  CK(c, cudaGetLastError());
+  CK(c, cudaMemcpyAsync(c->h_mm, c->mm_part + 2 * kMmBlocks, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  (void)n;
+  return ISING_SR_OK;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -985,6 +1221,12 @@ void ising_sr_destroy(ising_sr_ctx* c) {
   dfree(c, c->d_stats);
   dfree(c, c->ev_t);
   dfree(c, c->ev_s);
+  dfree(c, c->log_dm);
+  dfree(c, c->mm_ts);
+  dfree(c, c->mm_dm);
+  dfree(c, c->mm_cnt);
+  dfree(c, c->mm_csum);
+  dfree(c, c->mm_part);
   dfree(c, c->d_replay);
   dfree(c, c->d_nrep);
   dfree(c, c->d_edges);
@@ -1042,6 +1284,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   if (RY % world) return ISING_SR_E_PARTITION;
   if ((long long)RX * RY > 0x7fffffffLL) return ISING_SR_E_INVALID_ARG;
   const bool loopback = (cfg->flags & ISING_SR_FLAG_HALO_LOOPBACK) != 0;
+  if ((cfg->flags & ISING_SR_FLAG_MAG_MOMENTS) && world != 1) return ISING_SR_E_INVALID_ARG;  // needs the global order
   if (loopback && (world != 1 || !cfg->nccl_id)) return ISING_SR_E_INVALID_ARG;
   if (world > 1 && !cfg->nccl_id && !cfg->exchange) {
     // only the step-level API can drive such a ctx (the caller moves the ghost rows)
@@ -1052,6 +1295,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   if (!c) return ISING_SR_E_OOM;
   c->cfg = *cfg;
   c->cfg.world = world;
+  if (c->cfg.flags & ISING_SR_FLAG_MAG_MOMENTS) c->cfg.flags |= ISING_SR_FLAG_LOG_EVENTS | ISING_SR_FLAG_OBSERVABLES;
   if (!(cfg->W > 0.0)) {  // the paper's T_max = ln N / (lambda |dG_i|)
     double lam = 0.0;
     for (double r : cfg->rate) lam = std::max(lam, r);
@@ -1073,7 +1317,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   if (const char* e = std::getenv("ISING_SR_PIPELINE")) c->pipeline = std::atoi(e) != 0;
   if (const char* e = std::getenv("ISING_SR_REFILL")) c->refill = std::max(1, std::min(32, std::atoi(e)));
   if (const char* e = std::getenv("ISING_SR_K1_DELAY_NS")) c->delay_ns = (unsigned)std::max(0, std::atoi(e));
-  if ((cfg->flags & ISING_SR_FLAG_OBSERVABLES) && ops->warp && !big_enabled()) {
+  if ((c->cfg.flags & ISING_SR_FLAG_OBSERVABLES) && ops->warp && !big_enabled()) {
     delete c;
     return ISING_SR_E_INVALID_ARG;  // observables are accumulated by the lane-per-region K1 forms only
   }
@@ -1095,7 +1339,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
         dmalloc_bytes(c, (void**)&s.halo, n * ops->halo_bytes) != cudaSuccess || dmalloc(c, &s.ts, n) != cudaSuccess ||
         dmalloc(c, &s.R, n) != cudaSuccess || dmalloc(c, &s.n, n) != cudaSuccess || dmalloc(c, &s.dig, n) != cudaSuccess)
       return bail(ISING_SR_E_OOM);
-    if ((cfg->flags & ISING_SR_FLAG_OBSERVABLES) &&
+    if ((c->cfg.flags & ISING_SR_FLAG_OBSERVABLES) &&
         (dmalloc(c, &s.oM, n) != cudaSuccess || dmalloc(c, &s.oB, n) != cudaSuccess))
       return bail(ISING_SR_E_OOM);
   }
@@ -1123,7 +1367,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
     if (cudaEventCreate(&e) != cudaSuccess) return bail(ISING_SR_E_CUDA);
   for (auto& e : c->pev)
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return bail(ISING_SR_E_CUDA);
-  if (cfg->flags & ISING_SR_FLAG_LOG_EVENTS) {
+  if (c->cfg.flags & ISING_SR_FLAG_LOG_EVENTS) {
     // scratch event log: events per region per window at the largest rate,
     // at most 16 (a region with more is replayed at commit); the replay list
     double rmax = 0.0;
@@ -1192,7 +1436,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   }
   ops->init(dbuf, Lx, RX, c->RYl, c->row0, cfg->seed, cfg->eq_quantum, c->st[0], c->stream);
   c->launches++;
-  if ((cfg->flags & ISING_SR_FLAG_OBSERVABLES) && enqueue_snapshot(c, c->st[0]) != ISING_SR_OK)
+  if ((c->cfg.flags & ISING_SR_FLAG_OBSERVABLES) && enqueue_snapshot(c, c->st[0]) != ISING_SR_OK)
     return bail(ISING_SR_E_CUDA);
   cudaError_t e = cudaStreamSynchronize(c->stream);
   dfree(c, dbuf);
@@ -1338,6 +1582,7 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
   }
   CK(c, cudaGetLastError());
   const bool obs = (c->cfg.flags & ISING_SR_FLAG_OBSERVABLES) != 0;
+  const bool mag = (c->cfg.flags & ISING_SR_FLAG_MAG_MOMENTS) != 0;
   if (obs) {  // the window's int M dt, int B dt: fixed-order sums of the regions' integrals
     obs_partial<<<kObsBlocks, 256, 0, c->stream>>>(s1.oM, s1.oB, c->nreg, c->d_obs);
     obs_final<<<1, 256, 0, c->stream>>>(c->d_obs, c->d_obs + 2 * kObsBlocks);
@@ -1345,8 +1590,10 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
     CK(c, cudaGetLastError());
     CK(c, cudaMemcpyAsync(c->h_obs, c->d_obs + 2 * kObsBlocks, 2 * sizeof(double), cudaMemcpyDeviceToHost,
                           c->stream));
-    ising_sr_status ss = enqueue_snapshot(c, s1);  // the configuration at the new committed time
-    if (ss) return ss;
+    if (!mag) {  // (with MAG_MOMENTS after the moments, which start from M(t_c))
+      ising_sr_status ss = enqueue_snapshot(c, s1);  // the configuration at the new committed time
+      if (ss) return ss;
+    }
   }
   unsigned long long total = 0;
   CK(c, cudaMemcpyAsync(&total, c->d_total, sizeof total, cudaMemcpyDeviceToHost, c->stream));
@@ -1354,15 +1601,20 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
   c->win_events = total;
   if (log) {
     if ((long long)total > c->log_cap) {
-      dfree(c, c->log_t);
-      dfree(c, c->log_region);
-      dfree(c, c->log_site);
+      for (void* q : {(void*)c->log_t, (void*)c->log_region, (void*)c->log_site, (void*)c->log_dm,
+                      (void*)c->mm_ts, (void*)c->mm_dm})
+        dfree(c, q);
       c->log_t = nullptr;
       c->log_region = nullptr;
       c->log_site = nullptr;
+      c->log_dm = nullptr;
+      c->mm_ts = nullptr;
+      c->mm_dm = nullptr;
       const long long cap = std::max<long long>((long long)total * 5 / 4 + 1024, c->log_cap * 2);
       if (dmalloc(c, &c->log_t, cap) != cudaSuccess || dmalloc(c, &c->log_region, cap) != cudaSuccess ||
-          dmalloc(c, &c->log_site, cap) != cudaSuccess) {
+          dmalloc(c, &c->log_site, cap) != cudaSuccess ||
+          (mag && (dmalloc(c, &c->log_dm, cap) != cudaSuccess || dmalloc(c, &c->mm_ts, cap) != cudaSuccess ||
+                   dmalloc(c, &c->mm_dm, cap) != cudaSuccess))) {
         cudaGetLastError();
         c->log_cap = 0;
         return ISING_SR_E_OOM;
@@ -1377,7 +1629,7 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
     CK(c, cudaMemsetAsync(c->d_edges, 0, sizeof(unsigned long long), c->stream));
     compact_log_kernel<<<(c->nreg + 255) / 256, 256, 0, c->stream>>>(
         s1.n, s0.n, c->nreg, c->d_off, c->ev_t, c->ev_s, (long long)c->nreg, c->evC, c->RX, c->row0, c->log_t,
-        c->log_region, c->log_site, c->d_replay, c->d_nrep);
+        c->log_region, c->log_site, mag ? c->log_dm : nullptr, c->d_replay, c->d_nrep);
     c->launches++;
     CK(c, cudaGetLastError());
     KArgs a = base_args(c, c->Kglob + 1, false);
@@ -1388,6 +1640,7 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
     a.log_t = c->log_t;
     a.log_region = c->log_region;
     a.log_site = c->log_site;
+    a.log_dm = mag ? c->log_dm : nullptr;
     a.log_off = c->d_off;
     c->ops->replay(a, 148 * 4 * kThreads, c->stream);  // a fixed grid; tiles sized on the device
     c->launches++;
@@ -1401,6 +1654,11 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
     CK(c, cudaMemcpyAsync(&c->h_edges, c->d_edges, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
     c->log_n = (long long)total;
     c->win_bytes += (double)total * 14.0 + (double)c->nreg * 8.0;
+    if (mag) {  // int |M| dt, int M^2 dt over [t_c, t_w): the log in time order
+      ising_sr_status ms_ = mag_moments(c, (long long)total);
+      if (ms_) return ms_;
+      if ((ms_ = enqueue_snapshot(c, s1))) return ms_;
+    }
   }
   CK(c, cudaEventRecord(c->ev1, c->stream));
   CK(c, cudaEventSynchronize(c->ev1));
@@ -1428,6 +1686,12 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
     c->stats.ms_compact_total += cms;
     c->stats.edge_entries_last_window = (int64_t)c->h_edges;
     c->stats.log_replayed_last_window = (int64_t)c->h_nrep;
+  }
+  if (mag) {
+    c->stats.obs_absM_last = c->h_mm[0];
+    c->stats.obs_M2_last = c->h_mm[1];
+    c->stats.obs_absM_total += c->h_mm[0];
+    c->stats.obs_M2_total += c->h_mm[1];
   }
   if (obs) {
     c->stats.obs_M_last = c->h_obs[0];

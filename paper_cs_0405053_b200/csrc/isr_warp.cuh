@@ -248,18 +248,20 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
         if (lane == sr) row ^= 1u << sc;
         if (a.digest)
           dig = digest_step(dig, tc, site);
+        const unsigned up_new = (__shfl_sync(0xffffffffu, row, sr) >> sc) & 1u;  // the new spin (for dM)
         if (LOG) {
           if (lane == 0) {
             const unsigned long long o = a.log_off[idx] + n_ev_r;
             a.log_t[o] = tc;
             a.log_region[o] = gid;
             a.log_site[o] = (uint16_t)site;
+            if (a.log_dm) a.log_dm[o] = up_new ? 2 : -2;
           }
         } else {
           if (lane == 0 && a.ev_t && (int)n_ev_r < a.evC) {  // scratch event log
             const long long o = (long long)n_ev_r * a.ev_stride + idx;
             a.ev_t[o] = tc;
-            a.ev_s[o] = (uint16_t)site;
+            a.ev_s[o] = (uint16_t)(site | (up_new << 15));
           }
           bool on_edge = false;
 #pragma unroll
