@@ -173,3 +173,57 @@ def test_paper_window_tmax(b):
     sim.commit()
     assert sim.stats()["t_c"] == min(W, 2.0)
     sim.close()
+
+
+# ---------------------------------------------------------------------------
+# FLAG_MAG_MOMENTS: int |M| dt and int M^2 dt per
+# window from the device time sort of the committed log, against the
+# oracle's integrals over the global M(t) (ising_oracle.c obs[3], obs[4];
+# only the summation order differs: relative 1e-9), on lane and big regions
+# and with forced replays; and the time average of |M| against Onsager's m0
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("geom", [
+    (32, 32, 4, 4, 2.269, 0.0, 0.5, 4.0, 0), (24, 24, 2, 2, 1.8, 0.2, 0.7, 3.0, 0), (16, 16, 1, 1, 3.0, 0.0, 0.4, 2.0, 0),
+    (32, 32, 8, 8, 2.0, 0.0, 0.6, 4.0, 0), (64, 64, 16, 16, 2.269, 0.0, 1.0, 3.0, 0), (32, 32, 4, 4, 2.0, 0.1, 0.5, 3.0, 1),
+])
+def test_magnetisation_moments_against_oracle(geom):
+    from paper_cs_0405053_b200 import FLAG_MAG_MOMENTS
+    Lx, Ly, bx, by, T, H, W, t_end, cap = geom
+    w = workloads.Workload("mm", Lx, Ly, bx, by, T=T, H=H, W=W, t_end=t_end, seed=2)
+    sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed,
+                  flags=FLAG_DIGEST | FLAG_MAG_MOMENTS, log_capacity=cap)
+    sim.run()
+    st = sim.stats()
+    dig, _ = sim.digests()
+    sim.close()
+    ref = oracle.des_workload(w)
+    assert np.array_equal(dig, ref["digest"])
+    scale1 = Lx * Ly * t_end
+    assert abs(st["obs_absM_total"] - ref["obs"][3]) < 1e-9 * scale1, (st["obs_absM_total"], ref["obs"][3])
+    assert abs(st["obs_M2_total"] - ref["obs"][4]) < 1e-9 * scale1 * Lx * Ly, (st["obs_M2_total"], ref["obs"][4])
+    assert abs(st["obs_M_total"] - ref["obs"][2]) < 1e-9 * scale1
+
+
+def test_magnetisation_moments_onsager():
+    """256^2 at T = 2 from all up: the time average of |m| over t in [20, 60)
+    against Onsager's spontaneous magnetisation (correlation length ~2)."""
+    from paper_cs_0405053_b200 import FLAG_MAG_MOMENTS
+    T = 2.0
+    m0 = (1 - math.sinh(2 / T) ** -4) ** 0.125
+    w = workloads.Workload("ons", 256, 256, 4, 4, T=T, W=0.5, t_end=60.0, init="up", seed=3)
+    sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed, flags=FLAG_MAG_MOMENTS)
+    for _ in range(40):
+        sim.run_window()
+        sim.commit()
+    a = sim.stats()
+    sim.run()
+    b = sim.stats()
+    sim.close()
+    n = 256 * 256
+    tt = b["obs_time_total"] - a["obs_time_total"]
+    absm = (b["obs_absM_total"] - a["obs_absM_total"]) / (n * tt)
+    m2 = (b["obs_M2_total"] - a["obs_M2_total"]) / (n * n * tt)
+    assert tt == pytest.approx(40.0)
+    assert abs(absm - m0) < 0.01, (absm, m0)
+    assert m2 >= absm ** 2 - 1e-12  # <m^2> >= <|m|>^2
+    assert abs(math.sqrt(m2) - m0) < 0.012

@@ -14,7 +14,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import workloads  # noqa: E402
-from paper_cs_0405053_b200 import FLAG_DIGEST, IsingSR  # noqa: E402
+from paper_cs_0405053_b200 import FLAG_DIGEST, FLAG_LOG_EVENTS, IsingSR  # noqa: E402
 
 
 def main():
@@ -29,8 +29,7 @@ def main():
     if args.W:
         w = w.replace(W=args.W)
     torch.cuda.set_device(0)
-    sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed, flags=FLAG_DIGEST,
-                  stream=torch.cuda.current_stream().cuda_stream)
+    sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed, flags=FLAG_DIGEST | FLAG_LOG_EVENTS)
     for _ in range(args.skip):
         sim.run_window()
         sim.commit()
@@ -57,7 +56,10 @@ def main():
                 sim.end_iterations(it)
                 break
         ev = sim.commit()
-        out.append({"window": args.skip + k, "events": ev, "iters": rows})
+        st = sim.stats()
+        S = w.bx * w.by / 8 + (2 * w.bx + 2 * w.by) / 8 + 20  # SURVEY §8(d.3) committed state bytes
+        out.append({"window": args.skip + k, "events": ev, "iters": rows, "nreg": sim.n_regions,
+                    "h": st["edge_entries_last_window"], "S": S})
     print(json.dumps(out, indent=1))
 
 

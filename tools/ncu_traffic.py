@@ -37,17 +37,24 @@ def main():
     prof = json.loads(txt[txt.index("["):txt.rindex("]") + 1])
     iters = prof[0]["iters"]
     n = min(len(iters), len(launches))
-    alg = [iters[i]["MB"] * 1e6 for i in range(n)]
+    # a recomputation moves S + 3H, H = 4 + 9 h (h = the
+    # window's boundary-history entries per region)
+    S, h = prof[0]["S"], prof[0]["h"] / prof[0]["nreg"]
+    per_rec = S + 3 * (4 + 9 * h)
+    alg = [iters[i]["regions"] * per_rec for i in range(n)]
+    impl = [iters[i]["MB"] * 1e6 for i in range(n)]
     dram = [launches[i]["read"] + launches[i]["write"] for i in range(n)]
     res = {
         "kernel": rows[2][iname], "window": prof[0]["window"], "launches": n,
         "dram_bytes_per_launch": sum(dram) / n, "alg_bytes_per_launch": sum(alg) / n,
         "dram_over_alg": sum(dram) / sum(alg),
+        "dram_over_impl": sum(dram) / sum(impl), "alg_bytes_per_recomputation": per_rec,
         "per_launch": [{"iteration": i + 1, "regions": iters[i]["regions"], "alg_bytes": alg[i],
                         "dram_read": launches[i]["read"], "dram_write": launches[i]["write"],
                         "ncu_ms": launches[i]["ms"]} for i in range(n)],
         "note": "ncu --set full --clock-control none: one capture of every K1 launch of one c4 window "
-                "(cold caches, serialised); algorithmic bytes from the library's own count (DESIGN.md §6)",
+                "(cold caches, serialised); algorithmic bytes = SURVEY §8(d.3) A (S + 3H) with the window's "
+                "measured h; dram_over_impl against the library's own count of touched bytes (DESIGN.md §6)",
     }
     json.dump(res, open(out, "w"), indent=1)
     if md:
