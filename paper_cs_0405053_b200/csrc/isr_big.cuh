@@ -43,7 +43,7 @@ struct BigRegion {
   int t;                 // column (thread index)
   bool wrapX, wrapY;
   uint32_t gN, gS, gW, gE;  // ghost row above / below (bit = column), ghost columns (bit = row)
-  uint32_t Nw[5];           // class counts: N_k in half-word k & 1 of Nw[k >> 1]
+  unsigned long long Nq[2];  // class counts: N_k in the 12-bit field k % 5 of Nq[k / 5] (N_k <= 1024)
 
   __device__ __forceinline__ uint32_t row(int r) const { return S.rows[r][t]; }
   __device__ __forceinline__ uint32_t above(int r) const {
@@ -91,7 +91,9 @@ struct BigRegion {
     const uint32_t ue = c < BX - 1 ? (rw >> (c + 1)) & 1u : ebit(r, rw);
     return (int)(5u * s + un + us + uw + ue);
   }
-  __device__ __forceinline__ int N(int k) const { return (int)((Nw[k >> 1] >> (16 * (k & 1))) & 0xFFFFu); }
+  __device__ __forceinline__ int N(int k) const {
+    return (int)((Nq[k >= 5 ? 1 : 0] >> (12 * (k >= 5 ? k - 5 : k))) & 0xFFFull);
+  }
   // FLAG_OBSERVABLES: spins of the owned-bond partners of site (r, c) -- north
   // and west always (in-region, wrapped, or the ghost), south and east only
   // inside the region or wrapped (the bonds across the south/east border
@@ -128,9 +130,10 @@ struct BigRegion {
   }
   // N_k += d and the row count of class k in row r += d (d = +-1)
   __device__ __forceinline__ void add(int k, int r, int d) {
-    const uint32_t inc = (uint32_t)d << (16 * (k & 1));
-#pragma unroll
-    for (int i = 0; i < 5; ++i) Nw[i] += (k >> 1) == i ? inc : 0u;
+    const bool hi = k >= 5;
+    const unsigned long long inc = (unsigned long long)(long long)d << (12 * (hi ? k - 5 : k));
+    Nq[0] += hi ? 0ull : inc;  // two's complement: a -1 borrows only inside the (nonzero) field
+    Nq[1] += hi ? inc : 0ull;
     S.rc[k][r >> 2][t] += (uint32_t)d << (8 * (r & 3));
   }
   // a site whose up-neighbour count changes by du (spin unchanged)
@@ -179,32 +182,40 @@ __device__ __forceinline__ int big_select(const BigRegion<BX, BY>& B, const doub
   if (j > nk - 1) j = nk - 1;
   if (j < 0) j = 0;
   int jj = (int)j;
-  // skip whole groups of 4 rows, then rows, using the per-row counts
-  int r = 0;
+  // skip whole groups of 4 rows, then rows, using the per-row counts: the
+  // class's RQ count words are read at once (independent loads), then the
+  // group holding the j-th site is found with a branch-free scan
   constexpr int RQ = BigSmem<BX, BY>::RQ;
+  uint32_t wq[RQ];
+#pragma unroll
+  for (int q = 0; q < RQ; ++q) wq[q] = B.S.rc[ks][q][B.t];
+  int qs = RQ - 1;
+  uint32_t w = wq[RQ - 1];
+  bool found = false;
+#pragma unroll
   for (int q = 0; q < RQ; ++q) {
-    const uint32_t w = B.S.rc[ks][q][B.t];
-    const int s = (int)((w * 0x01010101u) >> 24);  // sum of the 4 byte counts (<= 128)
-    if (jj < s) {
-      int c0 = (int)(w & 0xFFu);
-      r = 4 * q;
+    const int s = (int)((wq[q] * 0x01010101u) >> 24);  // sum of the 4 byte counts (<= 128)
+    const bool here = !found && jj < s;
+    qs = here ? q : qs;
+    w = here ? wq[q] : w;
+    jj -= (!found && !here) ? s : 0;
+    found = found || here;
+  }
+  int r = 4 * qs;
+  int c0 = (int)(w & 0xFFu);
+  if (jj >= c0) {
+    jj -= c0;
+    ++r;
+    c0 = (int)((w >> 8) & 0xFFu);
+    if (jj >= c0) {
+      jj -= c0;
+      ++r;
+      c0 = (int)((w >> 16) & 0xFFu);
       if (jj >= c0) {
         jj -= c0;
         ++r;
-        c0 = (int)((w >> 8) & 0xFFu);
-        if (jj >= c0) {
-          jj -= c0;
-          ++r;
-          c0 = (int)((w >> 16) & 0xFFu);
-          if (jj >= c0) {
-            jj -= c0;
-            ++r;
-          }
-        }
       }
-      break;
     }
-    jj -= s;
   }
   return r * BX + nth_bit<uint32_t, 32>(B.class_mask(r, ks), jj);
 }
@@ -236,7 +247,7 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
     const int r = idx / a.RX, c = idx - r * a.RX;
     const uint32_t gid = (uint32_t)((a.row0 + r) * a.RX + c);
     ++n_reg;
-    BR B{SM, t, wrapX, wrapY, 0u, 0u, 0u, 0u, {0u, 0u, 0u, 0u, 0u}};
+    BR B{SM, t, wrapX, wrapY, 0u, 0u, 0u, 0u, {0ull, 0ull}};
     // ---- committed state ----
     {
       const uint32_t* src = (const uint32_t*)a.in.spins + (long long)idx * BY;
@@ -250,6 +261,33 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
     }
     double ts = a.fresh_w ? a.t_c : a.in.ts[idx], R = a.in.R[idx];
     uint32_t n = a.in.n[idx];
+    // the paper's presimulated list ("reuse the random numbers"):
+    // the window's pairs of this region, (E(U_m), V_m) for m = n0, n0 + 1, ...,
+    // are kept from the recomputation that first drew them, so that the
+    // following recomputations of the window read them instead of drawing
+    const uint32_t n0 = n;
+    unsigned pfill = 0;
+    if (a.pcache) {
+      const uint2 pm = a.pmeta[idx];
+      pfill = pm.x == K0 ? pm.y : 0u;
+    }
+    const long long pbase = (long long)idx * a.PC;
+    auto get_pair = [&](uint32_t m, double& E, double& Vm) {
+      const unsigned q = m - n0;
+      if (a.pcache && q < pfill) {
+        const double2 c = a.pcache[pbase + q];
+        E = c.x;
+        Vm = c.y;
+      } else {
+        double Um;
+        draw_pair(a.seed, gid, m, Um, Vm, a.gen);
+        E = budget(a, Um);
+        if (a.pcache && q == pfill && q < (unsigned)a.PC) {
+          a.pcache[pbase + q] = make_double2(E, Vm);
+          ++pfill;
+        }
+      }
+    };
     unsigned long long dig = a.digest ? a.in.dig[idx] : 0ull;
     unsigned n_ev_r = 0, bev = 0;
     // FLAG_OBSERVABLES: M and the owned bond sum B now, their integrals since t_c
@@ -452,7 +490,7 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
 #pragma unroll
       for (int k = 0; k < 10; ++k) {
         SM.rc[k][q][t] = w[k];
-        B.Nw[k >> 1] += ((w[k] * 0x01010101u) >> 24) << (16 * (k & 1));
+        B.Nq[k >= 5 ? 1 : 0] += (unsigned long long)((w[k] * 0x01010101u) >> 24) << (12 * (k >= 5 ? k - 5 : k));
       }
     }
 
@@ -480,18 +518,14 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
       }
     }
 
-    double U, V;
-    draw_pair(a.seed, gid, n, U, V, a.gen);
-    if (a.fresh_w && lpos == 0) R = budget(a, U);  // the slate is wiped at t_c; a replay restored R
+    double E0, V;
+    get_pair(n, E0, V);
+    if (a.fresh_w && lpos == 0) R = E0;  // the slate is wiped at t_c; a replay restored R
     // pair n+1 drawn one event ahead: an event takes its new budget and atom
     // variate from here and draws the following pair off the step's critical
     // path (the region's serial step chain bounds every iteration, §6)
     double Rn, Vn;
-    {
-      double Un;
-      draw_pair(a.seed, gid, n + 1, Un, Vn, a.gen);
-      Rn = budget(a, Un);
-    }
+    get_pair(n + 1, Rn, Vn);
     double lam = big_fold(B, a.rate);
     double tc = cand_time(ts, R, lam);
 
@@ -583,11 +617,7 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
         // its instructions interleave with the flip's bookkeeping below
         R = Rn;
         V = Vn;
-        {
-          double Un;
-          draw_pair(a.seed, gid, n + 2, Un, Vn, a.gen);
-          Rn = budget(a, Un);
-        }
+        get_pair(n + 2, Rn, Vn);
         const int sr = site / BX, sc = site - sr * BX;
         code = (unsigned)site;
         if (OBS && !LOG) {
@@ -681,6 +711,7 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
     n_ev += n_ev_r;
     fmax = max(fmax, bev);
     if (!LOG && a.resume) a.lg_meta[idx] = make_uint2(K, lpos <= (unsigned)a.LC ? lpos : 0xffffffffu);
+    if (!LOG && a.pcache) a.pmeta[idx] = make_uint2(K0, pfill);
 
     if (!LOG && a.delay_ns) k1_delay(a.delay_ns);  // test knob: publish late
     if (!LOG) {

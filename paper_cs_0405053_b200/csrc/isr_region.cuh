@@ -107,6 +107,12 @@ struct KArgs {
   uint2* lg_meta;          // per region: {stamp of the recomputation that wrote the log, length}
   int LC;                  // log capacity (steps) per region
   int resume;
+  // big-region kernel: the window's pairs (E(U_m), V_m) per region, m = n0 ..
+  // n0 + fill - 1 (the paper's presimulated list); pmeta = {stamp
+  // of the window's first iteration, fill}
+  double2* pcache;
+  uint2* pmeta;
+  int PC;
   const uint32_t* wl_in;   // regions to recompute (nullptr: all regions)
   int n_work;              // number of regions to recompute
   const unsigned* n_work_dev;  // if set: the number is read here on the device (pool kernel)

@@ -590,6 +590,9 @@ struct ising_sr_ctx {
   uint2* lg_meta = nullptr;
   int LC = 0;
   bool resume = true;  // env ISING_SR_RESUME=0 disables
+  double2* pcache = nullptr;  // big-region kernel: the window's pairs per region (env ISING_SR_PCACHE=0 disables)
+  uint2* pmeta = nullptr;
+  int PC = 0;
   uint32_t* dirty = nullptr;          // dirty-region bitmaps [2][dwords] (iteration parity)
   int dwords = 0;
   uint32_t* wl[2] = {nullptr, nullptr};
@@ -828,6 +831,9 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   a.lg_meta = c->lg_meta;
   a.LC = c->LC;
   a.resume = (c->resume && c->lg_meta) ? 1 : 0;
+  a.pcache = c->pcache;
+  a.pmeta = c->pmeta;
+  a.PC = c->PC;
   a.refill = c->refill;
   a.delay_ns = c->delay_ns;
   {
@@ -1214,6 +1220,8 @@ void ising_sr_destroy(ising_sr_ctx* c) {
   dfree(c, c->lg_tR);
   dfree(c, c->lg_c);
   dfree(c, c->lg_meta);
+  dfree(c, c->pcache);
+  dfree(c, c->pmeta);
   dfree(c, c->wl[0]);
   dfree(c, c->wl[1]);
   dfree(c, c->d_wlc);
@@ -1405,6 +1413,30 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
         c->lg_tR = nullptr; c->lg_c = nullptr; c->lg_meta = nullptr;
         c->LC = 0;
       } else if (cudaMemsetAsync(c->lg_meta, 0, n * sizeof(uint2), c->stream) != cudaSuccess) {
+        return bail(ISING_SR_E_CUDA);
+      }
+    }
+  }
+  bool pcache_on = true;
+  if (const char* e = std::getenv("ISING_SR_PCACHE")) pcache_on = std::atoi(e) != 0;
+  if (ops->warp && big_enabled() && pcache_on) {
+    // the window's pairs per region: 1.25 x the expected events at the
+    // largest rate + slack, capped at 8192 and at 24 GB in all (a region
+    // with more events draws the rest)
+    double rmax = 0.0;
+    for (double r : cfg->rate) rmax = std::max(rmax, r);
+    const double Wd = std::min(c->cfg.W, std::max(cfg->t_end, 1e-9));
+    long long PC = (long long)std::ceil(1.25 * cfg->bx * cfg->by * rmax * Wd) + 32;
+    PC = std::min<long long>(PC, 8192);
+    PC = std::min<long long>(PC, (24LL << 30) / (16LL * std::max(1, c->nreg)));
+    if (PC >= 8) {
+      c->PC = (int)PC;
+      if (dmalloc(c, &c->pcache, (size_t)c->nreg * (size_t)PC) != cudaSuccess || dmalloc(c, &c->pmeta, n) != cudaSuccess) {
+        cudaGetLastError();
+        dfree(c, c->pcache); dfree(c, c->pmeta);
+        c->pcache = nullptr; c->pmeta = nullptr;
+        c->PC = 0;
+      } else if (cudaMemsetAsync(c->pmeta, 0, n * sizeof(uint2), c->stream) != cudaSuccess) {
         return bail(ISING_SR_E_CUDA);
       }
     }
