@@ -221,7 +221,9 @@ def run_ising(args):
     nwin = args.warmup + args.steps
     t_end = max(w.t_end, nwin * w.W)
     spins = w.spins()
-    flags = FLAG_DIGEST | FLAG_LOG_EVENTS  # the commit compacts the window's event log (K3) inside the timed region
+    # the commit compacts the window's event log (K3) inside the timed region;
+    # per-region digests (a verification device, R27) only with --digest
+    flags = FLAG_LOG_EVENTS | (FLAG_DIGEST if args.digest else 0)
     if args.jacobi_all:
         from paper_cs_0405053_b200 import FLAG_JACOBI_ALL
         flags |= FLAG_JACOBI_ALL
@@ -274,7 +276,6 @@ def run_ising(args):
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
         tot_ev, max_ms = int(t[0].item()), float(m[0].item())
         k1_bytes, alg_bytes, impl_bytes = (float(x) for x in t[1:].tolist())
-    digest, count = sim.digests()
     sim.close()
 
     # e2e: the public API from host buffers -- init (H2D of the lattice from
@@ -350,6 +351,7 @@ def run_ising(args):
                    "regions": w.n_regions, "l2": "inputs larger than L2 (state+histories >> 126 MB)",
                    "schedule": "jacobi_all" if args.jacobi_all else "worklist",
                    "event_log": "compacted at every commit (FLAG_LOG_EVENTS), in the timed region",
+                   "digests": bool(args.digest),
                    "parallelism": f"strips{world}"},
         "events": tot_ev,
         "iterations_per_window": {"mean": float(np.mean(gs)), "p50": float(np.percentile(gs, 50)),
@@ -465,6 +467,7 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--digest", action="store_true", help="also maintain the per-region event digests")
     ap.add_argument("--window", default="config", choices=["config", "tmax"],
                     help="W of the config, or the paper's T_max = ln N/(lambda |dG|) (P:502-515)")
     ap.add_argument("--jacobi-all", action="store_true",

@@ -309,61 +309,12 @@ __device__ __forceinline__ long long floor_div(double aq, double rk, double rinv
   return jl == jh ? jl : __double2ll_rd(__ddiv_rn(aq, rk));
 }
 
-// eq. biglambda, fixed fold order (R3): c_k = c_{k-1} + N_k r_k
-template <class G>
-__device__ __forceinline__ double fold_lambda(const Classes<G>& C, const ProdTable<G>& T) {
-  double c = 0.0;
-#pragma unroll
-  for (int k = 0; k < 10; ++k) c = __dadd_rn(c, T.at(k, popc_m(C.mask(k))));
-  return c;
-}
-
-// Phases 2-3 of atom selection (eqs. Wsum, Wstop, nores, vindex)
-// in x = V*Lambda space: k* = first k with x <= c_k,
-// j = min(floor((x - c_{k*-1}) / r_k*), N_k* - 1); returns the local site.
-// One pass: the fold's partial sums are compared with x as they are formed,
-// and the class mask of k* is captured on the way.
-template <class G>
-__device__ __forceinline__ int select_site2(const Classes<G>& C, const ProdTable<G>& T, const double* rate,
-                                            double V, double lam) {
-  using M = typename G::M;
-  const double x = __dmul_rn(V, lam);
-  double c = 0.0, cprev = 0.0;
-  int ks = -1, lastnz = 0;
-  M mk = 0, mlast = C.mask(0);
-#pragma unroll
-  for (int k = 0; k < 10; ++k) {
-    const M m = C.mask(k);
-    const int nk = popc_m(m);
-    const double cn = __dadd_rn(c, T.at(k, nk));
-    const bool hit = ks < 0 && x <= cn;
-    ks = hit ? k : ks;
-    cprev = hit ? c : cprev;
-    mk = hit ? m : mk;
-    lastnz = nk > 0 ? k : lastnz;
-    mlast = nk > 0 ? m : mlast;
-    c = cn;
-  }
-  if (ks < 0) {  // unreachable for V < 1 (x <= Lambda = c_9)
-    ks = lastnz;
-    mk = mlast;
-    cprev = 0.0;
-  }
-  const int nk = popc_m(mk);
-  const double aq = __dsub_rn(x, cprev);
-  const double rk = rate[ks];
-  const double q = rk == 1.0 ? aq : __ddiv_rn(aq, rk);  // aq / 1.0 == aq exactly
-  long long j = __double2ll_rd(q);                         // floor
-  j = j > nk - 1 ? nk - 1 : j;
-  j = j < 0 ? 0 : j;
-  return nth_bit<M, G::NS>(mk, (int)j);
-}
-
 // eq. biglambda followed at once by the atom selection for the next event
 // (eqs. Wsum..vindex) on the same state: the partial sums c_k are still in
-// registers, so the selection needs no second fold.  Identical decisions to
-// select_site2 on this state; returns the site (any value when Lambda = 0,
-// then no event can happen: the candidate time is +inf).
+// registers, so the selection needs no second fold.  The decisions of eqs.
+// Wstop/vindex with readings R8/R9 (first k with x <= c_k; j clamped);
+// returns the site (any value when Lambda = 0, then no event can happen: the
+// candidate time is +inf).
 template <class G>
 __device__ __forceinline__ int fold_select(const Classes<G>& C, const ProdTable<G>& T, const double* rate, double V,
                                            double& lam) {
@@ -377,24 +328,20 @@ __device__ __forceinline__ int fold_select(const Classes<G>& C, const ProdTable<
   }
   lam = c;
   const double x = __dmul_rn(V, lam);
-  int ks = -1, lastnz = 0;
+  // k* = the first k with x <= c_k = the number of k with c_k < x (the
+  // partial sums never decrease: every term is >= 0); x = fl(V lam) <= lam for
+  // V < 1, so k* <= 9, and the class k* has N_k* > 0 (x > 0)
+  int ks = 0;
   double cprev = 0.0;
-  M mk = 0, mlast = C.mask(0);
 #pragma unroll
-  for (int k = 0; k < 10; ++k) {
-    const M m = C.mask(k);
-    const bool hit = ks < 0 && x <= cs[k];
-    ks = hit ? k : ks;
-    cprev = hit ? (k > 0 ? cs[k - 1] : 0.0) : cprev;
-    mk = hit ? m : mk;
-    lastnz = m != 0 ? k : lastnz;
-    mlast = m != 0 ? m : mlast;
+  for (int k = 0; k < 9; ++k) {
+    const bool below = cs[k] < x;
+    ks += below ? 1 : 0;
+    cprev = below ? cs[k] : cprev;  // the last partial sum below x: c_{k*-1}
   }
-  if (ks < 0) {  // unreachable for V < 1 (x <= Lambda = c_9)
-    ks = lastnz;
-    mk = mlast;
-    cprev = 0.0;
-  }
+  const M s = ks >= 5 ? C.up : C.dn;
+  const int u = ks >= 5 ? ks - 5 : ks;
+  const M mk = s & (u == 0 ? C.m0 : u == 1 ? C.m1 : u == 2 ? C.m2 : u == 3 ? C.m3 : C.m4);
   const int nk = popc_m(mk);
   long long j = floor_div(__dsub_rn(x, cprev), rate[ks], T.rinv[ks]);
   j = j > nk - 1 ? nk - 1 : j;

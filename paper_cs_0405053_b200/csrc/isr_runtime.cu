@@ -184,20 +184,63 @@ const ShapeOps* find_ops(int bx, int by) {
 }
 
 // ---------------------------------------------------------------------------
-// exclusive scan of e_i = n_next[i] - n_comm[i] (log offsets for the replay)
+// exclusive scan of e_i = n_next[i] - n_comm[i] (the commit's log offsets):
+// 16 consecutive regions per thread (two 64-byte vector loads), 4096 per
+// block, then one block over the block sums
 // ---------------------------------------------------------------------------
-__global__ void scan_block_sums(const uint32_t* n1, const uint32_t* n0, int N, unsigned long long* bsum) {
-  __shared__ unsigned long long sh[32];
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned long long v = i < N ? (unsigned long long)(n1[i] - n0[i]) : 0ull;
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long s = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
-    bsum[blockIdx.x] = s;
+constexpr int kScanPer = 16, kScanThreads = 256, kScanBlock = kScanPer * kScanThreads;
+
+__device__ __forceinline__ unsigned scan_items(const uint32_t* n1, const uint32_t* n0, int N, int i0, unsigned* e) {
+  unsigned s = 0;
+  if (i0 + kScanPer <= N) {  // 16-byte aligned: i0 is a multiple of 16
+    const uint4* a = reinterpret_cast<const uint4*>(n1 + i0);
+    const uint4* b = reinterpret_cast<const uint4*>(n0 + i0);
+#pragma unroll
+    for (int v = 0; v < kScanPer / 4; ++v) {
+      const uint4 x = a[v], y = b[v];
+      e[4 * v] = x.x - y.x;
+      e[4 * v + 1] = x.y - y.y;
+      e[4 * v + 2] = x.z - y.z;
+      e[4 * v + 3] = x.w - y.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kScanPer; ++q) e[q] = i0 + q < N ? n1[i0 + q] - n0[i0 + q] : 0u;
   }
+#pragma unroll
+  for (int q = 0; q < kScanPer; ++q) s += e[q];
+  return s;
+}
+
+// block-wide exclusive scan of one value per thread; returns the prefix, *total = the block's sum
+__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long* total) {
+  __shared__ unsigned long long sh[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
+  }
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  unsigned long long pre = 0, tot = 0;
+#pragma unroll
+  for (int q = 0; q < kScanThreads / 32; ++q) {
+    pre += q < w ? sh[q] : 0ull;
+    tot += sh[q];
+  }
+  *total = tot;
+  return pre + x - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_block_sums(const uint32_t* n1, const uint32_t* n0, int N,
+                                                                unsigned long long* bsum) {
+  unsigned e[kScanPer];
+  const unsigned s = scan_items(n1, n0, N, (blockIdx.x * kScanThreads + threadIdx.x) * kScanPer, e);
+  unsigned long long tot;
+  block_excl_scan(s, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
 }
 
 // sum of e_i = n1[i] - n0[i] (the window's committed events) without offsets
@@ -278,60 +321,108 @@ __global__ void scan_top(unsigned long long* bsum, int nb, unsigned long long* t
   if (threadIdx.x == 0) *total = carry;
 }
 
-__global__ void scan_apply(const uint32_t* n1, const uint32_t* n0, int N, const unsigned long long* bsum,
-                           unsigned long long* off) {
-  __shared__ unsigned long long sh[32];
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const unsigned long long v = i < N ? (unsigned long long)(n1[i] - n0[i]) : 0ull;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  unsigned long long x = v;
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long t = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += t;
+__global__ void __launch_bounds__(kScanThreads) scan_apply(const uint32_t* n1, const uint32_t* n0, int N,
+                                                           const unsigned long long* bsum, unsigned long long* off) {
+  unsigned e[kScanPer];
+  const int i0 = (blockIdx.x * kScanThreads + threadIdx.x) * kScanPer;
+  const unsigned s = scan_items(n1, n0, N, i0, e);
+  unsigned long long tot;
+  unsigned long long o = bsum[blockIdx.x] + block_excl_scan(s, &tot);
+#pragma unroll
+  for (int q = 0; q < kScanPer; ++q) {
+    if (i0 + q < N) off[i0 + q] = o;
+    o += e[q];
   }
-  if (lane == 31) sh[w] = x;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long s = 0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
-      const unsigned long long t = sh[q];
-      sh[q] = s;
-      s += t;
-    }
-  }
-  __syncthreads();
-  if (i < N) off[i] = bsum[blockIdx.x] + sh[w] + x - v;
 }
+
 
 // K3 (commit, FLAG_LOG_EVENTS): compact the window's event log -- time,
 // global region id, local site, ordered by region then time -- from the
 // scratch log K1 wrote in each region's final recomputation (event q of
-// region i at ev[q * stride + i], q < C).  A region with more than C events
-// is appended to `replay` (its log is rewritten there by a K1 replay).
+// region i at ev[q * stride + i], q < C).  A warp takes 32 consecutive
+// regions and writes their events with consecutive lanes on consecutive log
+// entries (each lane finds its region by a shuffle binary search over the
+// warp's prefix of event counts).  A region with more than C events is
+// appended to `replay` (its log is rewritten there by a K1 replay).  Also
+// counts h of SURVEY §8(d.3): one entry per region edge (not along an axis
+// the region wraps) that each event's site lies on.
+__device__ __forceinline__ unsigned edges_of_site(unsigned site, int lbx, int bx, int by, int wrapX, int wrapY) {
+  const int sr = (int)(site >> lbx), sc = (int)(site & (unsigned)(bx - 1));
+  return (unsigned)((!wrapY && sr == 0) + (!wrapY && sr == by - 1) + (!wrapX && sc == 0) + (!wrapX && sc == bx - 1));
+}
+
 __global__ void __launch_bounds__(256) compact_log_kernel(const uint32_t* n1, const uint32_t* n0, int N,
                                                           const unsigned long long* off, const double* ev_t,
                                                           const uint16_t* ev_s, long long stride, int C, int RX,
-                                                          int row0, double* log_t, uint32_t* log_region,
-                                                          uint16_t* log_site, int8_t* log_dm, uint32_t* replay,
-                                                          unsigned* n_replay) {
+                                                          int row0, int lbx, int bx, int by, int wrapX, int wrapY,
+                                                          double* log_t, uint32_t* log_region, uint16_t* log_site,
+                                                          int8_t* log_dm, uint32_t* replay, unsigned* n_replay,
+                                                          unsigned long long* edges) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * 256 + threadIdx.x;
-  if (i >= N) return;
-  const unsigned e = n1[i] - n0[i];
-  if (e == 0) return;
-  if ((int)e > C) {
-    replay[atomicAdd(n_replay, 1u)] = (uint32_t)i;
-    return;
+  const unsigned e = i < N ? n1[i] - n0[i] : 0u;
+  const bool over = (int)e > C;
+  if (over) replay[atomicAdd(n_replay, 1u)] = (uint32_t)i;
+  const unsigned ec = over ? 0u : e;  // events compacted here
+  unsigned pre = ec;                 // inclusive warp scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned t = __shfl_up_sync(full, pre, o);
+    if (lane >= o) pre += t;
   }
-  const unsigned long long o = off[i];
-  const int r = i / RX;
-  const uint32_t gid = (uint32_t)((row0 + r) * RX + (i - r * RX));
-  for (unsigned q = 0; q < e; ++q) {
-    const unsigned sv = ev_s[(long long)q * stride + i];  // bit 15: the flipped site's new spin
-    log_t[o + q] = ev_t[(long long)q * stride + i];
-    log_region[o + q] = gid;
-    log_site[o + q] = (uint16_t)(sv & 0x7FFFu);
-    if (log_dm) log_dm[o + q] = (sv >> 15) ? 2 : -2;
+  const unsigned T = __shfl_sync(full, pre, 31);
+  pre -= ec;  // exclusive
+  const unsigned long long my_off = i < N ? off[i] : 0ull;
+  const int i_w = i - lane;  // the warp's first region
+  unsigned long long ne = 0;
+  for (unsigned base = 0; base < T; base += 32) {
+    const unsigned k = base + lane;
+    // the lane j whose range [pre_j, pre_j + ec_j) holds k: the largest j with pre_j <= k
+    int j = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+      const unsigned pc = __shfl_sync(full, pre, (j + step) & 31);
+      if (j + step < 32 && pc <= k) j += step;
+    }
+    const unsigned pj = __shfl_sync(full, pre, j);
+    const unsigned long long oj = __shfl_sync(full, my_off, j);
+    if (k < T) {
+      const unsigned q = k - pj;
+      const int r = i_w + j;
+      const long long src = (long long)q * stride + r;
+      const unsigned sv = ev_s[src];  // bit 15: the flipped site's new spin
+      const unsigned site = sv & 0x7FFFu;
+      const unsigned long long o = oj + q;
+      const int rr = r / RX;
+      log_t[o] = ev_t[src];
+      log_region[o] = (uint32_t)((row0 + rr) * RX + (r - rr * RX));
+      log_site[o] = (uint16_t)site;
+      if (log_dm) log_dm[o] = (sv >> 15) ? 2 : -2;
+      ne += edges_of_site(site, lbx, bx, by, wrapX, wrapY);
+    }
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ne += __shfl_xor_sync(full, ne, o);
+  if (lane == 0 && ne) atomicAdd(edges, ne);
+}
+
+// the edge entries of the replayed regions' events (after the replay wrote them)
+__global__ void __launch_bounds__(256) replay_edge_entries(const uint32_t* replay, const unsigned* n_replay,
+                                                           const uint32_t* n1, const uint32_t* n0,
+                                                           const unsigned long long* off, const uint16_t* log_site,
+                                                           int lbx, int bx, int by, int wrapX, int wrapY,
+                                                           unsigned long long* edges) {
+  const unsigned n = *n_replay;
+  unsigned long long ne = 0;
+  for (unsigned t = blockIdx.x * 256 + threadIdx.x; t < n; t += gridDim.x * 256) {
+    const uint32_t i = replay[t];
+    const unsigned e = n1[i] - n0[i];
+    for (unsigned q = 0; q < e; ++q) ne += edges_of_site(log_site[off[i] + q], lbx, bx, by, wrapX, wrapY);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ne += __shfl_xor_sync(0xffffffffu, ne, o);
+  if ((threadIdx.x & 31) == 0 && ne) atomicAdd(edges, ne);
 }
 
 // ---------------------------------------------------------------------------
@@ -518,23 +609,6 @@ __global__ void __launch_bounds__(1024) mm_final(const double* part, const doubl
     out[0] = __dadd_rn(__dmul_rn(fabs(M0), dt), s1[0]);
     out[1] = __dadd_rn(__dmul_rn(__dmul_rn(M0, M0), dt), s2[0]);
   }
-}
-
-// h of SURVEY §8(d.3): boundary-history entries of the window's fixed point,
-// one per region edge (N, S, W, E; not along an axis the region wraps) that
-// the site of each committed event lies on
-__global__ void __launch_bounds__(256) count_edge_entries(const uint16_t* site, const unsigned long long* n_total,
-                                                          int bx, int by, int wrapX, int wrapY,
-                                                          unsigned long long* out) {
-  const unsigned long long n = *n_total;
-  unsigned long long v = 0;
-  for (unsigned long long i = (unsigned long long)blockIdx.x * 256 + threadIdx.x; i < n;
-       i += (unsigned long long)gridDim.x * 256) {
-    const int st = site[i], sr = st / bx, sc = st - sr * bx;
-    v += (!wrapY && sr == 0) + (!wrapY && sr == by - 1) + (!wrapX && sc == 0) + (!wrapX && sc == bx - 1);
-  }
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
 }
 
 // Initial spins from the Philox init stream for the rows
@@ -1376,15 +1450,16 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   for (auto& e : c->pev)
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return bail(ISING_SR_E_CUDA);
   if (c->cfg.flags & ISING_SR_FLAG_LOG_EVENTS) {
-    // scratch event log: events per region per window at the largest rate,
-    // at most 16 (a region with more is replayed at commit); the replay list
+    // scratch event log: 1.5 x the expected events per region per window at
+    // the largest rate + 8, within 8 GB in all (a region with more events is
+    // replayed at commit -- a latency-bound K1 pass, so it should be rare)
     double rmax = 0.0;
     for (double r : cfg->rate) rmax = std::max(rmax, r);
-    int C = cfg->log_capacity > 0 ? cfg->log_capacity
-                                  : (int)std::ceil((double)cfg->bx * cfg->by * rmax * std::min(cfg->W, cfg->t_end));
-    C = std::max(2, std::min(C, 16));
-    if (cfg->log_capacity > 0) C = std::min(cfg->log_capacity, 1 << 16);
-    c->evC = C;
+    const double mu = (double)cfg->bx * cfg->by * rmax * std::min(c->cfg.W, std::max(cfg->t_end, 1e-9));
+    long long C = cfg->log_capacity > 0 ? cfg->log_capacity : (long long)std::ceil(1.5 * mu) + 8;
+    C = std::min<long long>(C, 65535);
+    if (cfg->log_capacity <= 0) C = std::max<long long>(2, std::min<long long>(C, (8LL << 30) / (10LL * std::max(1, c->nreg))));
+    c->evC = (int)C;
     if (dmalloc(c, &c->ev_t, n * (size_t)C) != cudaSuccess || dmalloc(c, &c->ev_s, n * (size_t)C) != cudaSuccess ||
         dmalloc(c, &c->d_replay, n) != cudaSuccess)
       return bail(ISING_SR_E_OOM);
@@ -1595,7 +1670,7 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
   if (!c->in_window || !c->converged) return ISING_SR_E_STATE;
   const StateView& s0 = c->st[c->comm];
   const StateView& s1 = c->st[c->comm ^ 1];
-  const int nb = (c->nreg + kThreads - 1) / kThreads;
+  const int nbs = (c->nreg + kScanBlock - 1) / kScanBlock;
   // e_i = n_next - n_comm: the window's total, and (event log) the scan for the log offsets
   const bool log = (c->cfg.flags & ISING_SR_FLAG_LOG_EVENTS) != 0;
   if (!log) {
@@ -1604,12 +1679,12 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
                                                                                              c->d_total);
     c->launches++;
   } else {
-    scan_block_sums<<<nb, kThreads, 0, c->stream>>>(s1.n, s0.n, c->nreg, c->d_bsum);
-    scan_top<<<1, 1024, 0, c->stream>>>(c->d_bsum, nb, c->d_total);
+    scan_block_sums<<<nbs, kScanThreads, 0, c->stream>>>(s1.n, s0.n, c->nreg, c->d_bsum);
+    scan_top<<<1, 1024, 0, c->stream>>>(c->d_bsum, nbs, c->d_total);
     c->launches += 2;
   }
   if (log) {
-    scan_apply<<<nb, kThreads, 0, c->stream>>>(s1.n, s0.n, c->nreg, c->d_bsum, c->d_off);
+    scan_apply<<<nbs, kScanThreads, 0, c->stream>>>(s1.n, s0.n, c->nreg, c->d_bsum, c->d_off);
     c->launches++;
   }
   CK(c, cudaGetLastError());
@@ -1659,9 +1734,13 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
     CK(c, cudaEventRecord(c->cev0, c->stream));
     CK(c, cudaMemsetAsync(c->d_nrep, 0, 4 * sizeof(unsigned), c->stream));
     CK(c, cudaMemsetAsync(c->d_edges, 0, sizeof(unsigned long long), c->stream));
+    int lbx = 0;
+    while ((1 << lbx) < c->cfg.bx) ++lbx;  // region widths are powers of two
+    const int wx = c->RX == 1 ? 1 : 0, wy = c->RYg == 1 ? 1 : 0;
     compact_log_kernel<<<(c->nreg + 255) / 256, 256, 0, c->stream>>>(
-        s1.n, s0.n, c->nreg, c->d_off, c->ev_t, c->ev_s, (long long)c->nreg, c->evC, c->RX, c->row0, c->log_t,
-        c->log_region, c->log_site, mag ? c->log_dm : nullptr, c->d_replay, c->d_nrep);
+        s1.n, s0.n, c->nreg, c->d_off, c->ev_t, c->ev_s, (long long)c->nreg, c->evC, c->RX, c->row0, lbx, c->cfg.bx,
+        c->cfg.by, wx, wy, c->log_t, c->log_region, c->log_site, mag ? c->log_dm : nullptr, c->d_replay, c->d_nrep,
+        c->d_edges);
     c->launches++;
     CK(c, cudaGetLastError());
     KArgs a = base_args(c, c->Kglob + 1, false);
@@ -1677,8 +1756,8 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
     c->ops->replay(a, 148 * 4 * kThreads, c->stream);  // a fixed grid; tiles sized on the device
     c->launches++;
     CK(c, cudaGetLastError());
-    count_edge_entries<<<148 * 4, 256, 0, c->stream>>>(c->log_site, c->d_total, c->cfg.bx, c->cfg.by,
-                                                       c->RX == 1 ? 1 : 0, c->RYg == 1 ? 1 : 0, c->d_edges);
+    replay_edge_entries<<<148, 256, 0, c->stream>>>(c->d_replay, c->d_nrep, s1.n, s0.n, c->d_off, c->log_site, lbx,
+                                                    c->cfg.bx, c->cfg.by, wx, wy, c->d_edges);
     c->launches++;
     CK(c, cudaGetLastError());
     CK(c, cudaEventRecord(c->cev1, c->stream));

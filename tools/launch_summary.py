@@ -1,36 +1,39 @@
 #!/usr/bin/env python
-"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list: per
-kernel launches, total/mean device time and share of all kernel time."""
-import csv
+"""Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv):
+launches, total and mean time and share per kernel.
+
+  python tools/launch_summary.py LAUNCHES.csv [--md OUT.md]
+"""
 import collections
+import csv
 import sys
 
 
-def main(path):
-    rows = []
-    with open(path) as f:
-        lines = [l for l in f if l.startswith('"')]
-    rd = csv.reader(lines)
-    hdr = next(rd)
-    h = {k: i for i, k in enumerate(hdr)}
+def main():
+    path = sys.argv[1]
+    md = sys.argv[sys.argv.index("--md") + 1] if "--md" in sys.argv else None
+    lines = [ln for ln in open(path) if ln.startswith('"')]
+    rows = list(csv.reader(lines))
+    h = rows[0]
+    ik, iv, iu, im = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit"), h.index("Metric Name")
     agg = collections.defaultdict(lambda: [0, 0.0])
-    for r in rd:
-        if r[h["Metric Name"]] != "gpu__time_duration.sum":
+    scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0}
+    for r in rows[1:]:
+        if r[im] != "gpu__time_duration.sum":
             continue
-        name = r[h["Kernel Name"]].split("(")[0]
-        unit = r[h["Metric Unit"]]
-        v = float(r[h["Metric Value"]].replace(",", ""))
-        scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}
-        v_ms = v * scale.get(unit, 1.0)
+        name = r[ik].split("(")[0].replace("void ", "")
         agg[name][0] += 1
-        agg[name][1] += v_ms
+        agg[name][1] += float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
     tot = sum(v[1] for v in agg.values())
-    print(f"| kernel | launches | total ms | mean us | share |")
-    print("|---|---|---|---|---|")
+    out = ["| kernel | launches | total ms | mean us | share |", "|---|---|---|---|---|"]
     for k, (n, ms) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-        print(f"| {k} | {n} | {ms:.2f} | {1e3 * ms / n:.1f} | {ms / tot * 100:.1f}% |")
-    print(f"\ntotal kernel time {tot:.2f} ms over {sum(v[0] for v in agg.values())} launches")
+        out.append(f"| {k} | {n} | {ms:.2f} | {1e3 * ms / n:.1f} | {100 * ms / tot:.1f}% |")
+    out.append(f"\ntotal kernel time {tot:.2f} ms over {sum(v[0] for v in agg.values())} launches")
+    txt = "\n".join(out)
+    print(txt)
+    if md:
+        open(md, "w").write(txt + "\n")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main()
