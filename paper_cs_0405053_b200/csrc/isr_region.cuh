@@ -1161,21 +1161,32 @@ __global__ void mark_kernel(const KArgs a, GhostView up, GhostView down) {
   mark_dirty(a, nidx, a.it_K + 1);
 }
 
-// Ordered worklist of the next iteration from its dirty bitmap (one word =
-// 32 regions per thread), compacted in region order within each block of
-// 8192 regions (one atomic per block); the bitmap is cleared for reuse two
-// iterations later.
-__global__ void __launch_bounds__(256) compact_kernel(uint32_t* bm, int nwords, int n, uint32_t* wl,
-                                                      unsigned* count) {
-  __shared__ unsigned wsum[8];
+// Ordered worklist of the next iteration from its dirty bitmap: 8
+// consecutive 32-bit words (256 regions) per thread, 2048 words per block,
+// compacted in region order within each block (one atomic per block); the
+// bitmap is cleared for reuse two iterations later.
+constexpr int kCompactWords = 8, kCompactThreads = 256;
+__global__ void __launch_bounds__(kCompactThreads) compact_kernel(uint32_t* bm, int nwords, int n, uint32_t* wl,
+                                                                  unsigned* count) {
+  __shared__ unsigned wsum[kCompactThreads / 32];
   __shared__ unsigned base;
-  const int i = blockIdx.x * 256 + threadIdx.x;
-  uint32_t w = 0;
-  if (i < nwords) {
-    w = bm[i];
-    if (w) bm[i] = 0u;
+  const int w0 = (blockIdx.x * kCompactThreads + threadIdx.x) * kCompactWords;
+  uint32_t w[kCompactWords];
+  if (w0 + kCompactWords <= nwords) {  // 32-byte aligned: two 16-byte loads
+    const uint4 x = reinterpret_cast<const uint4*>(bm + w0)[0], y = reinterpret_cast<const uint4*>(bm + w0)[1];
+    w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w; w[4] = y.x; w[5] = y.y; w[6] = y.z; w[7] = y.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < kCompactWords; ++q) w[q] = w0 + q < nwords ? bm[w0 + q] : 0u;
   }
-  const int c = __popc(w);
+  int c = 0;
+#pragma unroll
+  for (int q = 0; q < kCompactWords; ++q) c += __popc(w[q]);
+  if (c) {
+#pragma unroll
+    for (int q = 0; q < kCompactWords; ++q)
+      if (w[q]) bm[w0 + q] = 0u;
+  }
   const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int x = c;  // inclusive warp scan of the counts
 #pragma unroll
@@ -1187,7 +1198,7 @@ __global__ void __launch_bounds__(256) compact_kernel(uint32_t* bm, int nwords, 
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned s = 0;
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < kCompactThreads / 32; ++q) {
       const unsigned t = wsum[q];
       wsum[q] = s;
       s += t;
@@ -1196,11 +1207,15 @@ __global__ void __launch_bounds__(256) compact_kernel(uint32_t* bm, int nwords, 
   }
   __syncthreads();
   unsigned o = base + wsum[wid] + (unsigned)(x - c);
-  while (w) {
-    const int b = __ffs(w) - 1;
-    w &= w - 1u;
-    const int r = i * 32 + b;
-    if (r < n) wl[o++] = (uint32_t)r;
+#pragma unroll
+  for (int q = 0; q < kCompactWords; ++q) {
+    uint32_t v = w[q];
+    while (v) {
+      const int b = __ffs(v) - 1;
+      v &= v - 1u;
+      const int r = (w0 + q) * 32 + b;
+      if (r < n) wl[o++] = (uint32_t)r;
+    }
   }
 }
 

@@ -934,9 +934,14 @@ double iteration_bytes(const ising_sr_ctx* c, const unsigned long long* s) {
   return regions * (2.0 * S + c->ops->sel_read_bytes + 8.0) + 9.0 * ((double)s[1] + (double)s[2] + (double)s[3]);
 }
 
+int compact_grid(const ising_sr_ctx* c) {
+  const int per = isr::kCompactThreads * isr::kCompactWords;
+  return std::max(1, (c->dwords + per - 1) / per);
+}
+
 ising_sr_status compact_worklist(ising_sr_ctx* c) {
   const unsigned K = c->Kglob;
-  isr::compact_kernel<<<(c->dwords + 255) / 256, 256, 0, c->stream>>>(c->dirty + (size_t)((K + 1) & 1) * c->dwords,
+  isr::compact_kernel<<<compact_grid(c), isr::kCompactThreads, 0, c->stream>>>(c->dirty + (size_t)((K + 1) & 1) * c->dwords,
                                                                        c->dwords, c->nreg, c->wl[(K + 1) & 1],
                                                                      c->d_wlc + ((K + 1) & 1));
   ++c->launches;
@@ -1165,7 +1170,7 @@ ising_sr_status enqueue_pipelined(ising_sr_ctx* c, int bound) {
     ++c->launches;
     CK(c, cudaGetLastError());
   }
-  isr::compact_kernel<<<(c->dwords + 255) / 256, 256, 0, c->stream>>>(c->dirty + (size_t)((K + 1) & 1) * c->dwords,
+  isr::compact_kernel<<<compact_grid(c), isr::kCompactThreads, 0, c->stream>>>(c->dirty + (size_t)((K + 1) & 1) * c->dwords,
                                                                        c->dwords, c->nreg, c->wl[(K + 1) & 1],
                                                                        &sl->wl_next);
   ++c->launches;
@@ -1394,7 +1399,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   c->RYl = RY / world;
   c->row0 = cfg->rank * c->RYl;
   c->nreg = c->RX * c->RYl;
-  c->dwords = (c->nreg + 31) / 32;
+  c->dwords = ((c->nreg + 31) / 32 + 7) / 8 * 8;  // a multiple of 8 words: 32-byte aligned bitmaps (compact_kernel)
   std::memset(&c->stats, 0, sizeof c->stats);
   if (const char* e = std::getenv("ISING_SR_PIPELINE")) c->pipeline = std::atoi(e) != 0;
   if (const char* e = std::getenv("ISING_SR_REFILL")) c->refill = std::max(1, std::min(32, std::atoi(e)));
@@ -1425,7 +1430,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
         (dmalloc(c, &s.oM, n) != cudaSuccess || dmalloc(c, &s.oB, n) != cudaSuccess))
       return bail(ISING_SR_E_OOM);
   }
-  if (dmalloc(c, &c->sel, (size_t)ops->sel_words * n) != cudaSuccess || dmalloc(c, &c->dirty, 2 * ((n + 31) / 32)) != cudaSuccess ||
+  if (dmalloc(c, &c->sel, (size_t)ops->sel_words * n) != cudaSuccess || dmalloc(c, &c->dirty, 2 * (size_t)c->dwords) != cudaSuccess ||
       dmalloc(c, &c->wl[0], n) != cudaSuccess || dmalloc(c, &c->wl[1], n) != cudaSuccess ||
       dmalloc(c, &c->d_wlc, 2) != cudaSuccess || dmalloc(c, &c->d_flags, 4) != cudaSuccess ||
       dmalloc(c, &c->d_stats, 8) != cudaSuccess || dmalloc(c, &c->d_nrep, 4) != cudaSuccess ||
@@ -1439,7 +1444,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
       cudaMallocHost((void**)&c->h_slot, 2 * sizeof(IterSlot)) != cudaSuccess)
     return bail(ISING_SR_E_OOM);
   if (cudaMemsetAsync(c->sel, 0, n * 8 * (size_t)ops->sel_words, c->stream) != cudaSuccess ||
-      cudaMemsetAsync(c->dirty, 0, 2 * ((n + 31) / 32) * 4, c->stream) != cudaSuccess)
+      cudaMemsetAsync(c->dirty, 0, 2 * (size_t)c->dwords * 4, c->stream) != cudaSuccess)
     return bail(ISING_SR_E_CUDA);
   if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
       cudaEventCreate(&c->kev0) != cudaSuccess || cudaEventCreate(&c->kev1) != cudaSuccess ||
