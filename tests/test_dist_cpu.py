@@ -73,3 +73,33 @@ def test_strip_partition_rule():
     h = ctypes.c_void_p()
     s = np.zeros(16 * 12, dtype=np.uint8)
     assert L.ising_sr_init(ctypes.byref(c), s.ctypes.data, ctypes.byref(h)) == -3
+
+
+def _id_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_cs_0405053_b200.dist import shared_nccl_id
+        q.put((rank, shared_nccl_id(rank)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shared_nccl_id_broadcast(world):
+    """The bootstrap of the library's NCCL communicator (cfg.nccl_id): rank 0
+    creates a 128-byte ncclUniqueId (ising_sr_nccl_unique_id, NCCL loaded by
+    the library at run time) and every rank of the group receives the same
+    bytes -- the only torch.distributed step of the N > 1 bench path."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_id_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    ids = [res[r] for r in range(world)]
+    assert all(len(x) == 128 for x in ids) and all(x == ids[0] for x in ids) and any(ids[0])
