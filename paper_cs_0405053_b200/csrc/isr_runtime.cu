@@ -1469,7 +1469,18 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
         dmalloc(c, &c->d_replay, n) != cudaSuccess)
       return bail(ISING_SR_E_OOM);
   }
-  const int K0 = cfg->hist_capacity > 0 ? std::min(cfg->hist_capacity, ops->cnt_max) : auto_capacity(*cfg, ops->cnt_max);
+  int K0 = cfg->hist_capacity > 0 ? std::min(cfg->hist_capacity, ops->cnt_max) : auto_capacity(c->cfg, ops->cnt_max);
+  if (cfg->hist_capacity <= 0) {
+    // the automatic capacity never takes more than 60 % of the free device
+    // memory for the two history slots (4 edges x K entries x 9 bytes per
+    // region each); a longer history is caught by the overflow retry
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr > 0) {
+      const double per_k = 2.0 * 4.0 * (double)c->nreg * 9.0;
+      const int kmax = (int)std::max(2.0, 0.6 * (double)fr / per_k);
+      K0 = std::min(K0, kmax);
+    }
+  }
   ising_sr_status s = alloc_edges(c, K0);
   if (s != ISING_SR_OK) return bail(s);
   if (const char* e = std::getenv("ISING_SR_RESUME")) c->resume = std::atoi(e) != 0;

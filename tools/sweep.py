@@ -128,7 +128,16 @@ def main():
     rows = []
     with open(args.out, "a") as fo:
         for w in ws:
-            r = run_one(w)
+            try:
+                r = run_one(w)
+            except Exception as e:  # e.g. E_OOM for a point that does not fit: record it, go on
+                rec = {"config": w.name, "W": w.W, "error": str(e)}
+                rows.append(rec)
+                fo.write(json.dumps(rec) + "\n")
+                fo.flush()
+                print(json.dumps(rec), flush=True)
+                torch.cuda.empty_cache()
+                continue
             rec = record(w, r)
             if args.golden:
                 rec["parity_golden"] = golden_parity(w, r["sim"], rec["events"])
@@ -152,7 +161,7 @@ def main():
     if args.csv:
         keys = list(rows[0].keys())
         with open(args.csv, "w", newline="") as f:
-            wr = csv.DictWriter(f, fieldnames=keys)
+            wr = csv.DictWriter(f, fieldnames=keys, extrasaction="ignore")
             wr.writeheader()
             for r in rows:
                 wr.writerow(r)
