@@ -72,7 +72,7 @@ typedef enum {
  * committed window, accumulated per region inside K1 (each region owns its
  * internal bonds and the bonds to its north and west neighbours) and reduced
  * in a fixed order at commit (ising_sr_stats.obs_*).  Lane-per-region K1 forms
- * only (E_INVALID_ARG with ISING_SR_POOL=1 or ISING_SR_BIG=0). */
+ * only (E_INVALID_ARG with ISING_SR_BIG=0, the warp form). */
 #define ISING_SR_FLAG_OBSERVABLES 0x8u
 /* Paper-faithful Jacobi schedule: every relaxation iteration
  * recomputes every region, not only those whose incoming histories changed.

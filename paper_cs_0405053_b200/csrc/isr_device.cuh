@@ -9,10 +9,6 @@
 #pragma once
 #include <cstdint>
 
-#ifndef ISR_PHILOX_WIDE
-#define ISR_PHILOX_WIDE 0
-#endif
-
 namespace isr {
 
 // ---------------------------------------------------------------------------
@@ -27,22 +23,11 @@ struct U4 {
 __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-#if ISR_PHILOX_WIDE
-    // one 32x32->64 multiply each (IMAD.WIDE.U32): hi and lo words together
-    const unsigned long long p0 = (unsigned long long)0xD2511F53u * c.x;
-    const unsigned long long p1 = (unsigned long long)0xCD9E8D57u * c.z;
-    U4 n;
-    n.x = (uint32_t)(p1 >> 32) ^ c.y ^ k0;
-    n.y = (uint32_t)p1;
-    n.z = (uint32_t)(p0 >> 32) ^ c.w ^ k1;
-    n.w = (uint32_t)p0;
-#else
     U4 n;
     n.x = __umulhi(0xCD9E8D57u, c.z) ^ c.y ^ k0;
     n.y = 0xCD9E8D57u * c.z;
     n.z = __umulhi(0xD2511F53u, c.x) ^ c.w ^ k1;
     n.w = 0xD2511F53u * c.x;
-#endif
     c = n;
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
