@@ -86,7 +86,8 @@ class WindowLedger:
         k1 = A_tot * (self.S + 3.0 * H)
         commit = self.nreg * self.S + 14.0 * e
         self.rows.append({"A": A_tot / self.nreg, "h": h / self.nreg, "e": e / self.nreg, "g": st["g_last"],
-                          "f": st["f_last"], "k1_bytes": k1, "bytes": k1 + commit, "events": e})
+                          "f": st["f_last"], "k1_bytes": k1, "bytes": k1 + commit, "events": e,
+                          "ms": st["ms_last_window"]})
 
     def total(self, key):
         return sum(r[key] for r in self.rows)
@@ -198,6 +199,26 @@ def run_reference(args):
 # --------------------------------------------------------------------------
 # the B200 arm
 # --------------------------------------------------------------------------
+def golden_parity(config, sim, world, nwin, w):
+    """The run against tests/golden/full_size/<config>_t50.json (the oracle's
+    result, tools/make_goldens.py): total events, final spins and per-region
+    event counts, bit for bit (SHA-256).  Only at N = 1 and when the run ends
+    exactly at the golden's t_end."""
+    import hashlib
+    path = os.path.join(ROOT, "tests", "golden", "full_size", f"{config}_t{int(w.t_end)}.json")
+    if world != 1 or not os.path.exists(path):
+        return None
+    g = json.load(open(path))
+    if abs(nwin * w.W - g["t_end"]) > 1e-12:
+        return {"checked": False, "why": f"run ends at t = {nwin * w.W}, golden at {g['t_end']}"}
+    _, cnt = sim.digests()
+    spins = sim.spins()
+    sh = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    ok = {"events": sim.stats()["events_total"] == g["n_events"],
+          "spins": sh(spins) == g["sha256_spins"], "counts": sh(cnt.astype("<u8")) == g["sha256_count"]}
+    return {"checked": True, "bit_exact": all(ok.values()), **ok, "golden": os.path.relpath(path, ROOT)}
+
+
 def run_ising(args):
     import torch
     from paper_cs_0405053_b200 import FLAG_DIGEST, FLAG_LOG_EVENTS, IsingSR
@@ -267,6 +288,12 @@ def run_ising(args):
     impl_bytes = st1["region_bytes"] - st0["region_bytes"]
     nlaunch = st1["region_launches"] - st0["region_launches"]
     k1_bytes, alg_bytes = ledger.total("k1_bytes"), ledger.total("bytes")
+    # steady state: the second half of the timed windows (device time of each window, ev0 -> ev1)
+    half = ledger.rows[len(ledger.rows) // 2:]
+    steady = {"windows": f"{nwin - len(half)}..{nwin - 1}",
+              "events_per_s": sum(r["events"] for r in half) / max(sum(r["ms"] for r in half) * 1e-3, 1e-12)}
+    # parity of the run with the oracle's golden result when the run ends at the config's t_end
+    parity = golden_parity(args.config, sim, world, nwin, w)
     compact_ms = st1["ms_compact_total"] - st0["ms_compact_total"]
     if world > 1:
         import torch.distributed as dist
@@ -363,6 +390,8 @@ def run_ising(args):
                                   "e_events": ledger.mean("e"), "S_state_bytes": ledger.S,
                                   "f_max": int(max(r["f"] for r in ledger.rows))},
         "commit_compaction_ms_per_window": compact_ms / args.steps,
+        "steady_state_second_half": steady,
+        "parity": parity,
         "gpu_launches": launches,
         "roofline": roof,
         "cpu_baseline": cpu,
