@@ -313,8 +313,12 @@ def run_ising(args):
         pinned_out = torch.empty((w.Ly // world) * w.Lx, dtype=torch.uint8).pin_memory()
         barrier()
         t0 = time.perf_counter()
+        nccl_id2 = None
+        if world > 1:  # a fresh ncclUniqueId for the second communicator
+            from paper_cs_0405053_b200.dist import shared_nccl_id
+            nccl_id2 = shared_nccl_id(rank)
         sim2 = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), pinned.numpy(), w.W, t_end, w.seed, flags=flags,
-                       rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=nccl_id)
+                       rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=nccl_id2)
         ev2 = 0
         for _ in range(args.steps):
             sim2.run_window()
