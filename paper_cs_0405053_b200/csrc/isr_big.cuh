@@ -274,6 +274,7 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
     const long long pbase = (long long)idx * a.PC;
     auto get_pair = [&](uint32_t m, double& E, double& Vm) {
       const unsigned q = m - n0;
+      ISR_ASSERT(!a.pcache || pfill <= (unsigned)a.PC);
       if (a.pcache && q < pfill) {
         const double2 c = a.pcache[pbase + q];
         E = c.x;
@@ -647,6 +648,7 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
         const unsigned up_new = (SM.rows[sr][t] >> sc) & 1u;  // the flipped site's new spin (for dM)
         if (LOG) {
           const unsigned long long o = a.log_off[idx] + n_ev_r;
+          ISR_ASSERT(a.log_cap == 0 || (long long)o < a.log_cap);
           a.log_t[o] = tc;
           a.log_region[o] = gid;
           a.log_site[o] = (uint16_t)site;

@@ -8,6 +8,28 @@
 // DESIGN.md §3 and matches the paper's formulas as cited below.
 #pragma once
 #include <cstdint>
+#include <cstdio>
+
+// ISR_CHECK=1 (a debugging build, tools/build_variants.py checked=-DISR_CHECK=1):
+// bounds checks on the kernels' computed indices; a violation prints its
+// location and traps, so the launch fails with a CUDA error
+#ifndef ISR_CHECK
+#define ISR_CHECK 0
+#endif
+#if ISR_CHECK
+#define ISR_ASSERT(cond)                                                                              \
+  do {                                                                                                \
+    if (!(cond)) {                                                                                    \
+      printf("ISR_ASSERT failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__,     \
+             (int)blockIdx.x, (int)threadIdx.x);                                                      \
+      __trap();                                                                                       \
+    }                                                                                                 \
+  } while (0)
+#else
+#define ISR_ASSERT(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 namespace isr {
 

@@ -142,6 +142,7 @@ struct KArgs {
   uint32_t* log_region;
   uint16_t* log_site;
   const unsigned long long* log_off;
+  long long log_cap;  // entries allocated for the log (ISR_CHECK bounds)
 };
 
 // The budget drawn from U: E(U) (R25), or with eq_q > 0 (tie test
@@ -637,6 +638,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
         for (int q = 0; q < SG::CIN; ++q) {
           if (q < (int)cnt[d]) {
             const unsigned o = off + (unsigned)q * (unsigned)a.RX;
+            ISR_ASSERT(src[d] >= 2 ? (int)(o / (unsigned)a.RX) < a.K : (long long)o < a.tstride);
             cp_async8(&S.in_t[d][q][lane], T + o);
             cp_async4(&S.in_p[d][q][lane], word_of(P + o));
           }
@@ -710,6 +712,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
 
 // queue region i for the iteration with stamp `stamp` (bitmap of its parity)
 __device__ __forceinline__ void mark_dirty(const KArgs& a, int i, unsigned stamp) {
+  ISR_ASSERT(i >= 0 && (i >> 5) < a.dwords);
   atomicOr(a.dirty + (size_t)(stamp & 1u) * (size_t)a.dwords + (i >> 5), 1u << (i & 31));
 }
 
@@ -849,6 +852,7 @@ __device__ __forceinline__ unsigned hist_put(const KArgs& a, unsigned om, int e,
   unsigned dv = (om >> 17) & 1u;
   if ((int)k < a.K) {
     const unsigned o = obase + k * (unsigned)a.RX;
+    ISR_ASSERT((long long)o < a.tstride);
     double* Tn = (ps ? a.ed[0].t : a.ed[1].t) + e * a.tstride;
     uint8_t* Pn = (ps ? a.ed[0].pos : a.ed[1].pos) + e * a.tstride;
     Tn[o] = tc;
@@ -886,6 +890,7 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const
   if (a.digest) L.dig = digest_step(L.dig, L.tc, site);
   if (LOG) {
     const unsigned long long o = a.log_off[L.idx] + L.n_ev;
+    ISR_ASSERT(a.log_cap == 0 || (long long)o < a.log_cap);
     a.log_t[o] = L.tc;
     a.log_region[o] = L.gid;
     a.log_site[o] = (uint16_t)site;
@@ -1000,6 +1005,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
           if (item < 0) item = (int)atomicAdd(&q_next, 1u);
           if (item < s_tile_n) {
             const int idx = a.wl_in ? (int)a.wl_in[s_tile_begin + item] : s_tile_begin + item;
+            ISR_ASSERT(idx >= 0 && idx < a.RX * a.RYl);
             lane_load<G, LOG, SG, false, OBS, FIRST>(a, L, idx, S, PT, threadIdx.x);
             fresh = true;
             n_in += (L.hm[0] & 0xFFu) + (L.hm[1] & 0xFFu) + (L.hm[2] & 0xFFu) + (L.hm[3] & 0xFFu);

@@ -1769,6 +1769,7 @@ static ising_sr_status commit_impl(ising_sr_ctx* c, int64_t* events_out) {
     a.log_site = c->log_site;
     a.log_dm = mag ? c->log_dm : nullptr;
     a.log_off = c->d_off;
+    a.log_cap = c->log_cap;
     c->ops->replay(a, 148 * 4 * kThreads, c->stream);  // a fixed grid; tiles sized on the device
     c->launches++;
     CK(c, cudaGetLastError());
