@@ -235,7 +235,8 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
   __shared__ BigSmem<BX, BY> SM;
   const int t = threadIdx.x;
   const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
-  const unsigned K = a.it_K, K0 = a.it_K0;
+  const unsigned K = stamp_of(a), K0 = a.it_K0;
+  ktime_begin(a);
   unsigned long long n_ev = 0, n_out = 0, n_in = 0, n_cmp = 0, n_reg = 0;
   unsigned fmax = 0;
   bool changed = false, overflow = false;
@@ -791,6 +792,7 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
     }
   }
 
+  ktime_end(a);
   if (!LOG) {
     const unsigned full = 0xffffffffu;
     const unsigned anych = __ballot_sync(full, changed);

@@ -88,7 +88,12 @@ struct KArgs {
   int ghost;          // the strip's first/last region rows read ghost rows (world > 1, or halo loopback)
   int K;
   long long tstride;  // elements per edge in t/pos (RYl * K * RX)
-  unsigned it_K;      // global iteration stamp of this launch (>= 1)
+  unsigned it_K;      // global iteration stamp of this launch (>= 1); with `trip`: the stamp of loop trip 0
+  // device-side window loop (a CUDA graph with a conditional while node): the
+  // loop body holds two iterations, so this launch's stamp is it_K + 2 * (*trip)
+  const unsigned* trip;
+  // the launch's device time: min start / max end of its blocks (%globaltimer, ns)
+  unsigned long long* ktime;
   unsigned it_K0;     // stamp of the window's first iteration
   int first;          // window's first iteration: canonical assumption
   int digest;
@@ -144,6 +149,20 @@ struct KArgs {
   const unsigned long long* log_off;
   long long log_cap;  // entries allocated for the log (ISR_CHECK bounds)
 };
+
+__device__ __forceinline__ unsigned stamp_of(const KArgs& a) { return a.trip ? a.it_K + 2u * __ldcg(a.trip) : a.it_K; }
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// block-level start / end stamps of a launch (the graph loop's K1 timing)
+__device__ __forceinline__ void ktime_begin(const KArgs& a) {
+  if (a.ktime && threadIdx.x == 0) atomicMin(a.ktime, globaltimer_ns());
+}
+__device__ __forceinline__ void ktime_end(const KArgs& a) {
+  if (a.ktime && threadIdx.x == 0) atomicMax(a.ktime + 1, globaltimer_ns());
+}
 
 // The budget drawn from U: E(U) (R25), or with eq_q > 0 (tie test
 // mode, R30) the quantized (floor(E(U) eq_q) + 1) / eq_q, exact
@@ -564,7 +583,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
                                           int si) {
   using M = typename G::M;
   const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
-  const unsigned K = a.it_K, K0 = a.it_K0;
+  const unsigned K = stamp_of(a), K0 = a.it_K0;
   const int lane = si;
   const int r = div_rx(a, idx), c = idx - r * a.RX;
   L.idx = idx;
@@ -733,7 +752,7 @@ template <class G, bool OBS = false>
 __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& changed, bool& overflow) {
   const int idx = L.idx;
   const int r = div_rx(a, idx), c = idx - r * a.RX;
-  const unsigned K = a.it_K;
+  const unsigned K = stamp_of(a);
   unsigned chmask = 0;
   unsigned long long word = 0;
 #pragma unroll
@@ -979,6 +998,9 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
     s_tile_n = min(tile, n - (int)(blockIdx.x * tile));
     q_next = blockDim.x;  // the first blockDim items are taken statically
   }
+  __syncthreads();
+  if (s_tile_n <= 0) return;  // block-uniform: a grid sized for a longer worklist
+  ktime_begin(a);
   fill_prod<G>(PT, a.rate);
   __syncthreads();
 
@@ -1054,6 +1076,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
     }
   }
 
+  ktime_end(a);
   if (!LOG) {
     if (a.delay_ns) k1_delay(a.delay_ns);
     // warp-aggregated flags and counters (one atomic per warp)
@@ -1134,7 +1157,8 @@ __global__ void pack_kernel(const KArgs a, GhostView send_up, GhostView send_dow
   const GhostView& g = up ? send_up : send_down;
   const ulonglong2 wp = reinterpret_cast<const ulonglong2*>(a.sel)[(long long)r * a.RX + c];
   // latest as of the end of this iteration
-  const unsigned long long v = latest_word(wp, a.it_K + 1);
+  const unsigned K = stamp_of(a);
+  const unsigned long long v = latest_word(wp, K + 1);
   int cnt = 0;
   if (word_valid(v, a.it_K0)) {
     const EdgeView& E = word_slot(v, e) ? a.ed[1] : a.ed[0];
@@ -1148,9 +1172,9 @@ __global__ void pack_kernel(const KArgs a, GhostView send_up, GhostView send_dow
   g.cnt[c] = (uint16_t)cnt;
   // changed in this iteration: the word was rewritten now and edge e moved
   // slot relative to the previous latest word (the other one)
-  const unsigned long long other = latest_index(wp, a.it_K + 1) ? wp.x : wp.y;
-  const bool ch_now = (unsigned)(v >> 32) == a.it_K && (((v ^ other) >> e) & 1ull);
-  g.stamp[c] = ch_now ? a.it_K : 0u;
+  const unsigned long long other = latest_index(wp, K + 1) ? wp.x : wp.y;
+  const bool ch_now = (unsigned)(v >> 32) == K && (((v ^ other) >> e) & 1ull);
+  g.stamp[c] = ch_now ? K : 0u;
 }
 
 // after the exchange: regions next to a ghost row that changed in this
@@ -1161,10 +1185,11 @@ __global__ void mark_kernel(const KArgs a, GhostView up, GhostView down) {
   const bool isup = i < a.RX;
   const int c = isup ? i : i - a.RX;
   const GhostView& g = isup ? up : down;
-  if (g.stamp[c] != a.it_K) return;
+  const unsigned K = stamp_of(a);
+  if (g.stamp[c] != K) return;
   const int r = isup ? 0 : a.RYl - 1;
   const int nidx = r * a.RX + c;
-  mark_dirty(a, nidx, a.it_K + 1);
+  mark_dirty(a, nidx, K + 1);
 }
 
 // Ordered worklist of the next iteration from its dirty bitmap: 8

@@ -642,8 +642,60 @@ struct IterSlot {
   unsigned long long stats[8];
   unsigned wl_next;
   unsigned pad[3];
+  unsigned long long ktime[2];  // graph loop: K1's first block start / last block end (ns)
 };
 
+// device-side window loop (ISING_SR_GRAPH): what the loop's advance kernels
+// accumulate over the iterations of a window, read back once per window
+struct WinDev {
+  unsigned trip;   // completed loop trips (two iterations each)
+  int it;          // iterations up to and including the converged one
+  int g;           // the iteration at which no history changed (0: not yet)
+  int overflow;
+  unsigned long long active[64];
+  unsigned long long ev, s1, s2, s3, s5, fmax;
+  unsigned long long k1_ns;
+};
+
+__global__ void slot_reset(IterSlot* sl) {
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 4; ++k) sl->flags[k] = 0;
+    for (int k = 0; k < 8; ++k) sl->stats[k] = 0;
+    sl->wl_next = 0;
+    sl->ktime[0] = ~0ull;
+    sl->ktime[1] = 0;
+  }
+}
+
+// after each iteration of the device-side loop: account the iteration (until
+// the window has converged or overflowed), reset the slot of the iteration
+// after next, count the loop trip, and set the while-condition: continue
+// while histories change, no capacity overflowed and fewer than max
+// iterations ran ("UNTIL all PEs detect no difference")
+__global__ void advance_kernel(WinDev* w, const IterSlot* cur, IterSlot* next, int max_it,
+                               cudaGraphConditionalHandle h, int set_cond, int end_of_trip) {
+  if (threadIdx.x != 0) return;
+  if (w->g == 0 && !w->overflow) {
+    const int it = ++w->it;
+    w->active[min(it, 64) - 1] += cur->stats[5];
+    w->ev += cur->stats[0];
+    w->s1 += cur->stats[1];
+    w->s2 += cur->stats[2];
+    w->s3 += cur->stats[3];
+    w->s5 += cur->stats[5];
+    w->fmax = max(w->fmax, cur->stats[4]);
+    if (cur->ktime[1] > cur->ktime[0]) w->k1_ns += cur->ktime[1] - cur->ktime[0];
+    if (cur->flags[1]) w->overflow = 1;
+    else if (!cur->flags[0]) w->g = it;
+  }
+  for (int k = 0; k < 4; ++k) next->flags[k] = 0;
+  for (int k = 0; k < 8; ++k) next->stats[k] = 0;
+  next->wl_next = 0;
+  next->ktime[0] = ~0ull;
+  next->ktime[1] = 0;
+  if (end_of_trip) w->trip += 1;
+  if (set_cond) cudaGraphSetConditional(h, (w->g || w->overflow || w->it >= max_it) ? 0u : 1u);
+}
 struct ising_sr_ctx {
   ising_sr_config cfg;
   const ShapeOps* ops = nullptr;
@@ -738,6 +790,9 @@ struct ising_sr_ctx {
   cudaEvent_t pev[2] = {};  // pipelined: results of the iteration with stamp parity j copied to the host
   IterSlot* d_slot = nullptr;  // [2]
   IterSlot* h_slot = nullptr;  // pinned mirror [2]
+  int graph = 0;               // device-side window loop (env ISING_SR_GRAPH=1)
+  WinDev* d_win = nullptr;
+  WinDev* h_win = nullptr;     // pinned
   unsigned delay_ns = 0;  // test knob (env ISING_SR_K1_DELAY_NS): K1 publishes late
   int refill = 28;  // K1 batched-refill threshold (env ISING_SR_REFILL; 28 measured best after the shared fresh-load step)
   ising_sr_stats stats;
@@ -1220,6 +1275,151 @@ ising_sr_status run_window_pipelined(ising_sr_ctx* c) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Device-side window loop (ISING_SR_GRAPH=1; world 1): the whole relaxation of a window
+// is one CUDA graph -- iteration 1 (the canonical assumption) followed by a
+// conditional while node whose body runs two iterations, each K1 [+ pack,
+// NCCL send/recv, all-reduce, mark] + worklist compaction + an advance kernel
+// that accounts the iteration and decides whether to go on.  The body's two
+// iterations have fixed parities, so every pointer is fixed at capture; a
+// kernel's iteration stamp is it_K + 2 * trip with trip counted on the
+// device.  No host round trip per iteration; one synchronisation per window.
+// An iteration after the converged one (the body's second half) finds an
+// empty worklist and changes nothing, so g and every result are those of the
+// host loops.
+// ---------------------------------------------------------------------------
+ising_sr_status capture_iteration(ising_sr_ctx* c, unsigned K, bool first, const unsigned* trip,
+                                  cudaGraphConditionalHandle h, int set_cond, int end_of_trip) {
+  const int j = (int)(K & 1u);
+  IterSlot* sl = c->d_slot + j;
+  IterSlot* prev = c->d_slot + (j ^ 1);
+  KArgs a = base_args(c, K, first);
+  a.trip = trip;
+  a.ktime = sl->ktime;
+  a.flags = sl->flags;
+  a.stats = sl->stats;
+  a.wl_in = first ? nullptr : c->wl[K & 1];
+  a.n_work = c->nreg;
+  a.n_work_dev = first ? nullptr : &prev->wl_next;
+  a.tile = tile_for(c->nreg);
+  a.wl_out = c->wl[(K + 1) & 1];
+  a.wl_out_count = &sl->wl_next;
+  c->ops->region(a, c->nreg, c->stream);
+  CK(c, cudaGetLastError());
+  if (c->ghost) {
+    c->ops->pack(a, c->gsend[0], c->gsend[1], c->RX, c->stream);
+    CK(c, cudaGetLastError());
+    ising_sr_status s = nccl_exchange(c, sl->flags);
+    if (s) return s;
+    isr::mark_kernel<<<(2 * c->RX + 127) / 128, 128, 0, c->stream>>>(a, c->grecv[0], c->grecv[1]);
+    CK(c, cudaGetLastError());
+  }
+  isr::compact_kernel<<<compact_grid(c), isr::kCompactThreads, 0, c->stream>>>(
+      c->dirty + (size_t)((K + 1) & 1) * c->dwords, c->dwords, c->nreg, c->wl[(K + 1) & 1], &sl->wl_next);
+  CK(c, cudaGetLastError());
+  advance_kernel<<<1, 32, 0, c->stream>>>(c->d_win, sl, prev, c->cfg.max_iterations, h, set_cond, end_of_trip);
+  CK(c, cudaGetLastError());
+  return ISING_SR_OK;
+}
+
+ising_sr_status build_window_graph(ising_sr_ctx* c, cudaGraphExec_t* exec) {
+  const unsigned K0 = c->Kglob + 1;  // iteration 1's stamp (== c->K0)
+  cudaGraph_t g = nullptr;
+  CK(c, cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  cudaError_t e = cudaGraphConditionalHandleCreate(&h, g, 1u, cudaGraphCondAssignDefault);
+  const cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  std::vector<cudaGraphNode_t> leaf;
+  ising_sr_status st = ISING_SR_OK;
+  // prefix: reset the window's accumulators and iteration 1's slot, iteration 1
+  if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(c->stream, g, nullptr, nullptr, 0, mode);
+  if (e == cudaSuccess) {
+    cudaMemsetAsync(c->d_win, 0, sizeof(WinDev), c->stream);
+    slot_reset<<<1, 32, 0, c->stream>>>(c->d_slot + (K0 & 1u));
+    st = capture_iteration(c, K0, true, nullptr, h, 1, 0);
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamGetCaptureInfo(c->stream, &cs, nullptr, nullptr, &deps, &ndeps) == cudaSuccess)
+      leaf.assign(deps, deps + ndeps);
+    cudaGraph_t gg = nullptr;
+    e = cudaStreamEndCapture(c->stream, &gg);
+  }
+  // the loop: while (changed) { iteration K0 + 1 + 2 trip; iteration K0 + 2 + 2 trip }
+  cudaGraph_t body = nullptr;
+  if (e == cudaSuccess && st == ISING_SR_OK) {
+    alignas(cudaGraphNodeParams) unsigned char pbuf[sizeof(cudaGraphNodeParams)];
+    std::memset(pbuf, 0, sizeof pbuf);  // (the struct's union has no default constructor)
+    cudaGraphNodeParams& p = *reinterpret_cast<cudaGraphNodeParams*>(pbuf);
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    cudaGraphNode_t cn;
+    e = cudaGraphAddNode(&cn, g, leaf.data(), leaf.size(), &p);
+    if (e == cudaSuccess) body = p.conditional.phGraph_out[0];
+  }
+  if (e == cudaSuccess && st == ISING_SR_OK) {
+    e = cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, mode);
+    if (e == cudaSuccess) {
+      st = capture_iteration(c, K0 + 1, false, &c->d_win->trip, h, 0, 0);
+      if (st == ISING_SR_OK) st = capture_iteration(c, K0 + 2, false, &c->d_win->trip, h, 1, 1);
+      cudaGraph_t bb = nullptr;
+      const cudaError_t e2 = cudaStreamEndCapture(c->stream, &bb);
+      if (e == cudaSuccess) e = e2;
+    }
+  }
+  if (e == cudaSuccess && st == ISING_SR_OK) e = cudaGraphInstantiate(exec, g, 0);
+  cudaGraphDestroy(g);
+  if (st != ISING_SR_OK) return st;
+  return fail_cuda(c, e, "build_window_graph");
+}
+
+ising_sr_status run_window_graph(ising_sr_ctx* c) {
+  for (;;) {
+    const unsigned K0 = c->Kglob + 1;
+    cudaGraphExec_t exec = nullptr;
+    ising_sr_status s = build_window_graph(c, &exec);
+    if (s) return s;
+    cudaError_t e = cudaGraphLaunch(exec, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->h_win, c->d_win, sizeof(WinDev), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaGraphExecDestroy(exec);
+    CK(c, e);
+    const WinDev& w = *c->h_win;
+    // every launch of the graph: iteration 1 and two per loop trip
+    const int launched = 1 + 2 * (int)w.trip;
+    c->Kglob = K0 + 2 * w.trip;
+    c->launches += (long long)launched * (c->ghost ? 4 : 2) + launched + 2;
+    const double S = (double)c->ops->spin_bytes + (double)c->ops->halo_bytes + 8 + 8 + 4 +
+                     ((c->cfg.flags & ISING_SR_FLAG_DIGEST) ? 8 : 0);
+    const double ib = (double)w.s5 * (2.0 * S + c->ops->sel_read_bytes + 8.0) + 9.0 * ((double)w.s1 + (double)w.s2 + (double)w.s3);
+    for (int k = 0; k < 64; ++k) c->win_active[k] += (long long)w.active[k];
+    c->stats.region_launches += launched;
+    c->stats.region_ms += (double)w.k1_ns * 1e-6;
+    c->stats.region_bytes += ib;
+    c->stats.iterations_total += w.it;
+    c->stats.recomputations_total += (long long)w.s5;
+    c->win_bytes += ib;
+    c->win_events += w.ev;
+    c->win_f = std::max(c->win_f, (int)w.fmax);
+    if (w.overflow) {  // history capacity overflow: grow and restart the window
+      CK(c, cudaMemsetAsync(c->dirty, 0, 2 * (size_t)c->dwords * sizeof(uint32_t), c->stream));
+      if ((s = grow_capacity(c))) return s;
+      start_window(c);
+      continue;
+    }
+    if (!w.g) {
+      c->in_window = false;
+      return ISING_SR_E_DIVERGED;
+    }
+    c->converged = true;
+    c->g = w.g;
+    c->it = w.g;
+    return ISING_SR_OK;
+  }
+}
+
 // FLAG_MAG_MOMENTS: the window's int |M| dt and int M^2 dt into c->h_mm
 // (enqueued; read after the commit's synchronisation).  n = events of the
 // window (the log is complete on the stream).
@@ -1328,6 +1528,8 @@ void ising_sr_destroy(ising_sr_ctx* c) {
   cudaFreeHost(c->h_stats);
   cudaFreeHost(c->h_wlc);
   dfree(c, c->d_slot);
+  dfree(c, c->d_win);
+  if (c->h_win) cudaFreeHost(c->h_win);
   dfree(c, c->d_snap);
   cudaFreeHost(c->h_slot);
   dfree(c, c->log_t);
@@ -1404,6 +1606,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   if (const char* e = std::getenv("ISING_SR_PIPELINE")) c->pipeline = std::atoi(e) != 0;
   if (const char* e = std::getenv("ISING_SR_REFILL")) c->refill = std::max(1, std::min(32, std::atoi(e)));
   if (const char* e = std::getenv("ISING_SR_K1_DELAY_NS")) c->delay_ns = (unsigned)std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("ISING_SR_GRAPH")) c->graph = std::atoi(e) != 0;
   if ((c->cfg.flags & ISING_SR_FLAG_OBSERVABLES) && ops->warp && !big_enabled()) {
     delete c;
     return ISING_SR_E_INVALID_ARG;  // observables are accumulated by the lane-per-region K1 forms only
@@ -1441,6 +1644,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
       dmalloc(c, &c->d_off, n) != cudaSuccess || dmalloc(c, &c->d_bsum, (n + kThreads - 1) / kThreads) != cudaSuccess ||
       dmalloc(c, &c->d_total, 1) != cudaSuccess || dmalloc(c, &c->d_obs, 2 * kObsBlocks + 2) != cudaSuccess ||
       dmalloc(c, &c->d_slot, 2) != cudaSuccess || dmalloc(c, &c->d_snap, 2) != cudaSuccess ||
+      dmalloc(c, &c->d_win, 1) != cudaSuccess || cudaMallocHost((void**)&c->h_win, sizeof(WinDev)) != cudaSuccess ||
       cudaMallocHost((void**)&c->h_slot, 2 * sizeof(IterSlot)) != cudaSuccess)
     return bail(ISING_SR_E_OOM);
   if (cudaMemsetAsync(c->sel, 0, n * 8 * (size_t)ops->sel_words, c->stream) != cudaSuccess ||
@@ -1646,6 +1850,13 @@ ising_sr_status ising_sr_run_window(ising_sr_ctx* c, int32_t* g_out) {
   if (s) return s;
   if (c->ghost && !c->nccl && !c->cfg.exchange) return ISING_SR_E_INVALID_ARG;  // step-level API only
   if ((s = ising_sr_begin_window(c))) return s;
+  // (strips keep the host loop: NCCL's captured work is not allowed inside a
+  // conditional node's body -- cudaGraphAddNode/EndCapture reject it)
+  if (c->graph && c->pipeline && !(c->cfg.flags & ISING_SR_FLAG_JACOBI_ALL) && !c->ghost) {
+    if ((s = run_window_graph(c))) return s;
+    if (g_out) *g_out = c->g;
+    return ISING_SR_OK;
+  }
   if (c->pipeline && !(c->cfg.flags & ISING_SR_FLAG_JACOBI_ALL)) {
     if ((s = run_window_pipelined(c))) return s;
     if (g_out) *g_out = c->g;

@@ -139,7 +139,8 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
-  const unsigned K = a.it_K, K0 = a.it_K0;
+  const unsigned K = stamp_of(a), K0 = a.it_K0;
+  ktime_begin(a);
   unsigned long long n_ev = 0, n_out = 0, n_in = 0, n_cmp = 0, n_reg = 0;
   unsigned fmax = 0;
   bool changed = false, overflow = false;
@@ -392,6 +393,7 @@ __global__ void __launch_bounds__(128) region_kernel_w(const KArgs a) {
     }
   }
 
+  ktime_end(a);
   if (!LOG && lane == 0) {
     if (changed) atomicOr(&a.flags[0], 1);
     if (overflow) atomicOr(&a.flags[1], 1);
@@ -489,7 +491,8 @@ __global__ void pack_kernel_w(const KArgs a, GhostView send_up, GhostView send_d
   const int e = up ? EDGE_N : EDGE_S;
   const GhostView& g = up ? send_up : send_down;
   const ulonglong2 wp = reinterpret_cast<const ulonglong2*>(a.sel)[((long long)r * a.RX + c) * 4 + e];
-  const unsigned long long v = latest_word(wp, a.it_K + 1);
+  const unsigned K = stamp_of(a);
+  const unsigned long long v = latest_word(wp, K + 1);
   int cnt = 0;
   if (word_valid(v, a.it_K0)) {
     const EdgeView& E = ew_slot(v) ? a.ed[1] : a.ed[0];
@@ -501,7 +504,7 @@ __global__ void pack_kernel_w(const KArgs a, GhostView send_up, GhostView send_d
     }
   }
   g.cnt[c] = (uint16_t)cnt;
-  g.stamp[c] = (unsigned)(v >> 32) == a.it_K ? a.it_K : 0u;
+  g.stamp[c] = (unsigned)(v >> 32) == K ? K : 0u;
 }
 
 }  // namespace isr

@@ -471,3 +471,37 @@ def test_observables_snapshot_at_committed_times(geom):
     st = sim.stats()
     assert (st["obs_M_now"], st["obs_B_now"]) == direct()
     sim.close()
+
+
+# ---------------------------------------------------------------------------
+# the device-side window loop (ISING_SR_GRAPH=1: one CUDA graph per window,
+# iteration 1 + a conditional while node of two iterations per trip, the
+# decision taken on the device): same bits and the same g per window as the
+# host loops, incl. a capacity-overflow restart and divergence
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("geom", [(64, 64, 4, 4, 2.0, 0.5), (32, 32, 8, 8, 2.269, 1.0), (16, 16, 1, 1, 2.0, 0.5),
+                                  (64, 64, 16, 16, 2.269, 1.0), (64, 64, 32, 32, 4.0, 0.5)])
+def test_device_window_loop_bit_exact(geom, monkeypatch):
+    Lx, Ly, bx, by, T, W = geom
+    w = workloads.Workload("graph", Lx, Ly, bx, by, T=T, W=W, t_end=4.0, seed=9)
+    host = run_gpu(w)
+    monkeypatch.setenv("ISING_SR_GRAPH", "1")
+    ref, dev = check_against_oracle(w)
+    assert dev["g"] == host["g"]
+    assert dev["stats"]["recomputations_total"] == host["stats"]["recomputations_total"]
+    assert dev["stats"]["region_ms"] > 0.0
+
+
+def test_device_window_loop_overflow_and_divergence(monkeypatch):
+    monkeypatch.setenv("ISING_SR_GRAPH", "1")
+    w = workloads.Workload("cap", 32, 32, 4, 4, T=4.0, W=2.0, t_end=6.0, seed=2)
+    gpu = run_gpu(w, per_window_logs=False, hist_capacity=1)
+    assert gpu["stats"]["overflow_retries"] >= 1
+    check_against_oracle(w, gpu=gpu, logs=False)
+    w = workloads.Workload("div", 32, 32, 2, 2, T=2.0, W=4.0, t_end=8.0, seed=4)
+    sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed, max_iterations=2)
+    with pytest.raises(IsingSRError) as e:
+        sim.run_window()
+    assert e.value.status == -4
+    assert np.array_equal(sim.spins(), w.spins())
+    sim.close()
