@@ -120,8 +120,7 @@ struct KArgs {
   int PC;
   const uint32_t* wl_in;   // regions to recompute (nullptr: all regions)
   int n_work;              // number of regions to recompute
-  const unsigned* n_work_dev;  // if set: the number is read here on the device (pool kernel)
-  unsigned* work_ctr;          // if set: global work queue (persistent pool kernel), zeroed per launch
+  const unsigned* n_work_dev;  // if set: the number is read here on the device (pipelined / graph loop, replay)
   int tile;                // work items per block (lane-persistent scheduling)
   unsigned rx_M;           // idx / RX == (idx * rx_M) >> rx_k for idx < 2^31 (host-computed)
   int rx_k;
