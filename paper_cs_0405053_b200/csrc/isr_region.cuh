@@ -34,6 +34,11 @@ template <int BX_, int BY_>
 struct Geo {
   static constexpr int BX = BX_, BY = BY_, NS = BX * BY;
   static_assert(NS <= 64, "lane-per-region form holds <= 64 sites");
+  // 1x1 regions: the single site is on all four edges, so the four edge
+  // histories are identical; only edge 0's is stored (and read for every
+  // direction), the selector word repeats its slot and count for all edges
+  static constexpr bool SE = NS == 1;
+  __host__ __device__ static constexpr int arr(int e) { return SE ? 0 : e; }
   using M = typename std::conditional<(NS <= 32), uint32_t, unsigned long long>::type;  // site mask
   using ST = uint_for<NS>;                   // stored spins
   using HT = uint_for<2 * BX + 2 * BY>;      // stored ghost bits: N[BX] S[BX] W[BY] E[BY]
@@ -86,6 +91,7 @@ struct KArgs {
   GhostView gh_up, gh_down;     // world > 1: rows above / below the strip
   int RX, RYl, RYg, row0, world;
   int ghost;          // the strip's first/last region rows read ghost rows (world > 1, or halo loopback)
+  int single_edge;    // 1x1 regions: one stored edge history per region (Geo::SE)
   int K;
   long long tstride;  // elements per edge in t/pos (RYl * K * RX)
   unsigned it_K;      // global iteration stamp of this launch (>= 1); with `trip`: the stamp of loop trip 0
@@ -647,8 +653,8 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
     if (cnt[d] > 0) {
       const unsigned off = in_off(a, r, c, d, src[d]);
       L.hoff[d] = off;
-      const double* T = src_t(a, src[d], d ^ 1);
-      const uint8_t* P = src_p(a, src[d], d ^ 1);
+      const double* T = src_t(a, src[d], G::arr(d ^ 1));
+      const uint8_t* P = src_p(a, src[d], G::arr(d ^ 1));
       if (cnt[d] <= (unsigned)SG::CIN) {
         flags = 1u << 28;
         staged_any = true;
@@ -671,6 +677,10 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   // stage own latest histories for the diff
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
+    if (G::SE && e > 0) {  // the same history as edge 0's
+      L.om[e] = L.om[0];
+      continue;
+    }
     const unsigned pc = word_count(vown, e), ps = (unsigned)word_slot(vown, e);
     unsigned st = 0;
     if (SG::HAS_OWN && !LOG && pc > 0 && pc <= (unsigned)SG::CIO) {
@@ -695,7 +705,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
     for (int d = 0; d < 4; ++d) {
       if (!(L.hm[d] & (1u << 28))) continue;
       const unsigned off = L.hoff[d];
-      const uint8_t* P = src_p(a, (L.hm[d] >> 24) & 3u, d ^ 1);
+      const uint8_t* P = src_p(a, (L.hm[d] >> 24) & 3u, G::arr(d ^ 1));
 #pragma unroll
       for (int q = 0; q < SG::CIN; ++q)
         if (q < (int)(L.hm[d] & 0xFFu)) {
@@ -848,8 +858,8 @@ __device__ __forceinline__ void bp_pre2(const KArgs& a, Lane<G>& L, SG& S, int s
       const unsigned src = (hmd >> 24) & 3u;
       const unsigned hoff = dstar == 0 ? L.hoff[0] : dstar == 1 ? L.hoff[1] : dstar == 2 ? L.hoff[2] : L.hoff[3];
       const unsigned off = hoff + nx * (unsigned)a.RX;
-      tn = src_t(a, src, dstar ^ 1)[off];
-      pos = src_p(a, src, dstar ^ 1)[off];
+      tn = src_t(a, src, G::arr(dstar ^ 1))[off];
+      pos = src_p(a, src, G::arr(dstar ^ 1))[off];
     }
   }
   const unsigned hn = (hmd & 0xFF0000FFu) | (nx << 8) | (pos << 16);
@@ -938,6 +948,12 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const
       L.om[EDGE_E] = w ? L.om[EDGE_E] : om;
     }
     L.bev += (onV || onH) ? 1u : 0u;
+  } else if (G::SE) {  // 1x1: one stored history for the four edges
+    L.om[0] = hist_put(a, L.om[0], 0, L.obase, L.tc, (uint8_t)0, S, si, n_out, overflow);
+    L.om[1] = L.om[0];
+    L.om[2] = L.om[0];
+    L.om[3] = L.om[0];
+    L.bev += 1u;
   } else {
     bool on_edge = false;
 #pragma unroll
@@ -1162,7 +1178,7 @@ __global__ void pack_kernel(const KArgs a, GhostView send_up, GhostView send_dow
   if (word_valid(v, a.it_K0)) {
     const EdgeView& E = word_slot(v, e) ? a.ed[1] : a.ed[0];
     cnt = (int)word_count(v, e);
-    const long long base = (long long)e * a.tstride + ((long long)r * a.K) * a.RX + c;
+    const long long base = (long long)(a.single_edge ? 0 : e) * a.tstride + ((long long)r * a.K) * a.RX + c;
     for (int q = 0; q < cnt; ++q) {
       g.t[(long long)q * a.RX + c] = E.t[base + (long long)q * a.RX];
       g.pos[(long long)q * a.RX + c] = E.pos[base + (long long)q * a.RX];

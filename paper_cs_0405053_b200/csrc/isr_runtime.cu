@@ -46,6 +46,7 @@ constexpr int kThreads = isr::NT;  // K1 block (and the small kernels')
 struct ShapeOps {
   int bx, by;
   bool warp;         // warp-per-region form (regions > 64 sites)
+  bool single_edge;  // 1x1 regions: one stored edge history (the four are identical)
   size_t spin_bytes, halo_bytes;
   int sel_words;     // selector words per region (2: packed per region; 8: pair per edge)
   int cnt_max;       // largest history length the selector can record
@@ -66,6 +67,7 @@ ShapeOps make_ops() {
   o.bx = BX;
   o.by = BY;
   o.warp = false;
+  o.single_edge = G::SE;
   o.spin_bytes = sizeof(typename G::ST);
   o.halo_bytes = sizeof(typename G::HT);
   o.sel_words = 2;
@@ -129,6 +131,7 @@ ShapeOps make_ops_w() {
   o.bx = BX;
   o.by = BY;
   o.warp = true;
+  o.single_edge = false;
   o.spin_bytes = (size_t)BY * 4;
   o.halo_bytes = 16;
   o.sel_words = 8;
@@ -853,9 +856,9 @@ void free_edges(ising_sr_ctx* c) {
 ising_sr_status alloc_edges(ising_sr_ctx* c, int K) {
   free_edges(c);
   c->K = K;
-  const size_t cn = (size_t)4 * c->RYl * c->RX;
+  const size_t cn = (size_t)(c->ops->single_edge ? 1 : 4) * c->RYl * c->RX;
   const size_t tn = cn * (size_t)K;
-  if (tn / 4 >= (1ull << 32)) return ISING_SR_E_CAPACITY;  // offsets within one edge array are 32-bit
+  if ((size_t)c->RYl * c->RX * (size_t)K >= (1ull << 32)) return ISING_SR_E_CAPACITY;  // 32-bit offsets within one edge array
   for (auto& e : c->ed) {
     if (dmalloc(c, &e.t, tn) != cudaSuccess || dmalloc(c, &e.pos, tn) != cudaSuccess) {
       cudaGetLastError();
@@ -935,6 +938,7 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   a.row0 = c->row0;
   a.world = c->cfg.world;
   a.ghost = c->ghost ? 1 : 0;
+  a.single_edge = c->ops->single_edge ? 1 : 0;
   a.eq_q = c->cfg.eq_quantum;
   a.ev_t = c->ev_t;
   a.ev_s = c->ev_s;
@@ -1680,7 +1684,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
     // region each); a longer history is caught by the overflow retry
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr > 0) {
-      const double per_k = 2.0 * 4.0 * (double)c->nreg * 9.0;
+      const double per_k = 2.0 * (ops->single_edge ? 1.0 : 4.0) * (double)c->nreg * 9.0;
       const int kmax = (int)std::max(2.0, 0.6 * (double)fr / per_k);
       K0 = std::min(K0, kmax);
     }

@@ -29,10 +29,13 @@ import workloads  # noqa: E402
 from paper_cs_0405053_b200 import FLAG_DIGEST, IsingSR  # noqa: E402
 
 
+MAX_IT = 0  # 0: the library's default (1000)
+
+
 def run_one(w, digest=True):
     stream = torch.cuda.Stream()
     sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), w.spins(), w.W, w.t_end, w.seed, J=w.J, H=w.H, T=w.T,
-                  flags=FLAG_DIGEST if digest else 0, stream=stream.cuda_stream)
+                  flags=FLAG_DIGEST if digest else 0, stream=stream.cuda_stream, max_iterations=MAX_IT)
     gs, fs, evs, wms = [], [], [], []
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -108,9 +111,12 @@ def main():
     ap.add_argument("--oracle", action="store_true", help="also run the CPU oracle (test infrastructure) for parity")
     ap.add_argument("--golden", action="store_true", help="bit-exact parity against tests/golden/full_size")
     ap.add_argument("--window", default="config", choices=["config", "tmax"])
+    ap.add_argument("--max-iterations", type=int, default=0)
     ap.add_argument("--out", required=True)
     ap.add_argument("--csv", default="")
     args = ap.parse_args()
+    global MAX_IT
+    MAX_IT = args.max_iterations
     torch.cuda.set_device(0)
     ws = [workloads.get(c) for c in args.configs.split(",") if c]
     if args.c5:
