@@ -309,6 +309,10 @@ ising_sr_status ising_sr_checkpoint_size(const ising_sr_ctx* ctx, int64_t* bytes
 ising_sr_status ising_sr_checkpoint_save(ising_sr_ctx* ctx, void* buf, int64_t cap);
 ising_sr_status ising_sr_checkpoint_load(ising_sr_ctx* ctx, const void* buf, int64_t len);
 
+/* sizeof of the ABI structs as compiled into the library (binding checks:
+ * 0 = ising_sr_config, 1 = ising_sr_stats, 2 = ising_sr_halo; else 0). */
+size_t ising_sr_struct_size(int32_t which);
+
 /* Number of kernel launches issued by this ctx so far (instrumentation). */
 int64_t ising_sr_launch_count(const ising_sr_ctx* ctx);
 

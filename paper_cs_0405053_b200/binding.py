@@ -93,6 +93,7 @@ EXPORTS = ["ising_sr_init", "ising_sr_run_window", "ising_sr_commit", "ising_sr_
            "ising_sr_end_iterations",
            "ising_sr_checkpoint_size", "ising_sr_checkpoint_save", "ising_sr_checkpoint_load",
            "ising_sr_launch_count", "ising_sr_destroy", "ising_sr_strerror", "ising_sr_nccl_unique_id",
+           "ising_sr_struct_size",
            "ising_cb_sweeps", "ising_cb_run"]
 
 
@@ -129,10 +130,12 @@ def load_library(path: str = LIB_PATH):
     L.ising_sr_strerror.argtypes = [i32]
     L.ising_sr_strerror.restype = ctypes.c_char_p
     L.ising_sr_nccl_unique_id.argtypes = [vp]
+    L.ising_sr_struct_size.argtypes = [i32]
+    L.ising_sr_struct_size.restype = ctypes.c_size_t
     L.ising_cb_sweeps.argtypes = [vp, i32, i32, vp, ctypes.c_uint64, i64, i32, vp, vp]
     L.ising_cb_run.argtypes = [vp, vp, i32, i32, vp, ctypes.c_uint64, i64, i32, ctypes.POINTER(i64), i32]
     for name in EXPORTS:
-        if name not in ("ising_sr_launch_count", "ising_sr_destroy", "ising_sr_strerror"):
+        if name not in ("ising_sr_launch_count", "ising_sr_destroy", "ising_sr_strerror", "ising_sr_struct_size"):
             getattr(L, name).restype = i32
     _lib = L
     return L

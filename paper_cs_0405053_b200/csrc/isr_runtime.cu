@@ -2257,4 +2257,8 @@ ising_sr_status ising_sr_checkpoint_load(ising_sr_ctx* c, const void* buf, int64
 
 int64_t ising_sr_launch_count(const ising_sr_ctx* c) { return c ? c->launches : 0; }
 
+size_t ising_sr_struct_size(int32_t which) {
+  return which == 0 ? sizeof(ising_sr_config) : which == 1 ? sizeof(ising_sr_stats) : which == 2 ? sizeof(ising_sr_halo) : 0;
+}
+
 }  // extern "C"

@@ -97,3 +97,13 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     monkeypatch.setattr(binding, "_lib", None)
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         binding.load_library(str(tmp_path / "nope.so"))
+
+
+def test_struct_layouts_match_the_library(lib):
+    """The ctypes mirrors of ising_sr_config / ising_sr_stats / ising_sr_halo
+    have the sizes the library was compiled with (a field added on one side
+    only would shift every later field)."""
+    assert lib.ising_sr_struct_size(0) == ctypes.sizeof(binding.Config)
+    assert lib.ising_sr_struct_size(1) == ctypes.sizeof(binding.Stats)
+    assert lib.ising_sr_struct_size(2) == ctypes.sizeof(binding.Halo)
+    assert lib.ising_sr_struct_size(9) == 0
