@@ -61,7 +61,8 @@ class _Out(ctypes.Structure):
                 ("sample_t", ctypes.c_void_p), ("n_samples", ctypes.c_int32),
                 ("sample_M", ctypes.c_void_p), ("sample_B", ctypes.c_void_p),
                 ("n_events", ctypes.c_int64), ("log_n", ctypes.c_int64),
-                ("obs", ctypes.c_double * 5), ("check_failures", ctypes.c_int32)]
+                ("obs", ctypes.c_double * 5), ("check_failures", ctypes.c_int32),
+                ("n_bumps", ctypes.c_int64)]
 
 
 def lib():
@@ -235,7 +236,7 @@ def _run(kind: str, Lx: int, Ly: int, bx: int, by: int, rates: Sequence[float], 
         "n_events": int(o.n_events),
         "log_t": lt[:n].copy(), "log_region": lr[:n].copy(), "log_site": ls[:n].copy(),
         "sample_M": sM[:ns].copy(), "sample_B": sB[:ns].copy(),
-        "obs": list(o.obs), "check_failures": int(o.check_failures),
+        "obs": list(o.obs), "check_failures": int(o.check_failures), "n_bumps": int(o.n_bumps),
     }
 
 

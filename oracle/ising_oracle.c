@@ -182,10 +182,16 @@ static double fold_lambda(const int32_t* N, const double* rate) {
 /* candidate time: eq. nextau / eq. newtau in remaining-budget form,
  * cand(t, R, Lambda) = t + R/Lambda (readings #1, #2, #11); +inf if
  * Lambda = 0; bumped to nextafter(t, +inf) if it rounds onto t. */
+/* candidates that rounded onto their start and were bumped (reading #11), per run */
+static int64_t n_bumps;
+
 static double cand_time(double t, double R, double lam) {
   if (lam == 0.0) return INFINITY;
   double tau = t + R / lam;
-  if (tau == t) tau = nextafter(t, INFINITY);
+  if (tau == t) {
+    tau = nextafter(t, INFINITY);
+    n_bumps++;
+  }
   return tau;
 }
 
@@ -383,6 +389,7 @@ int orc_des_run(const orc_cfg* cfg, const uint8_t* spins0, uint8_t* spins_out, o
   out->n_events = 0;
   out->log_n = 0;
   out->check_failures = 0;
+  n_bumps = 0;
   for (int q = 0; q < 5; ++q) out->obs[q] = 0.0;
 
   /* initial state of every region: tau_0 = 0 */
@@ -508,6 +515,7 @@ int orc_des_run(const orc_cfg* cfg, const uint8_t* spins0, uint8_t* spins_out, o
     }
   }
   out->log_n = out->n_events < out->log_cap ? out->n_events : out->log_cap;
+  out->n_bumps = n_bumps;
   if (spins_out) memcpy(spins_out, L.s, NS);
   if (out->digest) memcpy(out->digest, dig, sizeof(uint64_t) * NR);
   if (out->count) memcpy(out->count, nev, sizeof(uint64_t) * NR);

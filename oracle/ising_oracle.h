@@ -82,6 +82,7 @@ typedef struct {
   int64_t   log_n;         /* min(n_events, log_cap)                              */
   double    obs[5];        /* integrals over [t_obs0,t_end): dt, B dt, M dt, |M| dt, M^2 dt */
   int32_t   check_failures;
+  int64_t   n_bumps;       /* O1: candidates bumped to nextafter(t_s) (reading #11), for tests */
 } orc_out;
 
 /* Per-region-stream DES (O1). spins: Ly*Lx row-major, 1 = up (+1), 0 = down.

@@ -51,6 +51,8 @@ def test_tie_mode_bit_exact(geom):
     w = workloads.Workload("tie", Lx, Ly, bx, by, T=T, W=W, t_end=t_end, seed=3)
     ref, gpu = check_against_oracle(w, oracle_kw={"eq_quantum": 4.0}, eq_quantum=4.0)
     assert _ties(ref) > (10 if math.isinf(T) else 2), "the mode must produce exact ties across regions"
+    if math.isinf(T) and bx == 4:  # budgets clamped to 0 by a tied break point: candidates bumped (R11)
+        assert ref["n_bumps"] > 0
     assert gpu["events"] > 0
 
 

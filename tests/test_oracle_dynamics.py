@@ -234,3 +234,13 @@ def test_fresh_window_identity_and_effect():
     fresh = oracle.des_workload(w, fresh_W=0.5)
     assert not np.array_equal(fresh["digest"], base["digest"])
     assert fresh["check_failures"] == 0
+
+
+def test_tie_mode_exercises_the_candidate_bump():
+    """Quantized budgets at T = inf (all rates 1): break points tied with a
+    region's candidate clamp its budget to 0 and its next candidate is bumped
+    to nextafter(t_s) (reading #11); with continuous budgets that never happens."""
+    import math
+    w = workloads.Workload("tie", 32, 32, 4, 4, T=math.inf, W=0.5, t_end=3.0, seed=3)
+    assert oracle.des_workload(w, eq_quantum=4.0)["n_bumps"] > 0
+    assert oracle.des_workload(w)["n_bumps"] == 0
