@@ -78,32 +78,32 @@ __device__ __forceinline__ void draw_pair(unsigned long long seed, uint32_t regi
 // (P:247-252).  U = m 2^e, m in (sqrt2/2, sqrt2]; log m = 2 atanh(s),
 // s = (m-1)/(m+1), series in z = s^2 to z^10.
 // ---------------------------------------------------------------------------
+// The series coefficients 1/(2j+3), j = 9 .. 0, then ln2 split hi/lo and the
+// sqrt2 threshold, in constant memory: DMUL/DADD take them as c[bank][offset]
+// operands (a 64-bit immediate costs two UMOVs per use on the draw path)
+static __constant__ double kExpC[13] = {0x1.8618618618618p-5, 0x1.af286bca1af28p-5, 0x1.e1e1e1e1e1e1ep-5,
+                                        0x1.1111111111111p-4, 0x1.3b13b13b13b14p-4, 0x1.745d1745d1746p-4,
+                                        0x1.c71c71c71c71cp-4, 0x1.2492492492492p-3, 0x1.999999999999ap-3,
+                                        0x1.5555555555555p-2, 0x1.62e42feep-1,      0x1.a39ef35793c76p-33,
+                                        0x1.6a09e667f3bcdp+0};
 __device__ __forceinline__ double expvar(double U) {
   const long long bits = __double_as_longlong(U);
   int e = (int)((bits >> 52) & 0x7ff) - 1023;
   double m = __longlong_as_double((bits & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
-  if (m > 0x1.6a09e667f3bcdp+0) {
+  if (m > kExpC[12]) {
     m = __dmul_rn(m, 0.5);
     e += 1;
   }
   const double f = __dsub_rn(m, 1.0);
   const double s = __ddiv_rn(f, __dadd_rn(2.0, f));
   const double z = __dmul_rn(s, s);
-  double P = 0x1.8618618618618p-5;
-  P = __dadd_rn(__dmul_rn(P, z), 0x1.af286bca1af28p-5);
-  P = __dadd_rn(__dmul_rn(P, z), 0x1.e1e1e1e1e1e1ep-5);
-  P = __dadd_rn(__dmul_rn(P, z), 0x1.1111111111111p-4);
-  P = __dadd_rn(__dmul_rn(P, z), 0x1.3b13b13b13b14p-4);
-  P = __dadd_rn(__dmul_rn(P, z), 0x1.745d1745d1746p-4);
-  P = __dadd_rn(__dmul_rn(P, z), 0x1.c71c71c71c71cp-4);
-  P = __dadd_rn(__dmul_rn(P, z), 0x1.2492492492492p-3);
-  P = __dadd_rn(__dmul_rn(P, z), 0x1.999999999999ap-3);
-  P = __dadd_rn(__dmul_rn(P, z), 0x1.5555555555555p-2);
+  double P = kExpC[0];
+#pragma unroll
+  for (int j = 1; j < 10; ++j) P = __dadd_rn(__dmul_rn(P, z), kExpC[j]);
   const double u = __dadd_rn(s, s);
   const double logm = __dadd_rn(u, __dmul_rn(u, __dmul_rn(z, P)));
   const double de = (double)e;
-  const double logU =
-      __dadd_rn(__dmul_rn(de, 0x1.62e42feep-1), __dadd_rn(__dmul_rn(de, 0x1.a39ef35793c76p-33), logm));
+  const double logU = __dadd_rn(__dmul_rn(de, kExpC[10]), __dadd_rn(__dmul_rn(de, kExpC[11]), logm));
   return -logU;
 }
 

@@ -215,11 +215,12 @@ __device__ __forceinline__ unsigned word_count(unsigned long long v, int e) {
   return (unsigned)((v >> (4 + CNT_BITS * e)) & CNT_MAX);
 }
 
-// bit-sliced per-site count of up neighbours: m[u] = sites with exactly u.
+// bit-sliced per-site count of up neighbours u = p2 p1 p0 (binary, u <= 4);
+// the sites of class k = 5 s + u are those with spin s and count u.
 template <class G>
 struct Classes {
   using M = typename G::M;
-  M up, dn, m0, m1, m2, m3, m4;
+  M up, p0, p1, p2;
 
   __device__ __forceinline__ void build(M spins, M gN, M gS, M gW, M gE, bool wrapX, bool wrapY) {
     constexpr M FULL = G::full();
@@ -245,22 +246,19 @@ struct Classes {
     // 4-input bit-sliced adder
     const M s1 = nN ^ nS, c1 = nN & nS;
     const M s2 = nW ^ nE, c2 = nW & nE;
-    const M p0 = s1 ^ s2, k = s1 & s2;
-    const M p1 = c1 ^ c2 ^ k;
-    const M p2 = (c1 & c2) | (k & (c1 ^ c2));
+    const M k = s1 & s2;
     up = spins;
-    dn = (M)(~spins) & FULL;
-    m0 = (M)(~(p0 | p1 | p2)) & FULL;
-    m1 = p0 & ~p1;
-    m2 = ~p0 & p1;
-    m3 = p0 & p1;
-    m4 = p2;
+    p0 = s1 ^ s2;
+    p1 = c1 ^ c2 ^ k;
+    p2 = (c1 & c2) | (k & (c1 ^ c2));
   }
+  // sites of class k (k may be a run-time value: selects, no branches)
   __device__ __forceinline__ M mask(int k) const {
-    const M s = k >= 5 ? up : dn;
-    const int u = k >= 5 ? k - 5 : k;
-    const M mu = u == 0 ? m0 : u == 1 ? m1 : u == 2 ? m2 : u == 3 ? m3 : m4;
-    return s & mu;
+    constexpr M FULL = G::full();
+    const bool hi = k >= 5;
+    const int u = hi ? k - 5 : k;
+    const M a0 = (u & 1) ? p0 : (M)~p0, a1 = (u & 2) ? p1 : (M)~p1, a2 = (u & 4) ? p2 : (M)~p2;
+    return (M)((hi ? up : (M)~up) & a0 & a1 & a2 & FULL);
   }
 };
 
@@ -327,10 +325,11 @@ __device__ __forceinline__ void fill_prod(ProdTable<G>& T, const double* rate) {
 // rounded reciprocal is within 1e-13 of the correctly rounded quotient, so it
 // decides the floor unless the quotient is that close to an integer; then
 // the IEEE division decides (bit-identical to always dividing)
+static __constant__ double kFloorEps = 1e-12;  // a c[] operand, not two UMOVs per use
 __device__ __forceinline__ long long floor_div(double aq, double rk, double rinv) {
   if (rk == 1.0) return __double2ll_rd(aq);  // aq / 1.0 == aq exactly
   const double qa = __dmul_rn(aq, rinv);
-  const long long jl = __double2ll_rd(__dsub_rn(qa, 1e-12)), jh = __double2ll_rd(__dadd_rn(qa, 1e-12));
+  const long long jl = __double2ll_rd(__dsub_rn(qa, kFloorEps)), jh = __double2ll_rd(__dadd_rn(qa, kFloorEps));
   return jl == jh ? jl : __double2ll_rd(__ddiv_rn(aq, rk));
 }
 
@@ -364,9 +363,7 @@ __device__ __forceinline__ int fold_select(const Classes<G>& C, const ProdTable<
     ks += below ? 1 : 0;
     cprev = below ? cs[k] : cprev;  // the last partial sum below x: c_{k*-1}
   }
-  const M s = ks >= 5 ? C.up : C.dn;
-  const int u = ks >= 5 ? ks - 5 : ks;
-  const M mk = s & (u == 0 ? C.m0 : u == 1 ? C.m1 : u == 2 ? C.m2 : u == 3 ? C.m3 : C.m4);
+  const M mk = C.mask(ks);
   const int nk = popc_m(mk);
   long long j = floor_div(__dsub_rn(x, cprev), rate[ks], T.rinv[ks]);
   j = j > nk - 1 ? nk - 1 : j;
@@ -1080,10 +1077,14 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
       if (go) {
         if (OBS && !LOG && !fresh)  // M and B after the step
           obs_counts<G>(L.spins, L.gN, L.gW, a.RX == 1, a.RYg == 1, L.Mi, L.Bi);
-        if (ev || fresh) {  // pair n: V picks the next atom, E(U) its budget
+        {  // pair n: V picks the next atom, E(U) its budget.  Drawn by every lane in one
+           // straight-line block with the refold (the Philox/E(U) and fold chains interleave); after a
+           // break point pair n is the pair already in use (the same V), so only an event (or a fresh_w
+           // load, whose budget restarts at t_c) takes its budget
           double U;
           draw_pair(a.seed, L.gid, L.n, U, L.V, a.gen);
-          if (ev || a.fresh_w) L.R = budget(a, U);  // (fresh_w: a loaded region restarts its budget at t_c)
+          const double Eu = budget(a, U);
+          if (ev || (fresh && a.fresh_w)) L.R = Eu;
         }
         refold<G>(a, L, PT);  // shared by both kinds of step
       }

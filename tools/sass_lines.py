@@ -21,7 +21,7 @@ import tempfile
 def line_map(lib, kernel):
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, check=True, capture_output=True)
-    cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
+    cub = [f for f in sorted(os.listdir(tmp)) if f.endswith(".cubin") and f.startswith("isr_runtime.")][0]
     out = subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
     inside = False
     cur = None
