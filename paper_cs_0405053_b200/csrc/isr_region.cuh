@@ -1087,6 +1087,10 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
           if (ev || (fresh && a.fresh_w)) L.R = Eu;
         }
         refold<G>(a, L, PT);  // shared by both kinds of step
+        // finished now: the candidate lies beyond the window and no break point is left (every incoming
+        // entry lies inside the window, so one left would come first) -- the decision the next round's
+        // next_bp2 would take, without spending that round
+        if (!(L.tc < a.t_w) && fmin(fmin(L.ht[0], L.ht[1]), fmin(L.ht[2], L.ht[3])) == dinf()) active = false;
       }
       fresh = false;
     }
