@@ -94,6 +94,7 @@ struct KArgs {
   int single_edge;    // 1x1 regions: one stored edge history per region (Geo::SE)
   int K;
   long long tstride;  // elements per edge in t/pos (RYl * K * RX)
+  long long sstride;  // elements from slot 0's arrays to slot 1's (ed[1].t == ed[0].t + sstride: one allocation)
   unsigned it_K;      // global iteration stamp of this launch (>= 1); with `trip`: the stamp of loop trip 0
   // device-side window loop (a CUDA graph with a conditional while node): the
   // loop body holds two iterations, so this launch's stamp is it_K + 2 * (*trip)
@@ -474,12 +475,14 @@ __device__ __forceinline__ int div_rx(const KArgs& a, int idx) {
 #define ISR_CI 3
 #endif
 #ifndef ISR_MINB
-#define ISR_MINB 0   // 0: per-shape default (5 resident blocks for 64-bit site masks, else ptxas' choice)
+#define ISR_MINB 6   // resident blocks asked of ptxas for <= 32-site regions (0: ptxas' choice, 96 registers)
 #endif
 // Launch bounds of K1: 8x8 regions (64-bit site masks) otherwise take 112
 // registers and 4 resident blocks; asking for 5 (region_kernel_mb) is 31 %
-// faster on the c5 8x8 points.  Smaller regions are left to ptxas (96
-// registers; an explicit minimum of 1 block would let it take 138).
+// faster on the c5 8x8 points.  Smaller regions: 6 blocks (80 registers, no
+// spills since the staged positions are packed, 31 KB of shared memory per
+// block): +3.8 % on c4 over ptxas' own 96 registers / 5 blocks; 7 blocks (72
+// registers) spill and lose 1.5 %.
 #ifndef ISR_NT
 #define ISR_NT 128
 #endif
@@ -493,10 +496,11 @@ struct StageT {
   static constexpr bool HAS_OWN = OWN;
   static constexpr int CIN = NCI;  // staged entries per incoming history
   static constexpr int CIO = NCO;  // ... per own latest history
+  static_assert(NCI <= 4 && NCO <= 4, "positions of a history are staged as the bytes of one word");
   double in_t[4][NCI][NC];
-  uint32_t in_p[4][NCI][NC];   // 4-byte word holding the position byte, then the byte itself
+  uint32_t in_p[4][NC];        // positions of the staged entries of direction d, entry q in byte q
   double own_t[4][OWN ? NCO : 1][OWN ? NC : 1];
-  uint32_t own_p[4][OWN ? NCO : 1][OWN ? NC : 1];
+  uint32_t own_p[4][OWN ? NC : 1];
 };
 #ifndef ISR_CO
 #define ISR_CO ISR_CI  // staged own latest entries per edge
@@ -552,18 +556,19 @@ __device__ __forceinline__ unsigned in_off(const KArgs& a, int r, int c, int d, 
 }
 
 // base of edge e's array in slot `src` (0/1), or of a ghost row (2 = above, 3 = below)
+// (the two slots are one allocation: slot s of edge e starts s * sstride + e * tstride elements in)
+__device__ __forceinline__ double* slot_t(const KArgs& a, unsigned s, int e) {
+  return a.ed[0].t + ((long long)s * a.sstride + (long long)e * a.tstride);
+}
+__device__ __forceinline__ uint8_t* slot_p(const KArgs& a, unsigned s, int e) {
+  return a.ed[0].pos + ((long long)s * a.sstride + (long long)e * a.tstride);
+}
 __device__ __forceinline__ const double* src_t(const KArgs& a, unsigned src, int e) {
-  return src == 0 ? a.ed[0].t + e * a.tstride : src == 1 ? a.ed[1].t + e * a.tstride
-       : src == 2 ? a.gh_up.t : a.gh_down.t;
+  return src < 2 ? slot_t(a, src, e) : src == 2 ? a.gh_up.t : a.gh_down.t;
 }
 __device__ __forceinline__ const uint8_t* src_p(const KArgs& a, unsigned src, int e) {
-  return src == 0 ? a.ed[0].pos + e * a.tstride : src == 1 ? a.ed[1].pos + e * a.tstride
-       : src == 2 ? a.gh_up.pos : a.gh_down.pos;
+  return src < 2 ? slot_p(a, src, e) : src == 2 ? a.gh_up.pos : a.gh_down.pos;
 }
-__device__ __forceinline__ const void* word_of(const uint8_t* p) {
-  return (const void*)((size_t)p & ~(size_t)3);
-}
-__device__ __forceinline__ unsigned byte_shift(const uint8_t* p) { return 8u * (unsigned)((size_t)p & 3); }
 
 // advance the integrals of M and B to time t (before a step at t)
 template <class G>
@@ -640,12 +645,16 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
     L.iB = 0.0;
     L.tpv = a.t_c;
   }
-  // stage incoming histories (above CI entries: read lazily from global)
+  // stage incoming histories (above CI entries: read lazily from global): the
+  // times global -> shared with cp.async, the position bytes loaded as they are
+  // and packed into one word per history after the wait
   bool staged_any = false;
+  unsigned ipos[4], opos[4];
 #pragma unroll
   for (int d = 0; d < 4; ++d) {
     L.ht[d] = dinf();
     L.hoff[d] = 0;
+    ipos[d] = 0;
     unsigned flags = 0;
     if (cnt[d] > 0) {
       const unsigned off = in_off(a, r, c, d, src[d]);
@@ -661,7 +670,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
             const unsigned o = off + (unsigned)q * (unsigned)a.RX;
             ISR_ASSERT(src[d] >= 2 ? (int)(o / (unsigned)a.RX) < a.K : (long long)o < a.tstride);
             cp_async8(&S.in_t[d][q][lane], T + o);
-            cp_async4(&S.in_p[d][q][lane], word_of(P + o));
+            ipos[d] |= (unsigned)P[o] << (8 * q);
           }
         }
       } else {
@@ -680,6 +689,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
     }
     const unsigned pc = word_count(vown, e), ps = (unsigned)word_slot(vown, e);
     unsigned st = 0;
+    opos[e] = 0;
     if (SG::HAS_OWN && !LOG && pc > 0 && pc <= (unsigned)SG::CIO) {
       st = 1;
       staged_any = true;
@@ -690,7 +700,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
         if (q < (int)pc) {
           const unsigned o = L.obase + (unsigned)q * (unsigned)a.RX;
           cp_async8(&S.own_t[e][q][lane], Et + o);
-          cp_async4(&S.own_p[e][q][lane], word_of(Ep + o));
+          opos[e] |= (unsigned)Ep[o] << (8 * q);
         }
       }
     }
@@ -701,27 +711,14 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
       if (!(L.hm[d] & (1u << 28))) continue;
-      const unsigned off = L.hoff[d];
-      const uint8_t* P = src_p(a, (L.hm[d] >> 24) & 3u, G::arr(d ^ 1));
-#pragma unroll
-      for (int q = 0; q < SG::CIN; ++q)
-        if (q < (int)(L.hm[d] & 0xFFu)) {
-          const unsigned o = off + (unsigned)q * (unsigned)a.RX;
-          S.in_p[d][q][lane] = (S.in_p[d][q][lane] >> byte_shift(P + o)) & 0xFFu;
-        }
-      L.hm[d] |= S.in_p[d][0][lane] << 16;
+      S.in_p[d][lane] = ipos[d];
+      L.hm[d] |= (ipos[d] & 0xFFu) << 16;
       L.ht[d] = S.in_t[d][0][lane];
     }
+    if (SG::HAS_OWN) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (!((L.om[e] >> 18) & 1u)) continue;
-      const uint8_t* Ep = src_p(a, (L.om[e] >> 16) & 1u, e);
-#pragma unroll
-      for (int q = 0; q < SG::CIO; ++q)
-        if (q < (int)((L.om[e] >> 8) & 0xFFu)) {
-          const unsigned o = L.obase + (unsigned)q * (unsigned)a.RX;
-          S.own_p[e][q][lane] = (S.own_p[e][q][lane] >> byte_shift(Ep + o)) & 0xFFu;
-        }
+      for (int e = 0; e < 4; ++e)
+        if ((L.om[e] >> 18) & 1u) S.own_p[e][lane] = opos[e];
     }
   }
   if (!FULL) return;
@@ -850,7 +847,7 @@ __device__ __forceinline__ void bp_pre2(const KArgs& a, Lane<G>& L, SG& S, int s
   if (nx < (hmd & 0xFFu)) {
     if (hmd & (1u << 28)) {
       tn = S.in_t[dstar][nx][lane];
-      pos = S.in_p[dstar][nx][lane];
+      pos = (S.in_p[dstar][lane] >> (8 * nx)) & 0xFFu;
     } else {
       const unsigned src = (hmd >> 24) & 3u;
       const unsigned hoff = dstar == 0 ? L.hoff[0] : dstar == 1 ? L.hoff[1] : dstar == 2 ? L.hoff[2] : L.hoff[3];
@@ -878,8 +875,8 @@ __device__ __forceinline__ unsigned hist_put(const KArgs& a, unsigned om, int e,
   if ((int)k < a.K) {
     const unsigned o = obase + k * (unsigned)a.RX;
     ISR_ASSERT((long long)o < a.tstride);
-    double* Tn = (ps ? a.ed[0].t : a.ed[1].t) + e * a.tstride;
-    uint8_t* Pn = (ps ? a.ed[0].pos : a.ed[1].pos) + e * a.tstride;
+    double* Tn = slot_t(a, ps ^ 1u, e);  // the other slot
+    uint8_t* Pn = slot_p(a, ps ^ 1u, e);
     Tn[o] = tc;
     Pn[o] = p;
     ++n_out;
@@ -887,12 +884,12 @@ __device__ __forceinline__ unsigned hist_put(const KArgs& a, unsigned om, int e,
       if (k >= pc) {
         dv = 1;
       } else if (SG::HAS_OWN && ((om >> 18) & 1u)) {
-        const unsigned pw = S.own_p[e][k][lane];
+        const unsigned pw = (S.own_p[e][lane] >> (8 * k)) & 0xFFu;
         dv = (__double_as_longlong(S.own_t[e][k][lane]) != __double_as_longlong(tc) || pw != p)
                  ? 1u : 0u;
       } else {
-        const double* To = (ps ? a.ed[1].t : a.ed[0].t) + e * a.tstride;
-        const uint8_t* Po = (ps ? a.ed[1].pos : a.ed[0].pos) + e * a.tstride;
+        const double* To = slot_t(a, ps, e);
+        const uint8_t* Po = slot_p(a, ps, e);
         dv = (__double_as_longlong(To[o]) != __double_as_longlong(tc) || Po[o] != p) ? 1u : 0u;
       }
     }

@@ -712,6 +712,7 @@ struct ising_sr_ctx {
   StateView st[2] = {};
   int comm = 0;  // index of the committed state
   EdgeView ed[2] = {};
+  long long sstride = 0;                  // elements from ed[0] to ed[1] (one allocation)
   unsigned long long* sel = nullptr;  // per region selector word
   // big-region step logs (resume; isr_big.cuh)
   double2* lg_tR = nullptr;
@@ -836,11 +837,9 @@ void dfree(ising_sr_ctx* c, void* p) {
 }
 
 void free_edges(ising_sr_ctx* c) {
-  for (auto& e : c->ed) {
-    dfree(c, e.t);
-    dfree(c, e.pos);
-    e = EdgeView{};
-  }
+  dfree(c, c->ed[0].t);  // one allocation holds both slots
+  dfree(c, c->ed[0].pos);
+  for (auto& e : c->ed) e = EdgeView{};
   dfree(c, c->gbuf);
   c->gbuf = nullptr;
   for (int i = 0; i < 2; ++i) {
@@ -859,13 +858,15 @@ ising_sr_status alloc_edges(ising_sr_ctx* c, int K) {
   const size_t cn = (size_t)(c->ops->single_edge ? 1 : 4) * c->RYl * c->RX;
   const size_t tn = cn * (size_t)K;
   if ((size_t)c->RYl * c->RX * (size_t)K >= (1ull << 32)) return ISING_SR_E_CAPACITY;  // 32-bit offsets within one edge array
-  for (auto& e : c->ed) {
-    if (dmalloc(c, &e.t, tn) != cudaSuccess || dmalloc(c, &e.pos, tn) != cudaSuccess) {
-      cudaGetLastError();
-      free_edges(c);
-      return ISING_SR_E_OOM;
-    }
+  // both slots in one allocation (slot 1 at + tn): the kernels address a slot arithmetically
+  if (dmalloc(c, &c->ed[0].t, 2 * tn) != cudaSuccess || dmalloc(c, &c->ed[0].pos, 2 * tn) != cudaSuccess) {
+    cudaGetLastError();
+    free_edges(c);
+    return ISING_SR_E_OOM;
   }
+  c->ed[1].t = c->ed[0].t + tn;
+  c->ed[1].pos = c->ed[0].pos + tn;
+  c->sstride = (long long)tn;
   if (c->ghost) {
     const size_t RX = (size_t)c->RX;
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
@@ -946,6 +947,7 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   a.ev_stride = c->nreg;
   a.K = c->K;
   a.tstride = (long long)c->RYl * c->K * c->RX;
+  a.sstride = c->sstride;
   a.it_K = K;
   a.it_K0 = c->K0;
   a.first = first ? 1 : 0;
