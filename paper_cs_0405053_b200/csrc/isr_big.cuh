@@ -673,8 +673,8 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
             const uint8_t p = (uint8_t)(e < 2 ? sc : sr);
             if ((int)k < a.K) {
               const unsigned o = obase + k * (unsigned)a.RX;
-              (ps[e] ? a.ed[0].t : a.ed[1].t)[e * a.tstride + o] = tc;
-              (ps[e] ? a.ed[0].pos : a.ed[1].pos)[e * a.tstride + o] = p;
+              slot_t(a, ps[e] ^ 1u, e)[o] = tc;  // the other slot
+              slot_p(a, ps[e] ^ 1u, e)[o] = p;
               ++n_out;
               if (!dv[e]) {
                 fdk[e] = k;  // first differing entry, if it differs here
@@ -753,10 +753,25 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
                 Pn[o] = pv[u];
               }
             }
-            for (; q < k0[e]; ++q) {
-              const unsigned o = obase + q * (unsigned)a.RX;
-              Tn[o] = To[o];
-              Pn[o] = Po[o];
+            if (q < k0[e]) {  // the last < 8 entries, also with their loads issued together
+              double tv[8];
+              uint8_t pv[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const unsigned o = obase + (q + u) * (unsigned)a.RX;
+                if (q + u < k0[e]) {
+                  tv[u] = __ldcg(To + o);
+                  pv[u] = __ldcg(Po + o);
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const unsigned o = obase + (q + u) * (unsigned)a.RX;
+                if (q + u < k0[e]) {
+                  Tn[o] = tv[u];
+                  Pn[o] = pv[u];
+                }
+              }
             }
           }
           const unsigned fd = min(dv[e] ? fdk[e] : min(oc[e], pc[e]), 0x7FFFu);
