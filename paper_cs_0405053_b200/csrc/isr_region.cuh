@@ -585,11 +585,11 @@ __device__ __forceinline__ void obs_advance(Lane<G>& L, double t) {
 // incoming histories to read or stage.  The own selector pair is still read:
 // the new word must flip the slot bit of every changed edge relative to the
 // other word (pack_kernel's change test for the strip exchange).
-template <class G, bool LOG, class SG, bool FULL = true, bool OBS = false, bool FIRST = false>
+template <class G, bool LOG, class SG, bool FULL = true, bool OBS = false, bool FIRST = false, bool PLAIN = false>
 __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, SG& S, const ProdTable<G>& PT,
                                           int si) {
   using M = typename G::M;
-  const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
+  const bool wrapX = !PLAIN && a.RX == 1, wrapY = !PLAIN && a.RYg == 1;
   const unsigned K = stamp_of(a), K0 = a.it_K0;
   const int lane = si;
   const int r = div_rx(a, idx), c = idx - r * a.RX;
@@ -608,7 +608,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
     src[d] = 0;
     const bool axis_off = (d < 2) ? wrapY : wrapX;
     if (FIRST || a.first || axis_off) continue;
-    const bool ghost = a.ghost && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
+    const bool ghost = !PLAIN && a.ghost && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
     if (ghost) {
       cnt[d] = (d == EDGE_N ? a.gh_up : a.gh_down).cnt[c];
       src[d] = d == EDGE_N ? 2u : 3u;
@@ -635,7 +635,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   // committed state (the old tau_m becomes tau_0)
   L.spins = (M)((const typename G::ST*)a.in.spins)[idx];
   expand_halo<G>((unsigned long long)((const typename G::HT*)a.in.halo)[idx], L.gN, L.gS, L.gW, L.gE);
-  L.ts = a.fresh_w ? a.t_c : a.in.ts[idx];  // fresh_w: every region starts afresh at t_c
+  L.ts = (!PLAIN && a.fresh_w) ? a.t_c : a.in.ts[idx];  // fresh_w: every region starts afresh at t_c
   L.R = a.in.R[idx];
   L.n = a.in.n[idx];
   L.dig = a.digest ? a.in.dig[idx] : 0ull;
@@ -751,7 +751,7 @@ __device__ __forceinline__ uint32_t neighbour_id(const KArgs& a, uint32_t gid, i
 // publish: selector word of the changed edges (the entry-by-entry diff was
 // taken while writing, hist_put), dirty bits of the neighbours across them,
 // and the tentative end-of-window state
-template <class G, bool OBS = false>
+template <class G, bool OBS = false, bool PLAIN = false>
 __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& changed, bool& overflow) {
   const int idx = L.idx;
   const int r = div_rx(a, idx), c = idx - r * a.RX;
@@ -775,7 +775,7 @@ __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& ch
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       if (!((chmask >> e) & 1u)) continue;
-      if (a.ghost && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
+      if (!PLAIN && a.ghost && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
       const int nr = e == EDGE_N ? wdec(r, a.RYl) : e == EDGE_S ? winc(r, a.RYl) : r;
       const int nc = e == EDGE_W ? wdec(c, a.RX) : e == EDGE_E ? winc(c, a.RX) : c;
       mark_dirty(a, nr * a.RX + nc, K + 1);
@@ -901,11 +901,11 @@ __device__ __forceinline__ unsigned hist_put(const KArgs& a, unsigned om, int e,
 
 // own event at tc, up to (not including) the refold; draws the next pair
 // DRAW = false: leave drawing the next pair to the caller (shared code)
-template <class G, bool LOG, class SG, bool DRAW = true>
+template <class G, bool LOG, class SG, bool DRAW = true, bool PLAIN = false>
 __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const ProdTable<G>& PT, int si,
                                         unsigned& n_out, bool& overflow) {
   constexpr int BX = G::BX, BY = G::BY;
-  const bool wrapX = a.RX == 1, wrapY = a.RYg == 1;
+  const bool wrapX = !PLAIN && a.RX == 1, wrapY = !PLAIN && a.RYg == 1;
   const int site = L.site;
   L.spins ^= G::ONE << site;
   const int sr = site / BX, sc = site - sr * BX;
@@ -971,10 +971,10 @@ __device__ __forceinline__ void ev_pre2(const KArgs& a, Lane<G>& L, SG& S, const
   L.R = budget(a, U);
 }
 
-template <class G>
+template <class G, bool PLAIN = false>
 __device__ __forceinline__ void refold(const KArgs& a, Lane<G>& L, const ProdTable<G>& PT) {
   Classes<G> C;
-  C.build(L.spins, L.gN, L.gS, L.gW, L.gE, a.RX == 1, a.RYg == 1);
+  C.build(L.spins, L.gN, L.gS, L.gW, L.gE, !PLAIN && a.RX == 1, !PLAIN && a.RYg == 1);
   L.site = fold_select<G>(C, PT, a.rate, L.V, L.lam);
   L.tc = cand_time(L.ts, L.R, L.lam);
 }
@@ -983,7 +983,9 @@ __device__ __forceinline__ void refold(const KArgs& a, Lane<G>& L, const ProdTab
 // n_work_dev (pipelined launch): the worklist length is read on the device;
 // the grid was sized for an upper bound, and the tile grows if the bound was
 // short.
-template <int BX, int BY, bool LOG, bool OBS, bool FIRST>
+// PLAIN: no ghost rows, no region spanning a lattice axis, no fresh-window
+// restart (the common case, chosen at launch): those checks compile out
+template <int BX, int BY, bool LOG, bool OBS, bool FIRST, bool PLAIN = false>
 __device__ __forceinline__ void region_body(const KArgs& a) {
   using G = Geo<BX, BY>;
   __shared__ unsigned q_next;
@@ -1027,7 +1029,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
     if (__popc(idle) >= REFILL || idle == 0xffffffffu) {
       if (!active) {
         if (pending) {
-          if (!LOG) lane_finish<G, OBS>(a, L, changed, overflow);
+          if (!LOG) lane_finish<G, OBS, PLAIN>(a, L, changed, overflow);
           n_ev += L.n_ev;
           n_bev = max(n_bev, L.bev);
           pending = false;
@@ -1037,7 +1039,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
           if (item < s_tile_n) {
             const int idx = a.wl_in ? (int)a.wl_in[s_tile_begin + item] : s_tile_begin + item;
             ISR_ASSERT(idx >= 0 && idx < a.RX * a.RYl);
-            lane_load<G, LOG, SG, false, OBS, FIRST>(a, L, idx, S, PT, threadIdx.x);
+            lane_load<G, LOG, SG, false, OBS, FIRST, PLAIN>(a, L, idx, S, PT, threadIdx.x);
             fresh = true;
             n_in += (L.hm[0] & 0xFFu) + (L.hm[1] & 0xFFu) + (L.hm[2] & 0xFFu) + (L.hm[3] & 0xFFu);
             n_cmp += ((L.om[0] >> 8) & 0xFFu) + ((L.om[1] >> 8) & 0xFFu) + ((L.om[2] >> 8) & 0xFFu) +
@@ -1067,7 +1069,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
           bp_pre2<G>(a, L, S, threadIdx.x, d, tb);
         } else {
           if (OBS && !LOG) obs_advance<G>(L, L.tc);
-          ev_pre2<G, LOG, SG, false>(a, L, S, PT, threadIdx.x, n_out, overflow);
+          ev_pre2<G, LOG, SG, false, PLAIN>(a, L, S, PT, threadIdx.x, n_out, overflow);
           ev = true;
         }
       }
@@ -1081,9 +1083,9 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
           double U;
           draw_pair(a.seed, L.gid, L.n, U, L.V, a.gen);
           const double Eu = budget(a, U);
-          if (ev || (fresh && a.fresh_w)) L.R = Eu;
+          if (ev || (fresh && !PLAIN && a.fresh_w)) L.R = Eu;
         }
-        refold<G>(a, L, PT);  // shared by both kinds of step
+        refold<G, PLAIN>(a, L, PT);  // shared by both kinds of step
         // finished now: the candidate lies beyond the window and no break point is left (every incoming
         // entry lies inside the window, so one left would come first) -- the decision the next round's
         // next_bp2 would take, without spending that round
@@ -1131,16 +1133,16 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
 #else
 #define ISR_K1_BOUNDS __launch_bounds__(NT)
 #endif
-template <int BX, int BY, bool LOG, bool OBS = false, bool FIRST = false>
+template <int BX, int BY, bool LOG, bool OBS = false, bool FIRST = false, bool PLAIN = false>
 __global__ void ISR_K1_BOUNDS region_kernel(const KArgs a) {
-  region_body<BX, BY, LOG, OBS, FIRST>(a);
+  region_body<BX, BY, LOG, OBS, FIRST, PLAIN>(a);
 }
 #ifndef ISR_MB_MINB
 #define ISR_MB_MINB 5
 #endif
-template <int BX, int BY, bool LOG, bool OBS = false, bool FIRST = false>
+template <int BX, int BY, bool LOG, bool OBS = false, bool FIRST = false, bool PLAIN = false>
 __global__ void __launch_bounds__(NT, ISR_MB_MINB) region_kernel_mb(const KArgs a) {
-  region_body<BX, BY, LOG, OBS, FIRST>(a);
+  region_body<BX, BY, LOG, OBS, FIRST, PLAIN>(a);
 }
 // the window's first iteration (≤ 32-site regions): no staging, so shared
 // memory no longer caps the resident blocks; ISR_FIRST_MINB asks ptxas for
@@ -1153,9 +1155,9 @@ __global__ void __launch_bounds__(NT, ISR_MB_MINB) region_kernel_mb(const KArgs 
 #else
 #define ISR_FIRST_BOUNDS __launch_bounds__(NT)
 #endif
-template <int BX, int BY, bool OBS = false>
+template <int BX, int BY, bool OBS = false, bool PLAIN = false>
 __global__ void ISR_FIRST_BOUNDS region_kernel_first(const KArgs a) {
-  region_body<BX, BY, false, OBS, true>(a);
+  region_body<BX, BY, false, OBS, true, PLAIN>(a);
 }
 
 // ---------------------------------------------------------------------------

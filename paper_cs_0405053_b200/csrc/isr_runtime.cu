@@ -59,6 +59,11 @@ struct ShapeOps {
   void (*snap)(StateView, int n, int RX, int RYg, unsigned long long* out, cudaStream_t);  // M, B of a state
 };
 
+#ifndef ISR_PLAIN
+#define ISR_PLAIN 1  // 0: every launch takes the general K1 instantiation
+#endif
+constexpr bool plain_k1 = ISR_PLAIN != 0;
+
 template <int BX, int BY>
 ShapeOps make_ops() {
   using G = isr::Geo<BX, BY>;
@@ -84,6 +89,15 @@ ShapeOps make_ops() {
       } else {
         if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, true><<<grid, kThreads, 0, s>>>(a);
         else isr::region_kernel<BX, BY, false, true><<<grid, kThreads, 0, s>>>(a);
+      }
+    } else if (plain_k1 && !a.ghost && !a.fresh_w && a.RX > 1 && a.RYg > 1) {
+      // the common case: ghost-row, axis-wrap and fresh-window code compiled out
+      if (a.first) {
+        if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, true, true><<<grid, kThreads, 0, s>>>(a);
+        else isr::region_kernel_first<BX, BY, false, true><<<grid, kThreads, 0, s>>>(a);
+      } else {
+        if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, false, true><<<grid, kThreads, 0, s>>>(a);
+        else isr::region_kernel<BX, BY, false, false, false, true><<<grid, kThreads, 0, s>>>(a);
       }
     } else if (a.first) {
       if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, true><<<grid, kThreads, 0, s>>>(a);
