@@ -132,6 +132,7 @@ struct KArgs {
   unsigned rx_M;           // idx / RX == (idx * rx_M) >> rx_k for idx < 2^31 (host-computed)
   int rx_k;
   int refill;              // idle lanes per warp that trigger a batched refill
+  int plain;               // launch the PLAIN instantiation where it applies (host dispatch only)
   uint32_t* wl_out;        // worklist of the next iteration
   unsigned* wl_out_count;
   uint32_t* dirty;         // dirty-region bitmaps [2][dwords], parity of the iteration they are for

@@ -59,11 +59,6 @@ struct ShapeOps {
   void (*snap)(StateView, int n, int RX, int RYg, unsigned long long* out, cudaStream_t);  // M, B of a state
 };
 
-#ifndef ISR_PLAIN
-#define ISR_PLAIN 1  // 0: every launch takes the general K1 instantiation
-#endif
-constexpr bool plain_k1 = ISR_PLAIN != 0;
-
 template <int BX, int BY>
 ShapeOps make_ops() {
   using G = isr::Geo<BX, BY>;
@@ -90,7 +85,7 @@ ShapeOps make_ops() {
         if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, true><<<grid, kThreads, 0, s>>>(a);
         else isr::region_kernel<BX, BY, false, true><<<grid, kThreads, 0, s>>>(a);
       }
-    } else if (plain_k1 && !a.ghost && !a.fresh_w && a.RX > 1 && a.RYg > 1) {
+    } else if (a.plain && !a.ghost && !a.fresh_w && a.RX > 1 && a.RYg > 1) {
       // the common case: ghost-row, axis-wrap and fresh-window code compiled out
       if (a.first) {
         if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, true, true><<<grid, kThreads, 0, s>>>(a);
@@ -812,6 +807,7 @@ struct ising_sr_ctx {
   WinDev* d_win = nullptr;
   WinDev* h_win = nullptr;     // pinned
   unsigned delay_ns = 0;  // test knob (env ISING_SR_K1_DELAY_NS): K1 publishes late
+  bool plain = true;           // K1's PLAIN instantiation where it applies (env ISING_SR_PLAIN=0: never)
   int refill = 28;  // K1 batched-refill threshold (env ISING_SR_REFILL; 28 measured best after the shared fresh-load step)
   ising_sr_stats stats;
 };
@@ -984,6 +980,7 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   a.pmeta = c->pmeta;
   a.PC = c->PC;
   a.refill = c->refill;
+  a.plain = c->plain ? 1 : 0;
   a.delay_ns = c->delay_ns;
   {
     // magic division by RX: k = 31 + ceil(log2 RX), M = ceil(2^k / RX) < 2^32;
@@ -1624,6 +1621,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   c->dwords = ((c->nreg + 31) / 32 + 7) / 8 * 8;  // a multiple of 8 words: 32-byte aligned bitmaps (compact_kernel)
   std::memset(&c->stats, 0, sizeof c->stats);
   if (const char* e = std::getenv("ISING_SR_PIPELINE")) c->pipeline = std::atoi(e) != 0;
+  if (const char* e = std::getenv("ISING_SR_PLAIN")) c->plain = std::atoi(e) != 0;
   if (const char* e = std::getenv("ISING_SR_REFILL")) c->refill = std::max(1, std::min(32, std::atoi(e)));
   if (const char* e = std::getenv("ISING_SR_K1_DELAY_NS")) c->delay_ns = (unsigned)std::max(0, std::atoi(e));
   if (const char* e = std::getenv("ISING_SR_GRAPH")) c->graph = std::atoi(e) != 0;

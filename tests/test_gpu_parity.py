@@ -188,11 +188,13 @@ def test_c5_geometry_sample_bit_exact():
 # ---------------------------------------------------------------------------
 # every schedule of K1 (lane-persistent with the pipelined host loop:
 # default; one iteration per host sync: ISING_SR_PIPELINE=0; the warp form of
-# big regions: ISING_SR_BIG=0; big regions without resume: ISING_SR_RESUME=0)
+# big regions: ISING_SR_BIG=0; big regions without resume: ISING_SR_RESUME=0;
+# the general K1 instantiation where the PLAIN one applies: ISING_SR_PLAIN=0)
 # and an extreme refill threshold give the oracle's bits
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("env", [
     {},
+    {"ISING_SR_PLAIN": "0"},
     {"ISING_SR_PIPELINE": "0"},
     {"ISING_SR_PIPELINE": "0", "ISING_SR_BIG": "0"},
     {"ISING_SR_REFILL": "1"},
