@@ -133,6 +133,11 @@ struct KArgs {
   int rx_k;
   int refill;              // idle lanes per warp that trigger a batched refill
   int plain;               // launch the PLAIN instantiation where it applies (host dispatch only)
+  // PLAIN iterations after the first: per worklist item {region, incoming
+  // counts (byte d), own latest counts (byte e), incoming slots (2 bits per d)
+  // | own latest slots << 8 | word to overwrite << 12}, written by
+  // describe_kernel from the selector words after the compaction
+  const uint4* desc;
   uint32_t* wl_out;        // worklist of the next iteration
   unsigned* wl_out_count;
   uint32_t* dirty;         // dirty-region bitmaps [2][dwords], parity of the iteration they are for
@@ -586,9 +591,10 @@ __device__ __forceinline__ void obs_advance(Lane<G>& L, double t) {
 // incoming histories to read or stage.  The own selector pair is still read:
 // the new word must flip the slot bit of every changed edge relative to the
 // other word (pack_kernel's change test for the strip exchange).
-template <class G, bool LOG, class SG, bool FULL = true, bool OBS = false, bool FIRST = false, bool PLAIN = false>
+template <class G, bool LOG, class SG, bool FULL = true, bool OBS = false, bool FIRST = false, bool PLAIN = false,
+          bool DESC = false>
 __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, SG& S, const ProdTable<G>& PT,
-                                          int si) {
+                                          int si, uint4 dsc = make_uint4(0u, 0u, 0u, 0u)) {
   using M = typename G::M;
   const bool wrapX = !PLAIN && a.RX == 1, wrapY = !PLAIN && a.RYg == 1;
   const unsigned K = stamp_of(a), K0 = a.it_K0;
@@ -599,14 +605,19 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   L.obase = (unsigned)(((long long)r * a.K) * a.RX + c);
   L.n_ev = 0;
   L.bev = 0;
-  // selector words first: they gate the history loads
+  // selector words first: they gate the history loads (DESC: resolved by describe_kernel)
   ulonglong2 wp_own = make_ulonglong2(0ull, 0ull);
-  if (!LOG) wp_own = reinterpret_cast<const ulonglong2*>(a.sel)[idx];
+  if (!LOG && !DESC) wp_own = reinterpret_cast<const ulonglong2*>(a.sel)[idx];
   unsigned cnt[4], src[4];
 #pragma unroll
   for (int d = 0; d < 4; ++d) {
     cnt[d] = 0;
     src[d] = 0;
+    if (DESC) {
+      cnt[d] = (dsc.y >> (8 * d)) & 0xFFu;
+      src[d] = (dsc.w >> (2 * d)) & 3u;
+      continue;
+    }
     const bool axis_off = (d < 2) ? wrapY : wrapX;
     if (FIRST || a.first || axis_off) continue;
     const bool ghost = !PLAIN && a.ghost && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
@@ -627,7 +638,13 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
   // own latest histories: slot and count per edge
   unsigned long long vown = 0ull;
   L.whalf = 0;
-  if (!LOG) {
+  if (DESC) {  // the same fields, from the descriptor
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      vown |= ((unsigned long long)((dsc.w >> (8 + e)) & 1u) << e) |
+              ((unsigned long long)((dsc.z >> (8 * e)) & 0xFFu) << (4 + CNT_BITS * e));
+    L.whalf = (int)((dsc.w >> 12) & 1u);
+  } else if (!LOG) {
     const int li = latest_index(wp_own, K);
     const unsigned long long v = li ? wp_own.y : wp_own.x;
     vown = word_valid(v, K0) ? v : (v & 0xFull);  // outside the window: slots only, counts 0
@@ -1038,9 +1055,12 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
         if (!exhausted) {
           if (item < 0) item = (int)atomicAdd(&q_next, 1u);
           if (item < s_tile_n) {
-            const int idx = a.wl_in ? (int)a.wl_in[s_tile_begin + item] : s_tile_begin + item;
+            constexpr bool DESC = PLAIN && !FIRST && !LOG && !OBS;  // (the host passes a.desc for these)
+            uint4 dsc = make_uint4(0u, 0u, 0u, 0u);
+            if (DESC) dsc = __ldcs(a.desc + s_tile_begin + item);
+            const int idx = DESC ? (int)dsc.x : a.wl_in ? (int)a.wl_in[s_tile_begin + item] : s_tile_begin + item;
             ISR_ASSERT(idx >= 0 && idx < a.RX * a.RYl);
-            lane_load<G, LOG, SG, false, OBS, FIRST, PLAIN>(a, L, idx, S, PT, threadIdx.x);
+            lane_load<G, LOG, SG, false, OBS, FIRST, PLAIN, DESC>(a, L, idx, S, PT, threadIdx.x, dsc);
             fresh = true;
             n_in += (L.hm[0] & 0xFFu) + (L.hm[1] & 0xFFu) + (L.hm[2] & 0xFFu) + (L.hm[3] & 0xFFu);
             n_cmp += ((L.om[0] >> 8) & 0xFFu) + ((L.om[1] >> 8) & 0xFFu) + ((L.om[2] >> 8) & 0xFFu) +
@@ -1267,6 +1287,48 @@ __global__ void __launch_bounds__(kCompactThreads) compact_kernel(uint32_t* bm, 
       const int r = (w0 + q) * 32 + b;
       if (r < n) wl[o++] = (uint32_t)r;
     }
+  }
+}
+
+// The worklist's descriptors for a PLAIN iteration with stamp K (no ghost
+// rows, no wrapped axis): each item's incoming (slot, count) pairs from the
+// neighbours' latest selector words with stamp < K and its own latest word --
+// what lane_load would read itself, resolved here with whole warps so that a
+// K1 refill starts with one coalesced 16-byte read.
+__global__ void __launch_bounds__(256) describe_kernel(const KArgs a, unsigned K, const uint32_t* wl,
+                                                       const unsigned* count, uint4* desc) {
+  const unsigned n = __ldcg(count), K0 = a.it_K0;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int idx = (int)wl[i];
+    const int r = div_rx(a, idx), c = idx - r * a.RX;
+    const ulonglong2* sel = reinterpret_cast<const ulonglong2*>(a.sel);
+    const ulonglong2 wp_own = __ldcg(sel + idx);
+    ulonglong2 wn[4];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const int nr = d == EDGE_N ? wdec(r, a.RYl) : d == EDGE_S ? winc(r, a.RYl) : r;
+      const int nc = d == EDGE_W ? wdec(c, a.RX) : d == EDGE_E ? winc(c, a.RX) : c;
+      wn[d] = __ldcg(sel + ((long long)nr * a.RX + nc));
+    }
+    uint32_t cnt4 = 0, pc4 = 0, bits = 0;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const unsigned long long v = latest_word(wn[d], K);
+      if (word_valid(v, K0)) {
+        cnt4 |= word_count(v, d ^ 1) << (8 * d);
+        bits |= (unsigned)word_slot(v, d ^ 1) << (2 * d);
+      }
+    }
+    const int li = latest_index(wp_own, K);
+    const unsigned long long vv = li ? wp_own.y : wp_own.x;
+    const unsigned long long vown = word_valid(vv, K0) ? vv : (vv & 0xFull);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      pc4 |= word_count(vown, e) << (8 * e);
+      bits |= (unsigned)word_slot(vown, e) << (8 + e);
+    }
+    bits |= (unsigned)(li ^ 1) << 12;
+    desc[i] = make_uint4((uint32_t)idx, cnt4, pc4, bits);
   }
 }
 

@@ -85,7 +85,7 @@ ShapeOps make_ops() {
         if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, true><<<grid, kThreads, 0, s>>>(a);
         else isr::region_kernel<BX, BY, false, true><<<grid, kThreads, 0, s>>>(a);
       }
-    } else if (a.plain && !a.ghost && !a.fresh_w && a.RX > 1 && a.RYg > 1) {
+    } else if (a.plain && !a.ghost && !a.fresh_w && a.RX > 1 && a.RYg > 1 && (a.first || a.desc)) {
       // the common case: ghost-row, axis-wrap and fresh-window code compiled out
       if (a.first) {
         if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, true, true><<<grid, kThreads, 0, s>>>(a);
@@ -808,6 +808,7 @@ struct ising_sr_ctx {
   WinDev* h_win = nullptr;     // pinned
   unsigned delay_ns = 0;  // test knob (env ISING_SR_K1_DELAY_NS): K1 publishes late
   bool plain = true;           // K1's PLAIN instantiation where it applies (env ISING_SR_PLAIN=0: never)
+  uint4* desc = nullptr;       // worklist descriptors of PLAIN iterations (describe_kernel)
   int refill = 28;  // K1 batched-refill threshold (env ISING_SR_REFILL; 28 measured best after the shared fresh-load step)
   ising_sr_stats stats;
 };
@@ -1011,6 +1012,22 @@ int compact_grid(const ising_sr_ctx* c) {
   return std::max(1, (c->dwords + per - 1) / per);
 }
 
+// iterations after the first run K1's PLAIN instantiation from worklist
+// descriptors when the strip has no ghost rows, no region spans an axis and
+// windows do not restart afresh (the general kernel reads the selectors itself)
+bool plain_desc(const ising_sr_ctx* c) {
+  return c->plain && c->desc && !c->ghost && !(c->cfg.flags & (ISING_SR_FLAG_FRESH_WINDOW | ISING_SR_FLAG_JACOBI_ALL)) &&
+         c->RX > 1 && c->RYg > 1 && !(c->cfg.flags & ISING_SR_FLAG_OBSERVABLES);
+}
+
+// descriptors of the worklist iteration K will read (its length read on the device)
+void describe(ising_sr_ctx* c, unsigned K, const unsigned* count) {
+  KArgs a = base_args(c, K, false);
+  const int grid = std::max(1, std::min((c->nreg + 255) / 256, 148 * 16));
+  isr::describe_kernel<<<grid, 256, 0, c->stream>>>(a, K, c->wl[K & 1], count, c->desc);
+  ++c->launches;
+}
+
 ising_sr_status compact_worklist(ising_sr_ctx* c) {
   const unsigned K = c->Kglob;
   isr::compact_kernel<<<compact_grid(c), isr::kCompactThreads, 0, c->stream>>>(c->dirty + (size_t)((K + 1) & 1) * c->dwords,
@@ -1018,6 +1035,10 @@ ising_sr_status compact_worklist(ising_sr_ctx* c) {
                                                                      c->d_wlc + ((K + 1) & 1));
   ++c->launches;
   CK(c, cudaGetLastError());
+  if (plain_desc(c)) {
+    describe(c, K + 1, c->d_wlc + ((K + 1) & 1));
+    CK(c, cudaGetLastError());
+  }
   return ISING_SR_OK;
 }
 
@@ -1033,6 +1054,7 @@ ising_sr_status launch_iteration(ising_sr_ctx* c) {
   CK(c, cudaMemsetAsync(c->d_wlc + ((K + 1) & 1), 0, sizeof(unsigned), c->stream));
   KArgs a = base_args(c, K, first);
   a.wl_in = all ? nullptr : c->wl[K & 1];
+  a.desc = (!all && plain_desc(c)) ? c->desc : nullptr;
   a.n_work = nw;
   a.tile = tile_for(nw);
   a.wl_out = c->wl[(K + 1) & 1];
@@ -1220,6 +1242,7 @@ ising_sr_status enqueue_pipelined(ising_sr_ctx* c, int bound) {
   a.flags = sl->flags;
   a.stats = sl->stats;
   a.wl_in = first ? nullptr : c->wl[K & 1];
+  a.desc = (!first && plain_desc(c)) ? c->desc : nullptr;
   a.n_work = nb;
   a.n_work_dev = first ? nullptr : &prev->wl_next;
   a.tile = tile_for(std::max(nb, 1));
@@ -1247,6 +1270,10 @@ ising_sr_status enqueue_pipelined(ising_sr_ctx* c, int bound) {
                                                                        &sl->wl_next);
   ++c->launches;
   CK(c, cudaGetLastError());
+  if (plain_desc(c)) {  // descriptors of iteration K + 1's worklist
+    describe(c, K + 1, &sl->wl_next);
+    CK(c, cudaGetLastError());
+  }
   CK(c, cudaMemcpyAsync(c->h_slot + j, sl, sizeof(IterSlot), cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaEventRecord(c->pev[j], c->stream));
   return ISING_SR_OK;
@@ -1525,6 +1552,7 @@ void ising_sr_destroy(ising_sr_ctx* c) {
   dfree(c, c->d_stats);
   dfree(c, c->ev_t);
   dfree(c, c->ev_s);
+  dfree(c, c->desc);
   dfree(c, c->log_dm);
   dfree(c, c->mm_ts);
   dfree(c, c->mm_dm);
@@ -1665,6 +1693,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
       dmalloc(c, &c->d_win, 1) != cudaSuccess || cudaMallocHost((void**)&c->h_win, sizeof(WinDev)) != cudaSuccess ||
       cudaMallocHost((void**)&c->h_slot, 2 * sizeof(IterSlot)) != cudaSuccess)
     return bail(ISING_SR_E_OOM);
+  if (!ops->warp && dmalloc(c, &c->desc, n) != cudaSuccess) return bail(ISING_SR_E_OOM);
   if (cudaMemsetAsync(c->sel, 0, n * 8 * (size_t)ops->sel_words, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->dirty, 0, 2 * (size_t)c->dwords * 4, c->stream) != cudaSuccess)
     return bail(ISING_SR_E_CUDA);
