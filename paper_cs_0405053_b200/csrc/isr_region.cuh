@@ -820,10 +820,14 @@ __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& ch
 // different kinds of step share those instructions.  An incoming head whose
 // history is exhausted reads as +inf.
 // ---------------------------------------------------------------------------
+// minimum of two times (never NaN): a compare and a select, where fmin also
+// handles NaN operands (~8 instructions for doubles)
+__device__ __forceinline__ double tmin(double x, double y) { return x < y ? x : y; }
+
 template <class G>
 __device__ __forceinline__ int next_bp2(const KArgs& a, const Lane<G>& L, double& tb) {
-  const double m01 = fmin(L.ht[0], L.ht[1]), m23 = fmin(L.ht[2], L.ht[3]);
-  tb = fmin(m01, m23);
+  const double m01 = tmin(L.ht[0], L.ht[1]), m23 = tmin(L.ht[2], L.ht[3]);
+  tb = tmin(m01, m23);
   if (!(tb <= L.tc) || tb == dinf()) return -1;
   const int neq = (L.ht[0] == tb) + (L.ht[1] == tb) + (L.ht[2] == tb) + (L.ht[3] == tb);
   const int dstar = L.ht[0] == tb ? 0 : L.ht[1] == tb ? 1 : L.ht[2] == tb ? 2 : 3;
@@ -1110,7 +1114,8 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
         // finished now: the candidate lies beyond the window and no break point is left (every incoming
         // entry lies inside the window, so one left would come first) -- the decision the next round's
         // next_bp2 would take, without spending that round
-        if (!(L.tc < a.t_w) && fmin(fmin(L.ht[0], L.ht[1]), fmin(L.ht[2], L.ht[3])) == dinf()) active = false;
+        if (!(L.tc < a.t_w) && L.ht[0] == dinf() && L.ht[1] == dinf() && L.ht[2] == dinf() && L.ht[3] == dinf())
+          active = false;
       }
       fresh = false;
     }
