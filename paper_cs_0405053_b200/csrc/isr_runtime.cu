@@ -1020,10 +1020,12 @@ bool plain_desc(const ising_sr_ctx* c) {
          c->RX > 1 && c->RYg > 1 && !(c->cfg.flags & ISING_SR_FLAG_OBSERVABLES);
 }
 
-// descriptors of the worklist iteration K will read (its length read on the device)
-void describe(ising_sr_ctx* c, unsigned K, const unsigned* count) {
+// descriptors of the worklist iteration K will read (its length read on the
+// device; `bound` sizes the grid -- worklists shrink as the relaxation
+// converges, and a longer one is covered by the grid-stride loop)
+void describe(ising_sr_ctx* c, unsigned K, const unsigned* count, int bound) {
   KArgs a = base_args(c, K, false);
-  const int grid = std::max(1, std::min((c->nreg + 255) / 256, 148 * 16));
+  const int grid = std::max(1, std::min((bound + 255) / 256, 148 * 16));
   isr::describe_kernel<<<grid, 256, 0, c->stream>>>(a, K, c->wl[K & 1], count, c->desc);
   ++c->launches;
 }
@@ -1036,7 +1038,7 @@ ising_sr_status compact_worklist(ising_sr_ctx* c) {
   ++c->launches;
   CK(c, cudaGetLastError());
   if (plain_desc(c)) {
-    describe(c, K + 1, c->d_wlc + ((K + 1) & 1));
+    describe(c, K + 1, c->d_wlc + ((K + 1) & 1), std::max(c->n_work, 1));
     CK(c, cudaGetLastError());
   }
   return ISING_SR_OK;
@@ -1271,7 +1273,7 @@ ising_sr_status enqueue_pipelined(ising_sr_ctx* c, int bound) {
   ++c->launches;
   CK(c, cudaGetLastError());
   if (plain_desc(c)) {  // descriptors of iteration K + 1's worklist
-    describe(c, K + 1, &sl->wl_next);
+    describe(c, K + 1, &sl->wl_next, nb);
     CK(c, cudaGetLastError());
   }
   CK(c, cudaMemcpyAsync(c->h_slot + j, sl, sizeof(IterSlot), cudaMemcpyDeviceToHost, c->stream));
