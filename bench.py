@@ -248,6 +248,12 @@ def run_ising(args):
     if args.jacobi_all:
         from paper_cs_0405053_b200 import FLAG_JACOBI_ALL
         flags |= FLAG_JACOBI_ALL
+    if args.halo_loopback:  # one strip through the strip exchange to itself (a one-rank communicator)
+        if world != 1:
+            raise SystemExit("--halo-loopback is a one-GPU measurement of the strip exchange")
+        from paper_cs_0405053_b200 import FLAG_HALO_LOOPBACK, nccl_unique_id
+        flags |= FLAG_HALO_LOOPBACK
+        nccl_id = nccl_unique_id()
     # the library's stream: every kernel of the path runs on it, and the
     # timing events are recorded on it
     stream = torch.cuda.Stream(device=local)
@@ -383,7 +389,9 @@ def run_ising(args):
                    "schedule": "jacobi_all" if args.jacobi_all else "worklist",
                    "event_log": "compacted at every commit (FLAG_LOG_EVENTS), in the timed region",
                    "digests": bool(args.digest),
-                   "parallelism": f"strips{world}"},
+                   "parallelism": f"strips{world}",
+                   "exchange": (None if world == 1 and not args.halo_loopback else
+                                os.environ.get("ISING_SR_EXCHANGE", "peer") + (" (loopback)" if args.halo_loopback else ""))},
         "events": tot_ev,
         "iterations_per_window": {"mean": float(np.mean(gs)), "p50": float(np.percentile(gs, 50)),
                                   "p99": float(np.percentile(gs, 99)), "max": int(max(gs)), "min": int(min(gs)),
@@ -503,6 +511,8 @@ def main():
     ap.add_argument("--digest", action="store_true", help="also maintain the per-region event digests")
     ap.add_argument("--window", default="config", choices=["config", "tmax"],
                     help="W of the config, or the paper's T_max = ln N/(lambda |dG|) (P:502-515)")
+    ap.add_argument("--halo-loopback", action="store_true",
+                    help="N=1: run the strip exchange to itself (ISING_SR_EXCHANGE=peer|sendrecv picks the transport)")
     ap.add_argument("--jacobi-all", action="store_true",
                     help="paper-faithful schedule: every region in every iteration (same bits and g)")
     args = ap.parse_args()

@@ -9,7 +9,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libising_sr.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("isr_runtime.cu", "isr_checkerboard.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("isr_region.cuh", "isr_warp.cuh", "isr_big.cuh", "isr_device.cuh", "isr_nccl.h")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("isr_region.cuh", "isr_warp.cuh", "isr_big.cuh", "isr_device.cuh", "isr_nccl.h",
+                                                  "isr_peer.cuh")] + [
     os.path.join(os.path.dirname(PKG), "include", "ising_sr.h")]
 
 NVCC_FLAGS = [
@@ -21,6 +22,18 @@ NVCC_FLAGS = [
     "-Xptxas", "-v",
     "-shared", "-Xcompiler", "-fPIC", "-ldl",
 ]
+
+
+def nccl_include() -> list:
+    """-I for NCCL >= 2.28's headers (nccl.h + the device API, nccl_device.h):
+    the torch-bundled nvidia-nccl wheel.  Without them the library builds
+    without the peer-memory exchange (isr_peer.cuh) and keeps send/recv."""
+    import sysconfig
+    for root in (sysconfig.get_paths().get("purelib"), "/opt/prime-rl/.venv/lib/python3.12/site-packages"):
+        inc = os.path.join(root or "", "nvidia", "nccl", "include")
+        if os.path.exists(os.path.join(inc, "nccl_device.h")):
+            return ["-I", inc]
+    return []
 
 
 def nvcc() -> str:
@@ -41,7 +54,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc()] + NVCC_FLAGS + ["-o", tmp] + SOURCES
+    cmd = [nvcc()] + NVCC_FLAGS + nccl_include() + ["-o", tmp] + SOURCES
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

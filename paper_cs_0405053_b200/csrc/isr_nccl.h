@@ -42,6 +42,14 @@ struct Api {
   Result (*Recv)(void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
   Result (*AllReduce)(const void*, void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(Result) = nullptr;
+  // NCCL >= 2.28 symmetric memory and device API (isr_peer.cuh); null if absent
+  void* MemAlloc = nullptr;             // ncclMemAlloc(void**, size_t)
+  void* MemFree = nullptr;              // ncclMemFree(void*)
+  void* CommWindowRegister = nullptr;   // ncclCommWindowRegister(comm, buf, size, ncclWindow_t*, flags)
+  void* CommWindowDeregister = nullptr; // ncclCommWindowDeregister(comm, ncclWindow_t)
+  void* DevCommCreate = nullptr;        // ncclDevCommCreate(comm, const ncclDevCommRequirements*, ncclDevComm*)
+  void* DevCommDestroy = nullptr;       // ncclDevCommDestroy(comm, const ncclDevComm*)
+  void* TeamLsa = nullptr;              // ncclTeam ncclTeamLsa(comm)
   bool ok = false;
 };
 
@@ -77,6 +85,13 @@ inline const Api& api() {
     a.Recv = (Result(*)(void*, size_t, int, int, Comm, cudaStream_t))sym("ncclRecv");
     a.AllReduce = (Result(*)(const void*, void*, size_t, int, int, Comm, cudaStream_t))sym("ncclAllReduce");
     a.GetErrorString = (const char* (*)(Result))sym("ncclGetErrorString");
+    a.MemAlloc = sym("ncclMemAlloc");
+    a.MemFree = sym("ncclMemFree");
+    a.CommWindowRegister = sym("ncclCommWindowRegister");
+    a.CommWindowDeregister = sym("ncclCommWindowDeregister");
+    a.DevCommCreate = sym("ncclDevCommCreate");
+    a.DevCommDestroy = sym("ncclDevCommDestroy");
+    a.TeamLsa = sym("ncclTeamLsa");
     a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.GroupStart && a.GroupEnd && a.Send && a.Recv &&
            a.AllReduce;
     return a;

@@ -1192,14 +1192,11 @@ __global__ void ISR_FIRST_BOUNDS region_kernel_first(const KArgs a) {
 // with the stamp of their last change (the neighbour marks its adjacent
 // regions dirty when the stamp equals the current iteration).
 // ---------------------------------------------------------------------------
-__global__ void pack_kernel(const KArgs a, GhostView send_up, GhostView send_down) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 2 * a.RX) return;
-  const bool up = i < a.RX;
-  const int c = up ? i : i - a.RX;
+// the latest history of column c's strip-edge region (up: first row, north
+// edge; else: last row, south edge) into ghost-row view g at column c
+__device__ __forceinline__ void pack_col(const KArgs& a, bool up, int c, const GhostView& g) {
   const int r = up ? 0 : a.RYl - 1;
   const int e = up ? EDGE_N : EDGE_S;
-  const GhostView& g = up ? send_up : send_down;
   const ulonglong2 wp = reinterpret_cast<const ulonglong2*>(a.sel)[(long long)r * a.RX + c];
   // latest as of the end of this iteration
   const unsigned K = stamp_of(a);
@@ -1220,6 +1217,13 @@ __global__ void pack_kernel(const KArgs a, GhostView send_up, GhostView send_dow
   const unsigned long long other = latest_index(wp, K + 1) ? wp.x : wp.y;
   const bool ch_now = (unsigned)(v >> 32) == K && (((v ^ other) >> e) & 1ull);
   g.stamp[c] = ch_now ? K : 0u;
+}
+
+__global__ void pack_kernel(const KArgs a, GhostView send_up, GhostView send_down) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 2 * a.RX) return;
+  const bool up = i < a.RX;
+  pack_col(a, up, up ? i : i - a.RX, up ? send_up : send_down);
 }
 
 // after the exchange: regions next to a ghost row that changed in this

@@ -24,6 +24,7 @@
 #include "isr_warp.cuh"
 #include "isr_big.cuh"
 #include "isr_nccl.h"
+#include "isr_peer.cuh"
 
 namespace {
 
@@ -748,6 +749,21 @@ struct ising_sr_ctx {
   bool ghost = false;
   size_t grow = 0;                        // bytes of one ghost row (4 chunks, contiguous)
   isr_nccl::Comm nccl = nullptr;          // the library's communicator (cfg.nccl_id)
+  // peer-memory exchange (isr_peer.cuh): ghost rows + flag inbox in an NCCL
+  // symmetric window, one fused kernel per iteration (env ISING_SR_EXCHANGE=
+  // sendrecv: the ncclSend/ncclRecv + ncclAllReduce path instead)
+  bool peer = false;
+  int peer_blocks = 0;
+  void* pbuf = nullptr;                   // ncclMemAlloc'ed window memory
+  size_t pbytes = 0;
+  void* pwin = nullptr;                   // ncclWindow_t
+  unsigned long long* d_peer = nullptr;   // [world + 1] window bases (LSA pointers; [world] = local)
+  unsigned long long h_peer[isr::kPeerMaxWorld + 1] = {};
+  isr::PeerArgs pargs{};
+#if ISR_HAVE_NCCL_DEVICE
+  ncclDevComm dcomm{};
+  bool dcomm_ok = false;
+#endif
   // scratch event log of K1 (FLAG_LOG_EVENTS) and the commit's replay list
   double* ev_t = nullptr;
   uint16_t* ev_s = nullptr;
@@ -944,6 +960,10 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   a.sel = c->sel;
   a.gh_up = c->grecv[0];
   a.gh_down = c->grecv[1];
+  if (c->peer) {  // the rows the neighbours stored at the previous iteration (stamp K - 1)
+    a.gh_up = isr::peer_row(c->pargs, c->pargs.mine, (int)((K - 1u) & 1u), 0);
+    a.gh_down = isr::peer_row(c->pargs, c->pargs.mine, (int)((K - 1u) & 1u), 1);
+  }
   a.RX = c->RX;
   a.RYl = c->RYl;
   a.RYg = c->RYg;
@@ -1030,6 +1050,8 @@ void describe(ising_sr_ctx* c, unsigned K, const unsigned* count, int bound) {
   ++c->launches;
 }
 
+ising_sr_status peer_exchange(ising_sr_ctx* c, const KArgs& a, int* flags);  // (below)
+
 ising_sr_status compact_worklist(ising_sr_ctx* c) {
   const unsigned K = c->Kglob;
   isr::compact_kernel<<<compact_grid(c), isr::kCompactThreads, 0, c->stream>>>(c->dirty + (size_t)((K + 1) & 1) * c->dwords,
@@ -1068,7 +1090,9 @@ ising_sr_status launch_iteration(ising_sr_ctx* c) {
     CK(c, cudaGetLastError());
   }
   CK(c, cudaEventRecord(c->kev1, c->stream));
-  if (c->ghost) {
+  if (c->ghost && c->peer) {
+    return peer_exchange(c, a, c->d_flags);
+  } else if (c->ghost) {
     c->ops->pack(a, c->gsend[0], c->gsend[1], c->RX, c->stream);
     ++c->launches;
     CK(c, cudaGetLastError());
@@ -1080,6 +1104,7 @@ ising_sr_status launch_iteration(ising_sr_ctx* c) {
 
 ising_sr_status mark_ghosts(ising_sr_ctx* c) {
   if (!c->ghost) return ISING_SR_OK;
+  if (c->peer) return compact_worklist(c);  // the fused launch marked already
   const unsigned K = c->Kglob;
   KArgs a = base_args(c, K, c->it == 1);
   a.wl_out = c->wl[(K + 1) & 1];
@@ -1158,11 +1183,124 @@ ising_sr_status nccl_exchange(ising_sr_ctx* c, int* flags) {
   return ok ? ISING_SR_OK : ISING_SR_E_NCCL;
 }
 
+// ---------------------------------------------------------------------------
+// Peer-memory exchange (isr_peer.cuh): the window of ghost rows + flag inbox
+// (collective over the ranks: every rank allocates, registers and frees it at
+// the same points -- init, capacity growth, destroy) and the fused launch.
+// ---------------------------------------------------------------------------
+#if ISR_HAVE_NCCL_DEVICE
+void peer_free_rows(ising_sr_ctx* c) {
+  const isr_nccl::Api& A = isr_nccl::api();
+  if (c->pwin)
+    ((ncclResult_t(*)(ncclComm_t, ncclWindow_t))A.CommWindowDeregister)((ncclComm_t)c->nccl, (ncclWindow_t)c->pwin);
+  if (c->pbuf) ((ncclResult_t(*)(void*))A.MemFree)(c->pbuf);
+  c->pwin = nullptr;
+  c->pbuf = nullptr;
+  c->pbytes = 0;
+}
+
+ising_sr_status peer_alloc_rows(ising_sr_ctx* c) {
+  const isr_nccl::Api& A = isr_nccl::api();
+  peer_free_rows(c);
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  isr::PeerArgs& p = c->pargs;
+  p.row = c->grow;
+  p.o_stamp = al(c->gchunk[0]);
+  p.o_t = p.o_stamp + al(c->gchunk[1]);
+  p.o_pos = p.o_t + al(c->gchunk[2]);
+  p.o_inbox = 4 * c->grow;
+  const size_t inbox = 2 * (size_t)isr::kPeerMaxWorld * 2 * sizeof(int);
+  c->pbytes = (4 * c->grow + inbox + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT *
+              NCCL_WIN_REQUIRED_ALIGNMENT;
+  if (!isr_nccl::report(((ncclResult_t(*)(void**, size_t))A.MemAlloc)(&c->pbuf, c->pbytes), "ncclMemAlloc")) {
+    c->pbuf = nullptr;
+    return ISING_SR_E_OOM;
+  }
+  // zeroed before the (collective) registration: no peer can store into it earlier
+  CK(c, cudaMemsetAsync(c->pbuf, 0, c->pbytes, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  ncclWindow_t win = nullptr;
+  if (!isr_nccl::report(((ncclResult_t(*)(ncclComm_t, void*, size_t, ncclWindow_t*, int))A.CommWindowRegister)(
+                            (ncclComm_t)c->nccl, c->pbuf, c->pbytes, &win, NCCL_WIN_COLL_SYMMETRIC),
+                        "ncclCommWindowRegister"))
+    return ISING_SR_E_NCCL;
+  c->pwin = win;
+  isr::peer_bases_kernel<<<1, isr::kPeerMaxWorld + 1, 0, c->stream>>>(win, c->cfg.world, c->d_peer);
+  CK(c, cudaGetLastError());
+  CK(c, cudaMemcpyAsync(c->h_peer, c->d_peer, sizeof(unsigned long long) * (c->cfg.world + 1), cudaMemcpyDeviceToHost,
+                        c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  p.peer = c->d_peer;
+  p.mine = (char*)c->h_peer[c->cfg.world];
+  p.rank = c->cfg.rank;
+  p.world = c->cfg.world;
+  return ISING_SR_OK;
+}
+
+// after ncclCommInitRank: the peer path if this NCCL has the device API, every
+// rank is load/store-reachable (one NVLink domain) and it was not switched off
+ising_sr_status peer_setup(ising_sr_ctx* c) {
+  const isr_nccl::Api& A = isr_nccl::api();
+  const char* e = std::getenv("ISING_SR_EXCHANGE");  // sendrecv: never; peer: required (else E_NCCL)
+  if (e && std::strcmp(e, "sendrecv") == 0) return ISING_SR_OK;
+  const ising_sr_status unavailable = (e && std::strcmp(e, "peer") == 0) ? ISING_SR_E_NCCL : ISING_SR_OK;
+  if (!A.MemAlloc || !A.MemFree || !A.CommWindowRegister || !A.CommWindowDeregister || !A.DevCommCreate ||
+      !A.DevCommDestroy || !A.TeamLsa || c->cfg.world > isr::kPeerMaxWorld)
+    return unavailable;
+  const ncclTeam lsa = ((ncclTeam(*)(ncclComm_t))A.TeamLsa)((ncclComm_t)c->nccl);
+  if (lsa.nRanks != c->cfg.world || lsa.rank != c->cfg.rank) return unavailable;  // not one NVLink domain
+  c->peer_blocks = (c->RX + isr::kPeerThreads - 1) / isr::kPeerThreads;
+  ncclDevCommRequirements req = {};
+  req.lsaBarrierCount = c->peer_blocks;  // one barrier per block of the fused kernel
+  if (!isr_nccl::report(((ncclResult_t(*)(ncclComm_t, const ncclDevCommRequirements*, ncclDevComm*))A.DevCommCreate)(
+                            (ncclComm_t)c->nccl, &req, &c->dcomm),
+                        "ncclDevCommCreate"))
+    return ISING_SR_E_NCCL;
+  c->dcomm_ok = true;
+  if (dmalloc(c, &c->d_peer, isr::kPeerMaxWorld + 1) != cudaSuccess) return ISING_SR_E_OOM;
+  c->peer = true;
+  return peer_alloc_rows(c);
+}
+
+void peer_teardown(ising_sr_ctx* c) {
+  if (!c->nccl) return;
+  peer_free_rows(c);
+  if (c->dcomm_ok)
+    ((ncclResult_t(*)(ncclComm_t, const ncclDevComm*))isr_nccl::api().DevCommDestroy)((ncclComm_t)c->nccl, &c->dcomm);
+  c->dcomm_ok = false;
+  c->peer = false;
+}
+
+// pack into the neighbours' rows + flags + barrier + mark, one launch
+ising_sr_status peer_exchange(ising_sr_ctx* c, const KArgs& a, int* flags) {
+  const auto x0 = std::chrono::steady_clock::now();
+  isr::PeerArgs p = c->pargs;
+  p.flags = flags;
+  if (c->ops->warp)
+    isr::xchg_kernel<true><<<c->peer_blocks, isr::kPeerThreads, 0, c->stream>>>(a, p, c->dcomm);
+  else
+    isr::xchg_kernel<false><<<c->peer_blocks, isr::kPeerThreads, 0, c->stream>>>(a, p, c->dcomm);
+  ++c->launches;
+  CK(c, cudaGetLastError());
+  c->stats.ms_exchange_total +=
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - x0).count();
+  return ISING_SR_OK;
+}
+#else
+ising_sr_status peer_setup(ising_sr_ctx*) {
+  const char* e = std::getenv("ISING_SR_EXCHANGE");
+  return (e && std::strcmp(e, "peer") == 0) ? ISING_SR_E_NCCL : ISING_SR_OK;
+}
+void peer_teardown(ising_sr_ctx*) {}
+ising_sr_status peer_alloc_rows(ising_sr_ctx*) { return ISING_SR_E_NCCL; }
+ising_sr_status peer_exchange(ising_sr_ctx*, const KArgs&, int*) { return ISING_SR_E_NCCL; }
+#endif
+
 // the exchange of one iteration (after K1 and pack): the library's NCCL
 // communicator, or the caller's callback (which must order its work on the
 // ctx stream); `flags` = the iteration's device {changed, overflow}
 ising_sr_status exchange(ising_sr_ctx* c, int* flags) {
-  if (!c->ghost) return ISING_SR_OK;
+  if (!c->ghost || c->peer) return ISING_SR_OK;  // (peer: done by the fused launch)
   const auto x0 = std::chrono::steady_clock::now();
   ising_sr_status s = ISING_SR_OK;
   if (c->nccl) {
@@ -1195,6 +1333,7 @@ ising_sr_status grow_capacity(ising_sr_ctx* c) {
   const int K = std::min(c->ops->cnt_max, c->K * 2);
   ising_sr_status s = alloc_edges(c, K);
   if (s != ISING_SR_OK) return s;
+  if (c->peer && (s = peer_alloc_rows(c)) != ISING_SR_OK) return s;
   c->stats.overflow_retries++;
   c->stats.hist_capacity = K;
   return ISING_SR_OK;
@@ -1257,7 +1396,10 @@ ising_sr_status enqueue_pipelined(ising_sr_ctx* c, int bound) {
     CK(c, cudaGetLastError());
   }
   CK(c, cudaEventRecord(c->bev[2 * j + 1], c->stream));
-  if (c->ghost) {  // strip edges: pack, C1 + C2, mark the regions next to changed ghosts
+  if (c->ghost && c->peer) {  // strip edges: one fused launch over peer memory
+    ising_sr_status s = peer_exchange(c, a, sl->flags);
+    if (s) return s;
+  } else if (c->ghost) {  // strip edges: pack, C1 + C2, mark the regions next to changed ghosts
     c->ops->pack(a, c->gsend[0], c->gsend[1], c->RX, c->stream);
     ++c->launches;
     CK(c, cudaGetLastError());
@@ -1352,7 +1494,10 @@ ising_sr_status capture_iteration(ising_sr_ctx* c, unsigned K, bool first, const
   a.wl_out_count = &sl->wl_next;
   c->ops->region(a, c->nreg, c->stream);
   CK(c, cudaGetLastError());
-  if (c->ghost) {
+  if (c->ghost && c->peer) {
+    ising_sr_status s = peer_exchange(c, a, sl->flags);
+    if (s) return s;
+  } else if (c->ghost) {
     c->ops->pack(a, c->gsend[0], c->gsend[1], c->RX, c->stream);
     CK(c, cudaGetLastError());
     ising_sr_status s = nccl_exchange(c, sl->flags);
@@ -1436,7 +1581,7 @@ ising_sr_status run_window_graph(ising_sr_ctx* c) {
     // every launch of the graph: iteration 1 and two per loop trip
     const int launched = 1 + 2 * (int)w.trip;
     c->Kglob = K0 + 2 * w.trip;
-    c->launches += (long long)launched * (c->ghost ? 4 : 2) + launched + 2;
+    c->launches += (long long)launched * (c->ghost ? (c->peer ? 3 : 4) : 2) + launched + 2;
     const double S = (double)c->ops->spin_bytes + (double)c->ops->halo_bytes + 8 + 8 + 4 +
                      ((c->cfg.flags & ISING_SR_FLAG_DIGEST) ? 8 : 0);
     const double ib = (double)w.s5 * (2.0 * S + c->ops->sel_read_bytes + 8.0) + 9.0 * ((double)w.s1 + (double)w.s2 + (double)w.s3);
@@ -1566,6 +1711,8 @@ void ising_sr_destroy(ising_sr_ctx* c) {
   dfree(c, c->d_edges);
   if (c->cev0) cudaEventDestroy(c->cev0);
   if (c->cev1) cudaEventDestroy(c->cev1);
+  peer_teardown(c);
+  dfree(c, c->d_peer);
   if (c->nccl) isr_nccl::api().CommDestroy(c->nccl);
   for (auto& e : c->bev)
     if (e) cudaEventDestroy(e);
@@ -1831,6 +1978,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
       c->nccl = nullptr;
       return bail(ISING_SR_E_NCCL);
     }
+    if (ising_sr_status ps = peer_setup(c)) return bail(ps);
   }
   *out = c;
   return ISING_SR_OK;
@@ -1861,7 +2009,7 @@ ising_sr_status ising_sr_iterate(ising_sr_ctx* c, int32_t flags_out[2]) {
 ising_sr_status ising_sr_halo_get(ising_sr_ctx* c, ising_sr_halo* out) {
   ising_sr_status s = check(c);
   if (s) return s;
-  if (!out || !c->in_window || c->it < 1 || !c->ghost) return ISING_SR_E_STATE;
+  if (!out || !c->in_window || c->it < 1 || !c->ghost || c->peer) return ISING_SR_E_STATE;
   fill_halo(c, out);
   return ISING_SR_OK;
 }
@@ -1901,7 +2049,7 @@ ising_sr_status ising_sr_run_window(ising_sr_ctx* c, int32_t* g_out) {
   if ((s = ising_sr_begin_window(c))) return s;
   // (strips keep the host loop: NCCL's captured work is not allowed inside a
   // conditional node's body -- cudaGraphAddNode/EndCapture reject it)
-  if (c->graph && c->pipeline && !(c->cfg.flags & ISING_SR_FLAG_JACOBI_ALL) && !c->ghost) {
+  if (c->graph && c->pipeline && !(c->cfg.flags & ISING_SR_FLAG_JACOBI_ALL) && (!c->ghost || c->peer)) {
     if ((s = run_window_graph(c))) return s;
     if (g_out) *g_out = c->g;
     return ISING_SR_OK;

@@ -481,15 +481,10 @@ __global__ void unpack_kernel_w(StateView st, int Lx, int RX, int RYl, uint8_t* 
   out[i] = (uint8_t)((row >> (x - c * BX)) & 1u);
 }
 
-// K4 for the per-edge selector layout
-__global__ void pack_kernel_w(const KArgs a, GhostView send_up, GhostView send_down) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 2 * a.RX) return;
-  const bool up = i < a.RX;
-  const int c = up ? i : i - a.RX;
+// K4 for the per-edge selector layout: column c of one direction
+__device__ __forceinline__ void pack_col_w(const KArgs& a, bool up, int c, const GhostView& g) {
   const int r = up ? 0 : a.RYl - 1;
   const int e = up ? EDGE_N : EDGE_S;
-  const GhostView& g = up ? send_up : send_down;
   const ulonglong2 wp = reinterpret_cast<const ulonglong2*>(a.sel)[((long long)r * a.RX + c) * 4 + e];
   const unsigned K = stamp_of(a);
   const unsigned long long v = latest_word(wp, K + 1);
@@ -505,6 +500,13 @@ __global__ void pack_kernel_w(const KArgs a, GhostView send_up, GhostView send_d
   }
   g.cnt[c] = (uint16_t)cnt;
   g.stamp[c] = (unsigned)(v >> 32) == K ? K : 0u;
+}
+
+__global__ void pack_kernel_w(const KArgs a, GhostView send_up, GhostView send_down) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 2 * a.RX) return;
+  const bool up = i < a.RX;
+  pack_col_w(a, up, up ? i : i - a.RX, up ? send_up : send_down);
 }
 
 }  // namespace isr
