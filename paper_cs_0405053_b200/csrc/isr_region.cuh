@@ -620,7 +620,7 @@ __device__ __forceinline__ void lane_load(const KArgs& a, Lane<G>& L, int idx, S
     }
     const bool axis_off = (d < 2) ? wrapY : wrapX;
     if (FIRST || a.first || axis_off) continue;
-    const bool ghost = !PLAIN && a.ghost && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
+    const bool ghost = a.ghost && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1));
     if (ghost) {
       cnt[d] = (d == EDGE_N ? a.gh_up : a.gh_down).cnt[c];
       src[d] = d == EDGE_N ? 2u : 3u;
@@ -793,7 +793,7 @@ __device__ __forceinline__ void lane_finish(const KArgs& a, Lane<G>& L, bool& ch
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       if (!((chmask >> e) & 1u)) continue;
-      if (!PLAIN && a.ghost && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;
+      if (a.ghost && ((e == EDGE_N && r == 0) || (e == EDGE_S && r == a.RYl - 1))) continue;  // another strip's
       const int nr = e == EDGE_N ? wdec(r, a.RYl) : e == EDGE_S ? winc(r, a.RYl) : r;
       const int nc = e == EDGE_W ? wdec(c, a.RX) : e == EDGE_E ? winc(c, a.RX) : c;
       mark_dirty(a, nr * a.RX + nc, K + 1);
@@ -1005,8 +1005,8 @@ __device__ __forceinline__ void refold(const KArgs& a, Lane<G>& L, const ProdTab
 // n_work_dev (pipelined launch): the worklist length is read on the device;
 // the grid was sized for an upper bound, and the tile grows if the bound was
 // short.
-// PLAIN: no ghost rows, no region spanning a lattice axis, no fresh-window
-// restart (the common case, chosen at launch): those checks compile out
+// PLAIN: no region spanning a lattice axis, no fresh-window restart (the
+// common case, chosen at launch; strip ghost rows come with the descriptors)
 template <int BX, int BY, bool LOG, bool OBS, bool FIRST, bool PLAIN = false>
 __device__ __forceinline__ void region_body(const KArgs& a) {
   using G = Geo<BX, BY>;
@@ -1299,11 +1299,12 @@ __global__ void __launch_bounds__(kCompactThreads) compact_kernel(uint32_t* bm, 
   }
 }
 
-// The worklist's descriptors for a PLAIN iteration with stamp K (no ghost
-// rows, no wrapped axis): each item's incoming (slot, count) pairs from the
-// neighbours' latest selector words with stamp < K and its own latest word --
-// what lane_load would read itself, resolved here with whole warps so that a
-// K1 refill starts with one coalesced 16-byte read.
+// The worklist's descriptors for a PLAIN iteration with stamp K (no wrapped
+// axis): each item's incoming (slot, count) pairs from the neighbours' latest
+// selector words with stamp < K (strip edges: the ghost row's count, source
+// 2 = the row above, 3 = below) and its own latest word -- what lane_load
+// would read itself, resolved here with whole warps so that a K1 refill
+// starts with one coalesced 16-byte read.
 __global__ void __launch_bounds__(256) describe_kernel(const KArgs a, unsigned K, const uint32_t* wl,
                                                        const unsigned* count, uint4* desc) {
   const unsigned n = __ldcg(count), K0 = a.it_K0;
@@ -1322,6 +1323,11 @@ __global__ void __launch_bounds__(256) describe_kernel(const KArgs a, unsigned K
     uint32_t cnt4 = 0, pc4 = 0, bits = 0;
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
+      if (a.ghost && ((d == EDGE_N && r == 0) || (d == EDGE_S && r == a.RYl - 1))) {
+        cnt4 |= (uint32_t)__ldcg((d == EDGE_N ? a.gh_up : a.gh_down).cnt + c) << (8 * d);
+        bits |= (d == EDGE_N ? 2u : 3u) << (2 * d);
+        continue;
+      }
       const unsigned long long v = latest_word(wn[d], K);
       if (word_valid(v, K0)) {
         cnt4 |= word_count(v, d ^ 1) << (8 * d);

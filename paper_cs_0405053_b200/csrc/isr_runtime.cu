@@ -86,8 +86,8 @@ ShapeOps make_ops() {
         if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, true><<<grid, kThreads, 0, s>>>(a);
         else isr::region_kernel<BX, BY, false, true><<<grid, kThreads, 0, s>>>(a);
       }
-    } else if (a.plain && !a.ghost && !a.fresh_w && a.RX > 1 && a.RYg > 1 && (a.first || a.desc)) {
-      // the common case: ghost-row, axis-wrap and fresh-window code compiled out
+    } else if (a.plain && !a.fresh_w && a.RX > 1 && a.RYg > 1 && (a.first || a.desc)) {
+      // the common case: axis-wrap and fresh-window code compiled out (ghost rows: the descriptors)
       if (a.first) {
         if constexpr (kMB) isr::region_kernel_mb<BX, BY, false, false, true, true><<<grid, kThreads, 0, s>>>(a);
         else isr::region_kernel_first<BX, BY, false, true><<<grid, kThreads, 0, s>>>(a);
@@ -1036,7 +1036,7 @@ int compact_grid(const ising_sr_ctx* c) {
 // descriptors when the strip has no ghost rows, no region spans an axis and
 // windows do not restart afresh (the general kernel reads the selectors itself)
 bool plain_desc(const ising_sr_ctx* c) {
-  return c->plain && c->desc && !c->ghost && !(c->cfg.flags & (ISING_SR_FLAG_FRESH_WINDOW | ISING_SR_FLAG_JACOBI_ALL)) &&
+  return c->plain && c->desc && !(c->cfg.flags & (ISING_SR_FLAG_FRESH_WINDOW | ISING_SR_FLAG_JACOBI_ALL)) &&
          c->RX > 1 && c->RYg > 1 && !(c->cfg.flags & ISING_SR_FLAG_OBSERVABLES);
 }
 
