@@ -167,7 +167,15 @@ typedef struct {
   /* world > 1 (or FLAG_HALO_LOOPBACK): the 128-byte ncclUniqueId shared by
    * all ranks (rank 0 gets one from ising_sr_nccl_unique_id and broadcasts
    * it, e.g. with torch.distributed); the library creates its communicator
-   * (ncclCommInitRank(world, id, rank)) and runs the exchange on `stream`.
+   * (ncclCommInitRank(world, id, rank)) and runs the exchange on `stream`:
+   * by default one fused kernel per iteration that stores the strip-edge
+   * histories straight into the neighbours' ghost rows in an NCCL symmetric
+   * window (NCCL >= 2.28 device API, all ranks in one NVLink team)
+   * and combines the flags through an inbox + LSA barrier; env
+   * ISING_SR_EXCHANGE=sendrecv uses ncclSend/ncclRecv + ncclAllReduce instead
+   * (=peer: the fused kernel or E_NCCL).  init, capacity growth and destroy
+   * are then collective over the ranks.  With the fused kernel the step-level
+   * halo_get returns E_STATE (there are no host-visible send rows).
    * NULL: the exchange callback (or the step-level API) moves the ghost rows.
    * Copied at init. */
   const void* nccl_id;
