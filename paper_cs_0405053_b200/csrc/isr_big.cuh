@@ -240,10 +240,15 @@ __global__ void ISR_BIG_BOUNDS region_kernel_big(const KArgs a) {
   unsigned long long n_ev = 0, n_out = 0, n_in = 0, n_cmp = 0, n_reg = 0;
   unsigned fmax = 0;
   bool changed = false, overflow = false;
-  const int stride = gridDim.x * BNT;
+  // a small worklist (late iterations, bounded by the slowest region's serial
+  // chain) is spread to one region per 2^spread_log2 lanes, so no region's
+  // chain waits on other lanes' divergent steps in its warp
+  const int sl = a.spread_log2;
+  const int stride = (gridDim.x * BNT) >> sl;
   const int n_all = a.n_work_dev ? (int)__ldcg(a.n_work_dev) : a.n_work;
+  const int first_item = (t & ((1 << sl) - 1)) ? n_all : (blockIdx.x * BNT + t) >> sl;  // idle lanes skip
 
-  for (int item = blockIdx.x * BNT + t; item < n_all; item += stride) {
+  for (int item = first_item; item < n_all; item += stride) {
     const int idx = a.wl_in ? (int)a.wl_in[item] : item;
     const int r = idx / a.RX, c = idx - r * a.RX;
     const uint32_t gid = (uint32_t)((a.row0 + r) * a.RX + c);

@@ -133,6 +133,7 @@ struct KArgs {
   int rx_k;
   int refill;              // idle lanes per warp that trigger a batched refill
   int plain;               // launch the PLAIN instantiation where it applies (host dispatch only)
+  int spread_log2;         // big-region K1: one region per 2^spread_log2 threads (small worklists)
   // PLAIN iterations after the first: per worklist item {region, incoming
   // counts (byte d), own latest counts (byte e), incoming slots (2 bits per d)
   // | own latest slots << 8 | word to overwrite << 12}, written by

@@ -150,9 +150,22 @@ ShapeOps make_ops_w() {
   // lane-per-region K1 for big regions (isr_big.cuh); ISING_SR_BIG=0: warp form
   o.region = [](const KArgs& a, int n, cudaStream_t s) {
     if (big_enabled()) {
-      const int grid = std::max(1, std::min((n + isr::BNT - 1) / isr::BNT, 148 * 32));
-      if (a.obs) isr::region_kernel_big<BX, BY, false, true><<<grid, isr::BNT, 0, s>>>(a);
-      else isr::region_kernel_big<BX, BY, false><<<grid, isr::BNT, 0, s>>>(a);
+      // small worklists: spread to one region per 2^sl lanes while the grid stays within ~one wave
+      static const int smax = [] {
+        const char* e = std::getenv("ISING_SR_BIG_SPREAD");
+        return e ? std::max(0, std::min(5, std::atoi(e))) : 5;
+      }();
+      static const long long cap = [] {  // threads the spread may fill: 148 SMs x BNT x this
+        const char* e = std::getenv("ISING_SR_BIG_SPREAD_CAP");
+        return 148LL * isr::BNT * (e ? std::max(1, std::atoi(e)) : 7);  // 7 = one wave (ISR_BIG_MINB): best of 2, 4, 7, 14, 28
+      }();
+      KArgs b = a;
+      b.spread_log2 = 0;
+      while (b.spread_log2 < smax && (long long)n << (b.spread_log2 + 1) <= cap) ++b.spread_log2;
+      const long long threads = (long long)n << b.spread_log2;
+      const int grid = (int)std::max(1LL, std::min((threads + isr::BNT - 1) / isr::BNT, 148LL * 32));
+      if (a.obs) isr::region_kernel_big<BX, BY, false, true><<<grid, isr::BNT, 0, s>>>(b);
+      else isr::region_kernel_big<BX, BY, false><<<grid, isr::BNT, 0, s>>>(b);
     } else {
       const int grid = std::max(1, std::min((n + 3) / 4, 148 * 16));
       isr::region_kernel_w<BX, BY, false><<<grid, kThreads, 0, s>>>(a);
