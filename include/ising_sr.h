@@ -173,7 +173,9 @@ typedef struct {
    * window (NCCL >= 2.28 device API, all ranks in one NVLink team)
    * and combines the flags through an inbox + LSA barrier; env
    * ISING_SR_EXCHANGE=sendrecv uses ncclSend/ncclRecv + ncclAllReduce instead
-   * (=peer: the fused kernel or E_NCCL).  init, capacity growth and destroy
+   * (=peer: the fused kernel or E_NCCL; unset: send/recv also where the
+   * device API, one NVLink team or the symmetric window is unavailable, with
+   * a note on stderr).  init, capacity growth and destroy
    * are then collective over the ranks.  With the fused kernel the step-level
    * halo_get returns E_STATE (there are no host-visible send rows).
    * NULL: the exchange callback (or the step-level API) moves the ghost rows.

@@ -1250,6 +1250,8 @@ ising_sr_status peer_alloc_rows(ising_sr_ctx* c) {
   return ISING_SR_OK;
 }
 
+void peer_teardown(ising_sr_ctx* c);
+
 // after ncclCommInitRank: the peer path if this NCCL has the device API, every
 // rank is load/store-reachable (one NVLink domain) and it was not switched off
 ising_sr_status peer_setup(ising_sr_ctx* c) {
@@ -1265,14 +1267,24 @@ ising_sr_status peer_setup(ising_sr_ctx* c) {
   c->peer_blocks = (c->RX + isr::kPeerThreads - 1) / isr::kPeerThreads;
   ncclDevCommRequirements req = {};
   req.lsaBarrierCount = c->peer_blocks;  // one barrier per block of the fused kernel
+  // a failure from here on (no symmetric memory on this machine, ...) is the
+  // same on every rank of one node: fall back to the send/recv transport
+  // unless the peer one was asked for by name
+  auto fallback = [&](const char* what) {
+    std::fprintf(stderr, "ising_sr: peer-memory exchange unavailable (%s); using ncclSend/ncclRecv\n", what);
+    peer_teardown(c);
+    return unavailable;
+  };
   if (!isr_nccl::report(((ncclResult_t(*)(ncclComm_t, const ncclDevCommRequirements*, ncclDevComm*))A.DevCommCreate)(
                             (ncclComm_t)c->nccl, &req, &c->dcomm),
                         "ncclDevCommCreate"))
-    return ISING_SR_E_NCCL;
+    return fallback("ncclDevCommCreate");
   c->dcomm_ok = true;
   if (dmalloc(c, &c->d_peer, isr::kPeerMaxWorld + 1) != cudaSuccess) return ISING_SR_E_OOM;
   c->peer = true;
-  return peer_alloc_rows(c);
+  const ising_sr_status s = peer_alloc_rows(c);
+  if (s == ISING_SR_E_NCCL || s == ISING_SR_E_OOM) return fallback("symmetric window");
+  return s;
 }
 
 void peer_teardown(ising_sr_ctx* c) {
