@@ -353,11 +353,11 @@ def run_ising(args):
     # committed ncu capture of every K1 launch of one c4 window
     # (tools/ncu_traffic.py) times this run's algorithmic bytes per launch
     traffic, traffic_src = None, None
-    tp = os.path.join(ROOT, "profiles", "k1_traffic_r03.json")
+    tp = os.path.join(ROOT, "profiles", "k1_traffic_r05.json")
     if args.config == "c4" and os.path.exists(tp):
         t = json.load(open(tp))
         traffic = t["dram_over_alg"] * k1_alg_per_launch
-        traffic_src = (f"profiles/k1_traffic_r03.json: ncu --set full of all {t['launches']} K1 launches of c4 "
+        traffic_src = (f"profiles/k1_traffic_r05.json: ncu --set full of all {t['launches']} K1 launches of c4 "
                        f"window {t['window']}, DRAM / §8(d.3) K1 bytes = {t['dram_over_alg']:.2f}")
     window_bw = alg_bytes / (max_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
