@@ -265,7 +265,8 @@ def run_ising(args):
         torch.cuda.synchronize()
 
     sim = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), spins, w.W, t_end, w.seed, J=w.J, H=w.H, T=w.T,
-                  flags=flags, rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=nccl_id)
+                  flags=flags, rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=nccl_id,
+                  torch_alloc=args.torch_alloc)
     for _ in range(args.warmup):
         sim.run_window()
         sim.commit()
@@ -324,7 +325,8 @@ def run_ising(args):
             from paper_cs_0405053_b200.dist import shared_nccl_id
             nccl_id2 = shared_nccl_id(rank)
         sim2 = IsingSR(w.Lx, w.Ly, w.bx, w.by, w.rates(), pinned.numpy(), w.W, t_end, w.seed, flags=flags,
-                       rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=nccl_id2)
+                       rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=nccl_id2,
+                       torch_alloc=args.torch_alloc)
         ev2 = 0
         for _ in range(args.steps):
             sim2.run_window()
@@ -508,6 +510,8 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--torch-alloc", action="store_true",
+                    help="device buffers from torch's caching allocator (the e2e context reuses the first one's blocks)")
     ap.add_argument("--digest", action="store_true", help="also maintain the per-region event digests")
     ap.add_argument("--window", default="config", choices=["config", "tmax"],
                     help="W of the config, or the paper's T_max = ln N/(lambda |dG|) (P:502-515)")
