@@ -229,6 +229,7 @@ def run_ising(args):
     if args.gpus != world and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries the one JSON line
     nccl_id = None
     if world > 1:
         import torch.distributed as dist
@@ -344,7 +345,9 @@ def run_ising(args):
         e2e = {"value": ev2 / dt, "unit": UNIT,
                "h2d_bytes_per_step": spins.nbytes / args.steps,
                "d2h_bytes_per_step": (out.nbytes * world + 8 * args.steps) / args.steps,
-               "includes": "ising_sr_init from pinned host spins (H2D + pack) + K windows + D2H of final spins"}
+               "includes": "ising_sr_init from pinned host spins (H2D + pack) + K windows + D2H of final spins",
+               "device_buffers": ("torch caching allocator (blocks of the first context reused)" if args.torch_alloc
+                                  else "cudaMalloc inside the timed region")}
 
     if rank != 0:
         return 0
@@ -510,8 +513,10 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--torch-alloc", action="store_true",
-                    help="device buffers from torch's caching allocator (the e2e context reuses the first one's blocks)")
+    ap.add_argument("--torch-alloc", action=argparse.BooleanOptionalAction, default=True,
+                    help="device buffers from torch's caching allocator (binding option torch_alloc; the e2e context "
+                         "then reuses the blocks the first context returned instead of fresh cudaMalloc calls, whose "
+                         "cost varied 50-450 ms between boxes); --no-torch-alloc: the library's own cudaMalloc")
     ap.add_argument("--digest", action="store_true", help="also maintain the per-region event digests")
     ap.add_argument("--window", default="config", choices=["config", "tmax"],
                     help="W of the config, or the paper's T_max = ln N/(lambda |dG|) (P:502-515)")

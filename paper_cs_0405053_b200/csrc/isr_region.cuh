@@ -134,6 +134,7 @@ struct KArgs {
   int refill;              // idle lanes per warp that trigger a batched refill
   int plain;               // launch the PLAIN instantiation where it applies (host dispatch only)
   int spread_log2;         // big-region K1: one region per 2^spread_log2 threads (small worklists)
+  int lane_spread;         // lane K1: the largest k of its spread (one region per 2^k lanes; 0 = off)
   // PLAIN iterations after the first: per worklist item {region, incoming
   // counts (byte d), own latest counts (byte e), incoming slots (2 bits per d)
   // | own latest slots << 8 | word to overwrite << 12}, written by
@@ -490,10 +491,14 @@ __device__ __forceinline__ int div_rx(const KArgs& a, int idx) {
 // spills since the staged positions are packed, 31 KB of shared memory per
 // block): +3.8 % on c4 over ptxas' own 96 registers / 5 blocks; 7 blocks (72
 // registers) spill and lose 1.5 %.
+#ifndef ISR_SPREAD
+#define ISR_SPREAD 1  // small worklists spread to one region per 2^k lanes (KArgs.lane_spread = max k)
+#endif
 #ifndef ISR_NT
 #define ISR_NT 128
 #endif
 constexpr int NT = ISR_NT;   // threads per block of K1
+constexpr int kSpreadBlocks = 148 * 6;  // the spread's room: one wave of K1 blocks
 constexpr int CI = ISR_CI;   // staged entries per history
 
 // Staged history entries, column si per region in flight: incoming
@@ -1019,7 +1024,7 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
   __shared__ SG S;
   __shared__ ProdTable<G> PT;
   // the block's tile (block-uniform, kept in shared memory)
-  __shared__ int s_tile_begin, s_tile_n;
+  __shared__ int s_tile_begin, s_tile_n, s_spread;
   if (threadIdx.x == 0) {
     int tile = a.tile, n = a.n_work;
     if (a.n_work_dev) {  // the host's tile rule (tile_for) on the actual length, >= n / grid
@@ -1028,6 +1033,16 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
       const int need = (n + (int)gridDim.x - 1) / (int)gridDim.x;
       tile = max(NT * per, (need + NT - 1) / NT * NT);
     }
+    // a small worklist (late iterations: a handful of regions, each a serial chain of steps) is
+    // spread to one region per 2^k lanes, the largest k <= 5 the launched grid (at most one wave)
+    // covers, so a region's chain does not wait on the divergent steps of other regions in its warp
+    int k = 0;
+#if ISR_SPREAD
+    const long long room = (long long)min((int)gridDim.x, kSpreadBlocks) * NT;
+    while (k < a.lane_spread && ((long long)n << (k + 1)) <= room) ++k;
+    if (k > 0) tile = NT >> k;
+#endif
+    s_spread = k;
     s_tile_begin = blockIdx.x * tile;
     s_tile_n = min(tile, n - (int)(blockIdx.x * tile));
     q_next = blockDim.x;  // the first blockDim items are taken statically
@@ -1047,6 +1062,8 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
   const int REFILL = a.refill;
   bool active = false, pending = false, exhausted = false, fresh = false;
   int item = (int)threadIdx.x;
+  if (s_spread > 0)  // one region per 2^k lanes: the other lanes find the tile exhausted
+    item = (threadIdx.x & ((1u << s_spread) - 1u)) ? s_tile_n : (int)(threadIdx.x >> s_spread);
   for (;;) {
     const unsigned idle = __ballot_sync(0xffffffffu, !active);
     if (__popc(idle) >= REFILL || idle == 0xffffffffu) {

@@ -75,7 +75,12 @@ ShapeOps make_ops() {
   o.cnt_max = isr::CNT_MAX;
   o.sel_read_bytes = 5 * 16.0;
   o.region = [](const KArgs& a, int n, cudaStream_t s) {
-    const int grid = (n + a.tile - 1) / a.tile;
+    int grid = (n + a.tile - 1) / a.tile;
+    {  // a small worklist: blocks for one region per 2^k lanes within one wave (the kernel derives k from the grid)
+      int k = 0;
+      while (k < a.lane_spread && ((long long)n << (k + 1)) <= (long long)isr::kSpreadBlocks * kThreads) ++k;
+      grid = std::max(grid, (int)((((long long)n << k) + kThreads - 1) / kThreads));
+    }
     // instantiations: FLAG_OBSERVABLES (integrate M and B) x the window's first
     // iteration (no incoming histories: break-point and staging code compiled out)
     if (a.obs) {
@@ -838,6 +843,7 @@ struct ising_sr_ctx {
   unsigned delay_ns = 0;  // test knob (env ISING_SR_K1_DELAY_NS): K1 publishes late
   bool plain = true;           // K1's PLAIN instantiation where it applies (env ISING_SR_PLAIN=0: never)
   uint4* desc = nullptr;       // worklist descriptors of PLAIN iterations (describe_kernel)
+  int lane_spread = 5;  // lane K1: small worklists spread to one region per 2^k lanes, k <= this (env ISING_SR_LANE_SPREAD; 0 = off)
   int refill = 28;  // K1 batched-refill threshold (env ISING_SR_REFILL; 28 measured best after the shared fresh-load step)
   ising_sr_stats stats;
 };
@@ -1014,6 +1020,7 @@ KArgs base_args(ising_sr_ctx* c, unsigned K, bool first) {
   a.pmeta = c->pmeta;
   a.PC = c->PC;
   a.refill = c->refill;
+  a.lane_spread = c->lane_spread;
   a.plain = c->plain ? 1 : 0;
   a.delay_ns = c->delay_ns;
   {
@@ -1824,6 +1831,7 @@ ising_sr_status ising_sr_init(const ising_sr_config* cfg, const uint8_t* spins, 
   std::memset(&c->stats, 0, sizeof c->stats);
   if (const char* e = std::getenv("ISING_SR_PIPELINE")) c->pipeline = std::atoi(e) != 0;
   if (const char* e = std::getenv("ISING_SR_PLAIN")) c->plain = std::atoi(e) != 0;
+  if (const char* e = std::getenv("ISING_SR_LANE_SPREAD")) c->lane_spread = std::max(0, std::min(5, std::atoi(e)));
   if (const char* e = std::getenv("ISING_SR_REFILL")) c->refill = std::max(1, std::min(32, std::atoi(e)));
   if (const char* e = std::getenv("ISING_SR_K1_DELAY_NS")) c->delay_ns = (unsigned)std::max(0, std::atoi(e));
   if (const char* e = std::getenv("ISING_SR_GRAPH")) c->graph = std::atoi(e) != 0;

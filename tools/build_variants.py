@@ -18,7 +18,8 @@ def one(spec):
     name, _, flags = spec.partition("=")
     out = os.path.join(ROOT, "build_variants", name + ".so")
     os.makedirs(os.path.dirname(out), exist_ok=True)
-    cmd = [_build.nvcc()] + _build.NVCC_FLAGS + [f for f in flags.split(",") if f] + ["-o", out] + _build.SOURCES
+    cmd = ([_build.nvcc()] + _build.NVCC_FLAGS + _build.nccl_include() + [f for f in flags.split(",") if f] +
+           ["-o", out] + _build.SOURCES)  # (the NCCL headers: without them a variant has no peer-memory exchange)
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         sys.stderr.write(r.stderr)
