@@ -211,6 +211,24 @@ def test_k1_schedules_bit_exact(env, monkeypatch):
         check_against_oracle(w, logs=False)
 
 
+# ---------------------------------------------------------------------------
+# small worklists spread to one region per 2^k lanes (both lane-per-region
+# kernels): lattices whose worklists pass through every k on
+# the way down (n 2^k <= one wave), with the spread off, capped and full
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("env", [{}, {"ISING_SR_LANE_SPREAD": "0", "ISING_SR_BIG_SPREAD": "0"},
+                                 {"ISING_SR_LANE_SPREAD": "2", "ISING_SR_BIG_SPREAD": "2"},
+                                 {"ISING_SR_PIPELINE": "0"}, {"ISING_SR_GRAPH": "1"}])
+def test_small_worklist_spread_bit_exact(env, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for Lx, Ly, bx, by, T, W, t_end in [(512, 512, 4, 4, 2.0, 0.5, 1.5), (512, 512, 2, 2, 2.269, 0.5, 1.0),
+                                        (512, 256, 8, 8, 2.269, 1.0, 2.0), (512, 512, 16, 16, 2.269, 1.0, 2.0),
+                                        (128, 128, 1, 1, 1.0, 0.5, 1.0)]:
+        w = workloads.Workload("spread", Lx, Ly, bx, by, T=T, W=W, t_end=t_end, seed=21)
+        check_against_oracle(w, logs=False)
+
+
 @pytest.mark.parametrize("b,T,t_end", [(8, 2.269, 0.05), (32, 4.0, 0.05), (2, 1.0, 0.02)])
 def test_c5_full_lattice_prefix(b, T, t_end):
     """c5 at its full size (8192^2) for b x b regions on a prefix of the run:
