@@ -494,9 +494,6 @@ __device__ __forceinline__ int div_rx(const KArgs& a, int idx) {
 #ifndef ISR_SPREAD
 #define ISR_SPREAD 1  // small worklists spread to one region per 2^k lanes (KArgs.lane_spread = max k)
 #endif
-#ifndef ISR_DRAWSKIP
-#define ISR_DRAWSKIP 0
-#endif
 #ifndef ISR_NT
 #define ISR_NT 128
 #endif
@@ -1126,16 +1123,10 @@ __device__ __forceinline__ void region_body(const KArgs& a) {
            // straight-line block with the refold (the Philox/E(U) and fold chains interleave); after a
            // break point pair n is the pair already in use (the same V), so only an event (or a fresh_w
            // load, whose budget restarts at t_c) takes its budget
-#if ISR_DRAWSKIP
-          // a spread worklist (one region per 2^k lanes: latency-bound chains) redraws nothing after a break point
-          if (s_spread == 0 || ev || fresh)
-#endif
-          {
-            double U;
-            draw_pair(a.seed, L.gid, L.n, U, L.V, a.gen);
-            const double Eu = budget(a, U);
-            if (ev || (fresh && !PLAIN && a.fresh_w)) L.R = Eu;
-          }
+          double U;
+          draw_pair(a.seed, L.gid, L.n, U, L.V, a.gen);
+          const double Eu = budget(a, U);
+          if (ev || (fresh && !PLAIN && a.fresh_w)) L.R = Eu;
         }
         refold<G, PLAIN>(a, L, PT);  // shared by both kinds of step
         // finished now: the candidate lies beyond the window and no break point is left (every incoming
