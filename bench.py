@@ -377,6 +377,15 @@ def run_ising(args):
                        "formula": "B_alg = [A (S + 3H) + S + L] / e per committed event (SURVEY §8(d.3))"},
             "impl_bytes_per_event": impl_bytes / max(tot_ev, 1),
             "impl_bytes_note": "the library's own count of what K1 touches (DESIGN.md §6), not the roofline numerator"}
+    # what actually bounds K1: instruction issue, not HBM -- the issue rate and lane
+    # utilisation of the same committed ncu capture, as context beside the HBM fraction the metric asks for
+    ip = os.path.join(ROOT, "profiles", "k1_issue_r05.json")
+    if args.config == "c4" and os.path.exists(ip):
+        t = json.load(open(ip))
+        roof["issue"] = {"issued_ipc_active": t["issued_ipc_active_time_weighted"], "peak_ipc": t["peak_ipc"],
+                         "frac": t["issued_ipc_active_time_weighted"] / t["peak_ipc"],
+                         "active_lanes_per_warp_instruction": t["active_lanes_per_warp_instruction"],
+                         "source": t["source"], "note": "from a capture under ncu, not measured in this run"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         n_ev, secs, sample = oracle_sample()
