@@ -199,23 +199,50 @@ def run_reference(args):
 # --------------------------------------------------------------------------
 # the B200 arm
 # --------------------------------------------------------------------------
-def golden_parity(config, sim, world, nwin, w):
+def golden_parity(config, sim, world, nwin, w, rank=0, device=0, path=None):
     """The run against tests/golden/full_size/<config>_t50.json (the oracle's
     result, tools/make_goldens.py): total events, final spins and per-region
-    event counts, bit for bit (SHA-256).  Only at N = 1 and when the run ends
-    exactly at the golden's t_end."""
+    event counts, bit for bit (SHA-256).  Only when the run ends exactly at
+    the golden's t_end.  N > 1: the strips' spins and counts are hashed in
+    rank order on rank 0 (received one strip at a time); every rank takes the
+    same decisions, so the sends and receives match."""
     import hashlib
-    path = os.path.join(ROOT, "tests", "golden", "full_size", f"{config}_t{int(w.t_end)}.json")
-    if world != 1 or not os.path.exists(path):
+    path = path or os.path.join(ROOT, "tests", "golden", "full_size", f"{config}_t{int(w.t_end)}.json")
+    if not os.path.exists(path):
         return None
     g = json.load(open(path))
     if abs(nwin * w.W - g["t_end"]) > 1e-12:
         return {"checked": False, "why": f"run ends at t = {nwin * w.W}, golden at {g['t_end']}"}
     _, cnt = sim.digests()
-    spins = sim.spins()
-    sh = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
-    ok = {"events": sim.stats()["events_total"] == g["n_events"],
-          "spins": sh(spins) == g["sha256_spins"], "counts": sh(cnt.astype("<u8")) == g["sha256_count"]}
+    spins = np.ascontiguousarray(sim.spins())
+    cnt = np.ascontiguousarray(cnt.astype("<u8"))
+    events = sim.stats()["events_total"]
+    hs, hc = hashlib.sha256(), hashlib.sha256()
+    if world == 1:
+        hs.update(spins.tobytes())
+        hc.update(cnt.tobytes())
+    else:
+        import torch
+        import torch.distributed as dist
+        dev = torch.device(f"cuda:{device}") if torch.cuda.is_available() else torch.device("cpu")  # (cpu: the gloo test)
+        ev = torch.tensor([events], dtype=torch.int64, device=dev)
+        dist.all_reduce(ev)
+        events = int(ev.item())
+        mine = [torch.from_numpy(spins.reshape(-1)).to(dev), torch.from_numpy(cnt.view(np.uint8).reshape(-1)).to(dev)]
+        if rank == 0:
+            hs.update(spins.tobytes())
+            hc.update(cnt.tobytes())
+            for r in range(1, world):  # equal strips: the same sizes on every rank
+                for buf, h in zip(mine, (hs, hc)):
+                    tmp = torch.empty_like(buf)
+                    dist.recv(tmp, src=r)
+                    h.update(tmp.cpu().numpy().tobytes())
+        else:
+            for buf in mine:
+                dist.send(buf, dst=0)
+            return None
+    ok = {"events": events == g["n_events"],
+          "spins": hs.hexdigest() == g["sha256_spins"], "counts": hc.hexdigest() == g["sha256_count"]}
     return {"checked": True, "bit_exact": all(ok.values()), **ok, "golden": os.path.relpath(path, ROOT)}
 
 
@@ -301,7 +328,7 @@ def run_ising(args):
     steady = {"windows": f"{nwin - len(half)}..{nwin - 1}",
               "events_per_s": sum(r["events"] for r in half) / max(sum(r["ms"] for r in half) * 1e-3, 1e-12)}
     # parity of the run with the oracle's golden result when the run ends at the config's t_end
-    parity = golden_parity(args.config, sim, world, nwin, w)
+    parity = golden_parity(args.config, sim, world, nwin, w, rank, local)
     compact_ms = st1["ms_compact_total"] - st0["ms_compact_total"]
     if world > 1:
         import torch.distributed as dist

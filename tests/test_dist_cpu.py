@@ -103,3 +103,73 @@ def test_shared_nccl_id_broadcast(world):
         p.join(timeout=60)
     ids = [res[r] for r in range(world)]
     assert all(len(x) == 128 for x in ids) and all(x == ids[0] for x in ids) and any(ids[0])
+
+
+# ---------------------------------------------------------------------------
+# bench.py's N > 1 golden parity: the strips' spins and per-region counts
+# hashed in rank order on rank 0 must equal the hashes of the whole lattice
+# ---------------------------------------------------------------------------
+class _FakeStrip:
+    def __init__(self, spins, count, events):
+        self._s, self._c, self._e = spins, count, events
+
+    def digests(self):
+        return None, self._c
+
+    def spins(self):
+        return self._s
+
+    def stats(self):
+        return {"events_total": self._e}
+
+
+def _parity_worker(rank, world, port, q, path, corrupt):
+    import numpy as np
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import types
+
+        import bench
+        rng = np.random.default_rng(5)
+        Lx, Ly, b = 24, 12 * world, 4
+        spins = rng.integers(0, 2, size=(Ly, Lx), dtype=np.uint8)
+        count = rng.integers(0, 50, size=(Ly // b) * (Lx // b), dtype=np.uint32)
+        rows, rr = Ly // world, (Ly // b) // world * (Lx // b)
+        my_spins = spins[rank * rows:(rank + 1) * rows].copy()
+        my_count = count[rank * rr:(rank + 1) * rr].copy()
+        if corrupt and rank == world - 1:
+            my_spins[0, 0] ^= 1
+        sim = _FakeStrip(my_spins, my_count, int(my_count.sum()))
+        w = types.SimpleNamespace(t_end=2.0, W=0.5)
+        q.put((rank, bench.golden_parity("fake", sim, world, 4, w, rank, 0, path=path)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,corrupt", [(2, False), (3, False), (2, True)])
+def test_bench_multi_rank_golden_parity(world, corrupt, tmp_path):
+    import hashlib
+    import json
+
+    import numpy as np
+    rng = np.random.default_rng(5)
+    Lx, Ly, b = 24, 12 * world, 4
+    spins = rng.integers(0, 2, size=(Ly, Lx), dtype=np.uint8)
+    count = rng.integers(0, 50, size=(Ly // b) * (Lx // b), dtype=np.uint32)
+    path = str(tmp_path / "g.json")
+    json.dump({"t_end": 2.0, "n_events": int(count.sum()), "sha256_spins": hashlib.sha256(spins.tobytes()).hexdigest(),
+               "sha256_count": hashlib.sha256(count.astype("<u8").tobytes()).hexdigest()}, open(path, "w"))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_parity_worker, args=(r, world, port, q, path, corrupt)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res[r] is None for r in range(1, world))
+    assert res[0]["checked"] and res[0]["events"] and res[0]["counts"]
+    assert res[0]["spins"] == (not corrupt) and res[0]["bit_exact"] == (not corrupt)
