@@ -79,7 +79,7 @@ ShapeOps make_ops() {
     {  // a small worklist: blocks for one region per 2^k lanes within one wave (the kernel derives k from the grid)
       int k = 0;
       while (k < a.lane_spread && ((long long)n << (k + 1)) <= (long long)isr::kSpreadBlocks * kThreads) ++k;
-      grid = std::max(grid, (int)((((long long)n << k) + kThreads - 1) / kThreads));
+      if (k > 0) grid = std::max(grid, (int)((((long long)n << k) + kThreads - 1) / kThreads));
     }
     // instantiations: FLAG_OBSERVABLES (integrate M and B) x the window's first
     // iteration (no incoming histories: break-point and staging code compiled out)
