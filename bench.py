@@ -385,11 +385,11 @@ def run_ising(args):
     # committed ncu capture of every K1 launch of one c4 window
     # (tools/ncu_traffic.py) times this run's algorithmic bytes per launch
     traffic, traffic_src = None, None
-    tp = os.path.join(ROOT, "profiles", "k1_traffic_r05.json")
+    tp = os.path.join(ROOT, "profiles", "k1_traffic_r08.json")
     if args.config == "c4" and os.path.exists(tp):
         t = json.load(open(tp))
         traffic = t["dram_over_alg"] * k1_alg_per_launch
-        traffic_src = (f"profiles/k1_traffic_r05.json: ncu --set full of all {t['launches']} K1 launches of c4 "
+        traffic_src = (f"profiles/k1_traffic_r08.json: ncu --set full of all {t['launches']} K1 launches of c4 "
                        f"window {t['window']}, DRAM / §8(d.3) K1 bytes = {t['dram_over_alg']:.2f}")
     window_bw = alg_bytes / (max_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -406,7 +406,7 @@ def run_ising(args):
             "impl_bytes_note": "the library's own count of what K1 touches (DESIGN.md §6), not the roofline numerator"}
     # what actually bounds K1: instruction issue, not HBM -- the issue rate and lane
     # utilisation of the same committed ncu capture, as context beside the HBM fraction the metric asks for
-    ip = os.path.join(ROOT, "profiles", "k1_issue_r05.json")
+    ip = os.path.join(ROOT, "profiles", "k1_issue_r08.json")
     if args.config == "c4" and os.path.exists(ip):
         t = json.load(open(ip))
         roof["issue"] = {"issued_ipc_active": t["issued_ipc_active_time_weighted"], "peak_ipc": t["peak_ipc"],
